@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""Benchmark of the MoDM cache-retrieval hot path on B200 (one JSON line on rank 0).
+
+Metric (BASELINE.json): cache lookups/sec at a 100k-entry cache; % of the
+HBM / tensor roofline.  Default workload = BASELINE config 2: 100,000
+entries x 768 dims, batch-1 lookups, one FIFO insert per request.  A step is
+one lookup batch + its insert.  Config 3 (100k x 1024, batch 256) is measured
+in the same run and reported under "c3".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+value  = device time of K steps with inputs already in HBM (CUDA events on the
+         library's stream, L2 flushed between steps, max over ranks);
+e2e    = the same steps through the public API (SemanticCache.retrieve + add)
+         from host buffers: H2D of the query and the inserted row and D2H of
+         the decision are inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HBM_FALLBACK, TC_FALLBACK = 6650.0, 1590.0
+METRIC = "cache lookups/sec at 100k-entry cache (batch 1 and 256); % of HBM/tensor roofline"
+DATA = "synthetic clustered unit embeddings (reference generator model, spread 0.0554*sqrt(384/D), calibrated beta)"
+C2_CONFIG = {"workload": "C2: 100k-entry FIFO cache, 768-dim, batch-1 lookup + FIFO insert per request",
+             "entries": 100_000, "dim": 768, "batch": 1}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    return HBM_FALLBACK, TC_FALLBACK, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- workloads
+def make_workload(dim: int, n_entries: int, n_queries: int, seed: int = 17):
+    from paper_2503_11972_b200.workload import ClusteredWorkload
+
+    wl = ClusteredWorkload(dim, n_clusters=512, seed=seed)
+    rows = wl.cache_rows(n_entries)
+    Q = wl.queries(n_queries)
+    new_rows = wl.images(Q)
+    return rows, Q, new_rows
+
+
+def cpu_baseline(rows, Q, new_rows, insert: bool, seconds: float = 12.0, batch: int = 1):
+    """The oracle port (float64 numpy/OpenBLAS, all host threads) timed on a bounded sample."""
+    from oracle.retrieval import OracleCache, OracleEntry, OracleTable, blas_info
+
+    n, dim = rows.shape
+    o = OracleCache(n, dim)
+    for i, v in enumerate(rows):
+        o.insert(OracleEntry(f"e{i}", v, "large", i, 0.0))
+    t = OracleTable()
+    done = 0
+    seq = n
+    o.retrieve(Q[0], t)  # warm-up
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds and done < len(Q):
+        for b in range(batch):  # the reference has no batch API: B sequential retrieves
+            o.retrieve(Q[(done + b) % len(Q)], t)
+        if insert:
+            o.insert(OracleEntry(f"n{seq}", new_rows[done % len(new_rows)], "large", seq, 0.0))
+            seq += 1
+        done += batch
+    dt = time.perf_counter() - t0
+    threads = None
+    try:
+        from threadpoolctl import threadpool_info
+
+        threads = max((d.get("num_threads") or 0) for d in threadpool_info() if d.get("user_api") == "blas")
+    except Exception:
+        pass
+    return {
+        "value": done / dt, "unit": "lookups/s", "cores": threads or os.cpu_count(), "kind": "port",
+        "sample": f"{done} sequential retrieve{'+insert' if insert else ''} calls on a {n}x{dim} float64 "
+                  f"cache ({dt:.1f} s); {blas_info()}; host cpu_count={os.cpu_count()}",
+    }
+
+
+# --------------------------------------------------------------------------- our arm
+def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, device=0):
+    import paper_2503_11972_b200 as mc
+    from paper_2503_11972_b200 import CacheEntry, SemanticCache, ThresholdTable
+
+    total = warmup + steps
+    rows, Q, new_rows = make_workload(dim, n_entries, (2 * total + 8) * B)
+    cache = SemanticCache(capacity=n_entries, dim=dim, device=device)
+    cache.ring.append(rows)  # bulk preload (device ring), host metadata alongside
+    cache._store.extend(CacheEntry(f"e{i}", rows[i], "large", i, 0.0) for i in range(n_entries))
+    cache._next_seq = n_entries
+    table = ThresholdTable.default()
+    cache.ring.set_table(table.pairs, table.total_steps)
+
+    # value: device-timed steps, inputs resident in HBM
+    qd = Q[: total * B].reshape(total, B, dim)
+    rd = new_rows[:total] if insert else None
+    if warmup:
+        cache.ring.profile_steps(qd[:warmup], None if rd is None else rd[:warmup], warmup, flush_bytes)
+    with ClockSampler(device) as clk:
+        prof = cache.ring.profile_steps(qd[warmup:], None if rd is None else rd[warmup:], steps, flush_bytes)
+    # keep host metadata in step with the ring (the profile appended `total` rows)
+    if insert:
+        for i in range(total):
+            cache._store.append(CacheEntry(f"p{i}", new_rows[i], "large", cache._next_seq, 0.0))
+            cache._next_seq += 1
+            while len(cache._store) > cache.capacity:
+                cache._store.popleft()
+    step_ms = prof["step_ms"]
+    value = B / (step_ms * 1e-3)
+
+    # e2e: public API from host buffers
+    Qe = Q[total * B:].reshape(-1, B, dim)
+    re = new_rows[total:]
+    launches0 = cache.ring.stats()["kernel_launches"]
+    t_base = 1000.0
+    for i in range(warmup):
+        (cache.retrieve(Qe[i][0], table) if B == 1 else cache.retrieve_batch(Qe[i], table))
+        if insert:
+            cache.add(f"w{i}", re[i], "large", t_base + i)
+    t0 = time.perf_counter()
+    for i in range(warmup, warmup + steps):
+        r = cache.retrieve(Qe[i][0], table) if B == 1 else cache.retrieve_batch(Qe[i], table)
+        if insert:
+            cache.add(f"s{i}", re[i], "large", t_base + i)
+    e2e_s = time.perf_counter() - t0
+    e2e_launches = (cache.ring.stats()["kernel_launches"] - launches0) / (warmup + steps)
+    e2e = {
+        "value": B * steps / e2e_s, "unit": "lookups/s",
+        "h2d_bytes_per_step": B * dim * 8 + (dim * 8 if insert else 0),
+        "d2h_bytes_per_step": B * 24,
+        "kernel_launches_per_step": e2e_launches,
+    }
+    dp = (dim + 63) // 64 * 64
+    scan_bytes = n_entries * dp * 2 + B * dp * 8
+    flops = 2.0 * B * n_entries * dp
+    hbm, tc_burst, tc_sust, src = pk
+    scan_s = prof["scan_ms"] * 1e-3
+    t_hbm = scan_bytes / (hbm * 1e9)
+    t_tc = flops / (tc_burst * 1e12)
+    bound = "hbm" if t_hbm >= t_tc else "tensor"
+    if bound == "hbm":
+        roof = {"bound": "hbm", "achieved": scan_bytes / scan_s / 1e9, "peak": hbm, "unit": "GB/s"}
+    else:
+        roof = {"bound": "tensor", "achieved": flops / scan_s / 1e12, "peak": tc_burst, "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["peak_source"] = f"{src} (MEASURED_PEAKS.json)" if src == "measured" else "fallback (B200_PROFILING.md)"
+    roof["kernel"] = "k_gemv_scan" if B <= 4 else "k_tc_scan"
+    roof["algorithmic_bytes_per_launch"] = scan_bytes
+    roof["flops_per_launch"] = flops
+    roof["step_roofline_frac"] = max(t_hbm, t_tc) / (step_ms * 1e-3)
+    roof["traffic"] = traffic_from_profiles(roof["kernel"])
+    out = {
+        "value": value, "ms_per_step": step_ms, "e2e": e2e, "roofline": roof, "clocks": clk.summary(),
+        "gpu_launches": prof["launches_per_step"] * steps, "profile": prof,
+        "rows": rows, "Q": Q, "new_rows": new_rows, "stats": cache.ring.stats(),
+    }
+    cache.close()
+    return out
+
+
+def traffic_from_profiles(kernel: str):
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def reference_arm(args):
+    """The reference's CPU path (oracle port: numpy float64 / OpenBLAS, all host threads), same workload.
+
+    Each step = a bounded sample of the C2 workload: `per_step` sequential
+    retrieve + insert calls against the 100k x 768 cache.
+    """
+    from oracle.retrieval import OracleCache, OracleEntry, OracleTable, blas_info
+
+    per_step = 4
+    total = args.warmup + args.steps
+    rows, Q, new_rows = make_workload(768, 100_000, total * per_step + 8)
+    n, dim = rows.shape
+    o = OracleCache(n, dim)
+    for i, v in enumerate(rows):
+        o.insert(OracleEntry(f"e{i}", v, "large", i, 0.0))
+    t = OracleTable()
+    seq, j = n, 0
+    times = []
+    for s in range(total):
+        t0 = time.perf_counter()
+        for _ in range(per_step):
+            o.retrieve(Q[j], t)
+            o.insert(OracleEntry(f"n{seq}", new_rows[j], "large", seq, 0.0))
+            seq += 1
+            j += 1
+        times.append(time.perf_counter() - t0)
+    timed = sum(times[args.warmup:])
+    value = args.steps * per_step / timed
+    cb = {"value": value, "unit": "lookups/s", "cores": os.cpu_count(), "kind": "port",
+          "sample": f"{args.steps} steps x {per_step} sequential retrieve+insert calls on a {n}x{dim} float64 cache; "
+                    f"{blas_info()}"}
+    return {
+        "metric": METRIC, "value": value, "unit": "lookups/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * timed / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA, "config": dict(C2_CONFIG),
+        "impl": "reference", "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-c3", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.warmup < 3:
+        args.warmup = 3
+
+    if args.impl == "reference":
+        if rank != 0:
+            return  # rank 0 alone runs the CPU reference arm
+        print(json.dumps(reference_arm(args)))
+        return
+
+    pk = peaks()
+    flush = 256 << 20
+    c2 = run_config("c2", 768, 100_000, 1, args.steps, args.warmup, True, flush, pk)
+    line = {
+        "metric": METRIC,
+        "value": c2["value"], "unit": "lookups/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": c2["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16 scan / f32 accumulate / f64 rescoring",
+        "data": DATA,
+        "config": dict(C2_CONFIG, l2="flushed between steps (256 MiB write)",
+                       parallelism=f"replicas{world}" if world > 1 else "single"),
+        "e2e": c2["e2e"], "roofline": c2["roofline"], "clocks": c2["clocks"], "gpu_launches": c2["gpu_launches"],
+        "profile": c2["profile"], "native_stats": c2["stats"],
+    }
+    if not args.no_c3:
+        c3 = run_config("c3", 1024, 100_000, 256, max(10, args.steps // 10), args.warmup, False, flush, pk)
+        line["c3"] = {"workload": "C3: 100k entries, 1024-dim, batch-256 lookups", "value": c3["value"],
+                      "unit": "lookups/s", "ms_per_step": c3["ms_per_step"], "e2e": c3["e2e"],
+                      "roofline": c3["roofline"], "clocks": c3["clocks"], "gpu_launches": c3["gpu_launches"],
+                      "profile": c3["profile"]}
+    if rank == 0:
+        line["cpu_baseline"] = cpu_baseline(c2["rows"], c2["Q"], c2["new_rows"], insert=True, seconds=args.cpu_seconds)
+        print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,138 @@
+/*
+ * modmcache — C ABI of the B200-native MoDM cache-retrieval hot path.
+ *
+ * The reference (`mixserve`, /root/reference/pkg/src/mixserve/cache.py) has no
+ * FFI layer: its boundary is the Python class API of `SemanticCache`.  Each
+ * entry point below replaces one piece of that class's storage / arithmetic;
+ * the Python drop-in (paper_2503_11972_b200/cache.py) keeps every validation
+ * rule, exception and the CacheEntry metadata, and calls these through ctypes
+ * (see INTEGRATION.md for the binding).
+ *
+ * Conventions: plain pointers and sizes only; every function returns 0 on
+ * success or a negative MC_ERR_* code, with a thread-local message available
+ * from mc_last_error().  Host buffers belong to the caller.  Device memory
+ * belongs to the handle.  Calls on one handle are serialised by a mutex
+ * ("many readers or one writer", cache.py:144).  mc_retrieve_batch is
+ * synchronous: it returns after the results are in the caller's arrays.
+ */
+#ifndef MODMCACHE_H
+#define MODMCACHE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MC_OK 0
+#define MC_ERR_ARG (-1)
+#define MC_ERR_CUDA (-2)
+#define MC_ERR_STATE (-3)
+#define MC_ERR_NOMEM (-4)
+#define MC_ERR_UNSUPPORTED (-5)
+
+/* Per-query result flags (mc_retrieve_batch out_flags). */
+#define MC_FLAG_HIT 0x01u       /* best >= tau (cache.py:258); NaN best also counts, as in the reference */
+#define MC_FLAG_EMPTY 0x02u     /* cache had no live entries (cache.py:252-253) */
+#define MC_FLAG_TIE 0x04u       /* >= 2 live entries share the best float64 score; newest returned */
+#define MC_FLAG_NEAR_TIE 0x08u  /* runner-up within 1e-12 of best but not equal (ulp-ambiguous) */
+#define MC_FLAG_NEAR_TAU 0x10u  /* best within 1e-12 of some tau_k (ulp-ambiguous) */
+#define MC_FLAG_FALLBACK 0x20u  /* top-K' certificate failed; exhaustive exact rescan answered */
+#define MC_FLAG_NONFINITE 0x40u /* query had NaN/Inf; answered by exhaustive float64 scan */
+
+/* Scan-path selection for mc_set_path (default MC_PATH_AUTO). */
+#define MC_PATH_AUTO 0
+#define MC_PATH_GEMV 1 /* CUDA-core fp16 GEMV scan, register top-K'             */
+#define MC_PATH_GEMM 2 /* tcgen05/TMEM/TMA fp16 GEMM scan, fused top-K' epilogue */
+
+typedef struct mc_cache mc_cache;
+
+/* One shard's answer for one query, as exchanged between GPUs (32 bytes). */
+typedef struct mc_record {
+  double sim;     /* best float64 similarity among this shard's live entries */
+  double second;  /* runner-up similarity (-inf if none)                      */
+  int64_t pos;    /* global append position of the best entry (-1 if none)    */
+  uint32_t flags; /* MC_FLAG_TIE / _FALLBACK / _NONFINITE / _EMPTY              */
+  int32_t reserved;
+} mc_record;
+
+/* Replaces SemanticCache.__init__'s float64 `_buf` (cache.py:147-168):
+ * allocates a device-resident FIFO ring of `capacity` rows of `dim` floats
+ * (fp16 scan copy + float64 master) on CUDA device `device`. */
+int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device);
+int mc_destroy(mc_cache* h);
+
+/* Replaces ThresholdTable (cache.py:73-117): n strictly increasing (k, tau)
+ * pairs; tau of pair 0 is the hit threshold (cache.py:103-106), select_k is
+ * the largest k with sim >= tau_k (cache.py:112-117).  n <= 16. */
+int mc_set_thresholds(mc_cache* h, const int32_t* ks, const double* taus, int32_t n, int32_t total_steps);
+
+/* Replaces _append_row (cache.py:181-192): appends n float64 rows (row-major,
+ * stride dim) at the FIFO tail.  Rows beyond capacity displace the oldest,
+ * exactly like insert()'s append-then-evict (cache.py:230-233).  The copy
+ * into the ring is deferred and fused with the next lookup. */
+int mc_append(mc_cache* h, const double* rows, int64_t n);
+
+/* Replaces _evict_front (cache.py:194-196), n times. */
+int mc_evict_front(mc_cache* h, int64_t n);
+
+/* Live entry count (len(_store), cache.py:170-171). */
+int64_t mc_size(const mc_cache* h);
+
+/* Replaces retrieve (cache.py:244-260) for B queries at once, each against
+ * the same cache state.  queries: B x dim float64 row-major.  Outputs:
+ *   out_live  live index (0 = oldest) of the best entry, -1 if cache empty
+ *   out_sim   best float64 similarity (NaN if empty)
+ *   out_k     chosen k (select_k), 0 = none (miss or no k reached)
+ *   out_flags MC_FLAG_* bits; MC_FLAG_HIT decides hit/miss. */
+int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* out_live,
+                      double* out_sim, int32_t* out_k, uint32_t* out_flags);
+
+/* Force a scan path (tests / benchmarks).  MC_PATH_AUTO picks by batch size. */
+int mc_set_path(mc_cache* h, int32_t path);
+
+/* --- multi-GPU sharding (one process per GPU) -------------------------------
+ * Entries are dealt round-robin by global append position p: shard g of G
+ * stores p = g, g+G, g+2G, ...  mc_configure_shard must precede any append. */
+int mc_configure_shard(mc_cache* h, int32_t n_shards, int32_t shard_id);
+
+/* Local top-1 per query into a DEVICE buffer of B mc_records (e.g. the
+ * send buffer of an NCCL all-gather), enqueued on `stream` (cudaStream_t,
+ * NULL = the handle's stream); not synchronous. */
+int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream);
+
+/* Merge G x B gathered records (device pointer, shard-major) on the device and
+ * return final answers like mc_retrieve_batch.  p0 = global position of the
+ * oldest live entry (live index = pos - p0).  Synchronous. */
+int mc_merge_records(mc_cache* h, const void* dev_records, int32_t G, int32_t B, int64_t p0,
+                     void* stream, int64_t* out_live, double* out_sim, int32_t* out_k,
+                     uint32_t* out_flags);
+
+/* Measurement hook (bench.py): runs `iters` hot-path steps with all inputs
+ * already resident in HBM and times them with CUDA events on the handle's
+ * stream.  Step i = [append rows[i] if rows != NULL] + scan + certified merge
+ * + decision epilogue for queries[i] (B x dim).  Between steps (outside the
+ * timed events) a buffer of flush_bytes is written to evict L2 (0 = none).
+ * The appends advance the ring exactly like mc_append; results are discarded.
+ * out_ms[0] = mean step, [1] = mean scan kernel, [2] = mean merge+epilogue,
+ * [3] = mean append; out_counts[0] = kernel launches per step,
+ * [1] = steps whose certificate would have needed the exhaustive rescan. */
+int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int32_t B, int32_t iters,
+                     int64_t flush_bytes, double* out_ms, int64_t* out_counts);
+
+/* Counters since creation: [0] lookups, [1] certificate fallbacks,
+ * [2] non-finite queries, [3] exact ties, [4] candidates rescored,
+ * [5] GEMV launches, [6] GEMM launches, [7] kernel launches total. */
+int mc_stats(const mc_cache* h, int64_t* out8);
+
+/* Thread-local description of the last error on this thread. */
+const char* mc_last_error(void);
+
+/* Library version string. */
+const char* mc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MODMCACHE_H */

@@ -1,0 +1,25 @@
+"""B200-native MoDM cache-retrieval hot path (drop-in for mixserve.cache).
+
+Exports mirror pkg/src/mixserve/__init__.py:15-24 for the cache symbols.
+"""
+from .cache import (
+    DEFAULT_DIM,
+    DEFAULT_THRESHOLDS,
+    LARGE,
+    POLICIES,
+    SMALL,
+    STEP_CHOICES,
+    CacheEntry,
+    EmbeddingError,
+    RetrievalResult,
+    SemanticCache,
+    ThresholdTable,
+    cosine,
+    is_normalized,
+    linear_sigma_schedule,
+    noise_reentry_level,
+    normalize,
+    validate_sigma_schedule,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,198 @@
+"""ctypes binding of libmodmcache.so (the C ABI in include/modmcache.h).
+
+There is no fallback: if the shared library is missing or no sm_100 device is
+present, every call raises ``NativeError``.  ``DeviceRing`` is the thin
+object the drop-in ``SemanticCache`` drives; it holds one native handle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libmodmcache.so"
+
+MC_FLAG_HIT = 0x01
+MC_FLAG_EMPTY = 0x02
+MC_FLAG_TIE = 0x04
+MC_FLAG_NEAR_TIE = 0x08
+MC_FLAG_NEAR_TAU = 0x10
+MC_FLAG_FALLBACK = 0x20
+MC_FLAG_NONFINITE = 0x40
+
+PATH_AUTO, PATH_GEMV, PATH_GEMM = 0, 1, 2
+
+RECORD_DTYPE = np.dtype([("sim", "<f8"), ("second", "<f8"), ("pos", "<i8"), ("flags", "<u4"), ("reserved", "<i4")])
+
+EXPORTED = (
+    "mc_create", "mc_destroy", "mc_set_thresholds", "mc_append", "mc_evict_front", "mc_size",
+    "mc_retrieve_batch", "mc_set_path", "mc_configure_shard", "mc_retrieve_local_async",
+    "mc_merge_records", "mc_stats", "mc_last_error", "mc_version", "mc_profile_steps",
+)
+
+
+class NativeError(RuntimeError):
+    """Raised for any failure inside libmodmcache (message from mc_last_error)."""
+
+
+_lib = None
+
+
+def _declare(lib):
+    vp, i32, i64, dp = C.c_void_p, C.c_int32, C.c_int64, C.c_void_p
+    lib.mc_create.argtypes = [C.POINTER(vp), i64, i32, i32]
+    lib.mc_destroy.argtypes = [vp]
+    lib.mc_set_thresholds.argtypes = [vp, dp, dp, i32, i32]
+    lib.mc_append.argtypes = [vp, dp, i64]
+    lib.mc_evict_front.argtypes = [vp, i64]
+    lib.mc_size.argtypes = [vp]
+    lib.mc_size.restype = i64
+    lib.mc_retrieve_batch.argtypes = [vp, dp, i32, dp, dp, dp, dp]
+    lib.mc_set_path.argtypes = [vp, i32]
+    lib.mc_configure_shard.argtypes = [vp, i32, i32]
+    lib.mc_retrieve_local_async.argtypes = [vp, dp, i32, vp, vp]
+    lib.mc_merge_records.argtypes = [vp, vp, i32, i32, i64, vp, dp, dp, dp, dp]
+    lib.mc_stats.argtypes = [vp, dp]
+    lib.mc_profile_steps.argtypes = [vp, dp, dp, i32, i32, i64, dp, dp]
+    lib.mc_last_error.restype = C.c_char_p
+    lib.mc_version.restype = C.c_char_p
+    return lib
+
+
+def load(path: str | os.PathLike | None = None):
+    """Load (once) and return the native library; raises NativeError if absent."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise NativeError(
+            f"{p} is missing: build it with `python -m paper_2503_11972_b200.build` "
+            "(there is no CPU fallback for the retrieval path)"
+        )
+    try:
+        lib = _declare(C.CDLL(str(p)))
+    except OSError as exc:
+        raise NativeError(f"cannot load {p}: {exc}") from exc
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _check(lib, rc: int) -> None:
+    if rc != 0:
+        raise NativeError(f"libmodmcache error {rc}: {lib.mc_last_error().decode(errors='replace')}")
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class DeviceRing:
+    """One device-resident FIFO ring (fp16 scan copy + float64 master) on one GPU."""
+
+    def __init__(self, capacity: int, dim: int, device: int = 0):
+        self.lib = load()
+        self.capacity = int(capacity)
+        self.dim = int(dim)
+        self.device = int(device)
+        h = C.c_void_p()
+        _check(self.lib, self.lib.mc_create(C.byref(h), self.capacity, self.dim, self.device))
+        self._h = h
+        self._bcap = 0
+        self._ensure_out(1)
+        self._table_key = None
+
+    # -- lifecycle -----------------------------------------------------------
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), None
+        if h is not None and h.value:
+            self.lib.mc_destroy(h)
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order varies
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- configuration -------------------------------------------------------
+    def set_table(self, pairs, total_steps: int) -> None:
+        key = (tuple(pairs), int(total_steps))
+        if key == self._table_key:
+            return
+        ks = np.array([k for k, _ in pairs], dtype=np.int32)
+        taus = np.array([t for _, t in pairs], dtype=np.float64)
+        _check(self.lib, self.lib.mc_set_thresholds(self._h, _ptr(ks), _ptr(taus), len(ks), int(total_steps)))
+        self._table_key = key
+
+    def set_path(self, path: int) -> None:
+        _check(self.lib, self.lib.mc_set_path(self._h, int(path)))
+
+    def configure_shard(self, n_shards: int, shard_id: int) -> None:
+        _check(self.lib, self.lib.mc_configure_shard(self._h, int(n_shards), int(shard_id)))
+
+    # -- ring maintenance ----------------------------------------------------
+    def append(self, rows: np.ndarray) -> None:
+        rows = np.ascontiguousarray(rows, dtype=np.float64)
+        n = rows.shape[0] if rows.ndim == 2 else 1
+        _check(self.lib, self.lib.mc_append(self._h, _ptr(rows), n))
+
+    def evict_front(self, n: int) -> None:
+        if n:
+            _check(self.lib, self.lib.mc_evict_front(self._h, int(n)))
+
+    def __len__(self) -> int:
+        return int(self.lib.mc_size(self._h))
+
+    # -- lookups -------------------------------------------------------------
+    def _ensure_out(self, B: int) -> None:
+        if B <= self._bcap:
+            return
+        cap = max(B, 2 * self._bcap, 4)
+        self._live = np.empty(cap, dtype=np.int64)
+        self._sim = np.empty(cap, dtype=np.float64)
+        self._k = np.empty(cap, dtype=np.int32)
+        self._flags = np.empty(cap, dtype=np.uint32)
+        self._bcap = cap
+
+    def retrieve(self, Q: np.ndarray):
+        """Q: float64 [B, dim] -> (live[B], sim[B], k[B], flags[B]) views (valid until next call)."""
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        B = Q.shape[0]
+        self._ensure_out(B)
+        _check(self.lib, self.lib.mc_retrieve_batch(
+            self._h, _ptr(Q), B, _ptr(self._live), _ptr(self._sim), _ptr(self._k), _ptr(self._flags)))
+        return self._live[:B], self._sim[:B], self._k[:B], self._flags[:B]
+
+    def retrieve_local_async(self, Q: np.ndarray, dev_records_ptr: int, stream_ptr: int = 0) -> None:
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        _check(self.lib, self.lib.mc_retrieve_local_async(self._h, _ptr(Q), Q.shape[0], dev_records_ptr,
+                                                          stream_ptr or None))
+
+    def merge_records(self, dev_records_ptr: int, G: int, B: int, p0: int, stream_ptr: int = 0):
+        self._ensure_out(B)
+        _check(self.lib, self.lib.mc_merge_records(
+            self._h, dev_records_ptr, int(G), int(B), int(p0), stream_ptr or None,
+            _ptr(self._live), _ptr(self._sim), _ptr(self._k), _ptr(self._flags)))
+        return self._live[:B], self._sim[:B], self._k[:B], self._flags[:B]
+
+    def profile_steps(self, Q: np.ndarray, rows: np.ndarray | None, iters: int, flush_bytes: int):
+        """Device-timed steps (see mc_profile_steps). Q: [iters, B, dim]; rows: [iters, dim] or None."""
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        B = Q.shape[1]
+        r = None if rows is None else np.ascontiguousarray(rows, dtype=np.float64)
+        ms = np.zeros(4, dtype=np.float64)
+        cnt = np.zeros(2, dtype=np.int64)
+        _check(self.lib, self.lib.mc_profile_steps(self._h, _ptr(Q), None if r is None else _ptr(r), B, int(iters),
+                                                   int(flush_bytes), _ptr(ms), _ptr(cnt)))
+        return {"step_ms": ms[0], "scan_ms": ms[1], "merge_ms": ms[2], "append_ms": ms[3],
+                "launches_per_step": int(cnt[0]), "would_fallback": int(cnt[1])}
+
+    def stats(self) -> dict:
+        out = np.zeros(8, dtype=np.int64)
+        _check(self.lib, self.lib.mc_stats(self._h, _ptr(out)))
+        keys = ("lookups", "fallbacks", "nonfinite", "ties", "candidates", "gemv_launches", "gemm_launches",
+                "kernel_launches")
+        return dict(zip(keys, (int(x) for x in out)))

@@ -1,0 +1,623 @@
+// C ABI of libmodmcache.so (declared in include/modmcache.h).
+//
+// Host side of the device ring: owns the CUDA stream, the device buffers,
+// the pinned staging buffers, and a host mirror of the ring window that is
+// published to the device on every flush.  Every call is serialised by the
+// handle's mutex ("many readers or one writer", cache.py:144).
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "mc_internal.cuh"
+
+using namespace mc;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(MC_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+struct mc_cache {
+  std::mutex mu;
+  int dev = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  long long C = 0;
+  int D = 0, Dp = 0;
+  ShardMap shard{1, 0};
+
+  // host mirror of the ring window
+  long long head = 0, count = 0, jhead = 0, appended = 0;
+  bool state_dirty = false;
+
+  // device-resident ring
+  __half* ring16 = nullptr;
+  double* ring64 = nullptr;
+  RingState* d_state = nullptr;
+
+  // append staging
+  long long stage_cap = 0;
+  double* h_stage = nullptr;  // pinned [stage_cap][D]
+  double* d_stage = nullptr;  // [stage_cap][Dp]
+  long long n_pending = 0;
+  long long pending_first_slot = 0;
+  cudaEvent_t stage_ev = nullptr;
+  bool stage_inflight = false;
+
+  // per-batch buffers
+  int Bcap = 0;
+  double* h_q = nullptr;   // pinned [Bcap][D]
+  double* d_q64 = nullptr; // [Bcap][Dp]
+  float* d_part_s = nullptr;
+  long long* d_part_p = nullptr;
+  float* d_part_floor = nullptr;
+  int part_chunks = 0;
+  mc_record* d_rec = nullptr;
+  mc_record* d_scratch = nullptr;
+  OutRec* d_out = nullptr;
+  OutRec* h_out = nullptr;  // pinned
+  cudaEvent_t q_ev = nullptr;
+  bool q_inflight = false;
+
+  Thresholds thr{};
+  int path = MC_PATH_AUTO;
+  long long stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void free_batch(mc_cache* h) {
+  cudaFreeHost(h->h_q);
+  cudaFree(h->d_q64);
+  cudaFree(h->d_part_s);
+  cudaFree(h->d_part_p);
+  cudaFree(h->d_part_floor);
+  cudaFree(h->d_rec);
+  cudaFree(h->d_scratch);
+  cudaFree(h->d_out);
+  cudaFreeHost(h->h_out);
+  h->h_q = nullptr;
+  h->d_q64 = nullptr;
+  h->d_part_s = nullptr;
+  h->d_part_p = nullptr;
+  h->d_part_floor = nullptr;
+  h->d_rec = nullptr;
+  h->d_scratch = nullptr;
+  h->d_out = nullptr;
+  h->h_out = nullptr;
+  h->Bcap = 0;
+}
+
+int ensure_batch(mc_cache* h, int B) {
+  if (B <= h->Bcap) return MC_OK;
+  CU(cudaStreamSynchronize(h->stream));
+  free_batch(h);
+  int cap = 1;
+  while (cap < B) cap <<= 1;
+  cap = std::max(cap, 4);
+  const int chunks = std::max(gemv_grid(h->sm_count), exact_grid(h->sm_count));
+  CU(cudaMallocHost(&h->h_q, (size_t)cap * h->D * sizeof(double)));
+  CU(cudaMalloc(&h->d_q64, (size_t)cap * h->Dp * sizeof(double)));
+  CU(cudaMemset(h->d_q64, 0, (size_t)cap * h->Dp * sizeof(double)));
+  CU(cudaMalloc(&h->d_part_s, (size_t)cap * chunks * KP * sizeof(float)));
+  CU(cudaMalloc(&h->d_part_p, (size_t)cap * chunks * KP * sizeof(long long)));
+  CU(cudaMalloc(&h->d_part_floor, (size_t)cap * chunks * sizeof(float)));
+  CU(cudaMalloc(&h->d_rec, (size_t)cap * sizeof(mc_record)));
+  CU(cudaMalloc(&h->d_scratch, (size_t)cap * exact_grid(h->sm_count) * sizeof(mc_record)));
+  CU(cudaMalloc(&h->d_out, (size_t)cap * sizeof(OutRec)));
+  CU(cudaMallocHost(&h->h_out, (size_t)cap * sizeof(OutRec)));
+  h->part_chunks = chunks;
+  h->Bcap = cap;
+  return MC_OK;
+}
+
+RingState mirror(const mc_cache* h) { return RingState{h->head, h->count, h->jhead, h->C}; }
+
+// Publish pending appends / evictions to the device (stream-ordered).
+int flush(mc_cache* h) {
+  if (h->n_pending == 0 && !h->state_dirty) return MC_OK;
+  long long nw = 0, first = 0;
+  if (h->n_pending > 0) {
+    nw = std::min(h->n_pending, h->C);
+    const long long skip = h->n_pending - nw;
+    first = (h->pending_first_slot + skip) % h->C;
+    CU(cudaMemcpy2DAsync(h->d_stage, (size_t)h->Dp * sizeof(double), h->h_stage + (size_t)skip * h->D,
+                         (size_t)h->D * sizeof(double), (size_t)h->D * sizeof(double), (size_t)nw,
+                         cudaMemcpyHostToDevice, h->stream));
+    CU(cudaEventRecord(h->stage_ev, h->stream));
+    h->stage_inflight = true;
+  }
+  CU(launch_append(h->d_stage, nw, first, mirror(h), h->D, h->Dp, h->ring16, h->ring64, h->d_state, h->stream));
+  h->stats[7]++;
+  h->n_pending = 0;
+  h->state_dirty = false;
+  return MC_OK;
+}
+
+int wait_q(mc_cache* h) {
+  if (h->q_inflight) {
+    CU(cudaEventSynchronize(h->q_ev));
+    h->q_inflight = false;
+  }
+  return MC_OK;
+}
+
+// Upload B queries (row-major, stride D) into d_q64 (stride Dp).
+int upload_queries(mc_cache* h, const double* queries, int B) {
+  int rc = wait_q(h);
+  if (rc) return rc;
+  memcpy(h->h_q, queries, (size_t)B * h->D * sizeof(double));
+  CU(cudaMemcpy2DAsync(h->d_q64, (size_t)h->Dp * sizeof(double), h->h_q, (size_t)h->D * sizeof(double),
+                       (size_t)h->D * sizeof(double), (size_t)B, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaEventRecord(h->q_ev, h->stream));
+  h->q_inflight = true;
+  return MC_OK;
+}
+
+// Scan pass only: per-chunk top-K' lists for B queries at q64 (stride Dp).
+int scan(mc_cache* h, const double* q64, int B, Partials& part, const double** qscale, double* eps_rel) {
+  part = Partials{h->d_part_s, h->d_part_p, h->d_part_floor, gemv_grid(h->sm_count)};
+  *qscale = nullptr;
+  *eps_rel = gemv_eps_rel(h->Dp);
+  for (int b0 = 0; b0 < B; b0 += 4) {
+    const int nb = std::min(4, B - b0);
+    CU(launch_gemv_scan(h->ring16, h->d_state, h->Dp, q64 + (size_t)b0 * h->Dp, nb, part, b0,
+                        gemv_grid(h->sm_count), h->shard, h->stream));
+    h->stats[5]++;
+    h->stats[7]++;
+  }
+  return MC_OK;
+}
+
+// Scan + certified merge + (optionally, device-driven) exhaustive rescans into rec[0..B).
+int scan_and_merge(mc_cache* h, const double* q64, int B, mc_record* rec, bool always_rescan) {
+  Partials part;
+  const double* qscale;
+  double eps;
+  int rc = scan(h, q64, B, part, &qscale, &eps);
+  if (rc) return rc;
+  CU(launch_merge(h->d_state, h->ring64, h->D, h->Dp, q64, B, part, qscale, eps, eps_abs1(), rec, h->shard,
+                  h->stream));
+  h->stats[7]++;
+  if (always_rescan) {
+    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, q64, B, rec, h->d_scratch,
+                           exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
+    h->stats[7] += 2;
+  }
+  return MC_OK;
+}
+
+int copy_out(mc_cache* h, int B, int64_t* out_live, double* out_sim, int32_t* out_k, uint32_t* out_flags) {
+  for (int b = 0; b < B; ++b) {
+    const OutRec& o = h->h_out[b];
+    if (out_live) out_live[b] = o.live;
+    if (out_sim) out_sim[b] = o.sim;
+    if (out_k) out_k[b] = o.k;
+    const unsigned f = o.flags & 0xffffu;
+    if (out_flags) out_flags[b] = f;
+    if (f & MC_FLAG_FALLBACK) h->stats[1]++;
+    if (f & MC_FLAG_NONFINITE) h->stats[2]++;
+    if (f & MC_FLAG_TIE) h->stats[3]++;
+  }
+  h->stats[0] += B;
+  return MC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mc_last_error(void) { return g_err.c_str(); }
+
+const char* mc_version(void) { return "modmcache 0.1.0 (sm_100a)"; }
+
+int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
+  if (!out) return fail(MC_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (capacity < 1) return fail(MC_ERR_ARG, "capacity must be >= 1, got %lld", (long long)capacity);
+  if (dim < 1 || dim > 4096) return fail(MC_ERR_UNSUPPORTED, "dim must lie in [1, 4096], got %d", dim);
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(MC_ERR_ARG, "device %d out of range (%d devices)", device, ndev);
+  DeviceGuard guard(device);
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(MC_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a",
+                                    device, prop.major, prop.minor);
+  mc_cache* h = new mc_cache();
+  h->dev = device;
+  h->sm_count = prop.multiProcessorCount;
+  h->C = capacity;
+  h->D = dim;
+  h->Dp = (dim + 63) / 64 * 64;
+  auto cleanup = [&](int rc) {
+    mc_destroy(h);
+    return rc;
+  };
+  int rc;
+#define CUC(call)                                                                                     \
+  do {                                                                                                \
+    cudaError_t e_ = (call);                                                                          \
+    if (e_ != cudaSuccess)                                                                            \
+      return cleanup(fail(MC_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_))); \
+  } while (0)
+  CUC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  CUC(cudaEventCreateWithFlags(&h->stage_ev, cudaEventDisableTiming));
+  CUC(cudaEventCreateWithFlags(&h->q_ev, cudaEventDisableTiming));
+  const size_t n16 = (size_t)h->C * h->Dp * sizeof(__half);
+  const size_t n64 = (size_t)h->C * h->Dp * sizeof(double);
+  CUC(cudaMalloc(&h->ring16, n16));
+  CUC(cudaMalloc(&h->ring64, n64));
+  CUC(cudaMemsetAsync(h->ring16, 0, n16, h->stream));
+  CUC(cudaMemsetAsync(h->ring64, 0, n64, h->stream));
+  CUC(cudaMalloc(&h->d_state, sizeof(RingState)));
+  {
+    RingState z{0, 0, 0, h->C};
+    CUC(cudaMemcpyAsync(h->d_state, &z, sizeof z, cudaMemcpyHostToDevice, h->stream));
+  }
+  h->stage_cap = std::max<long long>(1, std::min<long long>(h->C, (16ll << 20) / ((long long)h->D * 8)));
+  CUC(cudaMallocHost(&h->h_stage, (size_t)h->stage_cap * h->D * sizeof(double)));
+  CUC(cudaMalloc(&h->d_stage, (size_t)h->stage_cap * h->Dp * sizeof(double)));
+  CUC(cudaMemsetAsync(h->d_stage, 0, (size_t)h->stage_cap * h->Dp * sizeof(double), h->stream));
+  rc = ensure_batch(h, 4);
+  if (rc) return cleanup(rc);
+  static const int ks[6] = {5, 10, 15, 20, 25, 30};
+  static const double taus[6] = {0.25, 0.26, 0.27, 0.28, 0.29, 0.30};  // cache.py:18
+  h->thr.n = 6;
+  h->thr.total_steps = 50;
+  for (int i = 0; i < 6; ++i) {
+    h->thr.ks[i] = ks[i];
+    h->thr.taus[i] = taus[i];
+  }
+  CUC(cudaStreamSynchronize(h->stream));
+#undef CUC
+  *out = h;
+  return MC_OK;
+}
+
+int mc_destroy(mc_cache* h) {
+  if (!h) return MC_OK;
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    DeviceGuard guard(h->dev);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    free_batch(h);
+    cudaFree(h->ring16);
+    cudaFree(h->ring64);
+    cudaFree(h->d_state);
+    cudaFreeHost(h->h_stage);
+    cudaFree(h->d_stage);
+    if (h->stage_ev) cudaEventDestroy(h->stage_ev);
+    if (h->q_ev) cudaEventDestroy(h->q_ev);
+    if (h->stream) cudaStreamDestroy(h->stream);
+  }
+  delete h;
+  return MC_OK;
+}
+
+int mc_set_thresholds(mc_cache* h, const int32_t* ks, const double* taus, int32_t n, int32_t total_steps) {
+  if (!h || !ks || !taus) return fail(MC_ERR_ARG, "NULL argument");
+  if (n < 1 || n > MAX_PAIRS) return fail(MC_ERR_ARG, "need 1..%d threshold pairs, got %d", MAX_PAIRS, n);
+  for (int i = 1; i < n; ++i)
+    if (!(ks[i] > ks[i - 1]) || !(taus[i] > taus[i - 1]))
+      return fail(MC_ERR_ARG, "k and tau must be strictly increasing");
+  std::lock_guard<std::mutex> lk(h->mu);
+  h->thr.n = n;
+  h->thr.total_steps = total_steps;
+  for (int i = 0; i < n; ++i) {
+    h->thr.ks[i] = ks[i];
+    h->thr.taus[i] = taus[i];
+  }
+  return MC_OK;
+}
+
+int mc_configure_shard(mc_cache* h, int32_t n_shards, int32_t shard_id) {
+  if (!h) return fail(MC_ERR_ARG, "NULL handle");
+  if (n_shards < 1 || shard_id < 0 || shard_id >= n_shards)
+    return fail(MC_ERR_ARG, "bad shard %d of %d", shard_id, n_shards);
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->appended != 0) return fail(MC_ERR_STATE, "configure the shard before the first append");
+  h->shard = ShardMap{n_shards, shard_id};
+  return MC_OK;
+}
+
+int mc_set_path(mc_cache* h, int32_t path) {
+  if (!h) return fail(MC_ERR_ARG, "NULL handle");
+  if (path < MC_PATH_AUTO || path > MC_PATH_GEMM) return fail(MC_ERR_ARG, "unknown path %d", path);
+  std::lock_guard<std::mutex> lk(h->mu);
+  h->path = path;
+  return MC_OK;
+}
+
+int64_t mc_size(const mc_cache* h) { return h ? h->count : -1; }
+
+int mc_append(mc_cache* h, const double* rows, int64_t n) {
+  if (!h || (!rows && n > 0)) return fail(MC_ERR_ARG, "NULL argument");
+  if (n < 0) return fail(MC_ERR_ARG, "negative row count");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  for (int64_t i = 0; i < n; ++i) {
+    if (h->n_pending == h->stage_cap) {
+      int rc = flush(h);
+      if (rc) return rc;
+    }
+    if (h->n_pending == 0 && h->stage_inflight) {
+      CU(cudaEventSynchronize(h->stage_ev));
+      h->stage_inflight = false;
+    }
+    if (h->count == h->C) {  // append-then-evict of cache.py:230-233, evicting first
+      h->head = (h->head + 1) % h->C;
+      h->count--;
+      h->jhead++;
+    }
+    const long long slot = (h->head + h->count) % h->C;
+    if (h->n_pending == 0) h->pending_first_slot = slot;
+    memcpy(h->h_stage + (size_t)h->n_pending * h->D, rows + (size_t)i * h->D, (size_t)h->D * sizeof(double));
+    h->n_pending++;
+    h->count++;
+    h->appended++;
+    h->state_dirty = true;
+  }
+  return MC_OK;
+}
+
+int mc_evict_front(mc_cache* h, int64_t n) {
+  if (!h) return fail(MC_ERR_ARG, "NULL handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (n < 0 || n > h->count) return fail(MC_ERR_STATE, "cannot evict %lld of %lld live rows", (long long)n,
+                                         (long long)h->count);
+  if (n == 0) return MC_OK;
+  h->head = (h->head + n) % h->C;
+  h->count -= n;
+  h->jhead += n;
+  h->state_dirty = true;
+  return MC_OK;
+}
+
+int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* out_live, double* out_sim,
+                      int32_t* out_k, uint32_t* out_flags) {
+  if (!h || (!queries && B > 0)) return fail(MC_ERR_ARG, "NULL argument");
+  if (B < 0) return fail(MC_ERR_ARG, "negative batch");
+  if (B == 0) return MC_OK;
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  if (h->count == 0) {  // cache.py:252-253
+    for (int b = 0; b < B; ++b) {
+      if (out_live) out_live[b] = -1;
+      if (out_sim) out_sim[b] = NAN;
+      if (out_k) out_k[b] = 0;
+      if (out_flags) out_flags[b] = MC_FLAG_EMPTY;
+    }
+    h->stats[0] += B;
+    return MC_OK;
+  }
+  int rc = ensure_batch(h, B);
+  if (rc) return rc;
+  rc = flush(h);
+  if (rc) return rc;
+  rc = upload_queries(h, queries, B);
+  if (rc) return rc;
+  rc = scan_and_merge(h, h->d_q64, B, h->d_rec, false);
+  if (rc) return rc;
+  CU(launch_finalize(h->d_rec, 1, B, -1, h->d_state, h->thr, h->d_out, h->stream));
+  h->stats[7]++;
+  CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  h->q_inflight = false;
+  bool need = false;
+  for (int b = 0; b < B; ++b) need |= (h->h_out[b].flags & FLAG_NEED_ANY) != 0;
+  if (need) {  // rare: certificate failed or exotic query -> exact rescan, then decide again
+    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, h->d_q64, B, h->d_rec, h->d_scratch,
+                           exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
+    CU(launch_finalize(h->d_rec, 1, B, -1, h->d_state, h->thr, h->d_out, h->stream));
+    h->stats[7] += 3;
+    CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+  }
+  return copy_out(h, B, out_live, out_sim, out_k, out_flags);
+}
+
+int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream) {
+  if (!h || !dev_records || (!queries && B > 0)) return fail(MC_ERR_ARG, "NULL argument");
+  if (B <= 0) return fail(MC_ERR_ARG, "batch must be positive");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  mc_record* rec = static_cast<mc_record*>(dev_records);
+  int rc = ensure_batch(h, B);
+  if (rc) return rc;
+  rc = flush(h);
+  if (rc) return rc;
+  rc = upload_queries(h, queries, B);
+  if (rc) return rc;
+  if (h->count == 0) {
+    CU(cudaMemsetAsync(rec, 0xff, (size_t)B * sizeof(mc_record), h->stream));  // pos = -1 (NaN sims)
+  } else {
+    rc = scan_and_merge(h, h->d_q64, B, rec, true);
+    if (rc) return rc;
+  }
+  if (stream && stream != h->stream) {
+    cudaEvent_t ev;
+    CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CU(cudaEventRecord(ev, h->stream));
+    CU(cudaStreamWaitEvent((cudaStream_t)stream, ev, 0));
+    CU(cudaEventDestroy(ev));
+  }
+  h->stats[0] += B;
+  return MC_OK;
+}
+
+int mc_merge_records(mc_cache* h, const void* dev_records, int32_t G, int32_t B, int64_t p0, void* stream,
+                     int64_t* out_live, double* out_sim, int32_t* out_k, uint32_t* out_flags) {
+  if (!h || !dev_records) return fail(MC_ERR_ARG, "NULL argument");
+  if (G < 1 || B <= 0 || p0 < 0) return fail(MC_ERR_ARG, "bad merge shape G=%d B=%d p0=%lld", G, B, (long long)p0);
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  int rc = ensure_batch(h, B);
+  if (rc) return rc;
+  cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+  CU(launch_finalize(static_cast<const mc_record*>(dev_records), G, B, p0, h->d_state, h->thr, h->d_out, s));
+  CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  h->stats[7]++;
+  for (int b = 0; b < B; ++b) {
+    const OutRec& o = h->h_out[b];
+    if (out_live) out_live[b] = o.live;
+    if (out_sim) out_sim[b] = o.sim;
+    if (out_k) out_k[b] = o.k;
+    if (out_flags) out_flags[b] = o.flags & 0xffffu;
+  }
+  return MC_OK;
+}
+
+int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int32_t B, int32_t iters,
+                     int64_t flush_bytes, double* out_ms, int64_t* out_counts) {
+  if (!h || !queries || !out_ms || !out_counts) return fail(MC_ERR_ARG, "NULL argument");
+  if (B < 1 || iters < 1) return fail(MC_ERR_ARG, "need B >= 1 and iters >= 1");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  int rc = ensure_batch(h, B);
+  if (rc) return rc;
+  rc = flush(h);
+  if (rc) return rc;
+  if (h->count == 0 && !rows) return fail(MC_ERR_STATE, "profile needs a non-empty cache");
+  const size_t qbytes = (size_t)iters * B * h->Dp * sizeof(double);
+  double *d_qall = nullptr, *d_rows = nullptr;
+  OutRec* d_outs = nullptr;
+  void* d_flush = nullptr;
+  const int nev = 4;
+  std::vector<cudaEvent_t> ev((size_t)iters * nev, nullptr);
+  auto release = [&]() {
+    cudaStreamSynchronize(h->stream);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    cudaFree(d_qall);
+    cudaFree(d_rows);
+    cudaFree(d_outs);
+    cudaFree(d_flush);
+  };
+#define CUP(call)                                                                                      \
+  do {                                                                                                 \
+    cudaError_t e_ = (call);                                                                           \
+    if (e_ != cudaSuccess) {                                                                           \
+      release();                                                                                       \
+      return fail(MC_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_));    \
+    }                                                                                                  \
+  } while (0)
+  CUP(cudaMalloc(&d_qall, qbytes));
+  CUP(cudaMemset(d_qall, 0, qbytes));
+  CUP(cudaMemcpy2D(d_qall, (size_t)h->Dp * sizeof(double), queries, (size_t)h->D * sizeof(double),
+                   (size_t)h->D * sizeof(double), (size_t)iters * B, cudaMemcpyHostToDevice));
+  if (rows) {
+    CUP(cudaMalloc(&d_rows, (size_t)iters * h->Dp * sizeof(double)));
+    CUP(cudaMemset(d_rows, 0, (size_t)iters * h->Dp * sizeof(double)));
+    CUP(cudaMemcpy2D(d_rows, (size_t)h->Dp * sizeof(double), rows, (size_t)h->D * sizeof(double),
+                     (size_t)h->D * sizeof(double), (size_t)iters, cudaMemcpyHostToDevice));
+  }
+  CUP(cudaMalloc(&d_outs, (size_t)iters * B * sizeof(OutRec)));
+  if (flush_bytes > 0) CUP(cudaMalloc(&d_flush, (size_t)flush_bytes));
+  for (auto& e : ev) CUP(cudaEventCreate(&e));
+  const long long launches0 = h->stats[7];
+  for (int it = 0; it < iters; ++it) {
+    if (d_flush) CUP(cudaMemsetAsync(d_flush, it & 0xff, (size_t)flush_bytes, h->stream));
+    CUP(cudaEventRecord(ev[(size_t)it * nev + 0], h->stream));
+    if (rows) {
+      if (h->count == h->C) {
+        h->head = (h->head + 1) % h->C;
+        h->count--;
+        h->jhead++;
+      }
+      const long long slot = (h->head + h->count) % h->C;
+      h->count++;
+      h->appended++;
+      CUP(launch_append(d_rows + (size_t)it * h->Dp, 1, slot, mirror(h), h->D, h->Dp, h->ring16, h->ring64,
+                        h->d_state, h->stream));
+      h->stats[7]++;
+    }
+    CUP(cudaEventRecord(ev[(size_t)it * nev + 1], h->stream));
+    const double* q = d_qall + (size_t)it * B * h->Dp;
+    Partials part;
+    const double* qscale;
+    double eps;
+    rc = scan(h, q, B, part, &qscale, &eps);
+    if (rc) {
+      release();
+      return rc;
+    }
+    CUP(cudaEventRecord(ev[(size_t)it * nev + 2], h->stream));
+    CUP(launch_merge(h->d_state, h->ring64, h->D, h->Dp, q, B, part, qscale, eps, eps_abs1(), h->d_rec, h->shard,
+                     h->stream));
+    CUP(launch_finalize(h->d_rec, 1, B, -1, h->d_state, h->thr, d_outs + (size_t)it * B, h->stream));
+    h->stats[7] += 2;
+    CUP(cudaEventRecord(ev[(size_t)it * nev + 3], h->stream));
+  }
+  CUP(cudaStreamSynchronize(h->stream));
+  double tot = 0, t_app = 0, t_scan = 0, t_merge = 0;
+  for (int it = 0; it < iters; ++it) {
+    float a, b, c;
+    CUP(cudaEventElapsedTime(&a, ev[(size_t)it * nev + 0], ev[(size_t)it * nev + 1]));
+    CUP(cudaEventElapsedTime(&b, ev[(size_t)it * nev + 1], ev[(size_t)it * nev + 2]));
+    CUP(cudaEventElapsedTime(&c, ev[(size_t)it * nev + 2], ev[(size_t)it * nev + 3]));
+    t_app += a;
+    t_scan += b;
+    t_merge += c;
+    tot += a + b + c;
+  }
+  std::vector<OutRec> outs((size_t)iters * B);
+  CUP(cudaMemcpy(outs.data(), d_outs, outs.size() * sizeof(OutRec), cudaMemcpyDeviceToHost));
+  long long need = 0;
+  for (int it = 0; it < iters; ++it) {
+    bool any = false;
+    for (int b = 0; b < B; ++b) any |= (outs[(size_t)it * B + b].flags & FLAG_NEED_ANY) != 0;
+    need += any;
+  }
+  out_ms[0] = tot / iters;
+  out_ms[1] = t_scan / iters;
+  out_ms[2] = t_merge / iters;
+  out_ms[3] = t_app / iters;
+  out_counts[0] = (h->stats[7] - launches0) / iters;
+  out_counts[1] = need;
+  release();
+#undef CUP
+  return MC_OK;
+}
+
+int mc_stats(const mc_cache* h, int64_t* out8) {
+  if (!h || !out8) return fail(MC_ERR_ARG, "NULL argument");
+  for (int i = 0; i < 8; ++i) out8[i] = h->stats[i];
+  return MC_OK;
+}
+
+}  // extern "C"

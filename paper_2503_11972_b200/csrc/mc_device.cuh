@@ -1,0 +1,140 @@
+// Device helpers shared by the scan / rescore kernels.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "mc_internal.cuh"
+
+namespace mc {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ uint4 ld_stream16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Physical ring slot of live-local row i.
+__device__ __forceinline__ long long ring_slot(const RingState& st, long long i) {
+  long long s = st.head + i;
+  return s >= st.cap ? s - st.cap : s;
+}
+
+// Global append position of live-local row i on shard (G, g).
+__device__ __forceinline__ long long global_pos(const RingState& st, long long i, ShardMap sm) {
+  return (st.jhead + i) * (long long)sm.G + sm.g;
+}
+
+// Inverse: live-local row of global position p (p must belong to this shard and be live).
+__device__ __forceinline__ long long local_row(const RingState& st, long long p, ShardMap sm) {
+  return (p - sm.g) / sm.G - st.jhead;
+}
+
+// Knuth TwoSum: s + e == a + b exactly.  Symmetric in (a, b).
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  double z = s - a;
+  e = (a - (s - z)) + (b - z);
+}
+
+// Compensated (Ogita-Rump-Oishi Dot2) float64 dot product of one row with q,
+// one warp, fixed lane->element assignment and a fixed butterfly, so every
+// lane returns the same bits and identical rows always score identically.
+__device__ __forceinline__ double warp_dot64(const double* __restrict__ row, const double* __restrict__ q, int D,
+                                             int lane) {
+  double s = 0.0, c = 0.0;
+  for (int i = lane; i < D; i += 32) {
+    double a = row[i], b = q[i];
+    double p = a * b;
+    double ep = fma(a, b, -p);
+    double t, et;
+    two_sum(s, p, t, et);
+    s = t;
+    c += ep + et;
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    double s2 = __shfl_xor_sync(FULL, s, off);
+    double c2 = __shfl_xor_sync(FULL, c, off);
+    double t, et;
+    two_sum(s, s2, t, et);
+    s = t;
+    c = (c + c2) + et;
+  }
+  // Inf/NaN products poison the compensation term; the plain sum then carries
+  // the same (order-independent) Inf/NaN a naive summation would produce.
+  return isfinite(s) ? s + c : s;
+}
+
+// Composite order of (similarity, position): larger similarity wins; equal
+// similarities go to the larger (newer) position — cache.py:255-256.  NaN
+// ranks above everything (np.argmax returns the first NaN of the reversed
+// view, i.e. the newest NaN).
+__device__ __forceinline__ bool better(double a, long long pa, double b, long long pb) {
+  bool na = isnan(a), nb = isnan(b);
+  if (na || nb) {
+    if (na && nb) return pa > pb;
+    return na;
+  }
+  if (a != b) return a > b;
+  return pa > pb;
+}
+
+// Running best / runner-up tracker over float64 candidates.
+struct Best2 {
+  double s;
+  long long p;
+  double s2;  // best similarity among candidates other than (s, p)
+  int ties;   // candidates with similarity bit-equal to s (>= 1 once set)
+
+  __device__ __forceinline__ void init() {
+    s = -INFINITY;
+    p = -1;
+    s2 = -INFINITY;
+    ties = 0;
+  }
+  __device__ __forceinline__ void add(double v, long long pv) {
+    if (pv < 0) return;
+    if (p < 0 || better(v, pv, s, p)) {
+      if (p >= 0) s2 = fmax(s2, s);
+      ties = (p >= 0 && v == s) ? ties + 1 : 1;
+      s = v;
+      p = pv;
+    } else {
+      s2 = fmax(s2, v);
+      if (v == s) ties++;
+    }
+  }
+  __device__ __forceinline__ void merge(const Best2& o) {
+    if (o.p < 0) return;
+    if (p < 0) {
+      *this = o;
+      return;
+    }
+    if (better(o.s, o.p, s, p)) {
+      int t = (o.s == s) ? o.ties + ties : o.ties;
+      s2 = fmax(fmax(s2, s), o.s2);
+      s = o.s;
+      p = o.p;
+      ties = t;
+    } else {
+      if (o.s == s) ties += o.ties;
+      s2 = fmax(fmax(s2, o.s), o.s2);
+    }
+  }
+  __device__ __forceinline__ void shfl_merge(int off) {
+    Best2 o;
+    o.s = __shfl_xor_sync(FULL, s, off);
+    o.p = __shfl_xor_sync(FULL, p, off);
+    o.s2 = __shfl_xor_sync(FULL, s2, off);
+    o.ties = __shfl_xor_sync(FULL, ties, off);
+    merge(o);
+  }
+};
+
+}  // namespace mc

@@ -1,0 +1,106 @@
+// Internal declarations shared by the modmcache translation units.
+//
+// Data layout in HBM (per handle / per GPU):
+//   ring16  [C][Dp] fp16  — scan copy of every ring slot, D zero-padded to Dp
+//                           (multiple of 64 → 128-byte rows for TMA / UMMA K-blocks)
+//   ring64  [C][Dp] fp64  — master copy, used only to rescore top-K' candidates
+//   state   RingState     — (head slot, live count, local append index of head)
+// Live rows occupy slots head, head+1, ... (mod C), oldest first.  A row's
+// global append position is p = (jhead + live_local) * G + g for shard g of G.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/modmcache.h"
+
+namespace mc {
+
+constexpr int KP = 8;             // candidates kept per scan chunk (top-K')
+constexpr int MAX_PAIRS = 16;     // threshold table capacity
+constexpr double AMBIG = 1e-12;   // ulp-ambiguity band reported in flags
+
+// Internal record flag (not exported): certificate failed, needs exact rescan.
+constexpr uint32_t FLAG_NEED_FALLBACK = 0x10000u;
+// Internal record flag: query is non-finite / extreme; answer by exhaustive float64 scan.
+constexpr uint32_t FLAG_NEED_EXHAUSTIVE = 0x20000u;
+constexpr uint32_t FLAG_NEED_ANY = FLAG_NEED_FALLBACK | FLAG_NEED_EXHAUSTIVE;
+
+struct RingState {
+  long long head;   // physical slot of the oldest live row
+  long long count;  // live rows
+  long long jhead;  // local append index of the oldest live row
+  long long cap;    // ring capacity C (slots)
+};
+
+struct Thresholds {
+  int n;
+  int total_steps;
+  int ks[MAX_PAIRS];
+  double taus[MAX_PAIRS];
+};
+
+// Where a scan pass leaves its per-chunk top-K' lists (approximate scores).
+struct Partials {
+  float* s;          // [B][n_chunks][KP] approximate score (scaled units, see scale)
+  long long* p;      // [B][n_chunks][KP] global position (-1 = empty)
+  float* floor_;     // [B][n_chunks]  K'-th score if rows were dropped, else -inf
+  int n_chunks;
+};
+
+struct ShardMap {
+  int G;  // number of shards
+  int g;  // this shard
+};
+
+// ---- launch wrappers (each .cu owns its kernels) ---------------------------
+cudaError_t launch_append(const double* stage, long long n, long long first_slot, const RingState& new_state,
+                          int D, int Dp, __half* ring16, double* ring64, RingState* d_state,
+                          cudaStream_t s);
+
+// GEMV scan of up to 4 queries (q64 rows q0 .. q0+nb-1, stride Dp).
+cudaError_t launch_gemv_scan(const __half* ring16, const RingState* d_state, int Dp, const double* q64, int nb,
+                             const Partials& part, int part_b0, int grid, ShardMap sm, cudaStream_t s);
+int gemv_grid(int sm_count);
+
+// tcgen05 GEMM scan of B queries (fp16 queries q16 [Bp][Dp], scaled by 1/||q||).
+struct TcPlan;
+cudaError_t launch_tc_prep(const double* q64, int B, int Bp, int D, int Dp, __half* q16, double* qscale,
+                           cudaStream_t s);
+cudaError_t launch_tc_scan(TcPlan* plan, const RingState* d_state, int B, const Partials& part, ShardMap sm,
+                           cudaStream_t s);
+TcPlan* tc_plan_create(__half* ring16, long long C, int Dp, __half* q16, int Bcap, int sm_count, int device,
+                       char* err, int errlen);
+void tc_plan_destroy(TcPlan* p);
+int tc_chunks(const TcPlan* p, int B);
+
+// Merge per-chunk lists -> certified float64 best per query (mc_record).
+// qscale: per-query factor turning partial scores into similarity units (nullptr = 1).
+cudaError_t launch_merge(const RingState* d_state, const double* ring64, int D, int Dp, const double* q64, int B,
+                         const Partials& part, const double* qscale, double eps_rel, double eps_abs1,
+                         mc_record* rec, ShardMap sm, cudaStream_t s);
+
+// Exhaustive exact rescan for the queries whose record needs it.
+cudaError_t launch_exact_rescan(const __half* ring16, const double* ring64, const RingState* d_state, int D,
+                                int Dp, const double* q64, int B, mc_record* rec, mc_record* scratch,
+                                int grid, double eps_rel_gemv, double eps_abs1, ShardMap sm, cudaStream_t s);
+int exact_grid(int sm_count);
+
+// Final decision: merge G shard records per query, apply threshold / k.
+// p0 < 0 means "read jhead from d_state" (single-GPU).
+struct OutRec {
+  long long live;  // live index (0 = oldest), -1 if none
+  double sim;      // best float64 similarity
+  int k;           // select_k result, 0 = none
+  unsigned flags;  // MC_FLAG_*
+};
+cudaError_t launch_finalize(const mc_record* rec, int G, int B, long long p0, const RingState* d_state,
+                            Thresholds thr, OutRec* out, cudaStream_t s);
+
+// Error-bound coefficients of the two scan paths.
+double gemv_eps_rel(int Dp);
+double gemm_eps_rel(int Dp);
+double eps_abs1();
+
+}  // namespace mc

@@ -1,0 +1,57 @@
+"""CPU stand-in for the device ring — TEST INFRASTRUCTURE for host-logic tests only.
+
+It lets the CPU suite exercise SemanticCache's host logic (validation order,
+eviction bookkeeping, result mapping) without a GPU.  It mirrors the ring's
+FIFO semantics with a numpy float64 window and answers lookups with the
+oracle's scan formula.  The product never uses it.
+"""
+import numpy as np
+
+from oracle.retrieval import OracleTable
+from paper_2503_11972_b200 import _native
+
+
+class FakeRing:
+    def __init__(self, capacity, dim, device=0):
+        self.capacity, self.dim = capacity, dim
+        self.rows = []
+        self.pairs = None
+        self.appends = 0
+        self.evictions = 0
+
+    def close(self):
+        pass
+
+    def set_table(self, pairs, total_steps):
+        self.pairs = tuple(pairs)
+
+    def append(self, rows):
+        rows = np.asarray(rows, dtype=np.float64).reshape(-1, self.dim)
+        for r in rows:
+            if len(self.rows) == self.capacity:
+                self.rows.pop(0)
+            self.rows.append(r.copy())
+            self.appends += 1
+
+    def evict_front(self, n):
+        assert 0 <= n <= len(self.rows)
+        del self.rows[:n]
+        self.evictions += n
+
+    def __len__(self):
+        return len(self.rows)
+
+    def retrieve(self, Q):
+        Q = np.asarray(Q, dtype=np.float64)
+        t = OracleTable(self.pairs)
+        m = np.stack(self.rows)
+        out = [], [], [], []
+        for q in Q:
+            sims = m @ q
+            best = float(sims.max())
+            live = int(np.flatnonzero(sims == best)[-1])
+            k = t.select_k(best)
+            flags = 0 if best < t.tau else _native.MC_FLAG_HIT
+            for lst, v in zip(out, (live, best, k or 0, flags)):
+                lst.append(v)
+        return tuple(np.array(x) for x in out)

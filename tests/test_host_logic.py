@@ -1,0 +1,182 @@
+"""Host-side logic of the drop-in SemanticCache (CPU; device ring replaced by a test fake).
+
+Mirrors the reference's own unit tests (pkg/tests/test_cache.py:31-309) for
+everything that is decided on the host: validation order and exception
+types, FIFO / policy / age bookkeeping, snapshot round trips, result mapping.
+"""
+import numpy as np
+import pytest
+
+import paper_2503_11972_b200.cache as cache_mod
+from paper_2503_11972_b200 import (
+    CacheEntry,
+    EmbeddingError,
+    RetrievalResult,
+    SemanticCache,
+    ThresholdTable,
+    cosine,
+    linear_sigma_schedule,
+    noise_reentry_level,
+    normalize,
+    validate_sigma_schedule,
+)
+from tests.fake_ring import FakeRing
+from tests.golden_replay import SCENARIOS, expected, load, replay
+
+
+@pytest.fixture(autouse=True)
+def fake_ring(monkeypatch):
+    monkeypatch.setattr(cache_mod.SemanticCache, "_ring_factory", staticmethod(FakeRing))
+
+
+def unit(rng, d):
+    return normalize(rng.standard_normal(d))
+
+
+def entry(seq, emb, producer="large", t=0.0, eid=None):
+    return CacheEntry(eid or f"e{seq}", emb, producer, seq, t)
+
+
+class TestValidation:
+    def test_constructor_errors(self):
+        with pytest.raises(ValueError):
+            SemanticCache(capacity=0)
+        with pytest.raises(ValueError):
+            SemanticCache(capacity=4, policy="bogus")
+        with pytest.raises(ValueError):
+            SemanticCache(capacity=4, max_age_s=0)
+
+    def test_policy_drop_precedes_validation(self):
+        c = SemanticCache(capacity=4, dim=8, policy="large")
+        # a small-producer entry with a bad shape is silently dropped, not rejected (cache.py:211-212)
+        assert c.insert(CacheEntry("x", np.ones(3), "small", 0, 0.0)) == []
+
+    def test_unknown_producer(self):
+        with pytest.raises(ValueError):
+            SemanticCache(capacity=4, dim=8).insert(entry(0, unit(np.random.default_rng(0), 8), producer="mid"))
+
+    def test_shape_norm_seq(self):
+        rng = np.random.default_rng(1)
+        c = SemanticCache(capacity=4, dim=8)
+        with pytest.raises(EmbeddingError):
+            c.insert(entry(0, unit(rng, 7)))
+        with pytest.raises(EmbeddingError):
+            c.insert(CacheEntry("x", np.full(8, 0.5), "large", 0, 0.0))
+        c.insert(entry(5, unit(rng, 8)))
+        with pytest.raises(ValueError):
+            c.insert(entry(5, unit(rng, 8)))
+
+    def test_query_shape(self):
+        c = SemanticCache(capacity=4, dim=8)
+        with pytest.raises(EmbeddingError):
+            c.retrieve(normalize([1.0, 0.0]), ThresholdTable.default())
+
+    def test_empty_cache_never_touches_device(self):
+        c = SemanticCache(capacity=4, dim=8)
+        assert c.retrieve(unit(np.random.default_rng(2), 8), ThresholdTable.default()) == RetrievalResult(None, None, None)
+        assert c._ring is None
+
+
+class TestBookkeeping:
+    def test_fifo_eviction_mirrors_ring(self):
+        rng = np.random.default_rng(3)
+        c = SemanticCache(capacity=2, dim=8)
+        es = [entry(i, unit(rng, 8), t=float(i), eid=n) for i, n in enumerate("abc")]
+        assert c.insert(es[0]) == [] and c.insert(es[1]) == []
+        assert [e.id for e in c.insert(es[2])] == ["a"]
+        assert [e.id for e in c.entries()] == ["b", "c"]
+        assert len(c.ring) == len(c) == 2
+
+    def test_age_eviction_on_next_insert(self):
+        rng = np.random.default_rng(4)
+        c = SemanticCache(capacity=10, dim=8, max_age_s=4 * 3600.0)
+        c.insert(entry(0, unit(rng, 8), t=0.0, eid="stale"))
+        assert len(c) == 1
+        assert [e.id for e in c.insert(entry(1, unit(rng, 8), t=5 * 3600.0, eid="fresh"))] == ["stale"]
+        assert len(c.ring) == 1
+
+    def test_policy_is_mutable(self):
+        c = SemanticCache(capacity=4, dim=8)
+        c.policy = "disabled"
+        assert not c.admits("large")
+
+    def test_retained_set_is_most_recent_eligible(self):
+        rng = np.random.default_rng(5)
+        c = SemanticCache(capacity=5, dim=8, policy="large")
+        eligible = []
+        for i in range(40):
+            producer = "large" if rng.random() < 0.6 else "small"
+            c.insert(entry(i, unit(rng, 8), producer=producer, t=float(i)))
+            if producer == "large":
+                eligible.append(f"e{i}")
+        assert [e.id for e in c.entries()] == eligible[-5:]
+        assert len(c.ring) == 5
+
+
+def _retrieve(cache, q, table):
+    r = cache.retrieve(q, table)
+    live = None
+    if r.hit:
+        live = [e.seq for e in cache.entries()].index(r.entry.seq)
+    return (r.entry.seq if r.hit else None), live, r.similarity, r.k
+
+
+@pytest.mark.parametrize("name", SCENARIOS)
+def test_host_logic_replays_golden(name):
+    g = load(name)
+    got = replay(g, lambda cap, dim, pol, age: SemanticCache(cap, dim, pol, age), CacheEntry,
+                 lambda pairs, T: ThresholdTable(pairs, T), _retrieve)
+    want = expected(g)
+    for a, b in zip(got, want):
+        assert (a[0], a[1], a[3]) == (b[0], b[1], b[3])
+        assert (a[2] is None) == (b[2] is None)
+        if a[2] is not None:
+            assert abs(a[2] - b[2]) <= 1e-12
+
+
+def test_snapshot_round_trip(tmp_path):
+    rng = np.random.default_rng(10)
+    c = SemanticCache(capacity=20, dim=8)
+    for i in range(12):
+        c.insert(entry(i, unit(rng, 8), producer=("small" if i % 4 else "large"), t=i * 2.5))
+    p1, p2 = tmp_path / "a.jsonl", tmp_path / "b.jsonl"
+    c.export_jsonl(p1)
+    c2 = SemanticCache(capacity=20, dim=8)
+    assert c2.import_jsonl(p1) == 12
+    c2.export_jsonl(p2)
+    assert p1.read_bytes() == p2.read_bytes()
+    bad = tmp_path / "bad.jsonl"
+    bad.write_text('{"id": "a", "seq": 0}\n', encoding="utf-8")
+    with pytest.raises(ValueError, match="bad.jsonl:1"):
+        SemanticCache(capacity=4, dim=8).import_jsonl(bad)
+
+
+class TestPureHelpers:
+    def test_table(self):
+        t = ThresholdTable.default()
+        assert t.step_choices == (5, 10, 15, 20, 25, 30) and t.tau == 0.25
+        for s, k in [(0.305, 30), (0.265, 10), (1.0, 30), (0.25, 5), (0.2499999, None), (-1.0, None)]:
+            assert t.select_k(s) == k
+        for bad in ([(10, 0.3), (5, 0.2)], [(5, 0.3), (10, 0.2)], [], [(5, 1.5)]):
+            with pytest.raises(ValueError):
+                ThresholdTable(bad)
+        with pytest.raises(ValueError):
+            ThresholdTable([(5, 0.2), (50, 0.3)], total_steps=50)
+
+    def test_vectors(self):
+        assert np.allclose(normalize([3.0, 4.0]), [0.6, 0.8])
+        for bad in ([0.0, 0.0], [1.0, np.nan], [np.inf, 0.0]):
+            with pytest.raises(EmbeddingError):
+                normalize(bad)
+        assert cosine(normalize([3.0, 4.0]), normalize([4.0, 3.0])) == pytest.approx(0.96)
+        with pytest.raises(EmbeddingError):
+            cosine(normalize([1.0, 0.0]), normalize([1.0, 0.0, 0.0]))
+
+    def test_schedule(self):
+        s = linear_sigma_schedule(50)
+        validate_sigma_schedule(s)
+        assert noise_reentry_level(0, s) == 1.0 and noise_reentry_level(50, s) == 0.0
+        with pytest.raises(ValueError):
+            noise_reentry_level(51, s)
+        with pytest.raises(ValueError):
+            validate_sigma_schedule(np.array([1.0, 0.2, 0.5, 0.0]))
