@@ -79,6 +79,8 @@ struct mc_cache {
   cudaEvent_t q_ev = nullptr;
   bool q_inflight = false;
 
+  TcPlan* tc = nullptr;  // tensor-core scan plan, created on first batched lookup
+
   Thresholds thr{};
   int path = MC_PATH_AUTO;
   long long stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -187,8 +189,38 @@ int upload_queries(mc_cache* h, const double* queries, int B) {
   return MC_OK;
 }
 
+// Batch size from which the tensor-core scan replaces the GEMV scan: the GEMV
+// kernel reads the ring once per 4 queries, the tcgen05 scan once per batch.
+constexpr int GEMM_MIN_B = 5;
+
+bool use_gemm(const mc_cache* h, int B) {
+  return h->path == MC_PATH_GEMM || (h->path == MC_PATH_AUTO && B >= GEMM_MIN_B);
+}
+
+int ensure_tc(mc_cache* h, int B) {
+  if (h->tc && tc_bcap(h->tc) >= B) return MC_OK;
+  CU(cudaStreamSynchronize(h->stream));
+  tc_plan_destroy(h->tc);
+  h->tc = nullptr;
+  char err[256] = {0};
+  h->tc = tc_plan_create(h->ring16, h->C, h->Dp, std::max(B, 128), h->sm_count, err, sizeof err);
+  if (!h->tc) return fail(MC_ERR_CUDA, "tensor-core scan plan: %s", err);
+  return MC_OK;
+}
+
 // Scan pass only: per-chunk top-K' lists for B queries at q64 (stride Dp).
 int scan(mc_cache* h, const double* q64, int B, Partials& part, const double** qscale, double* eps_rel) {
+  if (use_gemm(h, B)) {
+    int rc = ensure_tc(h, B);
+    if (rc) return rc;
+    part = Partials{h->d_part_s, h->d_part_p, h->d_part_floor, tc_chunks(h->tc, B)};
+    *qscale = tc_qscale(h->tc);
+    *eps_rel = gemm_eps_rel(h->Dp);
+    CU(launch_tc_scan(h->tc, q64, B, h->D, h->d_state, part, h->shard, h->stream));
+    h->stats[6]++;
+    h->stats[7] += 2;
+    return MC_OK;
+  }
   part = Partials{h->d_part_s, h->d_part_p, h->d_part_floor, gemv_grid(h->sm_count)};
   *qscale = nullptr;
   *eps_rel = gemv_eps_rel(h->Dp);
@@ -315,6 +347,7 @@ int mc_destroy(mc_cache* h) {
     DeviceGuard guard(h->dev);
     if (h->stream) cudaStreamSynchronize(h->stream);
     free_batch(h);
+    tc_plan_destroy(h->tc);
     cudaFree(h->ring16);
     cudaFree(h->ring64);
     cudaFree(h->d_state);

@@ -64,16 +64,16 @@ cudaError_t launch_gemv_scan(const __half* ring16, const RingState* d_state, int
                              const Partials& part, int part_b0, int grid, ShardMap sm, cudaStream_t s);
 int gemv_grid(int sm_count);
 
-// tcgen05 GEMM scan of B queries (fp16 queries q16 [Bp][Dp], scaled by 1/||q||).
+// tcgen05 GEMM scan of B queries (scan_tc.cu).  The plan owns the fp16
+// query tile (q / ||q||), the per-query scale ||q|| and both TMA descriptors.
 struct TcPlan;
-cudaError_t launch_tc_prep(const double* q64, int B, int Bp, int D, int Dp, __half* q16, double* qscale,
-                           cudaStream_t s);
-cudaError_t launch_tc_scan(TcPlan* plan, const RingState* d_state, int B, const Partials& part, ShardMap sm,
-                           cudaStream_t s);
-TcPlan* tc_plan_create(__half* ring16, long long C, int Dp, __half* q16, int Bcap, int sm_count, int device,
-                       char* err, int errlen);
+TcPlan* tc_plan_create(__half* ring16, long long C, int Dp, int Bcap, int sm_count, char* err, int errlen);
 void tc_plan_destroy(TcPlan* p);
+int tc_bcap(const TcPlan* p);
 int tc_chunks(const TcPlan* p, int B);
+const double* tc_qscale(const TcPlan* p);
+cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const RingState* d_state,
+                           const Partials& part, ShardMap sm, cudaStream_t s);
 
 // Merge per-chunk lists -> certified float64 best per query (mc_record).
 // qscale: per-query factor turning partial scores into similarity units (nullptr = 1).

@@ -47,9 +47,14 @@ __device__ __forceinline__ float block_max(float v, float* sh) {
   return t;
 }
 
-__device__ Best2 block_best(Best2 b, Best2* sh) {
+// Block-wide merge of per-thread trackers.  `warp_uniform`: every lane of a
+// warp already holds the same tracker (warp-cooperative rescoring), so the
+// lanes must not be merged with each other — that would count each tie twice.
+__device__ Best2 block_best(Best2 b, Best2* sh, bool warp_uniform) {
+  if (!warp_uniform) {
 #pragma unroll
-  for (int off = 16; off; off >>= 1) b.shfl_merge(off);
+    for (int off = 16; off; off >>= 1) b.shfl_merge(off);
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __syncthreads();
   if (lane == 0) sh[warp] = b;
@@ -116,7 +121,7 @@ __global__ void __launch_bounds__(MERGE_THREADS)
     const double v = warp_dot64(ring64 + (size_t)slot * Dp, sq, D, lane);
     best.add(v, p);
   }
-  best = block_best(best, shb);
+  best = block_best(best, shb, true);
 
   const float* pf = part_floor + (size_t)b * n_chunks;
   int fail = 0;
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(EXACT_THREADS)
       }
       if (take) best.add(warp_dot64(ring64 + (size_t)slot * Dp, sq, D, lane), global_pos(st, row, sm));
     }
-    best = block_best(best, shb);
+    best = block_best(best, shb, true);
     if (threadIdx.x == 0) {
       mc_record r;
       r.sim = best.s;
@@ -243,7 +248,7 @@ __global__ void k_exact_reduce(const mc_record* __restrict__ scratch, int nparts
     o.ties = (int)r.flags;
     best.merge(o);
   }
-  best = block_best(best, shb);
+  best = block_best(best, shb, false);
   if (threadIdx.x == 0) {
     mc_record r;
     r.sim = best.s;

@@ -1,0 +1,527 @@
+// K3 — tensor-core scan for batched lookups (tcgen05 + TMEM + TMA, sm_100a).
+//
+// Replaces B sequential `_buf[_lo:_hi] @ q` dgemv calls (cache.py:254) with
+// one dense contraction S = Q · Rᵀ over the fp16 ring:
+//   A = queries  [Bp][Dp] fp16, K-major (q / ||q||, so every row is unit-scale)
+//   B = ring     [C ][Dp] fp16, K-major (the ring rows as stored — no transpose)
+//   D = scores   [128 queries][256 slots] fp32 in TMEM (double-buffered)
+// Queries sit on UMMA M (one 128-row M tile per CTA), ring slots on UMMA N.
+// Scores never reach HBM: the epilogue warps pull each accumulator out of
+// TMEM (tcgen05.ld 32x32b: thread t <-> query row t) and keep a per-query
+// register top-K' plus the largest dropped score (the chunk floor).  The
+// per-CTA lists go to the same Partials the GEMV path writes, so the
+// certified float64 merge (rescore.cu) is shared.
+//
+// Warp roles (192 threads, 1 CTA per SM, persistent):
+//   warp 0    TMA producer  (one lane): A 128x64 + B 256x64 per K block
+//   warp 1    MMA issuer    (one lane): 4 x tcgen05.mma 128x256x16 per K block;
+//             also owns the TMEM allocation (512 columns = 2 accumulators)
+//   warps 2-5 epilogue: TMEM lane quadrant (warp % 4), 32 queries each
+//
+// Schedule: grid = n_m * floor(SMs / n_m).  CTA c serves M tile (c % n_m) and
+// every (grid / n_m)-th live N tile starting at c / n_m — the n_m CTAs that
+// share an N tile run it at the same time, so the ring is read from HBM once
+// and from L2 n_m times.  Live N tiles start at the tile holding `head` and
+// wrap around the ring; slots outside the live window are masked in the
+// epilogue.
+//
+// Algorithmic work per launch: 2 * Bp * n_live * Dp flops; HBM bytes
+// n_live * Dp * 2 + Bp * Dp * 2.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "mc_device.cuh"
+
+namespace mc {
+
+constexpr int TC_BM = 128;      // queries per M tile (UMMA_M)
+constexpr int TC_BN = 256;      // ring slots per N tile (UMMA_N)
+constexpr int TC_BK = 64;       // fp16 per K block = one 128-byte swizzle row
+constexpr int TC_UK = 16;       // UMMA_K for kind::f16
+constexpr int TC_STAGES = 4;
+constexpr int TC_THREADS = 192;
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
+constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;  // 32 KB
+constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int TC_TMEM_COLS = 2 * TC_BN;  // two fp32 accumulators of 256 columns
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, 128-byte-swizzled operand tile: 8-row core groups 1024 B apart.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);      // start address
+  d |= (uint64_t)1 << 16;                      // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;            // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                      // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                      // SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: fp16 x fp16 -> fp32, both K-major, M x N.
+__host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N) {
+  return (1u << 4)                      // D format f32
+         | (0u << 7) | (0u << 10)       // A, B format f16
+         | ((uint32_t)(N >> 3) << 17)   // N
+         | ((uint32_t)(M >> 4) << 24);  // M
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------- schedule
+struct TileWindow {
+  int first;    // physical N tile holding the oldest live slot
+  int n_live;   // N tiles overlapping the live window
+  int n_total;  // N tiles covering the ring
+};
+
+__device__ __forceinline__ TileWindow tile_window(const RingState& st) {
+  TileWindow w;
+  w.n_total = (int)((st.cap + TC_BN - 1) / TC_BN);
+  if (st.count <= 0) {
+    w.first = 0;
+    w.n_live = 0;
+  } else if (st.count >= st.cap) {
+    w.first = 0;
+    w.n_live = w.n_total;
+  } else {
+    w.first = (int)(st.head / TC_BN);
+    const long long end = st.head + st.count;  // one past the newest slot, unwrapped
+    long long nl;
+    if (end <= st.cap)
+      nl = (end - 1) / TC_BN - w.first + 1;
+    else  // tiles first .. n_total-1, then 0 .. the tile of the newest wrapped slot
+      nl = (w.n_total - w.first) + (end - st.cap - 1) / TC_BN + 1;
+    w.n_live = nl < w.n_total ? (int)nl : w.n_total;
+  }
+  return w;
+}
+
+// Sorted (descending) register top-K' with newest-first order among equal scores.
+struct TopK {
+  float s[KP];
+  long long p[KP];
+  float drop;  // largest score not kept (chunk floor); -inf if nothing dropped
+
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int i = 0; i < KP; ++i) {
+      s[i] = -INFINITY;
+      p[i] = -1;
+    }
+    drop = -INFINITY;
+  }
+  __device__ __forceinline__ void push(float v, long long pv) {
+    if (p[KP - 1] >= 0) drop = fmaxf(drop, s[KP - 1]);
+    s[KP - 1] = v;
+    p[KP - 1] = pv;
+#pragma unroll
+    for (int i = KP - 1; i > 0; --i) {
+      const bool up = s[i] > s[i - 1] || (s[i] == s[i - 1] && p[i] > p[i - 1]);
+      if (up) {
+        const float ts = s[i];
+        s[i] = s[i - 1];
+        s[i - 1] = ts;
+        const long long tp = p[i];
+        p[i] = p[i - 1];
+        p[i - 1] = tp;
+      }
+    }
+  }
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_tc_scan(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap ring_map,
+              const RingState* __restrict__ d_state, int n_m, int B, int n_kb, float* __restrict__ part_s,
+              long long* __restrict__ part_p, float* __restrict__ part_floor, int n_chunks, ShardMap sm) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + TC_STAGES * TC_A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + TC_STAGES * TC_B_BYTES);
+  uint64_t* full = bars;                   // [S]  TMA -> MMA
+  uint64_t* empty = bars + TC_STAGES;      // [S]  MMA -> TMA
+  uint64_t* tfull = bars + 2 * TC_STAGES;  // [2]  MMA -> epilogue
+  uint64_t* tempty = tfull + 2;            // [2]  epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const RingState st = *d_state;
+  const TileWindow win = tile_window(st);
+  const int m_tile = blockIdx.x % n_m;
+  const int group = blockIdx.x / n_m;
+  const int n_groups = gridDim.x / n_m;
+  const int n_units = win.n_live > group ? (win.n_live - group + n_groups - 1) / n_groups : 0;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&q_map)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map)) : "memory");
+    for (int i = 0; i < TC_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TC_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = 0; u < n_units; ++u) {
+        const int t = (win.first + group + u * n_groups) % win.n_total;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], TC_A_BYTES + TC_B_BYTES);
+          tma_load_2d(smA + stage * TC_A_BYTES, &q_map, &full[stage], kb * TC_BK, m_tile * TC_BM);
+          tma_load_2d(smB + stage * TC_B_BYTES, &ring_map, &full[stage], kb * TC_BK, t * TC_BN);
+          if (++stage == TC_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = umma_idesc_f16(TC_BM, TC_BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = 0; u < n_units; ++u) {
+      const int acc = u & 1;
+      const uint32_t acc_phase = (u >> 1) & 1;
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TC_BN);
+      for (int kb = 0; kb < n_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(smA + stage * TC_A_BYTES);
+          const uint32_t b0 = smem_u32(smB + stage * TC_B_BYTES);
+#pragma unroll
+          for (int k = 0; k < TC_BK / TC_UK; ++k) {
+            umma_f16(d_tmem, umma_desc_sw128(a0 + k * TC_UK * 2), umma_desc_sw128(b0 + k * TC_UK * 2), idesc,
+                     (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+        }
+        __syncwarp();
+        if (++stage == TC_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int quad = warp & 3;  // TMEM lanes 32*quad .. 32*quad+31
+    const int row = quad * 32 + lane;
+    const int b = m_tile * TC_BM + row;
+    TopK top;
+    top.init();
+    for (int u = 0; u < n_units; ++u) {
+      const int acc = u & 1;
+      const uint32_t acc_phase = (u >> 1) & 1;
+      const int t = (win.first + group + u * n_groups) % win.n_total;
+      const long long slot0 = (long long)t * TC_BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      // live-local row of slot0 and whether every slot of the tile is live
+      long long l0 = slot0 - st.head;
+      if (l0 < 0) l0 += st.cap;
+      const bool all_live = (slot0 + TC_BN <= st.cap) && (l0 + TC_BN <= st.count);
+#pragma unroll 1
+      for (int c = 0; c < TC_BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN + c * 32), v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = c * 32 + j;
+          bool live = all_live;
+          long long l = l0 + n;
+          if (!all_live) {
+            const long long slot = slot0 + n;
+            if (slot >= st.cap) {
+              live = false;
+            } else {
+              if (l >= st.cap) l -= st.cap;
+              live = l < st.count;
+            }
+          }
+          if (live) {
+            if (v[j] > top.s[KP - 1]) {
+              if (l >= st.cap) l -= st.cap;
+              top.push(v[j], (st.jhead + l) * (long long)sm.G + sm.g);
+            } else {
+              top.drop = fmaxf(top.drop, v[j]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+    if (b < B) {
+      const size_t o = (size_t)b * n_chunks + group;
+#pragma unroll
+      for (int i = 0; i < KP; ++i) {
+        part_s[o * KP + i] = top.s[i];
+        part_p[o * KP + i] = top.p[i];
+      }
+      part_floor[o] = top.drop;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TC_TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// q16[b] = fp16(q[b] / ||q[b]||), zero rows for b >= B and zero padding columns;
+// qscale[b] = ||q[b]|| turns a scan score back into query units.
+__global__ void k_tc_prep(const double* __restrict__ q64, int B, int D, int Dp, __half* __restrict__ q16,
+                          double* __restrict__ qscale) {
+  __shared__ double red[32];
+  const int b = blockIdx.x;
+  double a = 0.0;
+  if (b < B)
+    for (int i = threadIdx.x; i < D; i += blockDim.x) {
+      const double x = q64[(size_t)b * Dp + i];
+      a += x * x;
+    }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) a += __shfl_xor_sync(FULL, a, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    red[0] = sqrt(t);
+  }
+  __syncthreads();
+  const double n = red[0];
+  const bool ok = b < B && n > 0.0 && isfinite(n);
+  const double inv = ok ? 1.0 / n : 0.0;
+  for (int i = threadIdx.x; i < Dp; i += blockDim.x)
+    q16[(size_t)b * Dp + i] = __double2half(ok && i < D ? q64[(size_t)b * Dp + i] * inv : 0.0);
+  if (threadIdx.x == 0 && b < B) qscale[b] = ok ? n : 0.0;
+}
+
+// ---------------------------------------------------------------- host side
+struct TcPlan {
+  __half* ring16 = nullptr;
+  long long C = 0;
+  int Dp = 0;
+  int Bcap = 0;  // multiple of TC_BM
+  int sm_count = 0;
+  __half* q16 = nullptr;
+  double* qscale = nullptr;
+  CUtensorMap q_map;
+  CUtensorMap ring_map;
+};
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static bool encode_2d(CUtensorMap* m, void* base, long long rows, int cols, int box_rows, char* err, int errlen) {
+  auto enc = get_encode();
+  if (!enc) {
+    snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable from the driver");
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(err, errlen, "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%d", (int)r, rows, cols);
+    return false;
+  }
+  return true;
+}
+
+TcPlan* tc_plan_create(__half* ring16, long long C, int Dp, int Bcap, int sm_count, char* err, int errlen) {
+  if (Dp % TC_BK != 0) {
+    snprintf(err, errlen, "tensor-core scan needs Dp %% %d == 0 (Dp=%d)", TC_BK, Dp);
+    return nullptr;
+  }
+  TcPlan* p = new TcPlan();
+  p->ring16 = ring16;
+  p->C = C;
+  p->Dp = Dp;
+  p->Bcap = (Bcap + TC_BM - 1) / TC_BM * TC_BM;
+  p->sm_count = sm_count;
+  if (cudaMalloc(&p->q16, (size_t)p->Bcap * Dp * sizeof(__half)) != cudaSuccess ||
+      cudaMalloc(&p->qscale, (size_t)p->Bcap * sizeof(double)) != cudaSuccess) {
+    snprintf(err, errlen, "cudaMalloc failed for the query tile");
+    tc_plan_destroy(p);
+    return nullptr;
+  }
+  if (!encode_2d(&p->q_map, p->q16, p->Bcap, Dp, TC_BM, err, errlen) ||
+      !encode_2d(&p->ring_map, ring16, C, Dp, TC_BN, err, errlen)) {
+    tc_plan_destroy(p);
+    return nullptr;
+  }
+  if (cudaFuncSetAttribute(k_tc_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) != cudaSuccess) {
+    snprintf(err, errlen, "cannot raise dynamic shared memory to %d bytes", TC_SMEM);
+    tc_plan_destroy(p);
+    return nullptr;
+  }
+  return p;
+}
+
+void tc_plan_destroy(TcPlan* p) {
+  if (!p) return;
+  cudaFree(p->q16);
+  cudaFree(p->qscale);
+  delete p;
+}
+
+int tc_bcap(const TcPlan* p) { return p->Bcap; }
+
+static int tc_nm(int B) { return (B + TC_BM - 1) / TC_BM; }
+
+int tc_chunks(const TcPlan* p, int B) {
+  const int nm = tc_nm(B);
+  return p->sm_count / nm;
+}
+
+const double* tc_qscale(const TcPlan* p) { return p->qscale; }
+
+cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const RingState* d_state,
+                           const Partials& part, ShardMap sm, cudaStream_t s) {
+  if (B < 1 || B > p->Bcap) return cudaErrorInvalidValue;
+  const int nm = tc_nm(B);
+  const int groups = p->sm_count / nm;
+  if (groups < 1 || groups > part.n_chunks) return cudaErrorInvalidValue;
+  k_tc_prep<<<nm * TC_BM, 128, 0, s>>>(q64, B, D, p->Dp, p->q16, p->qscale);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_tc_scan<<<nm * groups, TC_THREADS, TC_SMEM, s>>>(p->q_map, p->ring_map, d_state, nm, B, p->Dp / TC_BK, part.s,
+                                                     part.p, part.floor_, groups, sm);
+  return cudaGetLastError();
+}
+
+// Error bound of a tensor-core score relative to ||q||_2: entries and the
+// normalised query are both fp16-rounded (|de_i| <= u|e_i|, |dq_i| <= u|q_i|,
+// so sum |e_i q_i| (2u + u^2) <= (2u + u^2)(1 + 1e-6)), plus fp16 subnormal
+// rounding of q/||q|| (2^-25 per component, <= 2^-25 sqrt(Dp) in total), plus
+// fp32 accumulation inside the tensor core, bounded as Dp + 16 sequential
+// truncating adds (2 u32 each) of terms whose absolute sum is <= 1 + 1e-6.
+double gemm_eps_rel(int Dp) {
+  const double u16 = ldexp(1.0, -11), u32 = ldexp(1.0, -24);
+  const double rounding = (2 * u16 + u16 * u16) * (1.0 + 1e-6);
+  const double sub = ldexp(1.0, -25) * sqrt((double)Dp);
+  const double accum = (Dp + 16) * 2.0 * u32 * (1.0 + rounding);
+  return 1.25 * (rounding + sub + accum);
+}
+
+}  // namespace mc
