@@ -43,7 +43,8 @@ extern "C" {
 /* Scan-path selection for mc_set_path (default MC_PATH_AUTO). */
 #define MC_PATH_AUTO 0
 #define MC_PATH_GEMV 1 /* CUDA-core fp16 GEMV scan, register top-K'             */
-#define MC_PATH_GEMM 2 /* tcgen05/TMEM/TMA fp16 GEMM scan, fused top-K' epilogue */
+#define MC_PATH_GEMM 2 /* tcgen05/TMEM/TMA fp16 GEMM scan (CTA pairs), fused top-K' epilogue */
+#define MC_PATH_GEMM_1SM 3 /* same scan on single CTAs (cta_group::1), kept for cross-checks */
 
 typedef struct mc_cache mc_cache;
 

@@ -194,7 +194,7 @@ int upload_queries(mc_cache* h, const double* queries, int B) {
 constexpr int GEMM_MIN_B = 5;
 
 bool use_gemm(const mc_cache* h, int B) {
-  return h->path == MC_PATH_GEMM || (h->path == MC_PATH_AUTO && B >= GEMM_MIN_B);
+  return h->path == MC_PATH_GEMM || h->path == MC_PATH_GEMM_1SM || (h->path == MC_PATH_AUTO && B >= GEMM_MIN_B);
 }
 
 int ensure_tc(mc_cache* h, int B) {
@@ -213,6 +213,7 @@ int scan(mc_cache* h, const double* q64, int B, Partials& part, const double** q
   if (use_gemm(h, B)) {
     int rc = ensure_tc(h, B);
     if (rc) return rc;
+    tc_set_pair(h->tc, h->path != MC_PATH_GEMM_1SM);
     part = Partials{h->d_part_s, h->d_part_p, h->d_part_floor, tc_chunks(h->tc, B)};
     *qscale = tc_qscale(h->tc);
     *eps_rel = gemm_eps_rel(h->Dp);
@@ -389,7 +390,7 @@ int mc_configure_shard(mc_cache* h, int32_t n_shards, int32_t shard_id) {
 
 int mc_set_path(mc_cache* h, int32_t path) {
   if (!h) return fail(MC_ERR_ARG, "NULL handle");
-  if (path < MC_PATH_AUTO || path > MC_PATH_GEMM) return fail(MC_ERR_ARG, "unknown path %d", path);
+  if (path < MC_PATH_AUTO || path > MC_PATH_GEMM_1SM) return fail(MC_ERR_ARG, "unknown path %d", path);
   std::lock_guard<std::mutex> lk(h->mu);
   h->path = path;
   return MC_OK;

@@ -70,6 +70,7 @@ struct TcPlan;
 TcPlan* tc_plan_create(__half* ring16, long long C, int Dp, int Bcap, int sm_count, char* err, int errlen);
 void tc_plan_destroy(TcPlan* p);
 int tc_bcap(const TcPlan* p);
+void tc_set_pair(TcPlan* p, bool pair);  // CTA-pair kernel (default) or single-CTA kernel
 int tc_chunks(const TcPlan* p, int B);
 const double* tc_qscale(const TcPlan* p);
 cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const RingState* d_state,

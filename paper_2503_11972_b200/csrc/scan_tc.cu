@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "mc_device.cuh"
@@ -79,6 +80,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
   } while (!done);
+}
+
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void mbar_wait2(uint64_t* bar, uint32_t parity, bool spin) {
+  if (spin)
+    mbar_spin(bar, parity);
+  else
+    mbar_wait(bar, parity);
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -170,35 +192,69 @@ __device__ __forceinline__ TileWindow tile_window(const RingState& st) {
   return w;
 }
 
-// Sorted (descending) register top-K' with newest-first order among equal scores.
+// Register top-K' of one query over the slots a CTA scans: unsorted, with
+// the smallest kept score `mn`, the running maximum `runmax`, and the largest
+// score not kept (`drop`, the chunk floor).  Admission needs v > mn and
+// v > runmax - margin: with margin > 2 delta (delta = the scan's error bound
+// in these units) nothing dropped can reach the certified best, so lists stay
+// short and the merge's certificate holds; the merge re-checks it anyway.
+// Slots stay 32-bit physical ring indices until the list is written out.
 struct TopK {
   float s[KP];
-  long long p[KP];
-  float drop;  // largest score not kept (chunk floor); -inf if nothing dropped
+  int slot[KP];
+  float mn;
+  float runmax;
+  float drop;
 
   __device__ __forceinline__ void init() {
 #pragma unroll
     for (int i = 0; i < KP; ++i) {
       s[i] = -INFINITY;
-      p[i] = -1;
+      slot[i] = -1;
     }
+    mn = -INFINITY;
+    runmax = -INFINITY;
     drop = -INFINITY;
   }
-  __device__ __forceinline__ void push(float v, long long pv) {
-    if (p[KP - 1] >= 0) drop = fmaxf(drop, s[KP - 1]);
-    s[KP - 1] = v;
-    p[KP - 1] = pv;
+  // Precondition: v > mn.  Replaces one entry holding the minimum.
+  __device__ __forceinline__ void push(float v, int sl) {
+    drop = fmaxf(drop, mn);  // the evicted score (-inf while the list is filling)
+    bool done = false;
 #pragma unroll
-    for (int i = KP - 1; i > 0; --i) {
-      const bool up = s[i] > s[i - 1] || (s[i] == s[i - 1] && p[i] > p[i - 1]);
-      if (up) {
-        const float ts = s[i];
-        s[i] = s[i - 1];
-        s[i - 1] = ts;
-        const long long tp = p[i];
-        p[i] = p[i - 1];
-        p[i - 1] = tp;
+    for (int i = 0; i < KP; ++i) {
+      const bool here = !done && s[i] == mn;
+      s[i] = here ? v : s[i];
+      slot[i] = here ? sl : slot[i];
+      done |= here;
+    }
+    float m = s[0];
+#pragma unroll
+    for (int i = 1; i < KP; ++i) m = fminf(m, s[i]);
+    mn = m;
+  }
+  // 32 consecutive scores (non-live slots already set to -inf).
+  __device__ __forceinline__ void scan32(const float (&v)[32], int slot0, float margin) {
+    float m0 = fmaxf(v[0], v[1]), m1 = fmaxf(v[2], v[3]), m2 = fmaxf(v[4], v[5]), m3 = fmaxf(v[6], v[7]);
+#pragma unroll
+    for (int j = 8; j < 32; j += 8) {
+      m0 = fmaxf(m0, fmaxf(v[j + 0], v[j + 1]));
+      m1 = fmaxf(m1, fmaxf(v[j + 2], v[j + 3]));
+      m2 = fmaxf(m2, fmaxf(v[j + 4], v[j + 5]));
+      m3 = fmaxf(m3, fmaxf(v[j + 6], v[j + 7]));
+    }
+    const float cmax = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+    runmax = fmaxf(runmax, cmax);
+    const float thr = fmaxf(mn, runmax - margin);
+    if (cmax > thr) {  // a new or near maximum in this chunk
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (v[j] > fmaxf(mn, runmax - margin))
+          push(v[j], slot0 + j);
+        else
+          drop = fmaxf(drop, v[j]);
       }
+    } else {
+      drop = fmaxf(drop, cmax);
     }
   }
 };
@@ -206,7 +262,8 @@ struct TopK {
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tc_scan(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap ring_map,
               const RingState* __restrict__ d_state, int n_m, int B, int n_kb, float* __restrict__ part_s,
-              long long* __restrict__ part_p, float* __restrict__ part_floor, int n_chunks, ShardMap sm) {
+              long long* __restrict__ part_p, float* __restrict__ part_floor, int n_chunks, float margin,
+              ShardMap sm) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -317,37 +374,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const long long slot0 = (long long)t * TC_BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      // live-local row of slot0 and whether every slot of the tile is live
-      long long l0 = slot0 - st.head;
+      long long l0 = slot0 - st.head;  // live-local row of the tile's first slot
       if (l0 < 0) l0 += st.cap;
       const bool all_live = (slot0 + TC_BN <= st.cap) && (l0 + TC_BN <= st.count);
 #pragma unroll 1
       for (int c = 0; c < TC_BN / 32; ++c) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN + c * 32), v);
+        if (!all_live) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = c * 32 + j;
-          bool live = all_live;
-          long long l = l0 + n;
-          if (!all_live) {
-            const long long slot = slot0 + n;
-            if (slot >= st.cap) {
-              live = false;
-            } else {
-              if (l >= st.cap) l -= st.cap;
-              live = l < st.count;
-            }
-          }
-          if (live) {
-            if (v[j] > top.s[KP - 1]) {
-              if (l >= st.cap) l -= st.cap;
-              top.push(v[j], (st.jhead + l) * (long long)sm.G + sm.g);
-            } else {
-              top.drop = fmaxf(top.drop, v[j]);
-            }
+          for (int j = 0; j < 32; ++j) {
+            const long long slot = slot0 + c * 32 + j;
+            long long l = l0 + c * 32 + j;
+            if (l >= st.cap) l -= st.cap;
+            if (slot >= st.cap || l >= st.count) v[j] = -INFINITY;
           }
         }
+        top.scan32(v, (int)(slot0 + c * 32), margin);
       }
       tc_fence_before();
       __syncwarp();
@@ -357,8 +400,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const size_t o = (size_t)b * n_chunks + group;
 #pragma unroll
       for (int i = 0; i < KP; ++i) {
+        long long pos = -1;
+        if (top.slot[i] >= 0) {
+          long long l = (long long)top.slot[i] - st.head;
+          if (l < 0) l += st.cap;
+          pos = (st.jhead + l) * (long long)sm.G + sm.g;
+        }
         part_s[o * KP + i] = top.s[i];
-        part_p[o * KP + i] = top.p[i];
+        part_p[o * KP + i] = pos;
       }
       part_floor[o] = top.drop;
     }
@@ -369,6 +418,248 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_after();
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TC_TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- CTA-pair variant
+// cta_group::2: a cluster of two CTAs on one TPC computes a 256-query x
+// 256-slot tile per MMA.  CTA r loads queries [256 m + 128 r, +128) and ring
+// slots [256 t + 128 r, +128) into its own shared memory; the leader (r = 0)
+// issues tcgen05.mma.cta_group::2, which reads the B halves of both CTAs, and
+// each CTA's TMEM receives the scores of its own 128 queries against all 256
+// slots.  Per SM that is 32 KB of operands per K block instead of 48 KB, so a
+// 6-stage ring fits and the tensor pipe is no longer starved.
+constexpr int TP_STAGES = 6;
+constexpr int TP_A_BYTES = 128 * TC_BK * 2;  // 16 KB: this CTA's 128 queries
+constexpr int TP_B_BYTES = 128 * TC_BK * 2;  // 16 KB: this CTA's half of the slot tile
+constexpr int TP_SMEM = TP_STAGES * (TP_A_BYTES + TP_B_BYTES) + 1024 + 256;
+constexpr uint32_t PEER_BIT_MASK = 0xFEFFFFFFu;  // shared::cluster address -> leader CTA
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_BIT_MASK), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// Arrive on the barrier at the same offset in both CTAs once the leader's MMAs retire.
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    k_tc_scan_pair(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap ring_map,
+                   const RingState* __restrict__ d_state, int n_mp, int B, int n_kb, float* __restrict__ part_s,
+                   long long* __restrict__ part_p, float* __restrict__ part_floor, int n_chunks, float margin,
+                   ShardMap sm, int dbg) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + TP_STAGES * TP_A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + TP_STAGES * TP_B_BYTES);
+  uint64_t* full = bars;                   // [S]  leader only: TMA bytes of both CTAs
+  uint64_t* empty = bars + TP_STAGES;      // [S]  MMA commit, multicast to both CTAs
+  uint64_t* tfull = bars + 2 * TP_STAGES;  // [2]  MMA commit, multicast to both CTAs
+  uint64_t* tempty = tfull + 2;            // [2]  leader only: 4 epilogue warps x 2 CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int cid = blockIdx.x >> 1;
+  const int n_clusters = gridDim.x >> 1;
+  const RingState st = *d_state;
+  const TileWindow win = tile_window(st);
+  const int m_pair = cid % n_mp;
+  const int group = cid / n_mp;
+  const int n_groups = n_clusters / n_mp;
+  const int n_units = win.n_live > group ? (win.n_live - group + n_groups - 1) / n_groups : 0;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&q_map)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map)) : "memory");
+    for (int i = 0; i < TP_STAGES; ++i) {
+      mbar_init(&full[i], 2);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TC_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      const uint32_t leader_full0 = mapa_shared(smem_u32(&full[0]), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = 0; u < n_units; ++u) {
+        const int t = (win.first + group + u * n_groups) % win.n_total;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait2(&empty[stage], phase ^ 1, dbg & 16);
+          if (rank == 0)
+            mbar_expect_tx(&full[stage], (dbg & 1) ? 0 : 2 * (TP_A_BYTES + TP_B_BYTES));
+          else
+            mbar_arrive_remote(leader_full0 + stage * 8);
+          if (!(dbg & 1)) {
+            tma_load_2d_pair(smA + stage * TP_A_BYTES, &q_map, &full[stage], kb * TC_BK, m_pair * 256 + rank * 128);
+            tma_load_2d_pair(smB + stage * TP_B_BYTES, &ring_map, &full[stage], kb * TC_BK,
+                             ((dbg & 8) ? (t & 7) : t) * TC_BN + rank * 128);
+          }
+          if (++stage == TP_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (rank == 0) {
+      constexpr uint32_t idesc = umma_idesc_f16(256, TC_BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = 0; u < n_units; ++u) {
+        const int acc = u & 1;
+        const uint32_t acc_phase = (u >> 1) & 1;
+        mbar_wait2(&tempty[acc], acc_phase ^ 1, dbg & 16);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TC_BN);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait2(&full[stage], phase, dbg & 16);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(smA + stage * TP_A_BYTES);
+            const uint32_t b0 = smem_u32(smB + stage * TP_B_BYTES);
+#pragma unroll
+            for (int k = 0; k < TC_BK / TC_UK; ++k)
+              if (!(dbg & 2)) umma_f16_pair(d_tmem, umma_desc_sw128(a0 + k * TC_UK * 2), umma_desc_sw128(b0 + k * TC_UK * 2), idesc,
+                            (kb | k) != 0);
+            if (dbg & 32) {  // bisection only (valid with dbg & 2): plain arrives instead of the commit
+              mbar_arrive(&empty[stage]);
+              mbar_arrive_remote(mapa_shared(smem_u32(&empty[stage]), 1));
+            } else {
+              umma_commit_pair(&empty[stage]);
+            }
+          }
+          __syncwarp();
+          if (++stage == TP_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) umma_commit_pair(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const int b = m_pair * 256 + (int)rank * 128 + row;
+    const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    TopK top;
+    top.init();
+    for (int u = 0; u < n_units; ++u) {
+      const int acc = u & 1;
+      const uint32_t acc_phase = (u >> 1) & 1;
+      const int t = (win.first + group + u * n_groups) % win.n_total;
+      const long long slot0 = (long long)t * TC_BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      long long l0 = slot0 - st.head;
+      if (l0 < 0) l0 += st.cap;
+      const bool all_live = (slot0 + TC_BN <= st.cap) && (l0 + TC_BN <= st.count);
+#pragma unroll 1
+      for (int c = 0; c < TC_BN / 32; ++c) {
+        float v[32];
+        if (dbg & 4) break;
+        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN + c * 32), v);
+        if (!all_live) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const long long slot = slot0 + c * 32 + j;
+            long long l = l0 + c * 32 + j;
+            if (l >= st.cap) l -= st.cap;
+            if (slot >= st.cap || l >= st.count) v[j] = -INFINITY;
+          }
+        }
+        top.scan32(v, (int)(slot0 + c * 32), margin);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(leader_tempty0 + acc * 8);
+    }
+    if (b < B) {
+      const size_t o = (size_t)b * n_chunks + group;
+#pragma unroll
+      for (int i = 0; i < KP; ++i) {
+        long long pos = -1;
+        if (top.slot[i] >= 0) {
+          long long l = (long long)top.slot[i] - st.head;
+          if (l < 0) l += st.cap;
+          pos = (st.jhead + l) * (long long)sm.G + sm.g;
+        }
+        part_s[o * KP + i] = top.s[i];
+        part_p[o * KP + i] = pos;
+      }
+      part_floor[o] = top.drop;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TC_TMEM_COLS)
                  : "memory");
   }
 }
@@ -413,7 +704,10 @@ struct TcPlan {
   __half* q16 = nullptr;
   double* qscale = nullptr;
   CUtensorMap q_map;
-  CUtensorMap ring_map;
+  CUtensorMap ring_map;       // 256-slot boxes (single-CTA kernel)
+  CUtensorMap ring_map_half;  // 128-slot boxes (CTA-pair kernel)
+  bool pair = true;
+  int dbg = 0;  // MC_TC_DEBUG bisection switches: 1 no TMA, 2 no MMA, 4 no epilogue (timing only)
 };
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -457,8 +751,9 @@ TcPlan* tc_plan_create(__half* ring16, long long C, int Dp, int Bcap, int sm_cou
   p->ring16 = ring16;
   p->C = C;
   p->Dp = Dp;
-  p->Bcap = (Bcap + TC_BM - 1) / TC_BM * TC_BM;
+  p->Bcap = (Bcap + 255) / 256 * 256;
   p->sm_count = sm_count;
+  if (const char* e = getenv("MC_TC_DEBUG")) p->dbg = atoi(e);
   if (cudaMalloc(&p->q16, (size_t)p->Bcap * Dp * sizeof(__half)) != cudaSuccess ||
       cudaMalloc(&p->qscale, (size_t)p->Bcap * sizeof(double)) != cudaSuccess) {
     snprintf(err, errlen, "cudaMalloc failed for the query tile");
@@ -466,11 +761,13 @@ TcPlan* tc_plan_create(__half* ring16, long long C, int Dp, int Bcap, int sm_cou
     return nullptr;
   }
   if (!encode_2d(&p->q_map, p->q16, p->Bcap, Dp, TC_BM, err, errlen) ||
-      !encode_2d(&p->ring_map, ring16, C, Dp, TC_BN, err, errlen)) {
+      !encode_2d(&p->ring_map, ring16, C, Dp, TC_BN, err, errlen) ||
+      !encode_2d(&p->ring_map_half, ring16, C, Dp, 128, err, errlen)) {
     tc_plan_destroy(p);
     return nullptr;
   }
-  if (cudaFuncSetAttribute(k_tc_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) != cudaSuccess) {
+  if (cudaFuncSetAttribute(k_tc_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tc_scan_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, TP_SMEM) != cudaSuccess) {
     snprintf(err, errlen, "cannot raise dynamic shared memory to %d bytes", TC_SMEM);
     tc_plan_destroy(p);
     return nullptr;
@@ -487,26 +784,45 @@ void tc_plan_destroy(TcPlan* p) {
 
 int tc_bcap(const TcPlan* p) { return p->Bcap; }
 
-static int tc_nm(int B) { return (B + TC_BM - 1) / TC_BM; }
+void tc_set_pair(TcPlan* p, bool pair) { p->pair = pair; }
+
+// M tiles (single CTA, 128 queries) or M pairs (CTA pair, 256 queries) for B queries.
+static int tc_nm(const TcPlan* p, int B) { return p->pair ? (B + 255) / 256 : (B + TC_BM - 1) / TC_BM; }
 
 int tc_chunks(const TcPlan* p, int B) {
-  const int nm = tc_nm(B);
-  return p->sm_count / nm;
+  const int units = p->pair ? p->sm_count / 2 : p->sm_count;  // clusters or CTAs
+  return units / tc_nm(p, B);
 }
 
 const double* tc_qscale(const TcPlan* p) { return p->qscale; }
 
+double gemm_eps_rel(int Dp);
+
+// Admission margin in normalised score units: > 2 delta / ||q|| for every
+// query (delta / ||q|| <= eps_rel + eps_abs1 * ||q||_1 / ||q||_2 and
+// ||q||_1 <= sqrt(D) ||q||_2), plus slack for the fp32 subtraction.
+static float tc_margin(int Dp) {
+  return (float)(2.0 * (gemm_eps_rel(Dp) + eps_abs1() * sqrt((double)Dp)) * 1.01 + 1e-6);
+}
+
 cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const RingState* d_state,
                            const Partials& part, ShardMap sm, cudaStream_t s) {
   if (B < 1 || B > p->Bcap) return cudaErrorInvalidValue;
-  const int nm = tc_nm(B);
-  const int groups = p->sm_count / nm;
+  const int nm = tc_nm(p, B);
+  const int groups = tc_chunks(p, B);
   if (groups < 1 || groups > part.n_chunks) return cudaErrorInvalidValue;
-  k_tc_prep<<<nm * TC_BM, 128, 0, s>>>(q64, B, D, p->Dp, p->q16, p->qscale);
+  const int rows = nm * (p->pair ? 256 : TC_BM);
+  k_tc_prep<<<rows, 128, 0, s>>>(q64, B, D, p->Dp, p->q16, p->qscale);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_tc_scan<<<nm * groups, TC_THREADS, TC_SMEM, s>>>(p->q_map, p->ring_map, d_state, nm, B, p->Dp / TC_BK, part.s,
-                                                     part.p, part.floor_, groups, sm);
+  const float margin = tc_margin(p->Dp);
+  if (p->pair)
+    k_tc_scan_pair<<<2 * nm * groups, TC_THREADS, TP_SMEM, s>>>(p->q_map, p->ring_map_half, d_state, nm, B,
+                                                                p->Dp / TC_BK, part.s, part.p, part.floor_, groups,
+                                                                margin, sm, p->dbg);
+  else
+    k_tc_scan<<<nm * groups, TC_THREADS, TC_SMEM, s>>>(p->q_map, p->ring_map, d_state, nm, B, p->Dp / TC_BK,
+                                                       part.s, part.p, part.floor_, groups, margin, sm);
   return cudaGetLastError();
 }
 

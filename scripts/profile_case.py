@@ -19,9 +19,11 @@ ap.add_argument("case", choices=sorted(CASES))
 ap.add_argument("--iters", type=int, default=6)
 ap.add_argument("--path", default="auto")
 ap.add_argument("--batch", type=int, default=0)
+ap.add_argument("--entries", type=int, default=0)
 a = ap.parse_args()
 n, dim, B = CASES[a.case]
 B = a.batch or B
+n = a.entries or n
 wl = ClusteredWorkload(dim, n_clusters=512, seed=17)
 rows = wl.cache_rows(n)
 ring = _native.DeviceRing(n, dim, 0)

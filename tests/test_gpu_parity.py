@@ -283,7 +283,7 @@ def test_reference_suite_kats_on_gpu():
 
 def _paths(cache, Q, table):
     out = {}
-    for name, path in (("gemv", _native.PATH_GEMV), ("gemm", _native.PATH_GEMM)):
+    for name, path in (("gemv", _native.PATH_GEMV), ("gemm", _native.PATH_GEMM), ("gemm1", _native.PATH_GEMM_1SM)):
         cache.ring.set_path(path)
         out[name] = cache.retrieve_flags(Q, table)
     cache.ring.set_path(_native.PATH_AUTO)
@@ -309,6 +309,8 @@ def test_tensor_core_scan_matches_gemv_and_oracle(dim, cap, n_ins, B):
     keep = ~((fv | fm) & AMBIG).astype(bool)
     assert np.array_equal(lv[keep], lm[keep]) and np.array_equal(kv, km)
     assert np.array_equal(sv, sm_)  # both certified float64 rescoring: bit-identical
+    for a, b in zip(res["gemm"], res["gemm1"]):  # CTA-pair vs single-CTA tensor-core kernels
+        assert np.array_equal(a, b)
     c.ring.set_path(_native.PATH_GEMM)
     _check_against_scan(c, live_rows, Q, table, f"gemm d{dim} cap{cap} B{B}")
     st = c.ring.stats()
