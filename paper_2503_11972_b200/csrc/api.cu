@@ -72,6 +72,7 @@ struct mc_cache {
   long long* d_part_p = nullptr;
   float* d_part_floor = nullptr;
   int part_chunks = 0;
+  CtaRec* d_cta = nullptr;  // [Bcap][gemv grid] per-CTA exact records (GEMV path)
   mc_record* d_rec = nullptr;
   mc_record* d_scratch = nullptr;
   OutRec* d_out = nullptr;
@@ -80,6 +81,7 @@ struct mc_cache {
   bool q_inflight = false;
 
   TcPlan* tc = nullptr;  // tensor-core scan plan, created on first batched lookup
+  unsigned* d_counter = nullptr;  // last-CTA ticket of the fused GEMV scan (zero between launches)
 
   Thresholds thr{};
   int path = MC_PATH_AUTO;
@@ -107,6 +109,7 @@ void free_batch(mc_cache* h) {
   cudaFree(h->d_part_s);
   cudaFree(h->d_part_p);
   cudaFree(h->d_part_floor);
+  cudaFree(h->d_cta);
   cudaFree(h->d_rec);
   cudaFree(h->d_scratch);
   cudaFree(h->d_out);
@@ -116,6 +119,7 @@ void free_batch(mc_cache* h) {
   h->d_part_s = nullptr;
   h->d_part_p = nullptr;
   h->d_part_floor = nullptr;
+  h->d_cta = nullptr;
   h->d_rec = nullptr;
   h->d_scratch = nullptr;
   h->d_out = nullptr;
@@ -137,6 +141,7 @@ int ensure_batch(mc_cache* h, int B) {
   CU(cudaMalloc(&h->d_part_s, (size_t)cap * chunks * KP * sizeof(float)));
   CU(cudaMalloc(&h->d_part_p, (size_t)cap * chunks * KP * sizeof(long long)));
   CU(cudaMalloc(&h->d_part_floor, (size_t)cap * chunks * sizeof(float)));
+  CU(cudaMalloc(&h->d_cta, (size_t)cap * gemv_grid(h->sm_count) * sizeof(CtaRec)));
   CU(cudaMalloc(&h->d_rec, (size_t)cap * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_scratch, (size_t)cap * exact_grid(h->sm_count) * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_out, (size_t)cap * sizeof(OutRec)));
@@ -208,48 +213,36 @@ int ensure_tc(mc_cache* h, int B) {
   return MC_OK;
 }
 
-// Scan pass only: per-chunk top-K' lists for B queries at q64 (stride Dp).
-int scan(mc_cache* h, const double* q64, int B, Partials& part, const double** qscale, double* eps_rel) {
+// Scan + certified merge for B queries at q64 (stride Dp): records into rec[0..B)
+// and, when out != nullptr, decisions into out[0..B).  GEMV: one fused launch
+// per 4 queries.  Tensor cores: prep + scan, then the merge kernel (+ decision).
+// t_mid (optional) is recorded between the scan and the standalone merge.
+int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* out, cudaEvent_t t_mid = nullptr) {
   if (use_gemm(h, B)) {
     int rc = ensure_tc(h, B);
     if (rc) return rc;
     tc_set_pair(h->tc, h->path != MC_PATH_GEMM_1SM);
-    part = Partials{h->d_part_s, h->d_part_p, h->d_part_floor, tc_chunks(h->tc, B)};
-    *qscale = tc_qscale(h->tc);
-    *eps_rel = gemm_eps_rel(h->Dp);
+    const Partials part{h->d_part_s, h->d_part_p, h->d_part_floor, tc_chunks(h->tc, B)};
     CU(launch_tc_scan(h->tc, q64, B, h->D, h->d_state, part, h->shard, h->stream));
+    if (t_mid) CU(cudaEventRecord(t_mid, h->stream));
+    CU(launch_merge(h->d_state, h->ring64, h->D, h->Dp, q64, B, part, tc_qscale(h->tc), gemm_eps_rel(h->Dp),
+                    eps_abs1(), rec, h->shard, h->stream));
     h->stats[6]++;
-    h->stats[7] += 2;
+    h->stats[7] += 3;
+    if (out) {
+      CU(launch_finalize(rec, 1, B, -1, h->d_state, h->thr, out, h->stream));
+      h->stats[7]++;
+    }
     return MC_OK;
   }
-  part = Partials{h->d_part_s, h->d_part_p, h->d_part_floor, gemv_grid(h->sm_count)};
-  *qscale = nullptr;
-  *eps_rel = gemv_eps_rel(h->Dp);
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nb = std::min(4, B - b0);
-    CU(launch_gemv_scan(h->ring16, h->d_state, h->Dp, q64 + (size_t)b0 * h->Dp, nb, part, b0,
-                        gemv_grid(h->sm_count), h->shard, h->stream));
+    CU(launch_gemv_scan(h->ring16, h->d_state, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
+                        gemv_grid(h->sm_count), h->shard, h->d_counter, h->ring64, h->thr, rec, out, h->stream));
     h->stats[5]++;
     h->stats[7]++;
   }
-  return MC_OK;
-}
-
-// Scan + certified merge + (optionally, device-driven) exhaustive rescans into rec[0..B).
-int scan_and_merge(mc_cache* h, const double* q64, int B, mc_record* rec, bool always_rescan) {
-  Partials part;
-  const double* qscale;
-  double eps;
-  int rc = scan(h, q64, B, part, &qscale, &eps);
-  if (rc) return rc;
-  CU(launch_merge(h->d_state, h->ring64, h->D, h->Dp, q64, B, part, qscale, eps, eps_abs1(), rec, h->shard,
-                  h->stream));
-  h->stats[7]++;
-  if (always_rescan) {
-    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, q64, B, rec, h->d_scratch,
-                           exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
-    h->stats[7] += 2;
-  }
+  if (t_mid) CU(cudaEventRecord(t_mid, h->stream));
   return MC_OK;
 }
 
@@ -317,6 +310,8 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   CUC(cudaMemsetAsync(h->ring16, 0, n16, h->stream));
   CUC(cudaMemsetAsync(h->ring64, 0, n64, h->stream));
   CUC(cudaMalloc(&h->d_state, sizeof(RingState)));
+  CUC(cudaMalloc(&h->d_counter, sizeof(unsigned)));
+  CUC(cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned), h->stream));
   {
     RingState z{0, 0, 0, h->C};
     CUC(cudaMemcpyAsync(h->d_state, &z, sizeof z, cudaMemcpyHostToDevice, h->stream));
@@ -352,6 +347,7 @@ int mc_destroy(mc_cache* h) {
     cudaFree(h->ring16);
     cudaFree(h->ring64);
     cudaFree(h->d_state);
+    cudaFree(h->d_counter);
     cudaFreeHost(h->h_stage);
     cudaFree(h->d_stage);
     if (h->stage_ev) cudaEventDestroy(h->stage_ev);
@@ -464,10 +460,8 @@ int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* ou
   if (rc) return rc;
   rc = upload_queries(h, queries, B);
   if (rc) return rc;
-  rc = scan_and_merge(h, h->d_q64, B, h->d_rec, false);
+  rc = scan_merge(h, h->d_q64, B, h->d_rec, h->d_out);
   if (rc) return rc;
-  CU(launch_finalize(h->d_rec, 1, B, -1, h->d_state, h->thr, h->d_out, h->stream));
-  h->stats[7]++;
   CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
   h->q_inflight = false;
@@ -499,8 +493,11 @@ int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void*
   if (h->count == 0) {
     CU(cudaMemsetAsync(rec, 0xff, (size_t)B * sizeof(mc_record), h->stream));  // pos = -1 (NaN sims)
   } else {
-    rc = scan_and_merge(h, h->d_q64, B, rec, true);
+    rc = scan_merge(h, h->d_q64, B, rec, nullptr);
     if (rc) return rc;
+    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, h->d_q64, B, rec, h->d_scratch,
+                           exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
+    h->stats[7] += 2;
   }
   if (stream && stream != h->stream) {
     cudaEvent_t ev;
@@ -602,19 +599,11 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
     }
     CUP(cudaEventRecord(ev[(size_t)it * nev + 1], h->stream));
     const double* q = d_qall + (size_t)it * B * h->Dp;
-    Partials part;
-    const double* qscale;
-    double eps;
-    rc = scan(h, q, B, part, &qscale, &eps);
+    rc = scan_merge(h, q, B, h->d_rec, d_outs + (size_t)it * B, ev[(size_t)it * nev + 2]);
     if (rc) {
       release();
       return rc;
     }
-    CUP(cudaEventRecord(ev[(size_t)it * nev + 2], h->stream));
-    CUP(launch_merge(h->d_state, h->ring64, h->D, h->Dp, q, B, part, qscale, eps, eps_abs1(), h->d_rec, h->shard,
-                     h->stream));
-    CUP(launch_finalize(h->d_rec, 1, B, -1, h->d_state, h->thr, d_outs + (size_t)it * B, h->stream));
-    h->stats[7] += 2;
     CUP(cudaEventRecord(ev[(size_t)it * nev + 3], h->stream));
   }
   CUP(cudaStreamSynchronize(h->stream));

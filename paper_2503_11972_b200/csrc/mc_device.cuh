@@ -42,25 +42,45 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
   e = (a - (s - z)) + (b - z);
 }
 
-// Compensated (Ogita-Rump-Oishi Dot2) float64 dot product of one row with q,
-// one warp, fixed lane->element assignment and a fixed butterfly, so every
-// lane returns the same bits and identical rows always score identically.
-__device__ __forceinline__ double warp_dot64(const double* __restrict__ row, const double* __restrict__ q, int D,
+__device__ __forceinline__ void dot2_step(double a, double b, double& s, double& c) {
+  const double p = a * b;
+  const double ep = fma(a, b, -p);
+  double t, et;
+  two_sum(s, p, t, et);
+  s = t;
+  c += ep + et;
+}
+
+// Compensated (Ogita-Rump-Oishi Dot2) float64 dot product of one row with q
+// over n elements (n a multiple of 64, rows and q zero-padded), one warp.
+// Lane l owns elements 2l, 2l+1 of every 64-element block, accumulated in
+// increasing block order; the 16 loads of a 512-element block are issued
+// before any is used.  The lane->element map and the butterfly are fixed, so
+// every lane returns the same bits and identical rows always score
+// identically (exact ties stay exact).
+__device__ __forceinline__ double warp_dot64(const double* __restrict__ row, const double* __restrict__ q, int n,
                                              int lane) {
   double s = 0.0, c = 0.0;
-  for (int i = lane; i < D; i += 32) {
-    double a = row[i], b = q[i];
-    double p = a * b;
-    double ep = fma(a, b, -p);
-    double t, et;
-    two_sum(s, p, t, et);
-    s = t;
-    c += ep + et;
+  for (int base = 0; base < n; base += 512) {
+    double2 a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = base + 64 * j + 2 * lane;
+      a[j] = i < n ? __ldg(reinterpret_cast<const double2*>(row + i)) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = base + 64 * j + 2 * lane;
+      if (i < n) {
+        dot2_step(a[j].x, q[i], s, c);
+        dot2_step(a[j].y, q[i + 1], s, c);
+      }
+    }
   }
 #pragma unroll
   for (int off = 16; off; off >>= 1) {
-    double s2 = __shfl_xor_sync(FULL, s, off);
-    double c2 = __shfl_xor_sync(FULL, c, off);
+    const double s2 = __shfl_xor_sync(FULL, s, off);
+    const double c2 = __shfl_xor_sync(FULL, c, off);
     double t, et;
     two_sum(s, s2, t, et);
     s = t;

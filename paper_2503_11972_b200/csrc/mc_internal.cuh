@@ -49,9 +49,27 @@ struct Partials {
   int n_chunks;
 };
 
+// One CTA's exact answer for one query on the GEMV path: the float64 best over
+// the CTA's rescored candidates plus the certificate input (see scan_gemv.cu).
+struct CtaRec {
+  double s;     // best float64 similarity among the rescored candidates (-inf if none)
+  double s2;    // runner-up float64 similarity among them
+  long long p;  // global position of the best (-1 if none)
+  float ovf;    // largest approx score (query units) a full warp list had to drop (-inf if none)
+  int ties;     // rescored candidates bit-equal to s
+};
+
 struct ShardMap {
   int G;  // number of shards
   int g;  // this shard
+};
+
+// Final per-query answer written by the decision epilogue.
+struct OutRec {
+  long long live;  // live index (0 = oldest), -1 if none
+  double sim;      // best float64 similarity
+  int k;           // select_k result, 0 = none
+  unsigned flags;  // MC_FLAG_*
 };
 
 // ---- launch wrappers (each .cu owns its kernels) ---------------------------
@@ -59,9 +77,13 @@ cudaError_t launch_append(const double* stage, long long n, long long first_slot
                           int D, int Dp, __half* ring16, double* ring64, RingState* d_state,
                           cudaStream_t s);
 
-// GEMV scan of up to 4 queries (q64 rows q0 .. q0+nb-1, stride Dp).
-cudaError_t launch_gemv_scan(const __half* ring16, const RingState* d_state, int Dp, const double* q64, int nb,
-                             const Partials& part, int part_b0, int grid, ShardMap sm, cudaStream_t s);
+// GEMV scan of up to 4 queries (q64 rows q0 .. q0+nb-1, stride Dp) with the
+// certified merge fused into the last CTA: records go to rec[part_b0 + b] and,
+// if out != nullptr, decisions to out[part_b0 + b].  counter: zeroed device word.
+cudaError_t launch_gemv_scan(const __half* ring16, const RingState* d_state, int D, int Dp, const double* q64,
+                             int nb, CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter,
+                             const double* ring64, const Thresholds& thr, mc_record* rec, OutRec* out,
+                             cudaStream_t s);
 int gemv_grid(int sm_count);
 
 // tcgen05 GEMM scan of B queries (scan_tc.cu).  The plan owns the fp16
@@ -90,12 +112,7 @@ int exact_grid(int sm_count);
 
 // Final decision: merge G shard records per query, apply threshold / k.
 // p0 < 0 means "read jhead from d_state" (single-GPU).
-struct OutRec {
-  long long live;  // live index (0 = oldest), -1 if none
-  double sim;      // best float64 similarity
-  int k;           // select_k result, 0 = none
-  unsigned flags;  // MC_FLAG_*
-};
+
 cudaError_t launch_finalize(const mc_record* rec, int G, int B, long long p0, const RingState* d_state,
                             Thresholds thr, OutRec* out, cudaStream_t s);
 

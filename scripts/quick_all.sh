@@ -1,0 +1,4 @@
+set -x
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+tail -3 gpurun_out/pytest_gpu.log
+bash scripts/prof_c2.sh
