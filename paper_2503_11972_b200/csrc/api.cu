@@ -73,6 +73,7 @@ struct mc_cache {
   float* d_part_floor = nullptr;
   int part_chunks = 0;
   CtaRec* d_cta = nullptr;  // [Bcap][gemv grid] per-CTA exact records (GEMV path)
+  unsigned* d_gmax = nullptr;  // [Bcap] running max keys of the fused GEMV scan (zero between launches)
   mc_record* d_rec = nullptr;
   mc_record* d_scratch = nullptr;
   OutRec* d_out = nullptr;
@@ -110,6 +111,7 @@ void free_batch(mc_cache* h) {
   cudaFree(h->d_part_p);
   cudaFree(h->d_part_floor);
   cudaFree(h->d_cta);
+  cudaFree(h->d_gmax);
   cudaFree(h->d_rec);
   cudaFree(h->d_scratch);
   cudaFree(h->d_out);
@@ -120,6 +122,7 @@ void free_batch(mc_cache* h) {
   h->d_part_p = nullptr;
   h->d_part_floor = nullptr;
   h->d_cta = nullptr;
+  h->d_gmax = nullptr;
   h->d_rec = nullptr;
   h->d_scratch = nullptr;
   h->d_out = nullptr;
@@ -142,6 +145,8 @@ int ensure_batch(mc_cache* h, int B) {
   CU(cudaMalloc(&h->d_part_p, (size_t)cap * chunks * KP * sizeof(long long)));
   CU(cudaMalloc(&h->d_part_floor, (size_t)cap * chunks * sizeof(float)));
   CU(cudaMalloc(&h->d_cta, (size_t)cap * gemv_grid(h->sm_count) * sizeof(CtaRec)));
+  CU(cudaMalloc(&h->d_gmax, (size_t)cap * sizeof(unsigned)));
+  CU(cudaMemsetAsync(h->d_gmax, 0, (size_t)cap * sizeof(unsigned), h->stream));
   CU(cudaMalloc(&h->d_rec, (size_t)cap * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_scratch, (size_t)cap * exact_grid(h->sm_count) * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_out, (size_t)cap * sizeof(OutRec)));
@@ -153,24 +158,41 @@ int ensure_batch(mc_cache* h, int B) {
 
 RingState mirror(const mc_cache* h) { return RingState{h->head, h->count, h->jhead, h->C}; }
 
-// Publish pending appends / evictions to the device (stream-ordered).
-int flush(mc_cache* h) {
-  if (h->n_pending == 0 && !h->state_dirty) return MC_OK;
-  long long nw = 0, first = 0;
+// Largest pending-append batch folded into a GEMV launch; larger flushes use k_append.
+constexpr long long FUSE_APPEND_MAX = 256;
+
+// Copy pending appends to the device stage (stream-ordered) and describe them.
+int stage_pending(mc_cache* h, GemvAppendArgs& a) {
+  a = GemvAppendArgs{};
+  a.ring16 = h->ring16;
+  a.ring64 = h->ring64;
+  a.d_state = h->d_state;
   if (h->n_pending > 0) {
-    nw = std::min(h->n_pending, h->C);
+    const long long nw = std::min(h->n_pending, h->C);
     const long long skip = h->n_pending - nw;
-    first = (h->pending_first_slot + skip) % h->C;
     CU(cudaMemcpy2DAsync(h->d_stage, (size_t)h->Dp * sizeof(double), h->h_stage + (size_t)skip * h->D,
                          (size_t)h->D * sizeof(double), (size_t)h->D * sizeof(double), (size_t)nw,
                          cudaMemcpyHostToDevice, h->stream));
     CU(cudaEventRecord(h->stage_ev, h->stream));
     h->stage_inflight = true;
+    a.stage = h->d_stage;
+    a.n = nw;
+    a.first_slot = (h->pending_first_slot + skip) % h->C;
   }
-  CU(launch_append(h->d_stage, nw, first, mirror(h), h->D, h->Dp, h->ring16, h->ring64, h->d_state, h->stream));
-  h->stats[7]++;
   h->n_pending = 0;
   h->state_dirty = false;
+  return MC_OK;
+}
+
+// Publish pending appends / evictions to the device with k_append (stream-ordered).
+int flush(mc_cache* h) {
+  if (h->n_pending == 0 && !h->state_dirty) return MC_OK;
+  GemvAppendArgs a;
+  int rc = stage_pending(h, a);
+  if (rc) return rc;
+  CU(launch_append(h->d_stage, a.n, a.first_slot, mirror(h), h->D, h->Dp, h->ring16, h->ring64, h->d_state,
+                   h->stream));
+  h->stats[7]++;
   return MC_OK;
 }
 
@@ -217,9 +239,18 @@ int ensure_tc(mc_cache* h, int B) {
 // and, when out != nullptr, decisions into out[0..B).  GEMV: one fused launch
 // per 4 queries.  Tensor cores: prep + scan, then the merge kernel (+ decision).
 // t_mid (optional) is recorded between the scan and the standalone merge.
-int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* out, cudaEvent_t t_mid = nullptr) {
+// `pre`: appends already resident on the device (profiling), applied before the scan.
+int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* out, cudaEvent_t t_mid = nullptr,
+               const GemvAppendArgs* pre = nullptr) {
   if (use_gemm(h, B)) {
-    int rc = ensure_tc(h, B);
+    int rc = flush(h);
+    if (rc) return rc;
+    if (pre && pre->n > 0) {
+      CU(launch_append(pre->stage, pre->n, pre->first_slot, mirror(h), h->D, h->Dp, h->ring16, h->ring64,
+                       h->d_state, h->stream));
+      h->stats[7]++;
+    }
+    rc = ensure_tc(h, B);
     if (rc) return rc;
     tc_set_pair(h->tc, h->path != MC_PATH_GEMM_1SM);
     const Partials part{h->d_part_s, h->d_part_p, h->d_part_floor, tc_chunks(h->tc, B)};
@@ -235,10 +266,29 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
     }
     return MC_OK;
   }
+  // GEMV: small pending-append batches ride along with the first launch.
+  GemvAppendArgs app;
+  if (h->n_pending > FUSE_APPEND_MAX) {
+    int rc = flush(h);
+    if (rc) return rc;
+  }
+  int rc = stage_pending(h, app);
+  if (rc) return rc;
+  if (pre && pre->n > 0) {
+    if (app.n > 0) {  // host-staged rows first, then the device-resident ones
+      CU(launch_append(app.stage, app.n, app.first_slot, mirror(h), h->D, h->Dp, h->ring16, h->ring64, h->d_state,
+                       h->stream));
+      h->stats[7]++;
+    }
+    app = *pre;
+  }
+  const RingState st = mirror(h);
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nb = std::min(4, B - b0);
-    CU(launch_gemv_scan(h->ring16, h->d_state, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
-                        gemv_grid(h->sm_count), h->shard, h->d_counter, h->ring64, h->thr, rec, out, h->stream));
+    CU(launch_gemv_scan(h->ring16, st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
+                        gemv_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax, h->ring64, h->thr, rec, out, app,
+                        h->stream));
+    app.n = 0;  // written by the first launch
     h->stats[5]++;
     h->stats[7]++;
   }
@@ -456,8 +506,6 @@ int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* ou
   }
   int rc = ensure_batch(h, B);
   if (rc) return rc;
-  rc = flush(h);
-  if (rc) return rc;
   rc = upload_queries(h, queries, B);
   if (rc) return rc;
   rc = scan_merge(h, h->d_q64, B, h->d_rec, h->d_out);
@@ -486,11 +534,11 @@ int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void*
   mc_record* rec = static_cast<mc_record*>(dev_records);
   int rc = ensure_batch(h, B);
   if (rc) return rc;
-  rc = flush(h);
-  if (rc) return rc;
   rc = upload_queries(h, queries, B);
   if (rc) return rc;
   if (h->count == 0) {
+    rc = flush(h);
+    if (rc) return rc;
     CU(cudaMemsetAsync(rec, 0xff, (size_t)B * sizeof(mc_record), h->stream));  // pos = -1 (NaN sims)
   } else {
     rc = scan_merge(h, h->d_q64, B, rec, nullptr);
@@ -584,6 +632,7 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
   for (int it = 0; it < iters; ++it) {
     if (d_flush) CUP(cudaMemsetAsync(d_flush, it & 0xff, (size_t)flush_bytes, h->stream));
     CUP(cudaEventRecord(ev[(size_t)it * nev + 0], h->stream));
+    GemvAppendArgs pre;
     if (rows) {
       if (h->count == h->C) {
         h->head = (h->head + 1) % h->C;
@@ -593,13 +642,16 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
       const long long slot = (h->head + h->count) % h->C;
       h->count++;
       h->appended++;
-      CUP(launch_append(d_rows + (size_t)it * h->Dp, 1, slot, mirror(h), h->D, h->Dp, h->ring16, h->ring64,
-                        h->d_state, h->stream));
-      h->stats[7]++;
+      pre.stage = d_rows + (size_t)it * h->Dp;
+      pre.n = 1;
+      pre.first_slot = slot;
+      pre.ring16 = h->ring16;
+      pre.ring64 = h->ring64;
+      pre.d_state = h->d_state;
     }
     CUP(cudaEventRecord(ev[(size_t)it * nev + 1], h->stream));
     const double* q = d_qall + (size_t)it * B * h->Dp;
-    rc = scan_merge(h, q, B, h->d_rec, d_outs + (size_t)it * B, ev[(size_t)it * nev + 2]);
+    rc = scan_merge(h, q, B, h->d_rec, d_outs + (size_t)it * B, ev[(size_t)it * nev + 2], rows ? &pre : nullptr);
     if (rc) {
       release();
       return rc;
@@ -634,6 +686,21 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
   out_counts[1] = need;
   release();
 #undef CUP
+  return MC_OK;
+}
+
+// Measurement hook (MC_GEMV_TIMING=1): read (reset=0) or reset (reset=1) the
+// GEMV phase timestamps; 4 x u64 nanoseconds.  Not part of the stable ABI.
+int mc_debug_gemv_timing(unsigned long long* out4, int reset) {
+  unsigned long long* t = gemv_timing_buffer();
+  if (!t) return fail(MC_ERR_STATE, "set MC_GEMV_TIMING=1 before the first lookup");
+  CU(cudaDeviceSynchronize());
+  if (reset) {
+    const unsigned long long init4[4] = {~0ull, 0, 0, 0};
+    CU(cudaMemcpy(t, init4, sizeof init4, cudaMemcpyHostToDevice));
+  } else {
+    CU(cudaMemcpy(out4, t, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  }
   return MC_OK;
 }
 

@@ -77,14 +77,27 @@ cudaError_t launch_append(const double* stage, long long n, long long first_slot
                           int D, int Dp, __half* ring16, double* ring64, RingState* d_state,
                           cudaStream_t s);
 
-// GEMV scan of up to 4 queries (q64 rows q0 .. q0+nb-1, stride Dp) with the
-// certified merge fused into the last CTA: records go to rec[part_b0 + b] and,
-// if out != nullptr, decisions to out[part_b0 + b].  counter: zeroed device word.
-cudaError_t launch_gemv_scan(const __half* ring16, const RingState* d_state, int D, int Dp, const double* q64,
-                             int nb, CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter,
+// Pending appends folded into a GEMV launch: stage rows [0, n) -> ring slots
+// (first_slot + i) mod C; d_state receives the launch's window.
+struct GemvAppendArgs {
+  const double* stage = nullptr;
+  long long n = 0;
+  long long first_slot = 0;
+  __half* ring16 = nullptr;
+  double* ring64 = nullptr;
+  RingState* d_state = nullptr;
+};
+
+// GEMV scan of up to 4 queries (q64 rows q0 .. q0+nb-1, stride Dp) over the
+// window `st`, with the certified merge fused into the last CTA: records go to
+// rec[b0 + b] and, if out != nullptr, decisions to out[b0 + b].  counter and
+// gmax[b0 + b]: zeroed device words (the kernel leaves them zeroed).
+cudaError_t launch_gemv_scan(const __half* ring16, const RingState& st, int D, int Dp, const double* q64, int nb,
+                             CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
                              const double* ring64, const Thresholds& thr, mc_record* rec, OutRec* out,
-                             cudaStream_t s);
+                             const GemvAppendArgs& app, cudaStream_t s);
 int gemv_grid(int sm_count);
+unsigned long long* gemv_timing_buffer();  // MC_GEMV_TIMING=1 phase timestamps (measurement)
 
 // tcgen05 GEMM scan of B queries (scan_tc.cu).  The plan owns the fp16
 // query tile (q / ||q||), the per-query scale ||q|| and both TMA descriptors.

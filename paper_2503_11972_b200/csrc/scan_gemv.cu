@@ -24,6 +24,8 @@
 // writes the decision, so one launch does scan + rescoring + epilogue.
 //
 // Algorithmic bytes per lookup batch: count * Dp * 2 (the fp16 ring) + Dp * 8 per query.
+#include <cstdlib>
+
 #include "merge.cuh"
 
 namespace mc {
@@ -43,50 +45,147 @@ __device__ __forceinline__ void fma8(float& acc, const uint4& v, const float* q)
 
 struct GemvTail {
   unsigned* counter;      // zero between launches; the last CTA resets it
+  unsigned* gmax;         // [b0 + b] running max approx score (orderable key); zero between launches
   const double* ring64;   // float64 master (rescoring)
   int D;
   double eps_rel, eps_a1;
   Thresholds thr;
   mc_record* rec;         // per-query merged record (rescan requests live in its flags)
   OutRec* out;            // per-query decision (nullptr: records only, e.g. a shard's local answer)
+  unsigned long long* timing;  // optional [4]: min start, max scan end, max rescoring end, tail end (ns)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Pending FIFO appends folded into the scan (replaces k_append for small flushes):
+// stage rows [0, n) (float64, stride Dp, zero padded) belong to ring slots
+// (first_slot + i) mod C; the warp that scans a pending row converts it exactly
+// as k_append would and writes both ring copies.
+struct GemvAppend {
+  const double* stage;
+  long long n;
+  long long first_slot;
+  __half* ring16;
+  double* ring64;
+  RingState* d_state;  // receives the new window (block 0)
+};
+
+// One 16-byte chunk (8 values) of a pending row: float64 -> fp16 RN exactly as
+// k_append, written to both ring copies; returns the fp16 chunk for the scan.
+__device__ __noinline__ uint4 pending_chunk(const double* __restrict__ srow, int c, __half* r16, double* r64) {
+  __align__(16) __half hv[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const double d = srow[c * 8 + t];
+    r64[c * 8 + t] = d;
+    hv[t] = __double2half(d);
+  }
+  const uint4 h4 = *reinterpret_cast<const uint4*>(hv);
+  *reinterpret_cast<uint4*>(r16 + c * 8) = h4;
+  return h4;
+}
+
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* counter) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(counter) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ unsigned order_key(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float order_val(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
 
 template <int NJ, int NB, int R>
 __global__ void __launch_bounds__(GEMV_THREADS, (NJ * NB > 12) ? 1 : 2)
-    k_gemv_scan(const __half* __restrict__ ring16, const RingState* __restrict__ d_state, int Dp,
-                const double* __restrict__ q64, int nb, CtaRec* __restrict__ cta, int b0, float margin_rel,
-                ShardMap sm, GemvTail tail) {
-  extern __shared__ __align__(16) double sq[];  // [Dp] float64 query (rescoring)
+    k_gemv_scan(const __half* __restrict__ ring16, const RingState st, int Dp, const double* __restrict__ q64,
+                int nb, CtaRec* __restrict__ cta, int b0, float margin_rel, ShardMap sm, GemvTail tail,
+                GemvAppend app) {
+  extern __shared__ __align__(16) double sq[];  // [nb][Dp] float64 queries (rescoring), filled by warp 0
   __shared__ float sh_s[NB][GEMV_WARPS * KP];
   __shared__ long long sh_p[NB][GEMV_WARPS * KP];
   __shared__ float sh_run[NB][GEMV_WARPS];
   __shared__ float sh_ovf[NB][GEMV_WARPS];
+  __shared__ float sh_gmax[NB];
   __shared__ MergeScratch ms;
   __shared__ int sh_last;
 
-  const RingState st = *d_state;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int n16 = Dp >> 3;  // 16-byte chunks per row
+  if (blockIdx.x == 0 && threadIdx.x == 0 && app.d_state) *app.d_state = st;
+  if (tail.timing && threadIdx.x == 0) atomicMin(tail.timing + 0, gtimer());
 
-  // Query in fp32 registers: lane owns chunks lane + 32*j; admission margin per
-  // query = 2.02 delta (delta = eps_rel ||q||_2 + eps_a1 ||q||_1) + fp32 slack.
-  // A non-finite query gives a NaN margin: nothing is admitted, and the tail
-  // routes it to the exhaustive float64 scan.
+  const long long n = st.count;
+  const long long n_warps = (long long)gridDim.x * GEMV_WARPS;
+  const long long per = (n + n_warps - 1) / n_warps;
+  const long long r0 = ((long long)blockIdx.x * GEMV_WARPS + warp) * per;
+  const long long r1 = min(n, r0 + per);
+  const long long n_pend = min(app.n, n);      // pending rows still live: the newest n_pend
+  const long long pend0 = n - n_pend;          // live-local index of the first of them
+  const long long pend_skip = app.n - n_pend;  // stage rows already evicted
+
+  // One batch of R rows: 16-byte loads (lane owns chunks lane + 32 j).  A pending
+  // row comes from the stage (float64 -> fp16 RN, as k_append) and is written back.
+  auto load_batch = [&](long long base, uint4 (&v)[R][NJ]) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const long long row = base + r;
+      if (row < r1 && row < pend0) {
+        const __half* src = ring16 + (size_t)ring_slot(st, row) * Dp;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int c = lane + 32 * j;
+          v[r][j] = (c < n16) ? ld_stream16(src + c * 8) : make_uint4(0, 0, 0, 0);
+        }
+      } else if (row < r1) {  // pending row (rare, warp-uniform)
+        const long long slot = ring_slot(st, row);
+        const double* srow = app.stage + (size_t)(pend_skip + row - pend0) * Dp;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int c = lane + 32 * j;
+          v[r][j] = (c < n16) ? pending_chunk(srow, c, app.ring16 + (size_t)slot * Dp, app.ring64 + (size_t)slot * Dp)
+                              : make_uint4(0, 0, 0, 0);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) v[r][j] = make_uint4(0, 0, 0, 0);
+      }
+    }
+  };
+
+  // First batch in flight before the query loads, so both latencies overlap.
+  uint4 v[R][NJ];
+  load_batch(r0, v);
+
+  // Query in fp32 registers; delta (= eps_rel ||q||_2 + eps_a1 ||q||_1, float64)
+  // and the admission margin 2.02 delta + fp32 slack per query.  A non-finite
+  // query gives a NaN margin: nothing is admitted, and the tail routes it to
+  // the exhaustive float64 scan.
   float q[NB][NJ][8];
   float margin[NB];
+  double delta[NB];
+  bool exotic[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    float a2 = 0.f, a1 = 0.f;
+    double a2 = 0.0, a1 = 0.0;
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
       const int c = lane + 32 * j;
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
-        const float x = (b < nb && c < n16) ? (float)q64[(size_t)b * Dp + c * 8 + t] : 0.f;
-        q[b][j][t] = x;
-        a2 = fmaf(x, x, a2);
-        a1 += fabsf(x);
+        const double x = (b < nb && c < n16 && c * 8 + t < tail.D) ? q64[(size_t)b * Dp + c * 8 + t] : 0.0;
+        if (warp == 0 && b < nb && c < n16) sq[(size_t)b * Dp + c * 8 + t] = x;
+        q[b][j][t] = (float)x;
+        a2 = fma(x, x, a2);
+        a1 += fabs(x);
       }
     }
 #pragma unroll
@@ -94,8 +193,11 @@ __global__ void __launch_bounds__(GEMV_THREADS, (NJ * NB > 12) ? 1 : 2)
       a2 += __shfl_xor_sync(FULL, a2, off);
       a1 += __shfl_xor_sync(FULL, a1, off);
     }
-    margin[b] = 2.02f * (float)(tail.eps_rel * sqrt((double)a2) + tail.eps_a1 * (double)a1) * 1.001f +
-                margin_rel * sqrtf(a2);
+    // Rounded up past any summation-order difference with the host/merge norms.
+    const double n2 = sqrt(a2) * (1.0 + 1e-12), n1 = a1 * (1.0 + 1e-12);
+    exotic[b] = !(n1 <= 1e30) || !(n2 >= 1e-30);
+    delta[b] = tail.eps_rel * n2 + tail.eps_a1 * n1;
+    margin[b] = (float)(2.02 * delta[b]) + margin_rel * (float)n2;
   }
 
   // Per-warp sorted top-K': lane k < KP holds the k-th best (score, pos).
@@ -110,29 +212,8 @@ __global__ void __launch_bounds__(GEMV_THREADS, (NJ * NB > 12) ? 1 : 2)
     ovf[b] = -INFINITY;
   }
 
-  const long long n = st.count;
-  const long long n_warps = (long long)gridDim.x * GEMV_WARPS;
-  const long long per = (n + n_warps - 1) / n_warps;
-  const long long r0 = ((long long)blockIdx.x * GEMV_WARPS + warp) * per;
-  const long long r1 = min(n, r0 + per);
-
   for (long long base = r0; base < r1; base += R) {
-    uint4 v[R][NJ];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const long long row = base + r;
-      if (row < r1) {
-        const __half* src = ring16 + (size_t)ring_slot(st, row) * Dp;
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-          const int c = lane + 32 * j;
-          v[r][j] = (c < n16) ? ld_stream16(src + c * 8) : make_uint4(0, 0, 0, 0);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) v[r][j] = make_uint4(0, 0, 0, 0);
-      }
-    }
+    if (base != r0) load_batch(base, v);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const long long row = base + r;
@@ -171,6 +252,7 @@ __global__ void __launch_bounds__(GEMV_THREADS, (NJ * NB > 12) ? 1 : 2)
   }
 
   // ---------------------------------------------------------------- CTA rescoring
+  if (tail.timing && lane == 0) atomicMax(tail.timing + 1, gtimer());
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     if (lane < KP) {
@@ -182,27 +264,44 @@ __global__ void __launch_bounds__(GEMV_THREADS, (NJ * NB > 12) ? 1 : 2)
       sh_ovf[b][warp] = ovf[b];
     }
   }
+  __syncthreads();
+  // Publish this CTA's approximate maxima; a CTA more than 2 delta below the
+  // running global maximum holds no row that can reach (or tie within 1e-9)
+  // the certified best, so it skips the float64 rescoring.
+  if (threadIdx.x < nb) {
+    const int b = threadIdx.x;
+    float mc = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < GEMV_WARPS; ++w) mc = fmaxf(mc, sh_run[b][w]);
+    const unsigned mine = order_key(mc);
+    const unsigned old = atomicMax(tail.gmax + b0 + b, mine);
+    sh_gmax[b] = order_val(old > mine ? old : mine);
+  }
+  __syncthreads();
   for (int b = 0; b < nb; ++b) {
-    load_query(q64 + (size_t)b * Dp, tail.D, Dp, sq);  // ends with __syncthreads
-    double n2, n1;
-    q_norms(sq, tail.D, ms.shd, n2, n1);
-    const double delta = tail.eps_rel * n2 + tail.eps_a1 * n1;
     float mc = -INFINITY, ov = -INFINITY;
 #pragma unroll
     for (int w = 0; w < GEMV_WARPS; ++w) {
       mc = fmaxf(mc, sh_run[b][w]);
       ov = fmaxf(ov, sh_ovf[b][w]);
     }
-    const double thr = (double)mc - 2.0 * delta - 1e-9;
+    const double d2 = 2.0 * delta[b] + 1e-9;
     Best2 best;
     best.init();
-    for (int e = warp; e < GEMV_WARPS * KP; e += GEMV_WARPS) {
-      const long long p = sh_p[b][e];
-      if (p < 0 || (double)sh_s[b][e] < thr) continue;  // warp-uniform
-      const long long slot = ring_slot(st, local_row(st, p, sm));
-      best.add(warp_dot64(tail.ring64 + (size_t)slot * Dp, sq, Dp, lane), p);
+    if (mc > -INFINITY && (double)mc >= (double)sh_gmax[b] - d2) {  // block-uniform
+      const double thr = (double)mc - d2;
+      for (int e = warp; e < GEMV_WARPS * KP; e += GEMV_WARPS) {
+        const long long p = sh_p[b][e];
+        if (p < 0 || (double)sh_s[b][e] < thr) continue;  // warp-uniform
+        const long long l = local_row(st, p, sm);
+        // a row appended by this launch is read from the stage (the ring copy
+        // was written in this kernel and is not visible to the read-only path)
+        const double* row = l >= pend0 ? app.stage + (size_t)(pend_skip + l - pend0) * Dp
+                                        : tail.ring64 + (size_t)ring_slot(st, l) * Dp;
+        best.add(warp_dot64(row, sq + (size_t)b * Dp, Dp, lane), p);
+      }
+      best = block_best(best, ms.shb, true);
     }
-    best = block_best(best, ms.shb, true);
     if (threadIdx.x == 0) {
       CtaRec r;
       r.s = best.s;
@@ -214,26 +313,30 @@ __global__ void __launch_bounds__(GEMV_THREADS, (NJ * NB > 12) ? 1 : 2)
     }
   }
 
+  if (tail.timing && threadIdx.x == 0) atomicMax(tail.timing + 2, gtimer());
   if (!tail.counter) return;
   // ---------------------------------------------------------------- fused tail
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) sh_last = atomicAdd(tail.counter, 1u) == gridDim.x - 1;
+  // Thread 0 wrote this CTA's records; its acq_rel ticket releases them and, on
+  // the last CTA, acquires everyone else's (then bar.sync shares that view).
+  if (threadIdx.x == 0) sh_last = ticket_acq_rel(tail.counter) == gridDim.x - 1;
   __syncthreads();
   if (!sh_last) return;
-  __threadfence();
-  for (int b = 0; b < nb; ++b) {
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    if (b >= nb) break;
     const int gb = b0 + b;
-    load_query(q64 + (size_t)b * Dp, tail.D, Dp, sq);
-    double n2, n1;
-    q_norms(sq, tail.D, ms.shd, n2, n1);
-    const bool exotic = !(n1 <= 1e30) || !(n2 >= 1e-30);
-    const double delta = tail.eps_rel * n2 + tail.eps_a1 * n1;
+    const double dl = delta[b];
     Best2 best;
     best.init();
     float ov = -INFINITY;
     for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x) {
-      const CtaRec r = cta[(size_t)gb * gridDim.x + c];
+      CtaRec r;
+      const CtaRec* src = cta + (size_t)gb * gridDim.x + c;
+      r.s = __ldcg(&src->s);
+      r.s2 = __ldcg(&src->s2);
+      r.p = __ldcg(&src->p);
+      r.ovf = __ldcg(&src->ovf);
+      r.ties = __ldcg(&src->ties);
       ov = fmaxf(ov, r.ovf);
       if (r.p < 0) continue;
       Best2 o;
@@ -246,23 +349,42 @@ __global__ void __launch_bounds__(GEMV_THREADS, (NJ * NB > 12) ? 1 : 2)
     best = block_best(best, ms.shb, false);
     ov = block_max(ov, ms.shf);
     if (threadIdx.x == 0) {
-      const bool fail = best.p < 0 || !(ov == -INFINITY || (double)ov + delta < best.s);
+      const bool fail = best.p < 0 || !(ov == -INFINITY || (double)ov + dl < best.s);
       mc_record r;
       r.sim = best.s;
       r.second = best.s2;
       r.pos = best.p;
       r.flags = (best.ties >= 2 ? MC_FLAG_TIE : 0u) | (fail ? FLAG_NEED_FALLBACK : 0u) |
-                (exotic ? FLAG_NEED_EXHAUSTIVE : 0u);
+                (exotic[b] ? FLAG_NEED_EXHAUSTIVE : 0u);
       r.reserved = 0;
       tail.rec[gb] = r;
       if (tail.out) tail.out[gb] = decide(record_best(r), r.flags & FLAG_NEED_ANY, st.jhead, tail.thr);
+      tail.gmax[gb] = 0u;
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *tail.counter = 0u;
+  if (threadIdx.x == 0) {
+    *tail.counter = 0u;
+    if (tail.timing) tail.timing[3] = gtimer();
+  }
 }
 
 int gemv_grid(int sm_count) { return 2 * sm_count; }
+
+// MC_GEMV_TIMING=1: every GEMV launch records phase timestamps (measurement only).
+static unsigned long long* g_timing = nullptr;
+unsigned long long* gemv_timing_buffer() {
+  static bool init = false;
+  if (!init) {
+    init = true;
+    const char* e = getenv("MC_GEMV_TIMING");
+    if (e && atoi(e) && cudaMalloc(&g_timing, 4 * sizeof(unsigned long long)) == cudaSuccess) {
+      const unsigned long long init4[4] = {~0ull, 0, 0, 0};
+      cudaMemcpy(g_timing, init4, sizeof init4, cudaMemcpyHostToDevice);
+    }
+  }
+  return g_timing;
+}
 
 // Rows streamed per warp iteration: ~18 16-byte loads in flight per lane per query.
 constexpr int rows_for(int NJ, int NB) {
@@ -271,49 +393,54 @@ constexpr int rows_for(int NJ, int NB) {
 }
 
 template <int NJ, int NB>
-static cudaError_t launch_one(const __half* ring16, const RingState* d_state, int Dp, const double* q64, int nb,
+static cudaError_t launch_one(const __half* ring16, const RingState& st, int Dp, const double* q64, int nb,
                               CtaRec* cta, int b0, int grid, float margin_rel, ShardMap sm, const GemvTail& tail,
-                              cudaStream_t s) {
+                              const GemvAppend& app, cudaStream_t s) {
   constexpr int R = rows_for(NJ, NB);
   auto kern = k_gemv_scan<NJ, NB, R>;
-  const size_t smem = (size_t)Dp * sizeof(double);
+  const size_t smem = (size_t)NB * Dp * sizeof(double);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<grid, GEMV_THREADS, smem, s>>>(ring16, d_state, Dp, q64, nb, cta, b0, margin_rel, sm, tail);
+  kern<<<grid, GEMV_THREADS, smem, s>>>(ring16, st, Dp, q64, nb, cta, b0, margin_rel, sm, tail, app);
   return cudaGetLastError();
 }
 
 template <int NJ>
-static cudaError_t launch_nj(const __half* ring16, const RingState* d_state, int Dp, const double* q64, int nb,
+static cudaError_t launch_nj(const __half* ring16, const RingState& st, int Dp, const double* q64, int nb,
                              CtaRec* cta, int b0, int grid, float margin_rel, ShardMap sm, const GemvTail& tail,
-                             cudaStream_t s) {
-  if (nb == 1) return launch_one<NJ, 1>(ring16, d_state, Dp, q64, nb, cta, b0, grid, margin_rel, sm, tail, s);
-  if (nb == 2) return launch_one<NJ, 2>(ring16, d_state, Dp, q64, nb, cta, b0, grid, margin_rel, sm, tail, s);
-  return launch_one<NJ, 4>(ring16, d_state, Dp, q64, nb, cta, b0, grid, margin_rel, sm, tail, s);
+                             const GemvAppend& app, cudaStream_t s) {
+  if (nb == 1) return launch_one<NJ, 1>(ring16, st, Dp, q64, nb, cta, b0, grid, margin_rel, sm, tail, app, s);
+  if (nb == 2) return launch_one<NJ, 2>(ring16, st, Dp, q64, nb, cta, b0, grid, margin_rel, sm, tail, app, s);
+  return launch_one<NJ, 4>(ring16, st, Dp, q64, nb, cta, b0, grid, margin_rel, sm, tail, app, s);
 }
 
-cudaError_t launch_gemv_scan(const __half* ring16, const RingState* d_state, int D, int Dp, const double* q64,
-                             int nb, CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter,
+unsigned long long* gemv_timing_buffer();
+
+cudaError_t launch_gemv_scan(const __half* ring16, const RingState& st, int D, int Dp, const double* q64, int nb,
+                             CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
                              const double* ring64, const Thresholds& thr, mc_record* rec, OutRec* out,
-                             cudaStream_t s) {
+                             const GemvAppendArgs& a, cudaStream_t s) {
   const int nj = (Dp / 8 + 31) / 32;
   if (nb < 1 || nb > 4) return cudaErrorInvalidValue;
-  GemvTail tail{counter, ring64, D, gemv_eps_rel(Dp), eps_abs1(), thr, rec, out};
+  GemvTail tail{counter, gmax, ring64, D, gemv_eps_rel(Dp), eps_abs1(), thr, rec, out, gemv_timing_buffer()};
+  GemvAppend app{a.stage, a.n, a.first_slot, a.ring16, a.ring64, a.d_state};
   const float mrel = 1e-6f;  // slack for the fp32 arithmetic of the admission test
+#define MC_GEMV_CASE(NJV) return launch_nj<NJV>(ring16, st, Dp, q64, nb, cta, b0, grid, mrel, sm, tail, app, s)
   switch (nj) {
-    case 1: return launch_nj<1>(ring16, d_state, Dp, q64, nb, cta, b0, grid, mrel, sm, tail, s);
-    case 2: return launch_nj<2>(ring16, d_state, Dp, q64, nb, cta, b0, grid, mrel, sm, tail, s);
-    case 3: return launch_nj<3>(ring16, d_state, Dp, q64, nb, cta, b0, grid, mrel, sm, tail, s);
-    case 4: return launch_nj<4>(ring16, d_state, Dp, q64, nb, cta, b0, grid, mrel, sm, tail, s);
-    case 5: case 6: return launch_nj<6>(ring16, d_state, Dp, q64, nb, cta, b0, grid, mrel, sm, tail, s);
-    case 7: case 8: return launch_nj<8>(ring16, d_state, Dp, q64, nb, cta, b0, grid, mrel, sm, tail, s);
+    case 1: MC_GEMV_CASE(1);
+    case 2: MC_GEMV_CASE(2);
+    case 3: MC_GEMV_CASE(3);
+    case 4: MC_GEMV_CASE(4);
+    case 5: case 6: MC_GEMV_CASE(6);
+    case 7: case 8: MC_GEMV_CASE(8);
     default:
-      if (nj <= 12) return launch_nj<12>(ring16, d_state, Dp, q64, nb, cta, b0, grid, mrel, sm, tail, s);
-      if (nj <= 16) return launch_nj<16>(ring16, d_state, Dp, q64, nb, cta, b0, grid, mrel, sm, tail, s);
+      if (nj <= 12) MC_GEMV_CASE(12);
+      if (nj <= 16) MC_GEMV_CASE(16);
       return cudaErrorInvalidValue;
   }
+#undef MC_GEMV_CASE
 }
 
 // fp32 accumulation depth of one GEMV score: NJ*8 sequential FMAs + 5 butterfly adds.

@@ -35,3 +35,16 @@ Q = wl.queries(B * a.iters).reshape(a.iters, B, dim)
 for i in range(a.iters):
     live, sim, k, flags = ring.retrieve(Q[i])
 print(a.case, "ok", ring.stats())
+
+import os  # noqa: E402
+if os.environ.get("MC_GEMV_TIMING"):
+    import ctypes  # noqa: E402
+    lib = _native.load()
+    lib.mc_debug_gemv_timing.restype = ctypes.c_int
+    t = (ctypes.c_ulonglong * 4)()
+    for i in range(a.iters):
+        lib.mc_debug_gemv_timing(t, 1)  # reset
+        ring.retrieve(Q[i])
+        lib.mc_debug_gemv_timing(t, 0)
+        print("gemv phases (us): scan %.1f  rescore %.1f  tail %.1f  total %.1f" % (
+            (t[1] - t[0]) / 1e3, (t[2] - t[1]) / 1e3, (t[3] - t[2]) / 1e3, (t[3] - t[0]) / 1e3))
