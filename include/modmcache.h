@@ -121,6 +121,12 @@ int mc_merge_records(mc_cache* h, const void* dev_records, int32_t G, int32_t B,
 int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int32_t B, int32_t iters,
                      int64_t flush_bytes, double* out_ms, int64_t* out_counts);
 
+/* Measurement hook, active only when MC_GEMV_TIMING=1 was set before the first
+ * lookup: reads (reset = 0) or resets (reset = 1) four globaltimer stamps of the
+ * last GEMV launch(es): first CTA start, last scan end, last rescoring end,
+ * tail end (ns).  Not needed by the drop-in; used by scripts/profile_case.py. */
+int mc_debug_gemv_timing(unsigned long long* out4, int reset);
+
 /* Counters since creation: [0] lookups, [1] certificate fallbacks,
  * [2] non-finite queries, [3] exact ties, [4] candidates rescored,
  * [5] GEMV launches, [6] GEMM launches, [7] kernel launches total. */

@@ -2,17 +2,21 @@
 
 Exports mirror pkg/src/mixserve/__init__.py:15-24 for the cache symbols.
 """
-from .cache import (
+from .cache import SemanticCache
+from .records import (
     DEFAULT_DIM,
     DEFAULT_THRESHOLDS,
     LARGE,
+    NORM_TOL,
     POLICIES,
+    POLICY_ALL,
+    POLICY_DISABLED,
+    POLICY_LARGE,
     SMALL,
     STEP_CHOICES,
     CacheEntry,
     EmbeddingError,
     RetrievalResult,
-    SemanticCache,
     ThresholdTable,
     cosine,
     is_normalized,
@@ -22,4 +26,4 @@ from .cache import (
     validate_sigma_schedule,
 )
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"

@@ -29,7 +29,7 @@ RECORD_DTYPE = np.dtype([("sim", "<f8"), ("second", "<f8"), ("pos", "<i8"), ("fl
 EXPORTED = (
     "mc_create", "mc_destroy", "mc_set_thresholds", "mc_append", "mc_evict_front", "mc_size",
     "mc_retrieve_batch", "mc_set_path", "mc_configure_shard", "mc_retrieve_local_async",
-    "mc_merge_records", "mc_stats", "mc_last_error", "mc_version", "mc_profile_steps",
+    "mc_merge_records", "mc_stats", "mc_last_error", "mc_version", "mc_profile_steps", "mc_debug_gemv_timing",
 )
 
 
@@ -56,6 +56,7 @@ def _declare(lib):
     lib.mc_merge_records.argtypes = [vp, vp, i32, i32, i64, vp, dp, dp, dp, dp]
     lib.mc_stats.argtypes = [vp, dp]
     lib.mc_profile_steps.argtypes = [vp, dp, dp, i32, i32, i64, dp, dp]
+    lib.mc_debug_gemv_timing.argtypes = [dp, i32]
     lib.mc_last_error.restype = C.c_char_p
     lib.mc_version.restype = C.c_char_p
     return lib
@@ -101,6 +102,9 @@ class DeviceRing:
         h = C.c_void_p()
         _check(self.lib, self.lib.mc_create(C.byref(h), self.capacity, self.dim, self.device))
         self._h = h
+        self._hv = h.value  # plain int handle for the per-call fast paths
+        self._append = self.lib.mc_append
+        self._retrieve = self.lib.mc_retrieve_batch
         self._bcap = 0
         self._ensure_out(1)
         self._table_key = None
@@ -139,6 +143,14 @@ class DeviceRing:
         n = rows.shape[0] if rows.ndim == 2 else 1
         _check(self.lib, self.lib.mc_append(self._h, _ptr(rows), n))
 
+    def append1(self, row: np.ndarray) -> None:
+        """One float64 row (the per-insert path: no copy for contiguous float64 input)."""
+        if row.dtype != np.float64 or not row.flags.c_contiguous:
+            row = np.ascontiguousarray(row, dtype=np.float64)
+        rc = self._append(self._hv, row.ctypes.data, 1)
+        if rc:
+            _check(self.lib, rc)
+
     def evict_front(self, n: int) -> None:
         if n:
             _check(self.lib, self.lib.mc_evict_front(self._h, int(n)))
@@ -155,6 +167,9 @@ class DeviceRing:
         self._sim = np.empty(cap, dtype=np.float64)
         self._k = np.empty(cap, dtype=np.int32)
         self._flags = np.empty(cap, dtype=np.uint32)
+        self._qbuf = np.zeros((cap, self.dim), dtype=np.float64)
+        self._out_ptrs = tuple(a.ctypes.data for a in (self._live, self._sim, self._k, self._flags))
+        self._qptr = self._qbuf.ctypes.data
         self._bcap = cap
 
     def retrieve(self, Q: np.ndarray):
@@ -162,9 +177,16 @@ class DeviceRing:
         Q = np.ascontiguousarray(Q, dtype=np.float64)
         B = Q.shape[0]
         self._ensure_out(B)
-        _check(self.lib, self.lib.mc_retrieve_batch(
-            self._h, _ptr(Q), B, _ptr(self._live), _ptr(self._sim), _ptr(self._k), _ptr(self._flags)))
+        _check(self.lib, self.lib.mc_retrieve_batch(self._h, _ptr(Q), B, *self._out_ptrs))
         return self._live[:B], self._sim[:B], self._k[:B], self._flags[:B]
+
+    def retrieve1(self, q: np.ndarray):
+        """One query (1-d, length dim) -> (live, sim, k, flags) as Python scalars."""
+        self._qbuf[0] = q  # copies and converts; the buffer pointer never changes
+        rc = self._retrieve(self._hv, self._qptr, 1, *self._out_ptrs)
+        if rc:
+            _check(self.lib, rc)
+        return int(self._live[0]), float(self._sim[0]), int(self._k[0]), int(self._flags[0])
 
     def retrieve_local_async(self, Q: np.ndarray, dev_records_ptr: int, stream_ptr: int = 0) -> None:
         Q = np.ascontiguousarray(Q, dtype=np.float64)

@@ -1,9 +1,16 @@
 // C ABI of libmodmcache.so (declared in include/modmcache.h).
 //
-// Host side of the device ring: owns the CUDA stream, the device buffers,
-// the pinned staging buffers, and a host mirror of the ring window that is
-// published to the device on every flush.  Every call is serialised by the
-// handle's mutex ("many readers or one writer", cache.py:144).
+// Host side of the device ring: owns the CUDA stream, the device buffers, a
+// pinned "envelope" and a host mirror of the ring window.  Every call is
+// serialised by the handle's mutex ("many readers or one writer", cache.py:144).
+//
+// The envelope is the only host->device path of the hot loop:
+//   h_env / d_env  [env_rows][Dp] float64, zero-padded columns
+//   rows [0, n_pending)            pending FIFO appends (mc_append stages here)
+//   rows [n_pending, n_pending+B)  the lookup's queries
+// A lookup is one H2D copy of the used prefix, one fused GEMV launch (append +
+// scan + certified rescoring + decision) or the tensor-core sequence, one D2H
+// copy of the decisions and one stream synchronisation.
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -55,33 +62,28 @@ struct mc_cache {
   double* ring64 = nullptr;
   RingState* d_state = nullptr;
 
-  // append staging
-  long long stage_cap = 0;
-  double* h_stage = nullptr;  // pinned [stage_cap][D]
-  double* d_stage = nullptr;  // [stage_cap][Dp]
+  // envelope: pending appends, then queries (see the header comment)
+  long long stage_cap = 0;  // pending rows before a forced flush
+  int Bcap = 0;             // query rows
+  double* h_env = nullptr;  // pinned [stage_cap + Bcap][Dp]
+  double* d_env = nullptr;  // [stage_cap + Bcap][Dp]
   long long n_pending = 0;
   long long pending_first_slot = 0;
-  cudaEvent_t stage_ev = nullptr;
-  bool stage_inflight = false;
+  cudaEvent_t env_ev = nullptr;  // last async upload of the envelope (async paths only)
+  bool env_inflight = false;
 
-  // per-batch buffers
-  int Bcap = 0;
-  double* h_q = nullptr;   // pinned [Bcap][D]
-  double* d_q64 = nullptr; // [Bcap][Dp]
+  // per-batch device buffers
   float* d_part_s = nullptr;
   long long* d_part_p = nullptr;
   float* d_part_floor = nullptr;
-  int part_chunks = 0;
-  CtaRec* d_cta = nullptr;  // [Bcap][gemv grid] per-CTA exact records (GEMV path)
+  CtaRec* d_cta = nullptr;     // [Bcap][gemv grid] per-CTA exact records (GEMV path)
   unsigned* d_gmax = nullptr;  // [Bcap] running max keys of the fused GEMV scan (zero between launches)
   mc_record* d_rec = nullptr;
   mc_record* d_scratch = nullptr;
   OutRec* d_out = nullptr;
   OutRec* h_out = nullptr;  // pinned
-  cudaEvent_t q_ev = nullptr;
-  bool q_inflight = false;
 
-  TcPlan* tc = nullptr;  // tensor-core scan plan, created on first batched lookup
+  TcPlan* tc = nullptr;           // tensor-core scan plan, created on first batched lookup
   unsigned* d_counter = nullptr;  // last-CTA ticket of the fused GEMV scan (zero between launches)
 
   Thresholds thr{};
@@ -104,9 +106,17 @@ struct DeviceGuard {
   }
 };
 
+RingState mirror(const mc_cache* h) { return RingState{h->head, h->count, h->jhead, h->C}; }
+
+int wait_env(mc_cache* h) {
+  if (h->env_inflight) {
+    CU(cudaEventSynchronize(h->env_ev));
+    h->env_inflight = false;
+  }
+  return MC_OK;
+}
+
 void free_batch(mc_cache* h) {
-  cudaFreeHost(h->h_q);
-  cudaFree(h->d_q64);
   cudaFree(h->d_part_s);
   cudaFree(h->d_part_p);
   cudaFree(h->d_part_floor);
@@ -116,8 +126,6 @@ void free_batch(mc_cache* h) {
   cudaFree(h->d_scratch);
   cudaFree(h->d_out);
   cudaFreeHost(h->h_out);
-  h->h_q = nullptr;
-  h->d_q64 = nullptr;
   h->d_part_s = nullptr;
   h->d_part_p = nullptr;
   h->d_part_floor = nullptr;
@@ -127,20 +135,33 @@ void free_batch(mc_cache* h) {
   h->d_scratch = nullptr;
   h->d_out = nullptr;
   h->h_out = nullptr;
-  h->Bcap = 0;
 }
 
+// Grow the query capacity to >= B (power of two): per-batch buffers and the
+// envelope, whose pending rows are carried over.
 int ensure_batch(mc_cache* h, int B) {
   if (B <= h->Bcap) return MC_OK;
   CU(cudaStreamSynchronize(h->stream));
+  h->env_inflight = false;
   free_batch(h);
-  int cap = 1;
+  int cap = 4;
   while (cap < B) cap <<= 1;
-  cap = std::max(cap, 4);
   const int chunks = std::max(gemv_grid(h->sm_count), exact_grid(h->sm_count));
-  CU(cudaMallocHost(&h->h_q, (size_t)cap * h->D * sizeof(double)));
-  CU(cudaMalloc(&h->d_q64, (size_t)cap * h->Dp * sizeof(double)));
-  CU(cudaMemset(h->d_q64, 0, (size_t)cap * h->Dp * sizeof(double)));
+  const size_t row = (size_t)h->Dp * sizeof(double);
+  const size_t env_rows = (size_t)h->stage_cap + cap;
+  double* h_env = nullptr;
+  double* d_env = nullptr;
+  CU(cudaMallocHost(&h_env, env_rows * row));
+  memset(h_env, 0, env_rows * row);
+  if (h->h_env) {
+    memcpy(h_env, h->h_env, (size_t)h->n_pending * row);
+    cudaFreeHost(h->h_env);
+    cudaFree(h->d_env);
+  }
+  h->h_env = h_env;
+  CU(cudaMalloc(&d_env, env_rows * row));
+  CU(cudaMemsetAsync(d_env, 0, env_rows * row, h->stream));
+  h->d_env = d_env;
   CU(cudaMalloc(&h->d_part_s, (size_t)cap * chunks * KP * sizeof(float)));
   CU(cudaMalloc(&h->d_part_p, (size_t)cap * chunks * KP * sizeof(long long)));
   CU(cudaMalloc(&h->d_part_floor, (size_t)cap * chunks * sizeof(float)));
@@ -151,74 +172,70 @@ int ensure_batch(mc_cache* h, int B) {
   CU(cudaMalloc(&h->d_scratch, (size_t)cap * exact_grid(h->sm_count) * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_out, (size_t)cap * sizeof(OutRec)));
   CU(cudaMallocHost(&h->h_out, (size_t)cap * sizeof(OutRec)));
-  h->part_chunks = chunks;
   h->Bcap = cap;
   return MC_OK;
 }
 
-RingState mirror(const mc_cache* h) { return RingState{h->head, h->count, h->jhead, h->C}; }
-
-// Largest pending-append batch folded into a GEMV launch; larger flushes use k_append.
-constexpr long long FUSE_APPEND_MAX = 256;
-
-// Copy pending appends to the device stage (stream-ordered) and describe them.
-int stage_pending(mc_cache* h, GemvAppendArgs& a) {
-  a = GemvAppendArgs{};
+// Pending appends as a fused-append descriptor over device rows `dev_rows`
+// (the uploaded envelope prefix).  Clears the host pending state.
+GemvAppendArgs take_pending(mc_cache* h, const double* dev_rows) {
+  GemvAppendArgs a;
   a.ring16 = h->ring16;
   a.ring64 = h->ring64;
   a.d_state = h->d_state;
   if (h->n_pending > 0) {
-    const long long nw = std::min(h->n_pending, h->C);
+    const long long nw = std::min(h->n_pending, h->C);  // older rows were displaced before landing
     const long long skip = h->n_pending - nw;
-    CU(cudaMemcpy2DAsync(h->d_stage, (size_t)h->Dp * sizeof(double), h->h_stage + (size_t)skip * h->D,
-                         (size_t)h->D * sizeof(double), (size_t)h->D * sizeof(double), (size_t)nw,
-                         cudaMemcpyHostToDevice, h->stream));
-    CU(cudaEventRecord(h->stage_ev, h->stream));
-    h->stage_inflight = true;
-    a.stage = h->d_stage;
+    a.stage = dev_rows + (size_t)skip * h->Dp;
     a.n = nw;
     a.first_slot = (h->pending_first_slot + skip) % h->C;
   }
   h->n_pending = 0;
   h->state_dirty = false;
-  return MC_OK;
+  return a;
 }
 
-// Publish pending appends / evictions to the device with k_append (stream-ordered).
-int flush(mc_cache* h) {
-  if (h->n_pending == 0 && !h->state_dirty) return MC_OK;
-  GemvAppendArgs a;
-  int rc = stage_pending(h, a);
+// Upload the envelope prefix: pending rows, then B queries (row-major, stride D).
+int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse) {
+  int rc = wait_env(h);
   if (rc) return rc;
-  CU(launch_append(h->d_stage, a.n, a.first_slot, mirror(h), h->D, h->Dp, h->ring16, h->ring64, h->d_state,
-                   h->stream));
-  h->stats[7]++;
-  return MC_OK;
-}
-
-int wait_q(mc_cache* h) {
-  if (h->q_inflight) {
-    CU(cudaEventSynchronize(h->q_ev));
-    h->q_inflight = false;
+  const size_t row = (size_t)h->Dp * sizeof(double);
+  double* qdst = h->h_env + (size_t)h->n_pending * h->Dp;
+  if (h->D == h->Dp) {
+    memcpy(qdst, queries, (size_t)B * row);
+  } else {
+    for (int b = 0; b < B; ++b) memcpy(qdst + (size_t)b * h->Dp, queries + (size_t)b * h->D, h->D * sizeof(double));
+  }
+  CU(cudaMemcpyAsync(h->d_env, h->h_env, (size_t)(h->n_pending + B) * row, cudaMemcpyHostToDevice, h->stream));
+  if (async_reuse) {  // the caller returns before the copy completes
+    CU(cudaEventRecord(h->env_ev, h->stream));
+    h->env_inflight = true;
   }
   return MC_OK;
 }
 
-// Upload B queries (row-major, stride D) into d_q64 (stride Dp).
-int upload_queries(mc_cache* h, const double* queries, int B) {
-  int rc = wait_q(h);
+// Publish pending appends / evictions with k_append (stream-ordered).  Used
+// when the pending batch is too large to ride along with a lookup.
+int flush(mc_cache* h) {
+  if (h->n_pending == 0 && !h->state_dirty) return MC_OK;
+  int rc = wait_env(h);
   if (rc) return rc;
-  memcpy(h->h_q, queries, (size_t)B * h->D * sizeof(double));
-  CU(cudaMemcpy2DAsync(h->d_q64, (size_t)h->Dp * sizeof(double), h->h_q, (size_t)h->D * sizeof(double),
-                       (size_t)h->D * sizeof(double), (size_t)B, cudaMemcpyHostToDevice, h->stream));
-  CU(cudaEventRecord(h->q_ev, h->stream));
-  h->q_inflight = true;
+  if (h->n_pending > 0)
+    CU(cudaMemcpyAsync(h->d_env, h->h_env, (size_t)h->n_pending * h->Dp * sizeof(double), cudaMemcpyHostToDevice,
+                       h->stream));
+  const GemvAppendArgs a = take_pending(h, h->d_env);
+  CU(launch_append(a.stage, a.n, a.first_slot, mirror(h), h->D, h->Dp, h->ring16, h->ring64, h->d_state, h->stream));
+  CU(cudaEventRecord(h->env_ev, h->stream));
+  h->env_inflight = true;
+  h->stats[7]++;
   return MC_OK;
 }
 
 // Batch size from which the tensor-core scan replaces the GEMV scan: the GEMV
 // kernel reads the ring once per 4 queries, the tcgen05 scan once per batch.
 constexpr int GEMM_MIN_B = 5;
+// Largest pending-append batch folded into a GEMV launch; larger ones use k_append.
+constexpr long long FUSE_APPEND_MAX = 256;
 
 bool use_gemm(const mc_cache* h, int B) {
   return h->path == MC_PATH_GEMM || h->path == MC_PATH_GEMM_1SM || (h->path == MC_PATH_AUTO && B >= GEMM_MIN_B);
@@ -235,22 +252,20 @@ int ensure_tc(mc_cache* h, int B) {
   return MC_OK;
 }
 
-// Scan + certified merge for B queries at q64 (stride Dp): records into rec[0..B)
-// and, when out != nullptr, decisions into out[0..B).  GEMV: one fused launch
-// per 4 queries.  Tensor cores: prep + scan, then the merge kernel (+ decision).
+// Scan + certified merge for B queries at q64 (device, stride Dp): records
+// into rec[0..B) and, when out != nullptr, decisions into out[0..B).  `app`
+// describes appends already on the device that precede the scan (folded into
+// the first GEMV launch, or applied by k_append before a tensor-core scan).
 // t_mid (optional) is recorded between the scan and the standalone merge.
-// `pre`: appends already resident on the device (profiling), applied before the scan.
-int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* out, cudaEvent_t t_mid = nullptr,
-               const GemvAppendArgs* pre = nullptr) {
+int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
+               cudaEvent_t t_mid = nullptr) {
   if (use_gemm(h, B)) {
-    int rc = flush(h);
-    if (rc) return rc;
-    if (pre && pre->n > 0) {
-      CU(launch_append(pre->stage, pre->n, pre->first_slot, mirror(h), h->D, h->Dp, h->ring16, h->ring64,
-                       h->d_state, h->stream));
+    if (app.n > 0) {
+      CU(launch_append(app.stage, app.n, app.first_slot, mirror(h), h->D, h->Dp, h->ring16, h->ring64, h->d_state,
+                       h->stream));
       h->stats[7]++;
     }
-    rc = ensure_tc(h, B);
+    int rc = ensure_tc(h, B);
     if (rc) return rc;
     tc_set_pair(h->tc, h->path != MC_PATH_GEMM_1SM);
     const Partials part{h->d_part_s, h->d_part_p, h->d_part_floor, tc_chunks(h->tc, B)};
@@ -266,34 +281,37 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
     }
     return MC_OK;
   }
-  // GEMV: small pending-append batches ride along with the first launch.
-  GemvAppendArgs app;
-  if (h->n_pending > FUSE_APPEND_MAX) {
-    int rc = flush(h);
-    if (rc) return rc;
-  }
-  int rc = stage_pending(h, app);
-  if (rc) return rc;
-  if (pre && pre->n > 0) {
-    if (app.n > 0) {  // host-staged rows first, then the device-resident ones
-      CU(launch_append(app.stage, app.n, app.first_slot, mirror(h), h->D, h->Dp, h->ring16, h->ring64, h->d_state,
-                       h->stream));
-      h->stats[7]++;
-    }
-    app = *pre;
-  }
+  GemvAppendArgs a = app;
   const RingState st = mirror(h);
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nb = std::min(4, B - b0);
     CU(launch_gemv_scan(h->ring16, st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
-                        gemv_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax, h->ring64, h->thr, rec, out, app,
+                        gemv_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax, h->ring64, h->thr, rec, out, a,
                         h->stream));
-    app.n = 0;  // written by the first launch
+    a.n = 0;  // written by the first launch
     h->stats[5]++;
     h->stats[7]++;
   }
   if (t_mid) CU(cudaEventRecord(t_mid, h->stream));
   return MC_OK;
+}
+
+// Stage + upload + scan for B host queries; on return the records (and
+// decisions) are enqueued, not complete.  Returns the device query pointer.
+// The caller has run ensure_batch(h, B) (rec / out may be handle buffers).
+int lookup_enqueue(mc_cache* h, const double* queries, int B, mc_record* rec, OutRec* out, bool async_reuse,
+                   const double** q_dev) {
+  int rc;
+  if (h->n_pending > FUSE_APPEND_MAX) {
+    rc = flush(h);
+    if (rc) return rc;
+  }
+  rc = upload_envelope(h, queries, B, async_reuse);
+  if (rc) return rc;
+  const double* q = h->d_env + (size_t)h->n_pending * h->Dp;
+  const GemvAppendArgs app = take_pending(h, h->d_env);
+  *q_dev = q;
+  return scan_merge(h, q, B, rec, out, app);
 }
 
 int copy_out(mc_cache* h, int B, int64_t* out_live, double* out_sim, int32_t* out_k, uint32_t* out_flags) {
@@ -318,7 +336,7 @@ extern "C" {
 
 const char* mc_last_error(void) { return g_err.c_str(); }
 
-const char* mc_version(void) { return "modmcache 0.1.0 (sm_100a)"; }
+const char* mc_version(void) { return "modmcache 0.2.0 (sm_100a)"; }
 
 int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   if (!out) return fail(MC_ERR_ARG, "out is NULL");
@@ -351,8 +369,7 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
       return cleanup(fail(MC_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_))); \
   } while (0)
   CUC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-  CUC(cudaEventCreateWithFlags(&h->stage_ev, cudaEventDisableTiming));
-  CUC(cudaEventCreateWithFlags(&h->q_ev, cudaEventDisableTiming));
+  CUC(cudaEventCreateWithFlags(&h->env_ev, cudaEventDisableTiming));
   const size_t n16 = (size_t)h->C * h->Dp * sizeof(__half);
   const size_t n64 = (size_t)h->C * h->Dp * sizeof(double);
   CUC(cudaMalloc(&h->ring16, n16));
@@ -360,16 +377,13 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   CUC(cudaMemsetAsync(h->ring16, 0, n16, h->stream));
   CUC(cudaMemsetAsync(h->ring64, 0, n64, h->stream));
   CUC(cudaMalloc(&h->d_state, sizeof(RingState)));
-  CUC(cudaMalloc(&h->d_counter, sizeof(unsigned)));
-  CUC(cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned), h->stream));
   {
     RingState z{0, 0, 0, h->C};
     CUC(cudaMemcpyAsync(h->d_state, &z, sizeof z, cudaMemcpyHostToDevice, h->stream));
   }
-  h->stage_cap = std::max<long long>(1, std::min<long long>(h->C, (16ll << 20) / ((long long)h->D * 8)));
-  CUC(cudaMallocHost(&h->h_stage, (size_t)h->stage_cap * h->D * sizeof(double)));
-  CUC(cudaMalloc(&h->d_stage, (size_t)h->stage_cap * h->Dp * sizeof(double)));
-  CUC(cudaMemsetAsync(h->d_stage, 0, (size_t)h->stage_cap * h->Dp * sizeof(double), h->stream));
+  CUC(cudaMalloc(&h->d_counter, sizeof(unsigned)));
+  CUC(cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned), h->stream));
+  h->stage_cap = std::max<long long>(1, std::min<long long>(h->C, (16ll << 20) / ((long long)h->Dp * 8)));
   rc = ensure_batch(h, 4);
   if (rc) return cleanup(rc);
   static const int ks[6] = {5, 10, 15, 20, 25, 30};
@@ -394,14 +408,13 @@ int mc_destroy(mc_cache* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     free_batch(h);
     tc_plan_destroy(h->tc);
+    cudaFreeHost(h->h_env);
+    cudaFree(h->d_env);
     cudaFree(h->ring16);
     cudaFree(h->ring64);
     cudaFree(h->d_state);
     cudaFree(h->d_counter);
-    cudaFreeHost(h->h_stage);
-    cudaFree(h->d_stage);
-    if (h->stage_ev) cudaEventDestroy(h->stage_ev);
-    if (h->q_ev) cudaEventDestroy(h->q_ev);
+    if (h->env_ev) cudaEventDestroy(h->env_ev);
     if (h->stream) cudaStreamDestroy(h->stream);
   }
   delete h;
@@ -454,9 +467,9 @@ int mc_append(mc_cache* h, const double* rows, int64_t n) {
       int rc = flush(h);
       if (rc) return rc;
     }
-    if (h->n_pending == 0 && h->stage_inflight) {
-      CU(cudaEventSynchronize(h->stage_ev));
-      h->stage_inflight = false;
+    if (h->n_pending == 0) {
+      int rc = wait_env(h);  // the previous flush may still be reading the envelope
+      if (rc) return rc;
     }
     if (h->count == h->C) {  // append-then-evict of cache.py:230-233, evicting first
       h->head = (h->head + 1) % h->C;
@@ -465,7 +478,7 @@ int mc_append(mc_cache* h, const double* rows, int64_t n) {
     }
     const long long slot = (h->head + h->count) % h->C;
     if (h->n_pending == 0) h->pending_first_slot = slot;
-    memcpy(h->h_stage + (size_t)h->n_pending * h->D, rows + (size_t)i * h->D, (size_t)h->D * sizeof(double));
+    memcpy(h->h_env + (size_t)h->n_pending * h->Dp, rows + (size_t)i * h->D, (size_t)h->D * sizeof(double));
     h->n_pending++;
     h->count++;
     h->appended++;
@@ -504,19 +517,18 @@ int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* ou
     h->stats[0] += B;
     return MC_OK;
   }
-  int rc = ensure_batch(h, B);
+  int rc = ensure_batch(h, B);  // may reallocate d_rec / d_out: evaluate them after
   if (rc) return rc;
-  rc = upload_queries(h, queries, B);
-  if (rc) return rc;
-  rc = scan_merge(h, h->d_q64, B, h->d_rec, h->d_out);
+  const double* q = nullptr;
+  rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_out, false, &q);
   if (rc) return rc;
   CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
-  h->q_inflight = false;
+  h->env_inflight = false;
   bool need = false;
   for (int b = 0; b < B; ++b) need |= (h->h_out[b].flags & FLAG_NEED_ANY) != 0;
   if (need) {  // rare: certificate failed or exotic query -> exact rescan, then decide again
-    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, h->d_q64, B, h->d_rec, h->d_scratch,
+    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, q, B, h->d_rec, h->d_scratch,
                            exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
     CU(launch_finalize(h->d_rec, 1, B, -1, h->d_state, h->thr, h->d_out, h->stream));
     h->stats[7] += 3;
@@ -532,18 +544,17 @@ int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void*
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard guard(h->dev);
   mc_record* rec = static_cast<mc_record*>(dev_records);
-  int rc = ensure_batch(h, B);
-  if (rc) return rc;
-  rc = upload_queries(h, queries, B);
-  if (rc) return rc;
+  int rc0 = ensure_batch(h, B);
+  if (rc0) return rc0;
   if (h->count == 0) {
-    rc = flush(h);
+    int rc = flush(h);
     if (rc) return rc;
     CU(cudaMemsetAsync(rec, 0xff, (size_t)B * sizeof(mc_record), h->stream));  // pos = -1 (NaN sims)
   } else {
-    rc = scan_merge(h, h->d_q64, B, rec, nullptr);
+    const double* q = nullptr;
+    int rc = lookup_enqueue(h, queries, B, rec, nullptr, true, &q);
     if (rc) return rc;
-    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, h->d_q64, B, rec, h->d_scratch,
+    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, q, B, rec, h->d_scratch,
                            exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
     h->stats[7] += 2;
   }
@@ -632,26 +643,25 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
   for (int it = 0; it < iters; ++it) {
     if (d_flush) CUP(cudaMemsetAsync(d_flush, it & 0xff, (size_t)flush_bytes, h->stream));
     CUP(cudaEventRecord(ev[(size_t)it * nev + 0], h->stream));
-    GemvAppendArgs pre;
-    if (rows) {
+    GemvAppendArgs app;
+    app.ring16 = h->ring16;
+    app.ring64 = h->ring64;
+    app.d_state = h->d_state;
+    if (rows) {  // one FIFO insert per step, already resident on the device
       if (h->count == h->C) {
         h->head = (h->head + 1) % h->C;
         h->count--;
         h->jhead++;
       }
-      const long long slot = (h->head + h->count) % h->C;
+      app.stage = d_rows + (size_t)it * h->Dp;
+      app.n = 1;
+      app.first_slot = (h->head + h->count) % h->C;
       h->count++;
       h->appended++;
-      pre.stage = d_rows + (size_t)it * h->Dp;
-      pre.n = 1;
-      pre.first_slot = slot;
-      pre.ring16 = h->ring16;
-      pre.ring64 = h->ring64;
-      pre.d_state = h->d_state;
     }
     CUP(cudaEventRecord(ev[(size_t)it * nev + 1], h->stream));
     const double* q = d_qall + (size_t)it * B * h->Dp;
-    rc = scan_merge(h, q, B, h->d_rec, d_outs + (size_t)it * B, ev[(size_t)it * nev + 2], rows ? &pre : nullptr);
+    rc = scan_merge(h, q, B, h->d_rec, d_outs + (size_t)it * B, app, ev[(size_t)it * nev + 2]);
     if (rc) {
       release();
       return rc;

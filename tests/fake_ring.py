@@ -33,6 +33,13 @@ class FakeRing:
             self.rows.append(r.copy())
             self.appends += 1
 
+    def append1(self, row):
+        self.append(row)
+
+    def retrieve1(self, q):
+        live, sim, k, flags = self.retrieve(np.asarray(q, dtype=np.float64)[None, :])
+        return int(live[0]), float(sim[0]), int(k[0]), int(flags[0])
+
     def evict_front(self, n):
         assert 0 <= n <= len(self.rows)
         del self.rows[:n]
