@@ -188,16 +188,28 @@ class DeviceRing:
             _check(self.lib, rc)
         return int(self._live[0]), float(self._sim[0]), int(self._k[0]), int(self._flags[0])
 
-    def retrieve_local_async(self, Q: np.ndarray, dev_records_ptr: int, stream_ptr: int = 0) -> None:
+    def records_device(self):
+        """Device that holds this ring's records (for the collective's buffers)."""
+        import torch
+
+        return torch.device("cuda", self.device)
+
+    @staticmethod
+    def _addr(buf) -> int:
+        return buf if isinstance(buf, int) else buf.data_ptr()
+
+    def retrieve_local_async(self, Q: np.ndarray, dev_records, stream_ptr: int = 0) -> None:
+        """This shard's certified best per query -> B mc_records in device memory (a torch
+        uint8 tensor of B*32 bytes, or a raw pointer), ordered before `stream`."""
         Q = np.ascontiguousarray(Q, dtype=np.float64)
-        _check(self.lib, self.lib.mc_retrieve_local_async(self._h, _ptr(Q), Q.shape[0], dev_records_ptr,
+        _check(self.lib, self.lib.mc_retrieve_local_async(self._h, _ptr(Q), Q.shape[0], self._addr(dev_records),
                                                           stream_ptr or None))
 
-    def merge_records(self, dev_records_ptr: int, G: int, B: int, p0: int, stream_ptr: int = 0):
+    def merge_records(self, dev_records, G: int, B: int, p0: int, stream_ptr: int = 0):
+        """Merge G x B gathered records (shard-major) into decisions; p0 = oldest live global position."""
         self._ensure_out(B)
         _check(self.lib, self.lib.mc_merge_records(
-            self._h, dev_records_ptr, int(G), int(B), int(p0), stream_ptr or None,
-            _ptr(self._live), _ptr(self._sim), _ptr(self._k), _ptr(self._flags)))
+            self._h, self._addr(dev_records), int(G), int(B), int(p0), stream_ptr or None, *self._out_ptrs))
         return self._live[:B], self._sim[:B], self._k[:B], self._flags[:B]
 
     def profile_steps(self, Q: np.ndarray, rows: np.ndarray | None, iters: int, flush_bytes: int):

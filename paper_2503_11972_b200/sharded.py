@@ -1,0 +1,207 @@
+"""Entry-sharded cache across GPUs: one process per GPU, records merged over NCCL.
+
+Layout.  Global append position p (0, 1, 2, ... over the
+cache's lifetime) decides the owner: shard g of G stores p ≡ g (mod G), as
+local row j = p // G of its device ring (``mc_configure_shard``).  Every rank
+keeps the full metadata deque (the reference's ``_store``, cache.py:164), so
+validation, eviction decisions and the returned ``CacheEntry`` objects are
+identical on all ranks; only the embeddings are divided.
+
+A lookup is SPMD: every rank passes the same query batch, scans its shard
+with the certified local scan (``mc_retrieve_local_async`` -> one 32-byte
+``mc_record`` per query: exact float64 best, runner-up, global position,
+flags), the records are all-gathered (``torch.distributed``: NCCL on GPUs,
+gloo in the CPU tests) and each rank merges the G records on the device
+(``mc_merge_records``: max similarity, ties to the newer position, then the
+threshold / k epilogue).  That all-gather of B x 32 bytes per rank is the
+path's only collective.
+
+FIFO bookkeeping evicts before it appends — the capacity evictions an insert
+will cause are known up front — so a shard ring of ceil(C/G) rows never has
+to displace anything on its own.
+"""
+from __future__ import annotations
+
+import math
+from collections import deque
+
+import numpy as np
+
+from .cache import _HIT, _EMPTY, _MISS_EMPTY, _unit_norm, _default_device
+from .records import (
+    DEFAULT_DIM,
+    LARGE,
+    POLICIES,
+    POLICY_ALL,
+    POLICY_DISABLED,
+    POLICY_LARGE,
+    SMALL,
+    CacheEntry,
+    EmbeddingError,
+    RetrievalResult,
+    ThresholdTable,
+)
+
+RECORD_BYTES = 32  # sizeof(mc_record)
+
+
+def _count_owned(p_lo: int, n: int, g: int, G: int) -> int:
+    """How many of the global positions p_lo .. p_lo+n-1 satisfy p % G == g."""
+    if n <= 0:
+        return 0
+    first = p_lo + ((g - p_lo) % G)
+    return 0 if first >= p_lo + n else 1 + (p_lo + n - 1 - first) // G
+
+
+class ShardedSemanticCache:
+    """SemanticCache API over G entry shards (one per rank of a process group).
+
+    ``ring_factory(capacity, dim, device)`` builds the shard ring (default: the
+    native ``DeviceRing``); ``comm`` defaults to ``torch.distributed``.
+    """
+
+    def __init__(self, capacity: int, dim: int = DEFAULT_DIM, policy: str = POLICY_ALL,
+                 max_age_s: float | None = None, device: int | None = None, group=None,
+                 ring_factory=None):
+        if capacity < 1:
+            raise ValueError(f"capacity must be >= 1, got {capacity}")
+        if policy not in POLICIES:
+            raise ValueError(f"unknown cache policy {policy!r}, expected one of {POLICIES}")
+        if max_age_s is not None and max_age_s <= 0:
+            raise ValueError(f"max_age_s must be positive, got {max_age_s}")
+        import torch.distributed as dist
+
+        self._dist = dist
+        self._group = group
+        self.n_shards = dist.get_world_size(group)
+        self.shard = dist.get_rank(group)
+        self.capacity = int(capacity)
+        self.dim = int(dim)
+        self.policy = policy
+        self.max_age_s = max_age_s
+        self.device = _default_device() if device is None else int(device)
+        self._store: deque[CacheEntry] = deque()
+        self._next_seq = 0
+        self._appended = 0  # global append position of the next entry
+        if ring_factory is None:
+            from ._native import DeviceRing as ring_factory
+        self.ring = ring_factory(math.ceil(self.capacity / self.n_shards), self.dim, self.device)
+        self.ring.configure_shard(self.n_shards, self.shard)
+        self._table_key = None
+
+    # -- bookkeeping -------------------------------------------------------------
+    def __len__(self) -> int:
+        return len(self._store)
+
+    def entries(self) -> list[CacheEntry]:
+        return list(self._store)
+
+    @property
+    def next_seq(self) -> int:
+        return self._next_seq
+
+    @property
+    def oldest_position(self) -> int:
+        return self._appended - len(self._store)
+
+    def admits(self, producer: str) -> bool:
+        if self.policy == POLICY_DISABLED:
+            return False
+        if self.policy == POLICY_LARGE:
+            return producer == LARGE
+        return True
+
+    def _evict(self, n: int, evicted: list) -> None:
+        """Drop the n oldest entries everywhere; this shard drops the ones it owns."""
+        if n <= 0:
+            return
+        mine = _count_owned(self.oldest_position, n, self.shard, self.n_shards)
+        for _ in range(n):
+            evicted.append(self._store.popleft())
+        if mine:
+            self.ring.evict_front(mine)
+
+    def insert(self, entry: CacheEntry) -> list[CacheEntry]:
+        """cache.py:206-235 semantics, on every rank with the same entry stream."""
+        if not self.admits(entry.producer):
+            return []
+        if entry.producer not in (LARGE, SMALL):
+            raise ValueError(f"unknown producer {entry.producer!r}")
+        emb = entry.embedding
+        if emb.shape != (self.dim,):
+            raise EmbeddingError(f"entry embedding has shape {emb.shape}, cache dim is {self.dim}")
+        if not _unit_norm(emb):
+            raise EmbeddingError(f"entry {entry.id!r} embedding is not unit norm")
+        store = self._store
+        if store and entry.seq <= store[-1].seq:
+            raise ValueError(f"seq must increase: got {entry.seq} after {store[-1].seq}")
+        evicted: list[CacheEntry] = []
+        if self.max_age_s is not None:
+            horizon = entry.inserted_at - self.max_age_s
+            n_age = 0
+            for e in store:
+                if e.inserted_at < horizon:
+                    n_age += 1
+                else:
+                    break
+            self._evict(n_age, evicted)
+        # capacity eviction of the append below, applied first (see module doc)
+        self._evict(len(store) + 1 - self.capacity, evicted)
+        store.append(entry)
+        if self._appended % self.n_shards == self.shard:
+            self.ring.append1(emb)
+        self._appended += 1
+        if entry.seq >= self._next_seq:
+            self._next_seq = entry.seq + 1
+        return evicted
+
+    def add(self, id: str, embedding: np.ndarray, producer: str, inserted_at: float) -> list[CacheEntry]:
+        return self.insert(CacheEntry(id, embedding, producer, self._next_seq, inserted_at))
+
+    # -- lookups (SPMD: every rank passes the same queries) -----------------------
+    def _records(self, Q: np.ndarray):
+        """Local records -> all-gathered [G, B] record bytes, on the comm device."""
+        import torch
+
+        B = Q.shape[0]
+        dev = self.ring.records_device()
+        local = torch.empty(B * RECORD_BYTES, dtype=torch.uint8, device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream if dev.type == "cuda" else 0
+        self.ring.retrieve_local_async(Q, local, stream)
+        gathered = torch.empty(self.n_shards * B * RECORD_BYTES, dtype=torch.uint8, device=dev)
+        self._dist.all_gather_into_tensor(gathered, local, group=self._group)
+        return gathered, stream
+
+    def retrieve_batch(self, Q: np.ndarray, table: ThresholdTable) -> list[RetrievalResult]:
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        if Q.ndim != 2 or Q.shape[1] != self.dim:
+            raise EmbeddingError(f"query batch has shape {Q.shape}, cache dim is {self.dim}")
+        if Q.shape[0] == 0:
+            return []
+        if not self._store:
+            return [_MISS_EMPTY] * Q.shape[0]
+        key = (table.pairs, table.total_steps)
+        if key != self._table_key:
+            self.ring.set_table(table.pairs, table.total_steps)
+            self._table_key = key
+        gathered, stream = self._records(Q)
+        live, sim, k, flags = self.ring.merge_records(gathered, self.n_shards, Q.shape[0], self.oldest_position,
+                                                      stream)
+        store = self._store
+        out = []
+        for i, f in enumerate(np.asarray(flags).tolist()):
+            if f & _HIT:
+                out.append(RetrievalResult(store[int(live[i])], float(sim[i]), int(k[i]) or None))
+            elif f & _EMPTY:
+                out.append(_MISS_EMPTY)
+            else:
+                out.append(RetrievalResult(None, float(sim[i]), None))
+        return out
+
+    def retrieve(self, q: np.ndarray, table: ThresholdTable) -> RetrievalResult:
+        if q.shape != (self.dim,):
+            raise EmbeddingError(f"query has shape {q.shape}, cache dim is {self.dim}")
+        return self.retrieve_batch(q[None, :], table)[0]
+
+    def close(self) -> None:
+        self.ring.close()

@@ -1,0 +1,14 @@
+# ncu evidence for profiles/ (one GPU; never a multi-rank command).
+#  1. launch list of the bench command itself (cold-cache, serialised: compare shares)
+#  2. one --set full capture per top kernel (traffic = dram bytes per launch)
+set -x
+mkdir -p gpurun_out/ncu
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu/launches_bench.csv \
+    python bench.py --steps 4 --warmup 3 --cpu-seconds 0.5 > gpurun_out/ncu/bench_under_ncu.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_gemv_scan -s 3 -c 1 -o gpurun_out/ncu/gemv_c2 \
+    python scripts/profile_case.py c2 --iters 5 > gpurun_out/ncu/gemv.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_tc_scan_pair -s 2 -c 1 -o gpurun_out/ncu/tc_pair_c3 \
+    python scripts/profile_case.py c3 --iters 4 > gpurun_out/ncu/tc.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_merge -s 2 -c 1 -o gpurun_out/ncu/merge_c3 \
+    python scripts/profile_case.py c3 --iters 4 > gpurun_out/ncu/merge.log 2>&1
+ls -la gpurun_out/ncu

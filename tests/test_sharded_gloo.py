@@ -1,0 +1,96 @@
+"""Multi-process (gloo, world_size 2 and 3) tests of the sharded host path on CPU.
+
+Every rank runs ShardedSemanticCache over a FakeShardRing (numpy float64
+scan) and must return exactly the single-cache oracle's answers, through
+capacity churn, age eviction and the insertion policy; the record exchange
+is a real torch.distributed all-gather.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, errq):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from oracle.retrieval import OracleCache, OracleEntry, OracleTable
+        from paper_2503_11972_b200 import CacheEntry, ThresholdTable
+        from paper_2503_11972_b200.sharded import ShardedSemanticCache
+        from tests.fake_shard_ring import FakeShardRing
+
+        rng = np.random.default_rng(123)  # same stream on every rank (SPMD)
+        d, cap = 24, 37
+        sc = ShardedSemanticCache(cap, d, policy="all", max_age_s=60.0, ring_factory=FakeShardRing)
+        oc = OracleCache(cap, d, max_age_s=60.0)
+        table, ot = ThresholdTable.default(), OracleTable()
+        centers = rng.standard_normal((5, d))
+        t = 0.0
+        for i in range(400):
+            t += float(rng.exponential(1.0)) + (80.0 if i in (150, 151, 300) else 0.0)
+            v = centers[i % 5] + 0.7 * rng.standard_normal(d)
+            v /= np.linalg.norm(v)
+            prod = "large" if rng.random() < 0.8 else "small"
+            ev1 = sc.insert(CacheEntry(f"e{i}", v, prod, i, t))
+            ev2 = oc.insert(OracleEntry(f"e{i}", v, prod, i, t))
+            assert [e.id for e in ev1] == [e.id for e in ev2], (rank, i)
+            assert len(sc) == len(oc.meta)
+            if i % 9 == 0:
+                Q = centers[rng.integers(0, 5, 4)] + 0.7 * rng.standard_normal((4, d))
+                Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+                got = sc.retrieve_batch(Q, table)
+                for q, r in zip(Q, got):
+                    e, sim, k = oc.retrieve_entry(q, ot)
+                    assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (rank, i)
+                    assert r.k == k
+                    assert (r.similarity is None) == (sim is None)
+                    if sim is not None:
+                        assert abs(r.similarity - sim) < 1e-12
+        # shard sizes add up to the live window
+        sizes = [None] * world
+        dist.all_gather_object(sizes, len(sc.ring))
+        assert sum(sizes) == len(sc), (sizes, len(sc))
+        dist.destroy_process_group()
+    except BaseException as exc:  # pragma: no cover - reported to the parent
+        import traceback
+
+        errq.put(f"rank {rank}: {exc!r}\n{traceback.format_exc()}")
+        raise
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_cache_matches_oracle_over_gloo(world):
+    ctx = mp.get_context("spawn")
+    errq = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, errq)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    errors = []
+    while not errq.empty():
+        errors.append(errq.get())
+    assert not errors, "\n".join(errors)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+
+
+def test_count_owned():
+    from paper_2503_11972_b200.sharded import _count_owned
+
+    for G in (1, 2, 3, 8):
+        for g in range(G):
+            for lo in range(0, 20):
+                for n in range(0, 20):
+                    want = sum(1 for p in range(lo, lo + n) if p % G == g)
+                    assert _count_owned(lo, n, g, G) == want
