@@ -40,11 +40,15 @@ extern "C" {
 #define MC_FLAG_FALLBACK 0x20u  /* top-K' certificate failed; exhaustive exact rescan answered */
 #define MC_FLAG_NONFINITE 0x40u /* query had NaN/Inf; answered by exhaustive float64 scan */
 
-/* Scan-path selection for mc_set_path (default MC_PATH_AUTO). */
+/* Scan-path selection for mc_set_path (default MC_PATH_AUTO: B <= 4 -> the
+ * int8 GEMV when 64 | D, D <= 1024 (most such D), else the fp16 GEMV; B >= 5 ->
+ * the tcgen05 scan).  Every path returns the same certified answers. */
 #define MC_PATH_AUTO 0
-#define MC_PATH_GEMV 1 /* CUDA-core fp16 GEMV scan, register top-K'             */
+#define MC_PATH_GEMV 1 /* CUDA-core fp16 GEMV scan, register top-K' (cross-checks) */
 #define MC_PATH_GEMM 2 /* tcgen05/TMEM/TMA fp16 GEMM scan (CTA pairs), fused top-K' epilogue */
 #define MC_PATH_GEMM_1SM 3 /* same scan on single CTAs (cta_group::1), kept for cross-checks */
+#define MC_PATH_GEMM_PAIR 4 /* CTA pairs without the 4-CTA query multicast, kept for cross-checks */
+#define MC_PATH_GEMV8 5 /* int8 dp4a GEMV scan with per-row bounds (AUTO's choice for B <= 4) */
 
 typedef struct mc_cache mc_cache;
 

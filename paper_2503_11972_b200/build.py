@@ -11,7 +11,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libmodmcache.so"
-SOURCES = ["api.cu", "ring.cu", "scan_gemv.cu", "scan_tc.cu", "rescore.cu"]
+SOURCES = ["api.cu", "ring.cu", "scan_gemv.cu", "scan_gemv8.cu", "scan_tc.cu", "rescore.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -39,15 +39,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         "-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-O2", "-I", str(ROOT / "include"),
         "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
     ]
-    objs = []
-    for src in SOURCES:
+    jobs = []
+    for src in SOURCES:  # one nvcc per translation unit, in parallel
         obj = objdir / (Path(src).stem + ".o")
         cmd = [nvcc(), *common, "-c", str(CSRC / src), "-o", str(obj)]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
+        jobs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    objs = []
+    for src, obj, proc in jobs:
+        out, err = proc.communicate()
+        if proc.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n{out}\n{err}")
         if verbose:
-            print(r.stderr, file=sys.stderr)
+            print(err, file=sys.stderr)
         objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs]

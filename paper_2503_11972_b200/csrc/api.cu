@@ -57,9 +57,11 @@ struct mc_cache {
   long long head = 0, count = 0, jhead = 0, appended = 0;
   bool state_dirty = false;
 
-  // device-resident ring
+  // device-resident ring (every copy of every slot; see RingBufs)
   __half* ring16 = nullptr;
   double* ring64 = nullptr;
+  int8_t* ring8 = nullptr;
+  float2* ringq = nullptr;
   RingState* d_state = nullptr;
 
   // envelope: pending appends, then queries (see the header comment)
@@ -107,6 +109,8 @@ struct DeviceGuard {
 };
 
 RingState mirror(const mc_cache* h) { return RingState{h->head, h->count, h->jhead, h->C}; }
+
+RingBufs rbufs(const mc_cache* h) { return RingBufs{h->ring16, h->ring64, h->ring8, h->ringq}; }
 
 int wait_env(mc_cache* h) {
   if (h->env_inflight) {
@@ -180,8 +184,7 @@ int ensure_batch(mc_cache* h, int B) {
 // (the uploaded envelope prefix).  Clears the host pending state.
 GemvAppendArgs take_pending(mc_cache* h, const double* dev_rows) {
   GemvAppendArgs a;
-  a.ring16 = h->ring16;
-  a.ring64 = h->ring64;
+  a.rb = rbufs(h);
   a.d_state = h->d_state;
   if (h->n_pending > 0) {
     const long long nw = std::min(h->n_pending, h->C);  // older rows were displaced before landing
@@ -224,7 +227,7 @@ int flush(mc_cache* h) {
     CU(cudaMemcpyAsync(h->d_env, h->h_env, (size_t)h->n_pending * h->Dp * sizeof(double), cudaMemcpyHostToDevice,
                        h->stream));
   const GemvAppendArgs a = take_pending(h, h->d_env);
-  CU(launch_append(a.stage, a.n, a.first_slot, mirror(h), h->D, h->Dp, h->ring16, h->ring64, h->d_state, h->stream));
+  CU(launch_append(a.stage, a.n, a.first_slot, mirror(h), h->D, h->Dp, rbufs(h), h->d_state, h->stream));
   CU(cudaEventRecord(h->env_ev, h->stream));
   h->env_inflight = true;
   h->stats[7]++;
@@ -238,7 +241,9 @@ constexpr int GEMM_MIN_B = 5;
 constexpr long long FUSE_APPEND_MAX = 256;
 
 bool use_gemm(const mc_cache* h, int B) {
-  return h->path == MC_PATH_GEMM || h->path == MC_PATH_GEMM_1SM || (h->path == MC_PATH_AUTO && B >= GEMM_MIN_B);
+  if (h->path == MC_PATH_GEMV || h->path == MC_PATH_GEMV8) return false;
+  return h->path == MC_PATH_GEMM || h->path == MC_PATH_GEMM_1SM || h->path == MC_PATH_GEMM_PAIR ||
+         (h->path == MC_PATH_AUTO && B >= GEMM_MIN_B);
 }
 
 int ensure_tc(mc_cache* h, int B) {
@@ -261,13 +266,13 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
                cudaEvent_t t_mid = nullptr) {
   if (use_gemm(h, B)) {
     if (app.n > 0) {
-      CU(launch_append(app.stage, app.n, app.first_slot, mirror(h), h->D, h->Dp, h->ring16, h->ring64, h->d_state,
-                       h->stream));
+      CU(launch_append(app.stage, app.n, app.first_slot, mirror(h), h->D, h->Dp, rbufs(h), h->d_state, h->stream));
       h->stats[7]++;
     }
     int rc = ensure_tc(h, B);
     if (rc) return rc;
     tc_set_pair(h->tc, h->path != MC_PATH_GEMM_1SM);
+    tc_set_quad(h->tc, h->path != MC_PATH_GEMM_PAIR);
     const Partials part{h->d_part_s, h->d_part_p, h->d_part_floor, tc_chunks(h->tc, B)};
     CU(launch_tc_scan(h->tc, q64, B, h->D, h->d_state, part, h->shard, h->stream));
     if (t_mid) CU(cudaEventRecord(t_mid, h->stream));
@@ -283,11 +288,16 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
   }
   GemvAppendArgs a = app;
   const RingState st = mirror(h);
+  const bool int8 = h->path != MC_PATH_GEMV && gemv8_supported(h->Dp);
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nb = std::min(4, B - b0);
-    CU(launch_gemv_scan(h->ring16, st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
-                        gemv_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax, h->ring64, h->thr, rec, out, a,
-                        h->stream));
+    if (int8)
+      CU(launch_gemv8_scan(rbufs(h), st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
+                           gemv_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax, h->thr, rec, out, a, h->stream));
+    else
+      CU(launch_gemv_scan(h->ring16, st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
+                          gemv_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax, h->ring64, h->thr, rec, out, a,
+                          h->stream));
     a.n = 0;  // written by the first launch
     h->stats[5]++;
     h->stats[7]++;
@@ -372,10 +382,15 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   CUC(cudaEventCreateWithFlags(&h->env_ev, cudaEventDisableTiming));
   const size_t n16 = (size_t)h->C * h->Dp * sizeof(__half);
   const size_t n64 = (size_t)h->C * h->Dp * sizeof(double);
+  const size_t n8 = (size_t)h->C * h->Dp;
   CUC(cudaMalloc(&h->ring16, n16));
   CUC(cudaMalloc(&h->ring64, n64));
+  CUC(cudaMalloc(&h->ring8, n8));
+  CUC(cudaMalloc(&h->ringq, (size_t)h->C * sizeof(float2)));
   CUC(cudaMemsetAsync(h->ring16, 0, n16, h->stream));
   CUC(cudaMemsetAsync(h->ring64, 0, n64, h->stream));
+  CUC(cudaMemsetAsync(h->ring8, 0, n8, h->stream));
+  CUC(cudaMemsetAsync(h->ringq, 0, (size_t)h->C * sizeof(float2), h->stream));
   CUC(cudaMalloc(&h->d_state, sizeof(RingState)));
   {
     RingState z{0, 0, 0, h->C};
@@ -412,6 +427,8 @@ int mc_destroy(mc_cache* h) {
     cudaFree(h->d_env);
     cudaFree(h->ring16);
     cudaFree(h->ring64);
+    cudaFree(h->ring8);
+    cudaFree(h->ringq);
     cudaFree(h->d_state);
     cudaFree(h->d_counter);
     if (h->env_ev) cudaEventDestroy(h->env_ev);
@@ -449,7 +466,7 @@ int mc_configure_shard(mc_cache* h, int32_t n_shards, int32_t shard_id) {
 
 int mc_set_path(mc_cache* h, int32_t path) {
   if (!h) return fail(MC_ERR_ARG, "NULL handle");
-  if (path < MC_PATH_AUTO || path > MC_PATH_GEMM_1SM) return fail(MC_ERR_ARG, "unknown path %d", path);
+  if (path < MC_PATH_AUTO || path > MC_PATH_GEMV8) return fail(MC_ERR_ARG, "unknown path %d", path);
   std::lock_guard<std::mutex> lk(h->mu);
   h->path = path;
   return MC_OK;
@@ -644,8 +661,7 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
     if (d_flush) CUP(cudaMemsetAsync(d_flush, it & 0xff, (size_t)flush_bytes, h->stream));
     CUP(cudaEventRecord(ev[(size_t)it * nev + 0], h->stream));
     GemvAppendArgs app;
-    app.ring16 = h->ring16;
-    app.ring64 = h->ring64;
+    app.rb = rbufs(h);
     app.d_state = h->d_state;
     if (rows) {  // one FIFO insert per step, already resident on the device
       if (h->count == h->C) {

@@ -91,6 +91,50 @@ __device__ __forceinline__ double warp_dot64(const double* __restrict__ row, con
   return isfinite(s) ? s + c : s;
 }
 
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, off));
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(FULL, v, off);
+  return v;
+}
+
+// Per-row int8 scale: s >= max|e| / 127 (rounded up, so |e / s| <= 127 and
+// rint never leaves [-127, 127]); a zero row gets s = 1.
+__device__ __forceinline__ float int8_scale(double amax) {
+  return amax > 0.0 ? __double2float_ru(amax / 127.0) : 1.0f;
+}
+__device__ __forceinline__ int8_t int8_quant(double v, float s) {
+  return (int8_t)__double2int_rn(v / (double)s);
+}
+
+// One warp writes every device copy of a float64 row (zero-padded to Dp) into
+// ring slot `slot` (k_append's work, used by the fused scans for the few rows
+// appended since the last lookup).  Returns the row's int8 scale.
+static __device__ __noinline__ float write_row_all(const double* __restrict__ src, long long slot, const RingBufs& rb,
+                                            int Dp, int lane) {
+  double amax = 0.0, l1 = 0.0;
+  for (int i = lane; i < Dp; i += 32) {
+    const double v = src[i];
+    amax = fmax(amax, fabs(v));
+    l1 += fabs(v);
+  }
+  amax = warp_max_d(amax);
+  l1 = warp_sum_d(l1);
+  const float s = int8_scale(amax);
+  for (int i = lane; i < Dp; i += 32) {
+    const double v = src[i];
+    rb.r64[(size_t)slot * Dp + i] = v;
+    rb.r16[(size_t)slot * Dp + i] = __double2half(v);
+    rb.r8[(size_t)slot * Dp + i] = int8_quant(v, s);
+  }
+  if (lane == 0) rb.rq[slot] = make_float2(s, __double2float_ru(l1 * (1.0 + 1e-12)));
+  return s;
+}
+
 // Composite order of (similarity, position): larger similarity wins; equal
 // similarities go to the larger (newer) position — cache.py:255-256.  NaN
 // ranks above everything (np.argmax returns the first NaN of the reversed

@@ -59,6 +59,14 @@ struct CtaRec {
   int ties;     // rescored candidates bit-equal to s
 };
 
+// The device copies of every ring slot (all written by every append path).
+struct RingBufs {
+  __half* r16;     // [C][Dp] fp16 RN (tensor-core scan, exhaustive fallback)
+  double* r64;     // [C][Dp] float64 master (certified rescoring)
+  int8_t* r8;      // [C][Dp] int8, symmetric per-row scale (small-batch scan)
+  float2* rq;      // [C] (scale s >= max|e|/127, rounded up; ||e||_1, rounded up)
+};
+
 struct ShardMap {
   int G;  // number of shards
   int g;  // this shard
@@ -74,8 +82,7 @@ struct OutRec {
 
 // ---- launch wrappers (each .cu owns its kernels) ---------------------------
 cudaError_t launch_append(const double* stage, long long n, long long first_slot, const RingState& new_state,
-                          int D, int Dp, __half* ring16, double* ring64, RingState* d_state,
-                          cudaStream_t s);
+                          int D, int Dp, const RingBufs& rb, RingState* d_state, cudaStream_t s);
 
 // Pending appends folded into a GEMV launch: stage rows [0, n) -> ring slots
 // (first_slot + i) mod C; d_state receives the launch's window.
@@ -83,8 +90,7 @@ struct GemvAppendArgs {
   const double* stage = nullptr;
   long long n = 0;
   long long first_slot = 0;
-  __half* ring16 = nullptr;
-  double* ring64 = nullptr;
+  RingBufs rb{};
   RingState* d_state = nullptr;
 };
 
@@ -96,6 +102,14 @@ cudaError_t launch_gemv_scan(const __half* ring16, const RingState& st, int D, i
                              CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
                              const double* ring64, const Thresholds& thr, mc_record* rec, OutRec* out,
                              const GemvAppendArgs& app, cudaStream_t s);
+// int8 small-batch scan (scan_gemv8.cu): same contract as launch_gemv_scan.
+cudaError_t launch_gemv8_scan(const RingBufs& rb, const RingState& st, int D, int Dp, const double* q64, int nb,
+                              CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
+                              const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
+                              cudaStream_t s);
+
+bool gemv8_supported(int Dp);
+
 int gemv_grid(int sm_count);
 unsigned long long* gemv_timing_buffer();  // MC_GEMV_TIMING=1 phase timestamps (measurement)
 
@@ -105,7 +119,8 @@ struct TcPlan;
 TcPlan* tc_plan_create(__half* ring16, long long C, int Dp, int Bcap, int sm_count, char* err, int errlen);
 void tc_plan_destroy(TcPlan* p);
 int tc_bcap(const TcPlan* p);
-void tc_set_pair(TcPlan* p, bool pair);  // CTA-pair kernel (default) or single-CTA kernel
+void tc_set_pair(TcPlan* p, bool pair);  // CTA-pair kernels (default) or single-CTA kernel
+void tc_set_quad(TcPlan* p, bool quad);  // with pairs: 4-CTA clusters sharing the query operand (default)
 int tc_chunks(const TcPlan* p, int B);
 const double* tc_qscale(const TcPlan* p);
 cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const RingState* d_state,

@@ -1,41 +1,41 @@
 // K1 — FIFO ring maintenance (replaces cache.py:181-196's float64 `_buf`).
 //
-// Pending appends are staged host-side and copied in one H2D per flush; this
-// kernel writes each staged float64 row into its ring slot twice — the fp64
-// master and the round-to-nearest fp16 scan copy (padding columns zeroed) —
-// and publishes the new (head, count, jhead) so graph-captured scans read the
-// current window from device memory.
+// Pending appends are staged host-side (the envelope) and copied in one H2D;
+// this kernel writes each staged float64 row into every device copy of its
+// ring slot — the float64 master, the round-to-nearest fp16 scan copy and the
+// per-row-scaled int8 scan copy with its (scale, L1) pair — and publishes the
+// new (head, count, jhead).  Small flushes skip it: the fused scans write the
+// few rows appended since the last lookup themselves (write_row_all).
 #include "mc_device.cuh"
 
 namespace mc {
 
-__global__ void k_append(const double* __restrict__ stage, long long n, long long first_slot, long long C, int D,
-                         int Dp, __half* __restrict__ ring16, double* __restrict__ ring64, RingState* d_state,
-                         RingState ns) {
-  for (long long r = blockIdx.x; r < n; r += gridDim.x) {
+// One warp per staged row: float64 master, fp16 RN, int8 + (scale, L1).
+__global__ void k_append(const double* __restrict__ stage, long long n, long long first_slot, long long C, int Dp,
+                         RingBufs rb, RingState* d_state, RingState ns) {
+  const int lane = threadIdx.x & 31;
+  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = w0; r < n; r += nw) {
     long long slot = first_slot + r;
     if (slot >= C) slot -= C;
-    const double* src = stage + (size_t)r * Dp;
-    double* d64 = ring64 + (size_t)slot * Dp;
-    __half* d16 = ring16 + (size_t)slot * Dp;
-    for (int c = threadIdx.x; c < Dp; c += blockDim.x) {
-      const double v = c < D ? src[c] : 0.0;
-      d64[c] = v;
-      d16[c] = __double2half(v);
-    }
+    write_row_all(stage + (size_t)r * Dp, slot, rb, Dp, lane);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *d_state = ns;
 }
 
 __global__ void k_set_state(RingState* d_state, RingState ns) { *d_state = ns; }
 
+// Stage rows are zero-padded to Dp (the envelope keeps padding columns zero).
 cudaError_t launch_append(const double* stage, long long n, long long first_slot, const RingState& ns, int D,
-                          int Dp, __half* ring16, double* ring64, RingState* d_state, cudaStream_t s) {
+                          int Dp, const RingBufs& rb, RingState* d_state, cudaStream_t s) {
+  (void)D;
   if (n <= 0) {
     k_set_state<<<1, 1, 0, s>>>(d_state, ns);
   } else {
-    const int grid = (int)(n < 4096 ? n : 4096);
-    k_append<<<grid, 128, 0, s>>>(stage, n, first_slot, ns.cap, D, Dp, ring16, ring64, d_state, ns);
+    const long long blocks = (n + 3) / 4;  // 4 warps per block
+    const int grid = (int)(blocks < 4096 ? blocks : 4096);
+    k_append<<<grid, 128, 0, s>>>(stage, n, first_slot, ns.cap, Dp, rb, d_state, ns);
   }
   return cudaGetLastError();
 }

@@ -69,24 +69,16 @@ struct GemvAppend {
   const double* stage;
   long long n;
   long long first_slot;
-  __half* ring16;
-  double* ring64;
+  RingBufs rb;
   RingState* d_state;  // receives the new window (block 0)
 };
 
-// One 16-byte chunk (8 values) of a pending row: float64 -> fp16 RN exactly as
-// k_append, written to both ring copies; returns the fp16 chunk for the scan.
-__device__ __noinline__ uint4 pending_chunk(const double* __restrict__ srow, int c, __half* r16, double* r64) {
+// One 16-byte chunk (8 values) of a pending row as the fp16 scan sees it.
+__device__ __forceinline__ uint4 pending_chunk16(const double* __restrict__ srow, int c) {
   __align__(16) __half hv[8];
 #pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const double d = srow[c * 8 + t];
-    r64[c * 8 + t] = d;
-    hv[t] = __double2half(d);
-  }
-  const uint4 h4 = *reinterpret_cast<const uint4*>(hv);
-  *reinterpret_cast<uint4*>(r16 + c * 8) = h4;
-  return h4;
+  for (int t = 0; t < 8; ++t) hv[t] = __double2half(srow[c * 8 + t]);
+  return *reinterpret_cast<const uint4*>(hv);
 }
 
 __device__ __forceinline__ unsigned ticket_acq_rel(unsigned* counter) {
@@ -146,13 +138,12 @@ __global__ void __launch_bounds__(GEMV_THREADS, (NJ * NB > 12) ? 1 : 2)
           v[r][j] = (c < n16) ? ld_stream16(src + c * 8) : make_uint4(0, 0, 0, 0);
         }
       } else if (row < r1) {  // pending row (rare, warp-uniform)
-        const long long slot = ring_slot(st, row);
         const double* srow = app.stage + (size_t)(pend_skip + row - pend0) * Dp;
+        write_row_all(srow, ring_slot(st, row), app.rb, Dp, lane);
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
           const int c = lane + 32 * j;
-          v[r][j] = (c < n16) ? pending_chunk(srow, c, app.ring16 + (size_t)slot * Dp, app.ring64 + (size_t)slot * Dp)
-                              : make_uint4(0, 0, 0, 0);
+          v[r][j] = (c < n16) ? pending_chunk16(srow, c) : make_uint4(0, 0, 0, 0);
         }
       } else {
 #pragma unroll
@@ -349,7 +340,7 @@ __global__ void __launch_bounds__(GEMV_THREADS, (NJ * NB > 12) ? 1 : 2)
     best = block_best(best, ms.shb, false);
     ov = block_max(ov, ms.shf);
     if (threadIdx.x == 0) {
-      const bool fail = best.p < 0 || !(ov == -INFINITY || (double)ov + dl < best.s);
+      const bool fail = best.p < 0 || !(ov == -INFINITY || (double)ov + dl + 1e-9 < best.s);
       mc_record r;
       r.sim = best.s;
       r.second = best.s2;
@@ -425,7 +416,7 @@ cudaError_t launch_gemv_scan(const __half* ring16, const RingState& st, int D, i
   const int nj = (Dp / 8 + 31) / 32;
   if (nb < 1 || nb > 4) return cudaErrorInvalidValue;
   GemvTail tail{counter, gmax, ring64, D, gemv_eps_rel(Dp), eps_abs1(), thr, rec, out, gemv_timing_buffer()};
-  GemvAppend app{a.stage, a.n, a.first_slot, a.ring16, a.ring64, a.d_state};
+  GemvAppend app{a.stage, a.n, a.first_slot, a.rb, a.d_state};
   const float mrel = 1e-6f;  // slack for the fp32 arithmetic of the admission test
 #define MC_GEMV_CASE(NJV) return launch_nj<NJV>(ring16, st, Dp, q64, nb, cta, b0, grid, mrel, sm, tail, app, s)
   switch (nj) {

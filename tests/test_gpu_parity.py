@@ -283,7 +283,8 @@ def test_reference_suite_kats_on_gpu():
 
 def _paths(cache, Q, table):
     out = {}
-    for name, path in (("gemv", _native.PATH_GEMV), ("gemm", _native.PATH_GEMM), ("gemm1", _native.PATH_GEMM_1SM)):
+    for name, path in (("gemv", _native.PATH_GEMV), ("gemm", _native.PATH_GEMM), ("gemm1", _native.PATH_GEMM_1SM),
+                       ("gemm2", _native.PATH_GEMM_PAIR), ("gemv8", _native.PATH_GEMV8)):
         cache.ring.set_path(path)
         out[name] = cache.retrieve_flags(Q, table)
     cache.ring.set_path(_native.PATH_AUTO)
@@ -309,8 +310,12 @@ def test_tensor_core_scan_matches_gemv_and_oracle(dim, cap, n_ins, B):
     keep = ~((fv | fm) & AMBIG).astype(bool)
     assert np.array_equal(lv[keep], lm[keep]) and np.array_equal(kv, km)
     assert np.array_equal(sv, sm_)  # both certified float64 rescoring: bit-identical
-    for a, b in zip(res["gemm"], res["gemm1"]):  # CTA-pair vs single-CTA tensor-core kernels
-        assert np.array_equal(a, b)
+    l8, s8, k8, f8 = res["gemv8"]  # int8 GEMV: same certified answers
+    keep8 = ~((fv | f8) & AMBIG).astype(bool)
+    assert np.array_equal(lv[keep8], l8[keep8]) and np.array_equal(kv, k8) and np.array_equal(sv, s8)
+    for other in ("gemm1", "gemm2"):  # CTA-quad vs single-CTA vs CTA-pair tensor-core kernels
+        for a, b in zip(res["gemm"], res[other]):
+            assert np.array_equal(a, b)
     c.ring.set_path(_native.PATH_GEMM)
     _check_against_scan(c, live_rows, Q, table, f"gemm d{dim} cap{cap} B{B}")
     st = c.ring.stats()
@@ -341,3 +346,28 @@ def test_tensor_core_scan_partial_and_evicted_windows():
                 assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), i
                 assert r.k == k and _close(r.similarity, sim), (i, r, sim)
     assert c.ring.stats()["gemm_launches"] > 0
+
+
+@pytest.mark.parametrize("dim", [6, 64, 200, 384, 768, 1000, 1024])
+def test_int8_and_fp16_small_batch_paths_with_pending_appends(dim):
+    """B <= 4 paths (int8 dp4a with per-row bounds / fp16) through ring wrap with appends folded
+    into the lookup launch: every answer equals the float64 oracle's."""
+    wl = ClusteredWorkload(dim, n_clusters=24, seed=100 + dim)
+    cap = 1500
+    table, ot = ThresholdTable.default(), OracleTable()
+    for path in (_native.PATH_GEMV8, _native.PATH_GEMV):
+        c = SemanticCache(capacity=cap, dim=dim)
+        o = OracleCache(cap, dim)
+        c.ring.set_path(path)
+        rows = wl.cache_rows(2600)
+        for i, v in enumerate(rows):
+            c.insert(CacheEntry(f"e{i}", v, "large", i, float(i)))
+            o.insert(OracleEntry(f"e{i}", v, "large", i, float(i)))
+            if i % 151 == 0 or i > 2590:
+                Q = wl.queries(1 + i % 4)
+                got = c.retrieve_batch(Q, table) if len(Q) > 1 else [c.retrieve(Q[0], table)]
+                for q, r in zip(Q, got):
+                    e, sim, k = o.retrieve_entry(q, ot)
+                    assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (path, i)
+                    assert r.k == k and _close(r.similarity, sim), (path, i, r, sim)
+        c.close()
