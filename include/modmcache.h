@@ -45,9 +45,9 @@ extern "C" {
  * the tcgen05 scan).  Every path returns the same certified answers. */
 #define MC_PATH_AUTO 0
 #define MC_PATH_GEMV 1 /* CUDA-core fp16 GEMV scan, register top-K' (cross-checks) */
-#define MC_PATH_GEMM 2 /* tcgen05/TMEM/TMA fp16 GEMM scan (CTA pairs), fused top-K' epilogue */
+#define MC_PATH_GEMM 2 /* tcgen05/TMEM/TMA fp16 scan on CTA pairs (cta_group::2), fused top-K' epilogue */
 #define MC_PATH_GEMM_1SM 3 /* same scan on single CTAs (cta_group::1), kept for cross-checks */
-#define MC_PATH_GEMM_PAIR 4 /* CTA pairs without the 4-CTA query multicast, kept for cross-checks */
+#define MC_PATH_GEMM_QUAD 4 /* 4-CTA clusters multicasting the query operand (cross-checks) */
 #define MC_PATH_GEMV8 5 /* int8 dp4a GEMV scan with per-row bounds (AUTO's choice for B <= 4) */
 
 typedef struct mc_cache mc_cache;

@@ -8,6 +8,7 @@
 //   h_env / d_env  [env_rows][Dp] float64, zero-padded columns
 //   rows [0, n_pending)            pending FIFO appends (mc_append stages here)
 //   rows [n_pending, n_pending+B)  the lookup's queries
+//   then QPrep[B] and q̂[B][Dp]      the queries' int8 quantisation (quantize_query)
 // A lookup is one H2D copy of the used prefix, one fused GEMV launch (append +
 // scan + certified rescoring + decision) or the tensor-core sequence, one D2H
 // copy of the decisions and one stream synchronisation.
@@ -120,6 +121,39 @@ int wait_env(mc_cache* h) {
   return MC_OK;
 }
 
+// Bytes of the quantisation block for B queries: QPrep[B] (64-byte padded), q̂[B][Dp].
+size_t prep_head(int B) { return ((size_t)B * sizeof(QPrep) + 63) / 64 * 64; }
+size_t prep_bytes(const mc_cache* h, int B) { return prep_head(B) + (size_t)B * h->Dp; }
+
+// int8 quantisation of one query for the small-batch scan (scan_gemv8.cu):
+// s >= max|q|/127 rounded up (so |q/s| <= 127), q̂ = rint(q / s), and the
+// norms the certificate and the exhaustive-path decision need.
+void quantize_query(const double* q, int D, int Dp, QPrep* p, int8_t* q8) {
+  double amax = 0.0, a2 = 0.0, a1 = 0.0;
+  for (int i = 0; i < D; ++i) {
+    amax = std::max(amax, std::fabs(q[i]));
+    a2 = std::fma(q[i], q[i], a2);
+    a1 += std::fabs(q[i]);
+  }
+  const bool finite = std::isfinite(a1) && std::isfinite(amax) && amax <= 1e300;
+  float s = 0.0f;
+  if (finite && amax > 0.0) {
+    s = (float)(amax / 127.0);
+    if ((double)s < amax / 127.0) s = std::nextafter(s, INFINITY);
+  }
+  double l1 = 0.0;
+  for (int i = 0; i < Dp; ++i) {
+    const int qi = (i < D && s > 0.0f) ? (int)std::nearbyint(q[i] / (double)s) : 0;
+    q8[i] = (int8_t)qi;
+    l1 += std::fabs((double)qi);
+  }
+  p->q1 = l1 * (double)s;
+  p->n2 = std::sqrt(a2) * (1.0 + 1e-12);
+  p->n1 = a1 * (1.0 + 1e-12);
+  p->s = s;
+  p->exotic = !(p->n1 <= 1e30) || !(p->n2 >= 1e-30);
+}
+
 void free_batch(mc_cache* h) {
   cudaFree(h->d_part_s);
   cudaFree(h->d_part_p);
@@ -152,19 +186,19 @@ int ensure_batch(mc_cache* h, int B) {
   while (cap < B) cap <<= 1;
   const int chunks = std::max(gemv_grid(h->sm_count), exact_grid(h->sm_count));
   const size_t row = (size_t)h->Dp * sizeof(double);
-  const size_t env_rows = (size_t)h->stage_cap + cap;
+  const size_t env_bytes = ((size_t)h->stage_cap + cap) * row + prep_bytes(h, cap);
   double* h_env = nullptr;
   double* d_env = nullptr;
-  CU(cudaMallocHost(&h_env, env_rows * row));
-  memset(h_env, 0, env_rows * row);
+  CU(cudaMallocHost(&h_env, env_bytes));
+  memset(h_env, 0, env_bytes);
   if (h->h_env) {
     memcpy(h_env, h->h_env, (size_t)h->n_pending * row);
     cudaFreeHost(h->h_env);
     cudaFree(h->d_env);
   }
   h->h_env = h_env;
-  CU(cudaMalloc(&d_env, env_rows * row));
-  CU(cudaMemsetAsync(d_env, 0, env_rows * row, h->stream));
+  CU(cudaMalloc(&d_env, env_bytes));
+  CU(cudaMemsetAsync(d_env, 0, env_bytes, h->stream));
   h->d_env = d_env;
   CU(cudaMalloc(&h->d_part_s, (size_t)cap * chunks * KP * sizeof(float)));
   CU(cudaMalloc(&h->d_part_p, (size_t)cap * chunks * KP * sizeof(long long)));
@@ -198,8 +232,11 @@ GemvAppendArgs take_pending(mc_cache* h, const double* dev_rows) {
   return a;
 }
 
-// Upload the envelope prefix: pending rows, then B queries (row-major, stride D).
-int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse) {
+// Upload the envelope prefix: pending rows, B queries (row-major, stride D),
+// then their int8 quantisation.  Returns device pointers to the queries and
+// to the quantisation block.
+int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse, const double** q_dev,
+                    const QPrep** prep_dev, const int8_t** q8_dev) {
   int rc = wait_env(h);
   if (rc) return rc;
   const size_t row = (size_t)h->Dp * sizeof(double);
@@ -209,11 +246,20 @@ int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse)
   } else {
     for (int b = 0; b < B; ++b) memcpy(qdst + (size_t)b * h->Dp, queries + (size_t)b * h->D, h->D * sizeof(double));
   }
-  CU(cudaMemcpyAsync(h->d_env, h->h_env, (size_t)(h->n_pending + B) * row, cudaMemcpyHostToDevice, h->stream));
+  const size_t prep_off = (size_t)(h->n_pending + B) * row;
+  uint8_t* hp = reinterpret_cast<uint8_t*>(h->h_env) + prep_off;
+  QPrep* hq = reinterpret_cast<QPrep*>(hp);
+  int8_t* h8 = reinterpret_cast<int8_t*>(hp + prep_head(B));
+  for (int b = 0; b < B; ++b) quantize_query(qdst + (size_t)b * h->Dp, h->D, h->Dp, hq + b, h8 + (size_t)b * h->Dp);
+  CU(cudaMemcpyAsync(h->d_env, h->h_env, prep_off + prep_bytes(h, B), cudaMemcpyHostToDevice, h->stream));
   if (async_reuse) {  // the caller returns before the copy completes
     CU(cudaEventRecord(h->env_ev, h->stream));
     h->env_inflight = true;
   }
+  uint8_t* dp = reinterpret_cast<uint8_t*>(h->d_env) + prep_off;
+  *q_dev = h->d_env + (size_t)h->n_pending * h->Dp;
+  *prep_dev = reinterpret_cast<const QPrep*>(dp);
+  *q8_dev = reinterpret_cast<const int8_t*>(dp + prep_head(B));
   return MC_OK;
 }
 
@@ -242,7 +288,7 @@ constexpr long long FUSE_APPEND_MAX = 256;
 
 bool use_gemm(const mc_cache* h, int B) {
   if (h->path == MC_PATH_GEMV || h->path == MC_PATH_GEMV8) return false;
-  return h->path == MC_PATH_GEMM || h->path == MC_PATH_GEMM_1SM || h->path == MC_PATH_GEMM_PAIR ||
+  return h->path == MC_PATH_GEMM || h->path == MC_PATH_GEMM_1SM || h->path == MC_PATH_GEMM_QUAD ||
          (h->path == MC_PATH_AUTO && B >= GEMM_MIN_B);
 }
 
@@ -263,7 +309,7 @@ int ensure_tc(mc_cache* h, int B) {
 // the first GEMV launch, or applied by k_append before a tensor-core scan).
 // t_mid (optional) is recorded between the scan and the standalone merge.
 int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
-               cudaEvent_t t_mid = nullptr) {
+               const QPrep* prep, const int8_t* q8, cudaEvent_t t_mid = nullptr) {
   if (use_gemm(h, B)) {
     if (app.n > 0) {
       CU(launch_append(app.stage, app.n, app.first_slot, mirror(h), h->D, h->Dp, rbufs(h), h->d_state, h->stream));
@@ -272,7 +318,7 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
     int rc = ensure_tc(h, B);
     if (rc) return rc;
     tc_set_pair(h->tc, h->path != MC_PATH_GEMM_1SM);
-    tc_set_quad(h->tc, h->path != MC_PATH_GEMM_PAIR);
+    tc_set_quad(h->tc, h->path == MC_PATH_GEMM_QUAD);
     const Partials part{h->d_part_s, h->d_part_p, h->d_part_floor, tc_chunks(h->tc, B)};
     CU(launch_tc_scan(h->tc, q64, B, h->D, h->d_state, part, h->shard, h->stream));
     if (t_mid) CU(cudaEventRecord(t_mid, h->stream));
@@ -288,19 +334,20 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
   }
   GemvAppendArgs a = app;
   const RingState st = mirror(h);
-  const bool int8 = h->path != MC_PATH_GEMV && gemv8_supported(h->Dp);
+  const bool int8 = h->path != MC_PATH_GEMV && gemv8_supported(h->Dp) && prep != nullptr;
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nb = std::min(4, B - b0);
     if (int8)
       CU(launch_gemv8_scan(rbufs(h), st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
-                           gemv_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax, h->thr, rec, out, a, h->stream));
+                           nb == 1 ? gemv_grid(h->sm_count) : h->sm_count, h->shard, h->d_counter, h->d_gmax, h->thr, rec, out, a, prep + b0,
+                           q8 + (size_t)b0 * h->Dp, h->stream));
     else
       CU(launch_gemv_scan(h->ring16, st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
                           gemv_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax, h->ring64, h->thr, rec, out, a,
                           h->stream));
     a.n = 0;  // written by the first launch
     h->stats[5]++;
-    h->stats[7]++;
+    h->stats[7] += int8 ? 2 : 1;  // the int8 scan is preceded by its query-quantisation kernel
   }
   if (t_mid) CU(cudaEventRecord(t_mid, h->stream));
   return MC_OK;
@@ -316,12 +363,14 @@ int lookup_enqueue(mc_cache* h, const double* queries, int B, mc_record* rec, Ou
     rc = flush(h);
     if (rc) return rc;
   }
-  rc = upload_envelope(h, queries, B, async_reuse);
+  const double* q = nullptr;
+  const QPrep* prep = nullptr;
+  const int8_t* q8 = nullptr;
+  rc = upload_envelope(h, queries, B, async_reuse, &q, &prep, &q8);
   if (rc) return rc;
-  const double* q = h->d_env + (size_t)h->n_pending * h->Dp;
   const GemvAppendArgs app = take_pending(h, h->d_env);
   *q_dev = q;
-  return scan_merge(h, q, B, rec, out, app);
+  return scan_merge(h, q, B, rec, out, app, prep, q8);
 }
 
 int copy_out(mc_cache* h, int B, int64_t* out_live, double* out_sim, int32_t* out_k, uint32_t* out_flags) {
@@ -624,6 +673,8 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
   double *d_qall = nullptr, *d_rows = nullptr;
   OutRec* d_outs = nullptr;
   void* d_flush = nullptr;
+  QPrep* d_prep = nullptr;
+  int8_t* d_q8 = nullptr;
   const int nev = 4;
   std::vector<cudaEvent_t> ev((size_t)iters * nev, nullptr);
   auto release = [&]() {
@@ -634,6 +685,8 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
     cudaFree(d_rows);
     cudaFree(d_outs);
     cudaFree(d_flush);
+    cudaFree(d_prep);
+    cudaFree(d_q8);
   };
 #define CUP(call)                                                                                      \
   do {                                                                                                 \
@@ -654,6 +707,19 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
                      (size_t)h->D * sizeof(double), (size_t)iters, cudaMemcpyHostToDevice));
   }
   CUP(cudaMalloc(&d_outs, (size_t)iters * B * sizeof(OutRec)));
+  {  // the steps' query quantisation, prepared up front like the queries themselves
+    std::vector<QPrep> hp((size_t)iters * B);
+    std::vector<int8_t> h8((size_t)iters * B * h->Dp);
+    std::vector<double> qrow(h->Dp, 0.0);
+    for (size_t i = 0; i < hp.size(); ++i) {
+      memcpy(qrow.data(), queries + i * h->D, h->D * sizeof(double));
+      quantize_query(qrow.data(), h->D, h->Dp, &hp[i], &h8[i * h->Dp]);
+    }
+    CUP(cudaMalloc(&d_prep, hp.size() * sizeof(QPrep)));
+    CUP(cudaMalloc(&d_q8, h8.size()));
+    CUP(cudaMemcpy(d_prep, hp.data(), hp.size() * sizeof(QPrep), cudaMemcpyHostToDevice));
+    CUP(cudaMemcpy(d_q8, h8.data(), h8.size(), cudaMemcpyHostToDevice));
+  }
   if (flush_bytes > 0) CUP(cudaMalloc(&d_flush, (size_t)flush_bytes));
   for (auto& e : ev) CUP(cudaEventCreate(&e));
   const long long launches0 = h->stats[7];
@@ -677,7 +743,8 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
     }
     CUP(cudaEventRecord(ev[(size_t)it * nev + 1], h->stream));
     const double* q = d_qall + (size_t)it * B * h->Dp;
-    rc = scan_merge(h, q, B, h->d_rec, d_outs + (size_t)it * B, app, ev[(size_t)it * nev + 2]);
+    rc = scan_merge(h, q, B, h->d_rec, d_outs + (size_t)it * B, app, d_prep + (size_t)it * B,
+                    d_q8 + (size_t)it * B * h->Dp, ev[(size_t)it * nev + 2]);
     if (rc) {
       release();
       return rc;

@@ -103,10 +103,20 @@ cudaError_t launch_gemv_scan(const __half* ring16, const RingState& st, int D, i
                              const double* ring64, const Thresholds& thr, mc_record* rec, OutRec* out,
                              const GemvAppendArgs& app, cudaStream_t s);
 // int8 small-batch scan (scan_gemv8.cu): same contract as launch_gemv_scan.
+// Per-query int8 quantisation for the small-batch scan (computed on the host
+// by quantize_query, uploaded in the envelope next to the float64 query).
+struct QPrep {
+  double q1;      // ||s_q q̂||_1 (exact integer sum times s_q)
+  double n2, n1;  // ||q||_2, ||q||_1 (rounded up)
+  float s;        // s_q >= max|q|/127, rounded up (0: zero or non-finite query)
+  int exotic;     // non-finite / extreme query: answered by the exhaustive float64 scan
+};
+
+// prep / q8: the nb queries' quantisation (device pointers, q8 stride Dp).
 cudaError_t launch_gemv8_scan(const RingBufs& rb, const RingState& st, int D, int Dp, const double* q64, int nb,
                               CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
                               const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
-                              cudaStream_t s);
+                              const QPrep* prep, const int8_t* q8, cudaStream_t s);
 
 bool gemv8_supported(int Dp);
 

@@ -57,7 +57,18 @@ struct Gemv8Tail {
   Thresholds thr;
   mc_record* rec;
   OutRec* out;
+  unsigned long long* timing;  // optional phase stamps (MC_GEMV_TIMING=1)
+  const QPrep* prep;           // [nb] per-query quantisation (host-computed, in the envelope)
+  const int8_t* q8;            // [nb][Dp] q̂
 };
+
+unsigned long long* gemv_timing_buffer();
+
+__device__ __forceinline__ unsigned long long gtimer8() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct Gemv8Append {
   const double* stage;
@@ -65,12 +76,12 @@ struct Gemv8Append {
   RingState* d_state;
 };
 
-template <int N16>
+template <int N16, int LOADS>
 struct Geom {
   static constexpr int gcd(int a, int b) { return b ? gcd(b, a % b) : a; }
   static constexpr int G = 32 / gcd(N16, 32);        // rows per group
   static constexpr int LPG = G * N16 / 32;           // 16-byte loads per lane per group
-  static constexpr int RG0 = 12 / LPG > 0 ? 12 / LPG : 1;
+  static constexpr int RG0 = LOADS / LPG > 0 ? LOADS / LPG : 1;
   static constexpr int RG = RG0 * G > 32 ? 32 / G : RG0;  // groups per batch (<= 32 rows)
   static constexpr int ROWS = RG * G;
 };
@@ -79,7 +90,7 @@ template <int N16, int NB>
 __global__ void __launch_bounds__(G8_THREADS, NB == 1 ? 2 : 1)
     k_gemv8_scan(RingBufs rb, const RingState st, const double* __restrict__ q64, int nb, CtaRec* __restrict__ cta,
                  int b0, ShardMap sm, Gemv8Tail tail, Gemv8Append app) {
-  using Gm = Geom<N16>;
+  using Gm = Geom<N16, 12>;  // ~12 16-byte loads in flight per lane (2 CTAs / SM measured best)
   constexpr int G = Gm::G, LPG = Gm::LPG, RG = Gm::RG, ROWS = Gm::ROWS;
   constexpr int Dp = N16 * 16;
   extern __shared__ __align__(16) double sq[];  // [nb][Dp] float64 queries (rescoring)
@@ -95,6 +106,7 @@ __global__ void __launch_bounds__(G8_THREADS, NB == 1 ? 2 : 1)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0 && app.d_state) *app.d_state = st;
+  if (tail.timing && threadIdx.x == 0) atomicMin(tail.timing + 0, gtimer8());
 
   const long long n = st.count;
   const long long n_pend = min(app.n, n);
@@ -122,56 +134,29 @@ __global__ void __launch_bounds__(G8_THREADS, NB == 1 ? 2 : 1)
   float2 rq;
   load_batch(r0, v, rq);
 
-  // ---- query prologue: fp64 norms, int8 quantisation, q̂ chunks (registers for one
-  //      query, shared memory for up to four)
+  // ---- query side: q̂ chunks + scalars quantised by the host (quantize_query)
   uint4 qr[LPG];
-  double sq8[NB], q1[NB], n2v[NB], n1v[NB];
+  double sq8[NB], q1[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    double amax = 0.0, a2 = 0.0, a1 = 0.0;
-    for (int i = lane; i < Dp; i += 32) {
-      const double x = (b < nb && i < tail.D) ? q64[(size_t)b * Dp + i] : 0.0;
-      if (warp == 0 && b < nb) sq[(size_t)b * Dp + i] = x;
-      amax = fmax(amax, fabs(x));
-      a2 = fma(x, x, a2);
-      a1 += fabs(x);
-    }
-    amax = warp_max_d(amax);
-    a2 = warp_sum_d(a2);
-    a1 = warp_sum_d(a1);
-    const float s = (amax > 0.0 && amax <= 1e300) ? __double2float_ru(amax / 127.0) : 0.0f;
-    const float sdiv = s > 0.f ? s : 1.0f;
-    sq8[b] = s;
-    n2v[b] = sqrt(a2) * (1.0 + 1e-12);
-    n1v[b] = a1 * (1.0 + 1e-12);
-    double l1q = 0.0;
-    for (int i = lane; i < Dp; i += 32) {
-      const double x = (b < nb && i < tail.D && s > 0.f) ? q64[(size_t)b * Dp + i] : 0.0;
-      l1q += fabs((double)int8_quant(x, sdiv));
-    }
-    q1[b] = warp_sum_d(l1q) * (double)s;  // ||s_q q̂||_1: exact integer sum times s_q
-    auto chunk = [&](int col) {
-      __align__(16) int8_t qq[16];
-#pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int i = col * 16 + t;
-        const double x = (b < nb && i < tail.D && s > 0.f) ? q64[(size_t)b * Dp + i] : 0.0;
-        qq[t] = int8_quant(x, sdiv);
-      }
-      return *reinterpret_cast<const uint4*>(qq);
-    };
+    const QPrep pq = b < nb ? tail.prep[b] : QPrep{0.0, 0.0, 0.0, 0.f, 0};
+    sq8[b] = pq.s;
+    q1[b] = pq.q1;
+    const uint4* qc = reinterpret_cast<const uint4*>(tail.q8 + (size_t)b * Dp);
     if constexpr (NB == 1) {
 #pragma unroll
-      for (int j = 0; j < LPG; ++j) qr[j] = chunk((lane + 32 * j) % N16);
+      for (int j = 0; j < LPG; ++j) qr[j] = qc[(lane + 32 * j) % N16];
     } else {
       if (warp == 0)
-        for (int col = lane; col < N16; col += 32) sh_qc[b][col] = chunk(col);
+        for (int col = lane; col < N16; col += 32) sh_qc[b][col] = b < nb ? qc[col] : make_uint4(0, 0, 0, 0);
     }
   }
   if constexpr (NB > 1) __syncthreads();
 
   // ---- per-warp state: sorted top-K' by upper bound u over lanes 0..K'-1
-  float lu[NB], wmin[NB], ovf[NB];
+  // gk: the best known global lower bound (some row's l, possibly another warp's;
+  // published / refreshed through the gmax word whenever this warp's lo passes it)
+  float lu[NB], wmin[NB], ovf[NB], gk[NB];
   long long lp[NB];
   double lo[NB];
 #pragma unroll
@@ -181,6 +166,7 @@ __global__ void __launch_bounds__(G8_THREADS, NB == 1 ? 2 : 1)
     wmin[b] = -INFINITY;
     ovf[b] = -INFINITY;
     lo[b] = -INFINITY;
+    gk[b] = -INFINITY;
   }
 
   for (long long base = r0; base < r1; base += ROWS) {
@@ -219,7 +205,7 @@ __global__ void __launch_bounds__(G8_THREADS, NB == 1 ? 2 : 1)
           const double dl = (0.5 * sq8[b] * (double)e.y + 0.5 * (double)e.x * q1[b]) * (1.0 + 1e-9) + 1e-12;
           const double u = approx + dl, l = approx - dl;
           lo[b] = fmax(lo[b], l);
-          if (u < lo[b] - 1e-9) continue;  // strictly below the row that set lo
+          if (u < fmax(lo[b], (double)gk[b]) - 1e-9) continue;  // strictly below a row with l >= that
           const float uf = __double2float_ru(u);
           if (uf > wmin[b]) {
             const long long last_p = __shfl_sync(FULL, lp[b], KP - 1);
@@ -242,9 +228,23 @@ __global__ void __launch_bounds__(G8_THREADS, NB == 1 ? 2 : 1)
         }
       }
     }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const float lf = __double2float_rd(lo[b]);
+      if (b < nb && lf > gk[b]) {  // warp-uniform: share this warp's bound, learn the global one
+        float g = lf;
+        if (lane == 0) {
+          const unsigned mine = key_of(lf);
+          const unsigned old = atomicMax(tail.gmax + b0 + b, mine);
+          g = val_of(old > mine ? old : mine);
+        }
+        gk[b] = __shfl_sync(FULL, g, 0);
+      }
+    }
   }
 
   // ---------------------------------------------------------------- CTA rescoring
+  if (tail.timing && lane == 0) atomicMax(tail.timing + 1, gtimer8());
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     if (lane < KP) {
@@ -281,8 +281,9 @@ __global__ void __launch_bounds__(G8_THREADS, NB == 1 ? 2 : 1)
     const bool scan_part = umax > -INFINITY && (double)umax >= (double)sh_g[b] - 1e-9;
     const bool pend_part = blockIdx.x == 0 && n_pend > 0;
     if (scan_part || pend_part) {  // block-uniform
+      load_query(q64 + (size_t)b * Dp, tail.D, Dp, sq + (size_t)b * Dp);
       if (scan_part) {
-        const double thr = lc - 1e-9;
+        const double thr = fmax(lc, (double)sh_g[b]) - 1e-9;
         for (int e = warp; e < G8_WARPS * KP; e += G8_WARPS) {
           const long long p = sh_p[b][e];
           if (p < 0 || (double)sh_u[b][e] < thr) continue;  // warp-uniform
@@ -311,6 +312,7 @@ __global__ void __launch_bounds__(G8_THREADS, NB == 1 ? 2 : 1)
     }
   }
 
+  if (tail.timing && threadIdx.x == 0) atomicMax(tail.timing + 2, gtimer8());
   if (!tail.counter) return;
   // ---------------------------------------------------------------- fused tail
   if (threadIdx.x == 0) {
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(G8_THREADS, NB == 1 ? 2 : 1)
   for (int b = 0; b < NB; ++b) {
     if (b >= nb) break;
     const int gb = b0 + b;
-    const bool exotic = !(n1v[b] <= 1e30) || !(n2v[b] >= 1e-30);
+    const bool exotic = tail.prep[b].exotic != 0;
     Best2 best;
     best.init();
     float ov = -INFINITY;
@@ -362,7 +364,10 @@ __global__ void __launch_bounds__(G8_THREADS, NB == 1 ? 2 : 1)
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *tail.counter = 0u;
+  if (threadIdx.x == 0) {
+    *tail.counter = 0u;
+    if (tail.timing) tail.timing[3] = gtimer8();
+  }
 }
 
 template <int N16>
@@ -393,9 +398,9 @@ bool gemv8_supported(int Dp) {
 cudaError_t launch_gemv8_scan(const RingBufs& rb, const RingState& st, int D, int Dp, const double* q64, int nb,
                               CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
                               const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& a,
-                              cudaStream_t s) {
+                              const QPrep* prep, const int8_t* q8, cudaStream_t s) {
   if (nb < 1 || nb > 4 || !gemv8_supported(Dp)) return cudaErrorInvalidValue;
-  Gemv8Tail tail{counter, gmax, D, thr, rec, out};
+  Gemv8Tail tail{counter, gmax, D, thr, rec, out, gemv_timing_buffer(), prep, q8};
   Gemv8Append app{a.stage, a.n, a.d_state};
 #define MC_G8(K) \
   case K: return launch8<K * 4>(rb, st, q64, nb, cta, b0, grid, sm, tail, app, s)

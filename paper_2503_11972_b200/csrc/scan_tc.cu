@@ -917,7 +917,7 @@ struct TcPlan {
   CUtensorMap ring_map;       // 256-slot boxes (single-CTA kernel)
   CUtensorMap ring_map_half;  // 128-slot boxes (CTA-pair kernel)
   bool pair = true;
-  bool quad = true;  // CTA-quad (query multicast) when pair is set
+  bool quad = false;  // CTA-quad (query multicast): correct but measured slower than pairs (lockstep)
   int dbg = 0;  // MC_TC_DEBUG bisection switches: 1 no TMA, 2 no MMA, 4 no epilogue (timing only)
 };
 

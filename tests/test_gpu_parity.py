@@ -284,7 +284,7 @@ def test_reference_suite_kats_on_gpu():
 def _paths(cache, Q, table):
     out = {}
     for name, path in (("gemv", _native.PATH_GEMV), ("gemm", _native.PATH_GEMM), ("gemm1", _native.PATH_GEMM_1SM),
-                       ("gemm2", _native.PATH_GEMM_PAIR), ("gemv8", _native.PATH_GEMV8)):
+                       ("gemm4", _native.PATH_GEMM_QUAD), ("gemv8", _native.PATH_GEMV8)):
         cache.ring.set_path(path)
         out[name] = cache.retrieve_flags(Q, table)
     cache.ring.set_path(_native.PATH_AUTO)
@@ -313,7 +313,7 @@ def test_tensor_core_scan_matches_gemv_and_oracle(dim, cap, n_ins, B):
     l8, s8, k8, f8 = res["gemv8"]  # int8 GEMV: same certified answers
     keep8 = ~((fv | f8) & AMBIG).astype(bool)
     assert np.array_equal(lv[keep8], l8[keep8]) and np.array_equal(kv, k8) and np.array_equal(sv, s8)
-    for other in ("gemm1", "gemm2"):  # CTA-quad vs single-CTA vs CTA-pair tensor-core kernels
+    for other in ("gemm1", "gemm4"):  # CTA-pair vs single-CTA vs CTA-quad tensor-core kernels
         for a, b in zip(res["gemm"], res[other]):
             assert np.array_equal(a, b)
     c.ring.set_path(_native.PATH_GEMM)
