@@ -235,8 +235,8 @@ GemvAppendArgs take_pending(mc_cache* h, const double* dev_rows) {
 // Upload the envelope prefix: pending rows, B queries (row-major, stride D),
 // then their int8 quantisation.  Returns device pointers to the queries and
 // to the quantisation block.
-int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse, const double** q_dev,
-                    const QPrep** prep_dev, const int8_t** q8_dev) {
+int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse, bool quantise,
+                    const double** q_dev, const QPrep** prep_dev, const int8_t** q8_dev) {
   int rc = wait_env(h);
   if (rc) return rc;
   const size_t row = (size_t)h->Dp * sizeof(double);
@@ -250,16 +250,18 @@ int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse,
   uint8_t* hp = reinterpret_cast<uint8_t*>(h->h_env) + prep_off;
   QPrep* hq = reinterpret_cast<QPrep*>(hp);
   int8_t* h8 = reinterpret_cast<int8_t*>(hp + prep_head(B));
-  for (int b = 0; b < B; ++b) quantize_query(qdst + (size_t)b * h->Dp, h->D, h->Dp, hq + b, h8 + (size_t)b * h->Dp);
-  CU(cudaMemcpyAsync(h->d_env, h->h_env, prep_off + prep_bytes(h, B), cudaMemcpyHostToDevice, h->stream));
+  if (quantise)
+    for (int b = 0; b < B; ++b) quantize_query(qdst + (size_t)b * h->Dp, h->D, h->Dp, hq + b, h8 + (size_t)b * h->Dp);
+  CU(cudaMemcpyAsync(h->d_env, h->h_env, prep_off + (quantise ? prep_bytes(h, B) : 0), cudaMemcpyHostToDevice,
+                     h->stream));
   if (async_reuse) {  // the caller returns before the copy completes
     CU(cudaEventRecord(h->env_ev, h->stream));
     h->env_inflight = true;
   }
   uint8_t* dp = reinterpret_cast<uint8_t*>(h->d_env) + prep_off;
   *q_dev = h->d_env + (size_t)h->n_pending * h->Dp;
-  *prep_dev = reinterpret_cast<const QPrep*>(dp);
-  *q8_dev = reinterpret_cast<const int8_t*>(dp + prep_head(B));
+  *prep_dev = quantise ? reinterpret_cast<const QPrep*>(dp) : nullptr;
+  *q8_dev = quantise ? reinterpret_cast<const int8_t*>(dp + prep_head(B)) : nullptr;
   return MC_OK;
 }
 
@@ -347,7 +349,7 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
                           h->stream));
     a.n = 0;  // written by the first launch
     h->stats[5]++;
-    h->stats[7] += int8 ? 2 : 1;  // the int8 scan is preceded by its query-quantisation kernel
+    h->stats[7]++;
   }
   if (t_mid) CU(cudaEventRecord(t_mid, h->stream));
   return MC_OK;
@@ -366,7 +368,8 @@ int lookup_enqueue(mc_cache* h, const double* queries, int B, mc_record* rec, Ou
   const double* q = nullptr;
   const QPrep* prep = nullptr;
   const int8_t* q8 = nullptr;
-  rc = upload_envelope(h, queries, B, async_reuse, &q, &prep, &q8);
+  const bool int8 = !use_gemm(h, B) && h->path != MC_PATH_GEMV && gemv8_supported(h->Dp);
+  rc = upload_envelope(h, queries, B, async_reuse, int8, &q, &prep, &q8);
   if (rc) return rc;
   const GemvAppendArgs app = take_pending(h, h->d_env);
   *q_dev = q;
@@ -720,11 +723,14 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
     CUP(cudaMemcpy(d_prep, hp.data(), hp.size() * sizeof(QPrep), cudaMemcpyHostToDevice));
     CUP(cudaMemcpy(d_q8, h8.data(), h8.size(), cudaMemcpyHostToDevice));
   }
-  if (flush_bytes > 0) CUP(cudaMalloc(&d_flush, (size_t)flush_bytes));
+  if (flush_bytes > 0) {
+    CUP(cudaMalloc(&d_flush, (size_t)flush_bytes));
+    CUP(cudaMemsetAsync(d_flush, 1, (size_t)flush_bytes, h->stream));
+  }
   for (auto& e : ev) CUP(cudaEventCreate(&e));
   const long long launches0 = h->stats[7];
   for (int it = 0; it < iters; ++it) {
-    if (d_flush) CUP(cudaMemsetAsync(d_flush, it & 0xff, (size_t)flush_bytes, h->stream));
+    if (d_flush) CUP(launch_l2_flush(d_flush, (size_t)flush_bytes, h->stream));
     CUP(cudaEventRecord(ev[(size_t)it * nev + 0], h->stream));
     GemvAppendArgs app;
     app.rb = rbufs(h);

@@ -121,6 +121,7 @@ cudaError_t launch_gemv8_scan(const RingBufs& rb, const RingState& st, int D, in
 bool gemv8_supported(int Dp);
 
 int gemv_grid(int sm_count);
+cudaError_t launch_l2_flush(void* buf, size_t bytes, cudaStream_t s);  // measurement: evict L2 by reading
 unsigned long long* gemv_timing_buffer();  // MC_GEMV_TIMING=1 phase timestamps (measurement)
 
 // tcgen05 GEMM scan of B queries (scan_tc.cu).  The plan owns the fp16

@@ -40,4 +40,22 @@ cudaError_t launch_append(const double* stage, long long n, long long first_slot
   return cudaGetLastError();
 }
 
+// Measurement helper (mc_profile_steps): read a buffer larger than L2 so the
+// next step starts with the ring evicted and L2 holding only clean lines (a
+// write-based flush would leave ~126 MB of dirty lines to write back during
+// the timed kernel).
+__global__ void k_l2_flush(const uint4* __restrict__ p, size_t n16, unsigned* sink) {
+  unsigned acc = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 v = ld_stream16(p + i);
+    acc ^= v.x ^ v.w;
+  }
+  if (acc == 0x9e3779b9u) *sink = acc;
+}
+
+cudaError_t launch_l2_flush(void* buf, size_t bytes, cudaStream_t s) {
+  k_l2_flush<<<4 * 148, 256, 0, s>>>(static_cast<const uint4*>(buf), bytes / 16, static_cast<unsigned*>(buf));
+  return cudaGetLastError();
+}
+
 }  // namespace mc
