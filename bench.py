@@ -62,9 +62,10 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            self._wait_lines(1, 5.0)  # sampling is live before the timed region starts
         except OSError:
             self.proc = None
         return self
@@ -73,8 +74,14 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def _wait_lines(self, n, timeout):
+        t0 = time.time()
+        while len(self.lines) < n and time.time() - t0 < timeout and self.proc and self.proc.poll() is None:
+            time.sleep(0.005)
+
     def __exit__(self, *a):
         if self.proc:
+            self._wait_lines(len(self.lines) + 1, 1.0)  # one sample after the timed region ends
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -201,10 +208,10 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
         "kernel_launches_per_step": e2e_launches,
     }
     dp = (dim + 63) // 64 * 64
-    int8_path = B <= 4 and dp % 64 == 0 and dp <= 1024 and (dp // 64 <= 8 or (dp // 64) % 2 == 0)
-    if int8_path:  # K2q: int8 ring + per-row (scale, L1) + the float64 queries and their quantisation
-        scan_bytes = n_entries * (dp + 8) + B * (dp * 9 + 40)
-        kname = "k_gemv8_scan"
+    p8 = (dp + 127) // 128 * 128
+    if B <= 4 and dp <= 1024:  # K2s: TMA-streamed int8 ring + per-row (scale, L1) + float64 queries + quantisation
+        scan_bytes = n_entries * (p8 + 8) + B * (dp * 9 + 40)
+        kname = "k_stream8_scan"
     elif B <= 4:  # K2: fp16 ring
         scan_bytes = n_entries * dp * 2 + B * dp * 8
         kname = "k_gemv_scan"
@@ -223,7 +230,8 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
         roof = {"bound": "tensor", "achieved": flops / scan_s / 1e12, "peak": tc_burst, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["peak_source"] = f"{src} (MEASURED_PEAKS.json)" if src == "measured" else "fallback (B200_PROFILING.md)"
-    roof["kernel"] = {"k_gemv8_scan": "k_gemv8_scan (int8 dp4a scan + float64 rescoring + decision, fused)",
+    roof["kernel"] = {"k_stream8_scan": "k_stream8_scan (TMA-streamed int8 scan + in-scan float64 rescoring + "
+                                        "merge + decision, one launch)",
                       "k_gemv_scan": "k_gemv_scan (fp16 scan + float64 rescoring + decision, fused)",
                       "k_tc_scan_pair": "k_tc_scan_pair (tcgen05 cta_group::2)"}[kname]
     roof["algorithmic_bytes_per_launch"] = scan_bytes

@@ -41,14 +41,17 @@ extern "C" {
 #define MC_FLAG_NONFINITE 0x40u /* query had NaN/Inf; answered by exhaustive float64 scan */
 
 /* Scan-path selection for mc_set_path (default MC_PATH_AUTO: B <= 4 -> the
- * int8 GEMV when 64 | D, D <= 1024 (most such D), else the fp16 GEMV; B >= 5 ->
- * the tcgen05 scan).  Every path returns the same certified answers. */
+ * TMA-streamed int8 scan when 128 | Dp <= 1024 (Dp = D rounded up to 64), else
+ * the register int8 GEMV when it covers Dp, else the fp16 GEMV; B >= 5 -> the
+ * tcgen05 scan).  Every path returns the same certified answers. */
 #define MC_PATH_AUTO 0
 #define MC_PATH_GEMV 1 /* CUDA-core fp16 GEMV scan, register top-K' (cross-checks) */
 #define MC_PATH_GEMM 2 /* tcgen05/TMEM/TMA fp16 scan on CTA pairs (cta_group::2), fused top-K' epilogue */
 #define MC_PATH_GEMM_1SM 3 /* same scan on single CTAs (cta_group::1), kept for cross-checks */
 #define MC_PATH_GEMM_QUAD 4 /* 4-CTA clusters multicasting the query operand (cross-checks) */
-#define MC_PATH_GEMV8 5 /* int8 dp4a GEMV scan with per-row bounds (AUTO's choice for B <= 4) */
+#define MC_PATH_GEMV8 5 /* int8 dp4a register-streaming GEMV scan with per-row bounds (cross-checks) */
+#define MC_PATH_STREAM8 6 /* int8 scan streamed by TMA, lane-per-row dp4a, in-scan float64 rescoring
+                             (AUTO's choice for B <= 4 when 128 | Dp <= 1024) */
 
 typedef struct mc_cache mc_cache;
 
@@ -126,10 +129,12 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
                      int64_t flush_bytes, double* out_ms, int64_t* out_counts);
 
 /* Measurement hook, active only when MC_GEMV_TIMING=1 was set before the first
- * lookup: reads (reset = 0) or resets (reset = 1) four globaltimer stamps of the
- * last GEMV launch(es): first CTA start, last scan end, last rescoring end,
- * tail end (ns).  Not needed by the drop-in; used by scripts/profile_case.py. */
-int mc_debug_gemv_timing(unsigned long long* out4, int reset);
+ * lookup: reads (reset = 0) or resets (reset = 1) eight globaltimer stamps of the
+ * last small-batch launch(es): [0] first CTA start, [1] last scan end, [2] last
+ * rescoring end, [3] tail end, [4] merge start and [5] records loaded (streamed
+ * int8 scan only), [6..7] reserved (ns).  Not needed by the drop-in; used by
+ * scripts/profile_case.py. */
+int mc_debug_gemv_timing(unsigned long long* out8, int reset);
 
 /* Counters since creation: [0] lookups, [1] certificate fallbacks,
  * [2] non-finite queries, [3] exact ties, [4] candidates rescored,

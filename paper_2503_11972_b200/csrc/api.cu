@@ -52,6 +52,7 @@ struct mc_cache {
   cudaStream_t stream = nullptr;
   long long C = 0;
   int D = 0, Dp = 0;
+  int P8 = 0;  // int8 ring row stride (Dp rounded up to 128)
   ShardMap shard{1, 0};
 
   // host mirror of the ring window
@@ -80,13 +81,14 @@ struct mc_cache {
   long long* d_part_p = nullptr;
   float* d_part_floor = nullptr;
   CtaRec* d_cta = nullptr;     // [Bcap][gemv grid] per-CTA exact records (GEMV path)
-  unsigned* d_gmax = nullptr;  // [Bcap] running max keys of the fused GEMV scan (zero between launches)
+  unsigned* d_gmax = nullptr;  // [Bcap][256] running max keys of the fused scans (zero between launches)
   mc_record* d_rec = nullptr;
   mc_record* d_scratch = nullptr;
   OutRec* d_out = nullptr;
   OutRec* h_out = nullptr;  // pinned
 
   TcPlan* tc = nullptr;           // tensor-core scan plan, created on first batched lookup
+  S8Plan* s8 = nullptr;           // TMA-streamed int8 scan plan (tensor maps of ring8 / ringq)
   unsigned* d_counter = nullptr;  // last-CTA ticket of the fused GEMV scan (zero between launches)
 
   Thresholds thr{};
@@ -111,7 +113,7 @@ struct DeviceGuard {
 
 RingState mirror(const mc_cache* h) { return RingState{h->head, h->count, h->jhead, h->C}; }
 
-RingBufs rbufs(const mc_cache* h) { return RingBufs{h->ring16, h->ring64, h->ring8, h->ringq}; }
+RingBufs rbufs(const mc_cache* h) { return RingBufs{h->ring16, h->ring64, h->ring8, h->ringq, h->P8}; }
 
 int wait_env(mc_cache* h) {
   if (h->env_inflight) {
@@ -204,8 +206,9 @@ int ensure_batch(mc_cache* h, int B) {
   CU(cudaMalloc(&h->d_part_p, (size_t)cap * chunks * KP * sizeof(long long)));
   CU(cudaMalloc(&h->d_part_floor, (size_t)cap * chunks * sizeof(float)));
   CU(cudaMalloc(&h->d_cta, (size_t)cap * gemv_grid(h->sm_count) * sizeof(CtaRec)));
-  CU(cudaMalloc(&h->d_gmax, (size_t)cap * sizeof(unsigned)));
-  CU(cudaMemsetAsync(h->d_gmax, 0, (size_t)cap * sizeof(unsigned), h->stream));
+  // 256 words per query: the streamed scan keeps 8 replicas of its bound 128 B apart
+  CU(cudaMalloc(&h->d_gmax, (size_t)cap * 256 * sizeof(unsigned)));
+  CU(cudaMemsetAsync(h->d_gmax, 0, (size_t)cap * 256 * sizeof(unsigned), h->stream));
   CU(cudaMalloc(&h->d_rec, (size_t)cap * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_scratch, (size_t)cap * exact_grid(h->sm_count) * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_out, (size_t)cap * sizeof(OutRec)));
@@ -289,7 +292,7 @@ constexpr int GEMM_MIN_B = 5;
 constexpr long long FUSE_APPEND_MAX = 256;
 
 bool use_gemm(const mc_cache* h, int B) {
-  if (h->path == MC_PATH_GEMV || h->path == MC_PATH_GEMV8) return false;
+  if (h->path == MC_PATH_GEMV || h->path == MC_PATH_GEMV8 || h->path == MC_PATH_STREAM8) return false;
   return h->path == MC_PATH_GEMM || h->path == MC_PATH_GEMM_1SM || h->path == MC_PATH_GEMM_QUAD ||
          (h->path == MC_PATH_AUTO && B >= GEMM_MIN_B);
 }
@@ -336,10 +339,16 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
   }
   GemvAppendArgs a = app;
   const RingState st = mirror(h);
-  const bool int8 = h->path != MC_PATH_GEMV && gemv8_supported(h->Dp) && prep != nullptr;
+  const bool quant = h->path != MC_PATH_GEMV && prep != nullptr;
+  const bool s8 = quant && h->s8 && h->path != MC_PATH_GEMV8;
+  const bool int8 = quant && !s8 && gemv8_supported(h->Dp);
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nb = std::min(4, B - b0);
-    if (int8)
+    if (s8)
+      CU(launch_stream8_scan(h->s8, rbufs(h), st, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0, h->sm_count, h->shard,
+                             h->d_counter, h->d_gmax, h->thr, rec, out, a, prep + b0, q8 + (size_t)b0 * h->Dp,
+                             h->stream));
+    else if (int8)
       CU(launch_gemv8_scan(rbufs(h), st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
                            nb == 1 ? gemv_grid(h->sm_count) : h->sm_count, h->shard, h->d_counter, h->d_gmax, h->thr, rec, out, a, prep + b0,
                            q8 + (size_t)b0 * h->Dp, h->stream));
@@ -368,7 +377,7 @@ int lookup_enqueue(mc_cache* h, const double* queries, int B, mc_record* rec, Ou
   const double* q = nullptr;
   const QPrep* prep = nullptr;
   const int8_t* q8 = nullptr;
-  const bool int8 = !use_gemm(h, B) && h->path != MC_PATH_GEMV && gemv8_supported(h->Dp);
+  const bool int8 = !use_gemm(h, B) && h->path != MC_PATH_GEMV && (h->s8 || gemv8_supported(h->Dp));
   rc = upload_envelope(h, queries, B, async_reuse, int8, &q, &prep, &q8);
   if (rc) return rc;
   const GemvAppendArgs app = take_pending(h, h->d_env);
@@ -419,6 +428,7 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   h->C = capacity;
   h->D = dim;
   h->Dp = (dim + 63) / 64 * 64;
+  h->P8 = (h->Dp + 127) / 128 * 128;
   auto cleanup = [&](int rc) {
     mc_destroy(h);
     return rc;
@@ -434,19 +444,24 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   CUC(cudaEventCreateWithFlags(&h->env_ev, cudaEventDisableTiming));
   const size_t n16 = (size_t)h->C * h->Dp * sizeof(__half);
   const size_t n64 = (size_t)h->C * h->Dp * sizeof(double);
-  const size_t n8 = (size_t)h->C * h->Dp;
+  const size_t n8 = (size_t)h->C * h->P8;
   CUC(cudaMalloc(&h->ring16, n16));
   CUC(cudaMalloc(&h->ring64, n64));
   CUC(cudaMalloc(&h->ring8, n8));
-  CUC(cudaMalloc(&h->ringq, (size_t)h->C * sizeof(float2)));
+  CUC(cudaMalloc(&h->ringq, (size_t)(h->C + 2) * sizeof(float2)));  // +2: 16-byte aligned bulk copies
   CUC(cudaMemsetAsync(h->ring16, 0, n16, h->stream));
   CUC(cudaMemsetAsync(h->ring64, 0, n64, h->stream));
   CUC(cudaMemsetAsync(h->ring8, 0, n8, h->stream));
-  CUC(cudaMemsetAsync(h->ringq, 0, (size_t)h->C * sizeof(float2), h->stream));
+  CUC(cudaMemsetAsync(h->ringq, 0, (size_t)(h->C + 2) * sizeof(float2), h->stream));
   CUC(cudaMalloc(&h->d_state, sizeof(RingState)));
   {
     RingState z{0, 0, 0, h->C};
     CUC(cudaMemcpyAsync(h->d_state, &z, sizeof z, cudaMemcpyHostToDevice, h->stream));
+  }
+  if (stream8_supported(h->Dp)) {
+    char err[256] = {0};
+    h->s8 = s8_plan_create(h->ring8, h->ringq, h->C, h->Dp, h->P8, err, sizeof err);
+    if (!h->s8) return cleanup(fail(MC_ERR_CUDA, "int8 stream scan plan: %s", err));
   }
   CUC(cudaMalloc(&h->d_counter, sizeof(unsigned)));
   CUC(cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned), h->stream));
@@ -475,6 +490,7 @@ int mc_destroy(mc_cache* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     free_batch(h);
     tc_plan_destroy(h->tc);
+    s8_plan_destroy(h->s8);
     cudaFreeHost(h->h_env);
     cudaFree(h->d_env);
     cudaFree(h->ring16);
@@ -518,7 +534,7 @@ int mc_configure_shard(mc_cache* h, int32_t n_shards, int32_t shard_id) {
 
 int mc_set_path(mc_cache* h, int32_t path) {
   if (!h) return fail(MC_ERR_ARG, "NULL handle");
-  if (path < MC_PATH_AUTO || path > MC_PATH_GEMV8) return fail(MC_ERR_ARG, "unknown path %d", path);
+  if (path < MC_PATH_AUTO || path > MC_PATH_STREAM8) return fail(MC_ERR_ARG, "unknown path %d", path);
   std::lock_guard<std::mutex> lk(h->mu);
   h->path = path;
   return MC_OK;
@@ -678,7 +694,7 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
   void* d_flush = nullptr;
   QPrep* d_prep = nullptr;
   int8_t* d_q8 = nullptr;
-  const int nev = 4;
+  const int nev = 3;
   std::vector<cudaEvent_t> ev((size_t)iters * nev, nullptr);
   auto release = [&]() {
     cudaStreamSynchronize(h->stream);
@@ -729,6 +745,7 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
   }
   for (auto& e : ev) CUP(cudaEventCreate(&e));
   const long long launches0 = h->stats[7];
+  const bool gemm = use_gemm(h, B);  // tensor-core sequence: also time scan and merge separately
   for (int it = 0; it < iters; ++it) {
     if (d_flush) CUP(launch_l2_flush(d_flush, (size_t)flush_bytes, h->stream));
     CUP(cudaEventRecord(ev[(size_t)it * nev + 0], h->stream));
@@ -747,27 +764,28 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
       h->count++;
       h->appended++;
     }
-    CUP(cudaEventRecord(ev[(size_t)it * nev + 1], h->stream));
     const double* q = d_qall + (size_t)it * B * h->Dp;
     rc = scan_merge(h, q, B, h->d_rec, d_outs + (size_t)it * B, app, d_prep + (size_t)it * B,
-                    d_q8 + (size_t)it * B * h->Dp, ev[(size_t)it * nev + 2]);
+                    d_q8 + (size_t)it * B * h->Dp, gemm ? ev[(size_t)it * nev + 1] : nullptr);
     if (rc) {
       release();
       return rc;
     }
-    CUP(cudaEventRecord(ev[(size_t)it * nev + 3], h->stream));
+    CUP(cudaEventRecord(ev[(size_t)it * nev + 2], h->stream));
   }
   CUP(cudaStreamSynchronize(h->stream));
-  double tot = 0, t_app = 0, t_scan = 0, t_merge = 0;
+  double tot = 0, t_scan = 0, t_merge = 0;
   for (int it = 0; it < iters; ++it) {
-    float a, b, c;
-    CUP(cudaEventElapsedTime(&a, ev[(size_t)it * nev + 0], ev[(size_t)it * nev + 1]));
-    CUP(cudaEventElapsedTime(&b, ev[(size_t)it * nev + 1], ev[(size_t)it * nev + 2]));
-    CUP(cudaEventElapsedTime(&c, ev[(size_t)it * nev + 2], ev[(size_t)it * nev + 3]));
-    t_app += a;
-    t_scan += b;
-    t_merge += c;
-    tot += a + b + c;
+    float a = 0.f, b = 0.f;
+    if (gemm) {
+      CUP(cudaEventElapsedTime(&a, ev[(size_t)it * nev + 0], ev[(size_t)it * nev + 1]));
+      CUP(cudaEventElapsedTime(&b, ev[(size_t)it * nev + 1], ev[(size_t)it * nev + 2]));
+    } else {  // one fused launch per step: the step is the kernel
+      CUP(cudaEventElapsedTime(&a, ev[(size_t)it * nev + 0], ev[(size_t)it * nev + 2]));
+    }
+    t_scan += a;
+    t_merge += b;
+    tot += a + b;
   }
   std::vector<OutRec> outs((size_t)iters * B);
   CUP(cudaMemcpy(outs.data(), d_outs, outs.size() * sizeof(OutRec), cudaMemcpyDeviceToHost));
@@ -780,7 +798,7 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
   out_ms[0] = tot / iters;
   out_ms[1] = t_scan / iters;
   out_ms[2] = t_merge / iters;
-  out_ms[3] = t_app / iters;
+  out_ms[3] = 0.0;  // appends ride inside the scan launch (or its k_append, timed with the scan)
   out_counts[0] = (h->stats[7] - launches0) / iters;
   out_counts[1] = need;
   release();
@@ -789,16 +807,19 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
 }
 
 // Measurement hook (MC_GEMV_TIMING=1): read (reset=0) or reset (reset=1) the
-// GEMV phase timestamps; 4 x u64 nanoseconds.  Not part of the stable ABI.
-int mc_debug_gemv_timing(unsigned long long* out4, int reset) {
+// GEMV phase timestamps; 8 x u64 nanoseconds.  Not part of the stable ABI.
+int mc_debug_gemv_timing(unsigned long long* out8, int reset) {
   unsigned long long* t = gemv_timing_buffer();
   if (!t) return fail(MC_ERR_STATE, "set MC_GEMV_TIMING=1 before the first lookup");
   CU(cudaDeviceSynchronize());
-  if (reset) {
-    const unsigned long long init4[4] = {~0ull, 0, 0, 0};
-    CU(cudaMemcpy(t, init4, sizeof init4, cudaMemcpyHostToDevice));
+  if (reset == 2) {  // per-CTA stamps of the streamed scan: [cta][8] after the 8 globals
+    CU(cudaMemcpy(out8, t + 8, 8 * 512 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  } else if (reset) {
+    const unsigned long long init8[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+    CU(cudaMemset(t + 8, 0, 8 * 512 * sizeof(unsigned long long)));
+    CU(cudaMemcpy(t, init8, sizeof init8, cudaMemcpyHostToDevice));
   } else {
-    CU(cudaMemcpy(out4, t, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(out8, t, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   }
   return MC_OK;
 }

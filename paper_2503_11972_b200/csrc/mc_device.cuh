@@ -53,42 +53,61 @@ __device__ __forceinline__ void dot2_step(double a, double b, double& s, double&
 
 // Compensated (Ogita-Rump-Oishi Dot2) float64 dot product of one row with q
 // over n elements (n a multiple of 64, rows and q zero-padded), one warp.
-// Lane l owns elements 2l, 2l+1 of every 64-element block, accumulated in
-// increasing block order; the 16 loads of a 512-element block are issued
-// before any is used.  The lane->element map and the butterfly are fixed, so
-// every lane returns the same bits and identical rows always score
-// identically (exact ties stay exact).
+// Lane l owns elements 2l, 2l+1 of every 64-element block j.  Block j feeds
+// chain j % 4 (four independent error-free accumulation chains, so the
+// dependent latency is a quarter of a single chain's); blocks are visited in
+// increasing order and the chains are combined in a fixed tree, then the
+// butterfly.  All loads of a 1024-element batch are issued before the first
+// product.  The lane->element map, chain map and trees are fixed, so every
+// lane returns the same bits and identical rows always score identically
+// (exact ties stay exact) — on every path that rescores (scan tails, merge,
+// exhaustive rescan).
 __device__ __forceinline__ double warp_dot64(const double* __restrict__ row, const double* __restrict__ q, int n,
                                              int lane) {
-  double s = 0.0, c = 0.0;
-  for (int base = 0; base < n; base += 512) {
-    double2 a[8];
+  double s[4] = {0.0, 0.0, 0.0, 0.0}, c[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int base = 0; base < n; base += 1024) {
+    double2 a[16];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < 16; ++j) {
       const int i = base + 64 * j + 2 * lane;
       a[j] = i < n ? __ldg(reinterpret_cast<const double2*>(row + i)) : make_double2(0.0, 0.0);
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < 16; ++j) {
       const int i = base + 64 * j + 2 * lane;
       if (i < n) {
-        dot2_step(a[j].x, q[i], s, c);
-        dot2_step(a[j].y, q[i + 1], s, c);
+        const double2 b = *reinterpret_cast<const double2*>(q + i);
+        dot2_step(a[j].x, b.x, s[j & 3], c[j & 3]);
+        dot2_step(a[j].y, b.y, s[j & 3], c[j & 3]);
       }
     }
   }
+  double t, et;
+  two_sum(s[0], s[1], t, et);
+  s[0] = t;
+  c[0] = (c[0] + c[1]) + et;
+  two_sum(s[2], s[3], t, et);
+  s[2] = t;
+  c[2] = (c[2] + c[3]) + et;
+  two_sum(s[0], s[2], t, et);
+  double sum = t, comp = (c[0] + c[2]) + et;
 #pragma unroll
   for (int off = 16; off; off >>= 1) {
-    const double s2 = __shfl_xor_sync(FULL, s, off);
-    const double c2 = __shfl_xor_sync(FULL, c, off);
-    double t, et;
-    two_sum(s, s2, t, et);
-    s = t;
-    c = (c + c2) + et;
+    const double s2 = __shfl_xor_sync(FULL, sum, off);
+    const double c2 = __shfl_xor_sync(FULL, comp, off);
+    two_sum(sum, s2, t, et);
+    sum = t;
+    comp = (comp + c2) + et;
   }
   // Inf/NaN products poison the compensation term; the plain sum then carries
   // the same (order-independent) Inf/NaN a naive summation would produce.
-  return isfinite(s) ? s + c : s;
+  return isfinite(sum) ? sum + comp : sum;
+}
+
+// Kept as a name for the small-batch scans (n <= 1024: one load batch).
+__device__ __forceinline__ double warp_dot64_1k(const double* __restrict__ row, const double* __restrict__ q, int n,
+                                                int lane) {
+  return warp_dot64(row, q, n, lane);
 }
 
 __device__ __forceinline__ double warp_max_d(double v) {
@@ -129,7 +148,7 @@ static __device__ __noinline__ float write_row_all(const double* __restrict__ sr
     const double v = src[i];
     rb.r64[(size_t)slot * Dp + i] = v;
     rb.r16[(size_t)slot * Dp + i] = __double2half(v);
-    rb.r8[(size_t)slot * Dp + i] = int8_quant(v, s);
+    rb.r8[(size_t)slot * rb.p8 + i] = int8_quant(v, s);
   }
   if (lane == 0) rb.rq[slot] = make_float2(s, __double2float_ru(l1 * (1.0 + 1e-12)));
   return s;

@@ -63,8 +63,9 @@ struct CtaRec {
 struct RingBufs {
   __half* r16;     // [C][Dp] fp16 RN (tensor-core scan, exhaustive fallback)
   double* r64;     // [C][Dp] float64 master (certified rescoring)
-  int8_t* r8;      // [C][Dp] int8, symmetric per-row scale (small-batch scan)
+  int8_t* r8;      // [C][p8] int8, symmetric per-row scale (small-batch scan), zero beyond Dp
   float2* rq;      // [C] (scale s >= max|e|/127, rounded up; ||e||_1, rounded up)
+  int p8;          // int8 row stride: Dp rounded up to 128 (whole TMA swizzle rows)
 };
 
 struct ShardMap {
@@ -119,6 +120,17 @@ cudaError_t launch_gemv8_scan(const RingBufs& rb, const RingState& st, int D, in
                               const QPrep* prep, const int8_t* q8, cudaStream_t s);
 
 bool gemv8_supported(int Dp);
+
+// TMA-streamed int8 scan (scan_stream8.cu): same contract as launch_gemv8_scan,
+// grid = one CTA per SM.  The plan holds the ring's tensor maps.
+struct S8Plan;
+bool stream8_supported(int Dp);
+S8Plan* s8_plan_create(int8_t* ring8, float2* ringq, long long C, int Dp, int P8, char* err, int errlen);
+void s8_plan_destroy(S8Plan* p);
+cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingState& st, const double* q64, int nb,
+                                CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
+                                const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
+                                const QPrep* prep, const int8_t* q8, cudaStream_t s);
 
 int gemv_grid(int sm_count);
 cudaError_t launch_l2_flush(void* buf, size_t bytes, cudaStream_t s);  // measurement: evict L2 by reading

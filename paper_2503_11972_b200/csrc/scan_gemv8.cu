@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(G8_THREADS, NB == 1 ? 2 : 1)
       for (int j = 0; j < LPG; ++j) {
         const int f = lane + 32 * j;
         const long long row = base + g * G + f / N16;
-        v[g][j] = row < r1 ? ld_stream16(rb.r8 + (size_t)ring_slot(st, row) * Dp + (f % N16) * 16)
+        v[g][j] = row < r1 ? ld_stream16(rb.r8 + (size_t)ring_slot(st, row) * rb.p8 + (f % N16) * 16)
                            : make_uint4(0, 0, 0, 0);
       }
     const long long row = base + lane;

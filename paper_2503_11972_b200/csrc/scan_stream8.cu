@@ -1,0 +1,770 @@
+// K2s — batch-1..4 scan over the int8 ring copy, streamed through TMA.
+//
+// The default small-batch path (C2: 100k x 768, B = 1).  It replaces the
+// `_buf[_lo:_hi] @ q` dgemv of cache.py:254 for the filtering pass and keeps
+// the certified float64 decision of K2q (scan_gemv8.cu), with the same error
+// model and the same CtaRec / last-CTA merge contract:
+//
+//   per row e:  approx = s_e s_q Σ ê_i q̂_i   (exact int32 dot, exact scaling)
+//               delta_e = ½ s_q ||e||_1 + ½ s_e s_q ||q̂||_1  (rigorous bound)
+//               l = approx - delta_e <= e·q <= u = approx + delta_e
+//   a row with u < L - 1e-9, where L <= the exact score of some other row,
+//   can neither be nor tie the best; every other row is rescored in float64.
+//
+// Layout of one CTA (one per SM, persistent over its row range):
+//   warp 0      producer: one 1-D bulk copy (cp.async.bulk, TMA engine) of a
+//               stage's 32*R contiguous ring rows plus one of their
+//               (s_e, ||e||_1) pairs; nst stages in flight.  One large copy
+//               per stage: the TMA engine's per-operation cost caps small
+//               (4-8 KB) boxes well below HBM rate (scripts/tma_microbench.cu).
+//   warps 1..8  consumers: warp w owns stage buffer w; lane = row, so the
+//               int32 dot needs no cross-lane reduction.  Lane l walks its
+//               row's 16-byte chunks starting at chunk l (rotated order): with
+//               the row stride a multiple of 128 B, the 8 lanes of a shared-
+//               memory phase then hit 8 distinct bank groups.  A row that
+//               survives the bound is pushed to the warp's candidate queue.
+//   warp 9      rescorer: pending appends (CTA 0), a pool member, then the CTA
+//               record, the ticket and — in the last CTA — the merge and
+//               the decision (cache.py:255-260, select_k :112-117).
+//   warp 10     bound poller: while the CTA streams, folds the other CTAs'
+//               bound into the CTA's and prefetches the leading candidate's
+//               float64 row into L2.
+// Rescoring is lazy: it starts when the CTA's scan is over, and then the
+// rescorer and the eight consumer warps form a pool that claims candidates
+// best-first (see `pool`).
+// The lower bound L is shared three ways: per warp (registers), per CTA
+// (shared-memory atomicMax on an order-preserving float key) and across
+// CTAs (fire-and-forget atomicMax on 8 replicas of the global gmax word; the
+// poller folds the global value back into the CTA's).
+//
+// Pending appends (rows added since the last lookup) are not in the int8
+// copy yet: CTA 0's rescorer writes every ring copy and scores them exactly
+// from the envelope at kernel start.
+//
+// Algorithmic bytes per launch: count * (P8 + 8) + nb * (9 * Dp + 40), P8 = Dp rounded up to 128.
+#include <cstdio>
+#include <cstdlib>
+
+#include "merge.cuh"
+#include "sm100.cuh"
+
+namespace mc {
+
+constexpr int S8_CW = 8;                       // consumer warps (max)
+constexpr int S8_THREADS = (S8_CW + 3) * 32;   // producer + consumers + rescorer + bound poller
+constexpr int S8_QCAP = 128;                   // candidate queue entries per consumer warp
+constexpr int S8_GSTRIDE = 256;                // gmax words per query: S8_GREP replicas, 128 B apart
+constexpr int S8_GREP = 8;                     // replicas of the global bound (spreads the hot line)
+// Only the poller warp touches the global bound: a fence, an acquire/release
+// or a bar.sync waits for the warp's outstanding global operations, and a
+// red to a hot line can take microseconds — so the warps that synchronise
+// (consumers, pool, rescorer) never have one in flight.  For the same reason
+// measurement stamps go to shared memory and are written out at the end.
+constexpr int S8_PUB0 = 32 - S8_GREP;          // poller lanes S8_PUB0.. own one replica each
+// per-CTA measurement slots (MC_GEMV_TIMING=1), timing[8 + 8 * cta + k]
+enum { S8T_SCAN = 0, S8T_POOL, S8T_R0, S8T_R1, S8T_POOLX, S8T_REC, S8T_PUSH, S8T_RESC };
+
+__host__ __device__ constexpr int s8_rows_per_lane(int kb) { return kb >= 4 ? 1 : (kb == 1 ? 4 : 2); }
+
+__device__ __forceinline__ unsigned s8_key(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float s8_val(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+__device__ __forceinline__ int dp16x(const uint4& a, const uint4& b, int acc) {
+  acc = __dp4a((int)a.x, (int)b.x, acc);
+  acc = __dp4a((int)a.y, (int)b.y, acc);
+  acc = __dp4a((int)a.z, (int)b.z, acc);
+  return __dp4a((int)a.w, (int)b.w, acc);
+}
+
+__device__ __forceinline__ int ld_acq_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_vol_u32(const unsigned* p) { return *(const volatile unsigned*)p; }
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long s8_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct S8Args {
+  unsigned* counter;           // last-CTA ticket (zero between launches)
+  unsigned* gmax;              // [(b0 + b) * S8_GSTRIDE + 32 r] global lower-bound key replicas (zero between launches)
+  Thresholds thr;
+  mc_record* rec;
+  OutRec* out;
+  unsigned long long* timing;  // optional phase stamps (MC_GEMV_TIMING=1)
+  const QPrep* prep;           // [nb] per-query quantisation (host-computed, in the envelope)
+  const int8_t* q8;            // [nb][Dp] q̂
+  const double* stage;         // pending appends (float64, stride Dp)
+  long long n_app;
+  RingState* d_state;
+};
+
+// Rows [r0, r1) (live-local) of one CTA, cut into stages of up to `rows`
+// rows that never cross the physical end of the ring.
+struct S8Work {
+  long long r0, r1, w;  // w = first row that wraps to slot 0
+  int ns1, ns, rows;
+  __device__ void init(const RingState& st, long long n_scan, int cta, int grid, int rows_) {
+    rows = rows_;
+    r0 = n_scan * cta / grid;
+    r1 = n_scan * (cta + 1) / grid;
+    w = st.cap - st.head;
+    const long long e1 = min(r1, max(r0, w));
+    const long long b2 = max(r0, w);
+    ns1 = (int)((e1 - r0 + rows - 1) / rows);
+    ns = ns1 + (int)(r1 > b2 ? (r1 - b2 + rows - 1) / rows : 0);
+  }
+  // stage i -> first live row, row count, first physical slot
+  __device__ void stage(int i, const RingState& st, long long& row0, int& n, long long& slot0) const {
+    long long end;
+    if (i < ns1) {
+      row0 = r0 + (long long)i * rows;
+      end = min(row0 + rows, min(r1, max(r0, w)));
+    } else {
+      row0 = max(r0, w) + (long long)(i - ns1) * rows;
+      end = min(row0 + rows, r1);
+    }
+    n = (int)(end - row0);
+    slot0 = row0 < w ? st.head + row0 : st.head + row0 - st.cap;
+  }
+};
+
+template <int KB, int NB>
+__global__ void __launch_bounds__(S8_THREADS, 1)
+    k_stream8_scan(RingBufs rb, const RingState st,
+                   const double* __restrict__ q64, int nb, CtaRec* __restrict__ cta, int b0, ShardMap sm,
+                   S8Args a, int nst, int Dp) {
+  constexpr int P8 = KB * 128;                // int8 row stride (Dp rounded up to 128)
+  constexpr int R = s8_rows_per_lane(KB);
+  constexpr int SROWS = 32 * R;               // rows per stage
+  constexpr int NCH = P8 / 16;                // 16-byte chunks per int8 row (a multiple of 8)
+  constexpr int SDATA = SROWS * P8;           // int8 bytes of a stage
+  constexpr int RQS = SROWS + 2;              // (s, L1) entries per stage buffer (16-byte aligned copy)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stages = base;                                            // [nst][SDATA]
+  float2* rqs = reinterpret_cast<float2*>(base + (size_t)nst * SDATA);  // [nst][RQS]
+  int8_t* sq8 = reinterpret_cast<int8_t*>(rqs + (size_t)nst * RQS);     // [NB][P8]
+  double* sq64 = reinterpret_cast<double*>(sq8 + NB * P8);              // [NB][Dp] float64 queries
+
+  __shared__ __align__(8) uint64_t full[S8_CW], empty[S8_CW];
+  __shared__ float qu[S8_CW][S8_QCAP];
+  __shared__ long long qp[S8_CW][S8_QCAP];
+  __shared__ int qtail[S8_CW];
+  __shared__ float sh_ovf[S8_CW][NB];
+  __shared__ unsigned sh_bound[NB];
+  __shared__ int sh_done;
+  __shared__ int qc[S8_CW][S8_QCAP];      // claim flags of the rescoring pool
+  __shared__ Best2 sh_best[S8_CW + 1][NB];  // each pool warp's float64 best
+  __shared__ int sh_pool_done;
+  __shared__ unsigned long long sh_t[8];  // measurement stamps (MC_GEMV_TIMING=1)
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const long long n = st.count;
+  const long long n_pend = min(a.n_app, n);
+  const long long n_scan = n - n_pend;  // rows [n_scan, n) are scored exactly by CTA 0
+  S8Work wk;
+  wk.init(st, n_scan, blockIdx.x, gridDim.x, SROWS);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nst; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int b = 0; b < NB; ++b) sh_bound[b] = s8_key(-INFINITY);
+    sh_done = 0;
+    sh_pool_done = 0;
+    if (blockIdx.x == 0 && a.d_state) *a.d_state = st;
+    for (int k = 0; k < 8; ++k) sh_t[k] = 0ull;
+    sh_t[S8T_R0] = ~0ull;
+    if (a.timing) atomicMin(a.timing + 0, s8_timer());
+  }
+  if (threadIdx.x < S8_CW) qtail[threadIdx.x] = 0;
+  for (int i = threadIdx.x; i < S8_CW * S8_QCAP; i += blockDim.x) (&qc[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < NB * Dp; i += blockDim.x) sq64[i] = i < nb * Dp ? q64[i] : 0.0;
+  for (int i = threadIdx.x; i < NB * P8 / 16; i += blockDim.x) {  // q̂ (stride Dp) -> [NB][P8], zero-padded
+    const int b = i / (P8 / 16), c = i % (P8 / 16);
+    reinterpret_cast<uint4*>(sq8)[i] = (b < nb && c < Dp / 16)
+                                           ? reinterpret_cast<const uint4*>(a.q8 + (size_t)b * Dp)[c]
+                                           : make_uint4(0u, 0u, 0u, 0u);
+  }
+  __syncthreads();
+
+  const int ncw = min(nst, S8_CW);
+  unsigned* const gq = a.gmax + (size_t)b0 * S8_GSTRIDE;  // this launch's queries
+  auto raise = [&](int b, double sc) {  // an exact score is a lower bound for everyone (the poller publishes it)
+    if (lane == 0 && !isnan(sc)) atomicMax(&sh_bound[b], s8_key(__double2float_rd(sc)));
+  };
+  const bool timing = a.timing != nullptr;
+  auto stamp_max = [&](int k) { atomicMax(&sh_t[k], s8_timer()); };  // shared memory only
+  // Rescoring pool (the rescorer warp from the start, each consumer warp once
+  // its stages are done).  Best-first: claim the live candidate with the
+  // largest upper bound and rescore it in float64; its exact score then prunes
+  // the rest.  Candidates whose bound fell below the CTA's lower bound are
+  // retired without rescoring.  The poller also folds the global bound in.
+  // Rescoring pool: the rescorer warp and the consumer warps, once every
+  // consumer is done (a hardware barrier, no spinning beside the streaming
+  // warps).  Lazy: nothing is rescored while the CTA still streams (those
+  // loads would queue behind the scan's, and the bound keeps rising).
+  // Best-first: claim the live candidate with the largest upper bound and
+  // rescore it in float64; its exact score then prunes the rest.  Candidates
+  // whose bound fell below the CTA's lower bound are retired unscored.
+  auto pool = [&](int wid, Best2 (&best)[NB]) {
+    asm volatile("bar.sync 1, %0;" ::"n"((S8_CW + 1) * 32) : "memory");
+    if (timing && lane == 0) stamp_max(S8T_POOL);
+    int tails = 0;  // lane w < ncw: final tail of queue w
+    if (lane < ncw) tails = *(volatile int*)&qtail[lane];
+    while (true) {
+      float bu = -INFINITY;
+      int bi = -1;
+      for (int w = 0; w < ncw; ++w) {
+        const int t = __shfl_sync(FULL, tails, w);
+        for (int i = lane; i < t; i += 32) {
+          const float u = *(volatile float*)&qu[w][i];
+          if (u == -INFINITY || *(volatile int*)&qc[w][i]) continue;
+          const int b = (int)(qp[w][i] & 3);
+          if ((double)u < (double)s8_val(ld_vol_u32(&sh_bound[b])) - 1e-9) {
+            qu[w][i] = -INFINITY;  // retired: strictly below a row whose exact score is known to exceed it
+            continue;
+          }
+          if (u > bu) {
+            bu = u;
+            bi = w * S8_QCAP + i;
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const float ou = __shfl_xor_sync(FULL, bu, off);
+        const int oi = __shfl_xor_sync(FULL, bi, off);
+        if (ou > bu || (ou == bu && oi > bi)) {
+          bu = ou;
+          bi = oi;
+        }
+      }
+      if (bi < 0) break;  // nothing live and unclaimed is left (claimed ones finish with their claimer)
+      const int w = bi / S8_QCAP, i = bi % S8_QCAP;
+      int won = 0;
+      if (lane == 0) won = atomicCAS(&qc[w][i], 0, 1) == 0;
+      if (__shfl_sync(FULL, won, 0)) {
+        const long long pb = qp[w][i];
+        const int b = (int)(pb & 3);
+        const long long p = pb >> 2;
+        const long long slot = ring_slot(st, local_row(st, p, sm));
+        if (timing && lane == 0) atomicMin(&sh_t[S8T_R0], s8_timer());
+        const double sc = warp_dot64(rb.r64 + (size_t)slot * Dp, sq64 + (size_t)b * Dp, Dp, lane);
+        if (timing && lane == 0) stamp_max(S8T_R1);
+#pragma unroll
+        for (int bb = 0; bb < NB; ++bb)
+          if (bb == b) best[bb].add(sc, p);
+        raise(b, sc);
+        if (timing && lane == 0) atomicAdd(&sh_t[S8T_RESC], 1ull);
+        __syncwarp();
+        if (lane == 0) qu[w][i] = -INFINITY;
+      }
+      __syncwarp();
+    }
+    if (timing && lane == 0) stamp_max(S8T_POOLX);
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (lane == 0) sh_best[wid][b] = best[b];
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      atomicAdd(&sh_pool_done, 1);
+    }
+  };
+
+  if (warp == S8_CW + 2) {
+    // ------------------------------------------------------------ bound poller
+    // Until the pool is done: carry the CTA's bound to the other CTAs (lane
+    // S8_PUB0 + r owns replica r), fold theirs in (replica cta % S8_GREP), and
+    // while the CTA streams pull the leading candidate's float64 row into L2
+    // so its rescoring after the scan hits L2.  This warp never synchronises.
+    int pf = -1;
+    unsigned pub[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) pub[b] = 0u;
+    while (*(volatile int*)&sh_pool_done != S8_CW + 1) {
+      unsigned gk = 0;
+      if (lane >= S8_PUB0 && lane - S8_PUB0 < nb)
+        gk = ld_relaxed_gpu(gq + (lane - S8_PUB0) * S8_GSTRIDE + 32 * (blockIdx.x % S8_GREP));
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const unsigned mine = ld_vol_u32(&sh_bound[b]);
+        if (b < nb && mine > pub[b]) {
+          if (lane >= S8_PUB0) atomicMax(gq + b * S8_GSTRIDE + 32 * (lane - S8_PUB0), mine);
+          pub[b] = mine;
+        }
+      }
+      if (*(volatile int*)&sh_done != S8_CW) {
+        float bu = -INFINITY;
+        int bi = -1;
+        for (int w = 0; w < ncw; ++w) {
+          const int t = *(volatile int*)&qtail[w];
+          for (int i = lane; i < t; i += 32) {
+            const float u = *(volatile float*)&qu[w][i];
+            if (u > bu) {
+              bu = u;
+              bi = w * S8_QCAP + i;
+            }
+          }
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+          const float ou = __shfl_xor_sync(FULL, bu, off);
+          const int oi = __shfl_xor_sync(FULL, bi, off);
+          if (ou > bu || (ou == bu && oi > bi)) {
+            bu = ou;
+            bi = oi;
+          }
+        }
+        if (bi >= 0 && bi != pf) {
+          pf = bi;
+          const long long p = qp[bi / S8_QCAP][bi % S8_QCAP] >> 2;
+          const char* row = reinterpret_cast<const char*>(rb.r64 + (size_t)ring_slot(st, local_row(st, p, sm)) * Dp);
+          for (int off = lane * 128; off < Dp * 8; off += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + off));
+        }
+      }
+      if (gk && gk > ld_vol_u32(&sh_bound[lane - S8_PUB0])) atomicMax(&sh_bound[lane - S8_PUB0], gk);
+      __syncwarp();
+    }
+    return;
+  }
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      for (int i = 0; i < wk.ns; ++i) {
+        const int buf = i % nst;
+        mbar_wait(&empty[buf], ((i / nst) & 1) ^ 1);
+        long long row0, slot0;
+        int nr;
+        wk.stage(i, st, row0, nr, slot0);
+        const long long q0 = slot0 & ~1ll;    // (s, L1) pairs from a 16-byte aligned slot
+        const uint32_t qbytes = (uint32_t)(((slot0 - q0) + nr + 1) / 2 * 16);
+        const uint32_t dbytes = (uint32_t)nr * P8;
+        mbar_expect_tx(&full[buf], dbytes + qbytes);
+        bulk_load(stages + (size_t)buf * SDATA, rb.r8 + (size_t)slot0 * P8, dbytes, &full[buf]);
+        bulk_load(rqs + (size_t)buf * RQS, rb.rq + q0, qbytes, &full[buf]);
+      }
+    }
+  } else if (warp <= S8_CW) {
+    // ------------------------------------------------------------ consumers
+    const int cw = warp - 1;
+    double sq[NB], q1[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const QPrep pq = b < nb ? a.prep[b] : QPrep{0.0, 0.0, 0.0, 0.f, 0};
+      sq[b] = pq.s;
+      q1[b] = pq.q1;
+    }
+    float lo[NB], ovf[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      lo[b] = -INFINITY;
+      ovf[b] = -INFINITY;
+    }
+    int tail = 0;
+    if (cw < ncw) {
+      for (int i = cw; i < wk.ns; i += ncw) {
+        const int buf = i % nst;
+        long long row0, slot0;
+        int nr;
+        wk.stage(i, st, row0, nr, slot0);
+        mbar_wait(&full[buf], (i / nst) & 1);
+        const uint8_t* sb = stages + (size_t)buf * SDATA;
+        int acc[R][NB], acc2[R][NB];  // two chains per dot (exact integers: order is free)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int b = 0; b < NB; ++b) acc[r][b] = acc2[r][b] = 0;
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          int c = j + lane;  // rotated chunk order (conflict-free, see the header)
+          c = c >= NCH ? c - NCH : c;
+          c = c >= NCH ? c - NCH : c;
+          uint4 v[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) v[r] = *reinterpret_cast<const uint4*>(sb + (r * 32 + lane) * P8 + c * 16);
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            const uint4 qv = *reinterpret_cast<const uint4*>(sq8 + b * P8 + c * 16);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              if (j & 1)
+                acc2[r][b] = dp16x(v[r], qv, acc2[r][b]);
+              else
+                acc[r][b] = dp16x(v[r], qv, acc[r][b]);
+            }
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int b = 0; b < NB; ++b) acc[r][b] += acc2[r][b];
+        float2 e[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) e[r] = rqs[(size_t)buf * RQS + (slot0 & 1) + r * 32 + lane];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[buf]);
+
+        // bounds: the warp's own, then the CTA's (which carries the global one)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const bool valid = r * 32 + lane < nr;
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            if (b >= nb) break;
+            const double approx = (double)acc[r][b] * ((double)e[r].x * sq[b]);
+            const double dl = (0.5 * sq[b] * (double)e[r].y + 0.5 * (double)e[r].x * q1[b]) * (1.0 + 1e-9) + 1e-12;
+            float lf = valid ? __double2float_rd(approx - dl) : -INFINITY;
+#pragma unroll
+            for (int off = 16; off; off >>= 1) lf = fmaxf(lf, __shfl_xor_sync(FULL, lf, off));
+            float bnd = s8_val(ld_vol_u32(&sh_bound[b]));
+            if (lf > lo[b]) {
+              lo[b] = lf;
+              if (lf > bnd) {  // publish to the CTA (the poller carries it to the other CTAs)
+                if (lane == 0) atomicMax(&sh_bound[b], s8_key(lf));
+                bnd = lf;
+              }
+            }
+            const double u = approx + dl;
+            const bool keep = valid && u >= (double)bnd - 1e-9;
+            const unsigned m = __ballot_sync(FULL, keep);
+            if (m) {
+              const int idx = tail + __popc(m & ((1u << lane) - 1u));
+              if (keep) {
+                const float uf = __double2float_ru(u);
+                if (idx < S8_QCAP) {
+                  qu[cw][idx] = uf;
+                  qp[cw][idx] = (global_pos(st, row0 + r * 32 + lane, sm) << 2) | b;
+                } else {
+                  ovf[b] = fmaxf(ovf[b], uf);
+                }
+              }
+              if (timing && lane == 0) atomicAdd(&sh_t[S8T_PUSH], (unsigned long long)__popc(m));
+              tail = min(tail + __popc(m), S8_QCAP);
+              __syncwarp();
+              if (lane == 0) st_rel_cta(&qtail[cw], tail);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      float o = ovf[b];
+#pragma unroll
+      for (int off = 16; off; off >>= 1) o = fmaxf(o, __shfl_xor_sync(FULL, o, off));
+      if (lane == 0) sh_ovf[cw][b] = o;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      atomicAdd(&sh_done, 1);
+    }
+    if (timing && lane == 0) stamp_max(S8T_SCAN);
+    Best2 best[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) best[b].init();
+    pool(cw, best);
+  } else {
+    // ------------------------------------------------------------ rescorer
+    Best2 best[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) best[b].init();
+    if (blockIdx.x == 0 && n_pend > 0) {  // rows appended since the last lookup
+      for (long long i = 0; i < n_pend; ++i) {
+        const double* srow = a.stage + (size_t)(a.n_app - n_pend + i) * Dp;
+        const long long row = n_scan + i;
+        write_row_all(srow, ring_slot(st, row), rb, Dp, lane);
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          if (b >= nb) break;
+          const double sc = warp_dot64(srow, sq64 + (size_t)b * Dp, Dp, lane);
+          best[b].add(sc, global_pos(st, row, sm));
+          raise(b, sc);
+        }
+      }
+    }
+    pool(S8_CW, best);
+    if (lane == 0)
+      while (ld_acq_cta(&sh_pool_done) != S8_CW + 1) {
+      }
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      for (int w = 0; w < S8_CW; ++w) best[b].merge(sh_best[w][b]);
+    // CTA records
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      if (b >= nb) break;
+      float ov = -INFINITY;
+      for (int w = 0; w < ncw; ++w) ov = fmaxf(ov, sh_ovf[w][b]);
+      if (lane == 0) {
+        CtaRec r;
+        r.s = best[b].s;
+        r.s2 = best[b].s2;
+        r.p = best[b].p;
+        r.ovf = ov;
+        r.ties = best[b].ties;
+        cta[(size_t)(b0 + b) * gridDim.x + blockIdx.x] = r;
+      }
+    }
+    if (timing && lane == 0) sh_t[S8T_REC] = s8_timer();
+    __syncwarp();
+    auto dump = [&]() {  // measurement stamps, written once this CTA is off the critical path
+      if (timing && lane < 8) a.timing[8 + 8 * blockIdx.x + lane] = sh_t[lane];
+    };
+    unsigned exotic = 0;  // loaded before the ticket (off the tail's critical path)
+    if (lane < nb) exotic = a.prep[lane].exotic != 0 ? 1u : 0u;
+    // ticket; the last CTA merges every record and decides
+    unsigned old = 0;
+    if (lane == 0)
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.counter) : "memory");
+    old = __shfl_sync(FULL, old, 0);
+    if (old != gridDim.x - 1) {
+      dump();
+      return;
+    }
+    __threadfence();
+    if (lane == 0 && a.timing) a.timing[4] = s8_timer();
+    // Merge the per-CTA records with independent warp reductions (no chain of
+    // Best2 merges): best = max s; among records at best: max position and the
+    // summed tie counts; runner-up = max over the others' s and everyone's s2
+    // (a second record at the best makes the runner-up equal to it, as in
+    // Best2::merge).  Record similarities are finite here (exotic queries are
+    // flagged for the exhaustive path).
+    for (int b = 0; b < nb; ++b) {
+      const int gb = b0 + b;
+      constexpr int PER = 5;  // records per lane, all loaded before use (grid <= 160: one round trip)
+      double rs[PER], rs2[PER];
+      long long rp[PER];
+      int rt[PER];
+      float ro[PER];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int c = 32 * k + lane;
+        rp[k] = -1;
+        rs[k] = rs2[k] = -INFINITY;
+        rt[k] = 0;
+        ro[k] = -INFINITY;
+        if (c < (int)gridDim.x) {
+          const CtaRec* src = cta + (size_t)gb * gridDim.x + c;
+          rs[k] = __ldcg(&src->s);
+          rs2[k] = __ldcg(&src->s2);
+          rp[k] = __ldcg(&src->p);
+          rt[k] = __ldcg(&src->ties);
+          ro[k] = __ldcg(&src->ovf);
+        }
+      }
+      for (int c0 = 32 * PER; c0 < (int)gridDim.x; c0 += 32) {  // grids beyond 160 CTAs
+        const int c = c0 + lane;
+        if (c < (int)gridDim.x) {
+          const CtaRec* src = cta + (size_t)gb * gridDim.x + c;
+          const double xs = __ldcg(&src->s), xs2 = __ldcg(&src->s2);
+          const long long xp = __ldcg(&src->p);
+          const int xt = __ldcg(&src->ties);
+          ro[0] = fmaxf(ro[0], __ldcg(&src->ovf));
+          if (xp >= 0) {  // fold into slot 0 with Best2 semantics
+            Best2 m0, mx;
+            m0.init();
+            if (rp[0] >= 0) {
+              m0.s = rs[0];
+              m0.s2 = rs2[0];
+              m0.p = rp[0];
+              m0.ties = rt[0];
+            }
+            mx.s = xs;
+            mx.s2 = xs2;
+            mx.p = xp;
+            mx.ties = xt;
+            m0.merge(mx);
+            rs[0] = m0.s;
+            rs2[0] = m0.s2;
+            rp[0] = m0.p;
+            rt[0] = m0.ties;
+          }
+        }
+      }
+      if (b == 0 && lane == 0 && a.timing) a.timing[5] = s8_timer();
+      double bs = -INFINITY;
+      float ov = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        if (rp[k] >= 0) bs = fmax(bs, rs[k]);
+        ov = fmaxf(ov, ro[k]);
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        bs = fmax(bs, __shfl_xor_sync(FULL, bs, off));
+        ov = fmaxf(ov, __shfl_xor_sync(FULL, ov, off));
+      }
+      long long bp = -1;
+      int nt = 0, neq = 0;
+      double s2 = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        if (rp[k] < 0) continue;
+        if (rs[k] == bs) {
+          bp = max(bp, rp[k]);
+          nt += rt[k];
+          ++neq;
+        } else {
+          s2 = fmax(s2, rs[k]);
+        }
+        s2 = fmax(s2, rs2[k]);
+      }
+      nt = __reduce_add_sync(FULL, (unsigned)nt);
+      neq = __reduce_add_sync(FULL, (unsigned)neq);
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        bp = max(bp, __shfl_xor_sync(FULL, bp, off));
+        s2 = fmax(s2, __shfl_xor_sync(FULL, s2, off));
+      }
+      if (neq >= 2) s2 = bs;
+      const bool exo = __shfl_sync(FULL, exotic, b) != 0;
+      if (lane == 0) {
+        const bool fail = bp < 0 || !(ov == -INFINITY || (double)ov + 1e-9 < bs);
+        mc_record r;
+        r.sim = bs;
+        r.second = s2;
+        r.pos = bp;
+        r.flags = (nt >= 2 ? MC_FLAG_TIE : 0u) | (fail ? FLAG_NEED_FALLBACK : 0u) | (exo ? FLAG_NEED_EXHAUSTIVE : 0u);
+        r.reserved = 0;
+        a.rec[gb] = r;
+        if (a.out) a.out[gb] = decide(record_best(r), r.flags & FLAG_NEED_ANY, st.jhead, a.thr);
+      }
+      if (lane < S8_GREP) a.gmax[(size_t)gb * S8_GSTRIDE + 32 * lane] = 0u;
+    }
+    if (lane == 0) {
+      *a.counter = 0u;
+      if (a.timing) a.timing[3] = s8_timer();
+    }
+    dump();
+  }
+}
+
+// ---------------------------------------------------------------- host side
+struct S8Plan {
+  int Dp = 0;
+  int P8 = 0;
+  int nst[2] = {0, 0};      // stages in flight (NB = 1, 4)
+  size_t smem[2] = {0, 0};  // dynamic shared memory (NB = 1, 4)
+};
+
+bool stream8_supported(int Dp) { return Dp % 64 == 0 && Dp >= 64 && Dp <= 1024; }
+
+static size_t s8_smem(int P8, int Dp, int nst, int NB) {
+  const int rows = 32 * s8_rows_per_lane(P8 / 128);
+  return 1024 + (size_t)nst * rows * P8 + (size_t)nst * (rows + 2) * 8 + (size_t)NB * P8 + (size_t)NB * Dp * 8;
+}
+
+// Stage count: as many (<= S8_CW) as fit next to the kernel's static shared memory.
+static int s8_fit(int P8, int Dp, int NB, size_t static_smem, size_t optin) {
+  int nst = S8_CW;
+  while (nst > 1 && static_smem + s8_smem(P8, Dp, nst, NB) > optin) --nst;
+  return nst;
+}
+template <int KB>
+static cudaError_t s8_attr(S8Plan* p) {  // sizes the stages, raises the smem limit
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa1, fa4;
+  if ((e = cudaFuncGetAttributes(&fa1, k_stream8_scan<KB, 1>)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fa4, k_stream8_scan<KB, 4>)) != cudaSuccess) return e;
+  p->nst[0] = s8_fit(p->P8, p->Dp, 1, fa1.sharedSizeBytes, (size_t)optin);
+  p->nst[1] = s8_fit(p->P8, p->Dp, 4, fa4.sharedSizeBytes, (size_t)optin);
+  p->smem[0] = s8_smem(p->P8, p->Dp, p->nst[0], 1);
+  p->smem[1] = s8_smem(p->P8, p->Dp, p->nst[1], 4);
+  e = cudaFuncSetAttribute(k_stream8_scan<KB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem[0]);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_stream8_scan<KB, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem[1]);
+}
+
+S8Plan* s8_plan_create(int8_t* ring8, float2* ringq, long long C, int Dp, int P8, char* err, int errlen) {
+  (void)ring8;
+  (void)ringq;
+  (void)C;
+  if (!stream8_supported(Dp) || P8 % 128 != 0 || P8 < Dp) {
+    snprintf(err, errlen, "stream8 scan needs 64 | Dp <= 1024 and 128 | P8 (Dp=%d, P8=%d)", Dp, P8);
+    return nullptr;
+  }
+  S8Plan* p = new S8Plan();
+  p->Dp = Dp;
+  p->P8 = P8;
+  cudaError_t e;
+  switch (P8 / 128) {
+    case 1: e = s8_attr<1>(p); break;
+    case 2: e = s8_attr<2>(p); break;
+    case 3: e = s8_attr<3>(p); break;
+    case 4: e = s8_attr<4>(p); break;
+    case 5: e = s8_attr<5>(p); break;
+    case 6: e = s8_attr<6>(p); break;
+    case 7: e = s8_attr<7>(p); break;
+    default: e = s8_attr<8>(p); break;
+  }
+  if (e != cudaSuccess) {
+    snprintf(err, errlen, "cannot raise dynamic shared memory to %zu bytes: %s", p->smem[1], cudaGetErrorString(e));
+    delete p;
+    return nullptr;
+  }
+  return p;
+}
+
+void s8_plan_destroy(S8Plan* p) { delete p; }
+
+template <int KB>
+static cudaError_t s8_launch(const S8Plan* p, const RingBufs& rb, const RingState& st, const double* q64, int nb,
+                             CtaRec* cta, int b0, int grid, ShardMap sm, const S8Args& a, cudaStream_t s) {
+  if (nb == 1)
+    k_stream8_scan<KB, 1><<<grid, S8_THREADS, p->smem[0], s>>>(rb, st, q64, nb, cta, b0, sm, a,
+                                                                p->nst[0], p->Dp);
+  else
+    k_stream8_scan<KB, 4><<<grid, S8_THREADS, p->smem[1], s>>>(rb, st, q64, nb, cta, b0, sm, a,
+                                                                p->nst[1], p->Dp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingState& st, const double* q64, int nb,
+                                CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
+                                const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
+                                const QPrep* prep, const int8_t* q8, cudaStream_t s) {
+  if (!p || nb < 1 || nb > 4) return cudaErrorInvalidValue;
+  S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), prep, q8, app.stage, app.n, app.d_state};
+  switch (p->P8 / 128) {
+    case 1: return s8_launch<1>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
+    case 2: return s8_launch<2>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
+    case 3: return s8_launch<3>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
+    case 4: return s8_launch<4>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
+    case 5: return s8_launch<5>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
+    case 6: return s8_launch<6>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
+    case 7: return s8_launch<7>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
+    case 8: return s8_launch<8>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace mc

@@ -1,6 +1,6 @@
 """Drive one BASELINE config through the native ring for ncu / timing (no oracle, no host metadata).
 
-    python scripts/profile_case.py c2|c3 [--iters N] [--path auto|gemv|gemm]
+    python scripts/profile_case.py c2|c3 [--iters N] [--path auto|gemv|gemm|gemv8|stream8]
 """
 import argparse
 import sys
@@ -28,7 +28,7 @@ wl = ClusteredWorkload(dim, n_clusters=512, seed=17)
 rows = wl.cache_rows(n)
 ring = _native.DeviceRing(n, dim, 0)
 ring.append(rows)
-ring.set_path({"auto": 0, "gemv": 1, "gemm": 2}[a.path])
+ring.set_path({"auto": 0, "gemv": 1, "gemm": 2, "gemv8": 5, "stream8": 6}[a.path])
 t = ThresholdTable.default()
 ring.set_table(t.pairs, t.total_steps)
 Q = wl.queries(B * a.iters).reshape(a.iters, B, dim)
@@ -41,10 +41,33 @@ if os.environ.get("MC_GEMV_TIMING"):
     import ctypes  # noqa: E402
     lib = _native.load()
     lib.mc_debug_gemv_timing.restype = ctypes.c_int
-    t = (ctypes.c_ulonglong * 4)()
+    t = (ctypes.c_ulonglong * 8)()
+    per = (ctypes.c_ulonglong * (8 * 512))()
     for i in range(a.iters):
         lib.mc_debug_gemv_timing(t, 1)  # reset
         ring.retrieve(Q[i])
         lib.mc_debug_gemv_timing(t, 0)
-        print("gemv phases (us): scan %.1f  rescore %.1f  tail %.1f  total %.1f" % (
-            (t[1] - t[0]) / 1e3, (t[2] - t[1]) / 1e3, (t[3] - t[2]) / 1e3, (t[3] - t[0]) / 1e3))
+        if not t[4]:  # register GEMV kernels: four global stamps
+            print("gemv phases (us): scan %.1f  rescore %.1f  tail %.1f  total %.1f" % (
+                (t[1] - t[0]) / 1e3, (t[2] - t[1]) / 1e3, (t[3] - t[2]) / 1e3, (t[3] - t[0]) / 1e3))
+            continue
+        lib.mc_debug_gemv_timing(per, 2)
+        import numpy as _np
+        arr = _np.array(per[:8 * 148], dtype=_np.float64).reshape(148, 8)
+        t0 = float(t[0])
+        rel = lambda v: (v - t0) / 1e3  # noqa: E731
+        scan_end, pool, r0, r1, poolx, rec = (arr[:, k] for k in range(6))
+        r0 = _np.where(r0 > 1e19, _np.nan, r0)
+        print("stream8 (us): last scan end %.1f | last record %.1f | ticket->merge %.1f loads %.1f decide %.1f | total %.1f"
+              " | pushed %d rescored %d" % (rel(scan_end.max()), rel(rec.max()), (t[4] - rec.max()) / 1e3,
+                                             (t[5] - t[4]) / 1e3, (t[3] - t[5]) / 1e3, rel(t[3]),
+                                             arr[:, 6].sum(), arr[:, 7].sum()))
+        if i == a.iters - 1:
+            order = _np.argsort(-rec)
+            print("slowest CTAs: cta scan_end pool_entry resc_start resc_end pool_exit record n_resc (us)")
+            for c in order[:8]:
+                print("   %4d %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f %3d" % (c, rel(scan_end[c]), rel(pool[c]), rel(r0[c]),
+                                                                     rel(r1[c]) if r1[c] else _np.nan, rel(poolx[c]),
+                                                                     rel(rec[c]), arr[c, 7]))
+            print("median: scan_end %.1f pool_entry %.1f pool_exit %.1f record %.1f" % (
+                rel(_np.median(scan_end)), rel(_np.median(pool)), rel(_np.median(poolx)), rel(_np.median(rec))))

@@ -284,7 +284,8 @@ def test_reference_suite_kats_on_gpu():
 def _paths(cache, Q, table):
     out = {}
     for name, path in (("gemv", _native.PATH_GEMV), ("gemm", _native.PATH_GEMM), ("gemm1", _native.PATH_GEMM_1SM),
-                       ("gemm4", _native.PATH_GEMM_QUAD), ("gemv8", _native.PATH_GEMV8)):
+                       ("gemm4", _native.PATH_GEMM_QUAD), ("gemv8", _native.PATH_GEMV8),
+                       ("stream8", _native.PATH_STREAM8)):
         cache.ring.set_path(path)
         out[name] = cache.retrieve_flags(Q, table)
     cache.ring.set_path(_native.PATH_AUTO)
@@ -310,9 +311,10 @@ def test_tensor_core_scan_matches_gemv_and_oracle(dim, cap, n_ins, B):
     keep = ~((fv | fm) & AMBIG).astype(bool)
     assert np.array_equal(lv[keep], lm[keep]) and np.array_equal(kv, km)
     assert np.array_equal(sv, sm_)  # both certified float64 rescoring: bit-identical
-    l8, s8, k8, f8 = res["gemv8"]  # int8 GEMV: same certified answers
-    keep8 = ~((fv | f8) & AMBIG).astype(bool)
-    assert np.array_equal(lv[keep8], l8[keep8]) and np.array_equal(kv, k8) and np.array_equal(sv, s8)
+    for name in ("gemv8", "stream8"):  # int8 scans: same certified answers
+        l8, s8, k8, f8 = res[name]
+        keep8 = ~((fv | f8) & AMBIG).astype(bool)
+        assert np.array_equal(lv[keep8], l8[keep8]) and np.array_equal(kv, k8) and np.array_equal(sv, s8), name
     for other in ("gemm1", "gemm4"):  # CTA-pair vs single-CTA vs CTA-quad tensor-core kernels
         for a, b in zip(res["gemm"], res[other]):
             assert np.array_equal(a, b)
@@ -355,7 +357,7 @@ def test_int8_and_fp16_small_batch_paths_with_pending_appends(dim):
     wl = ClusteredWorkload(dim, n_clusters=24, seed=100 + dim)
     cap = 1500
     table, ot = ThresholdTable.default(), OracleTable()
-    for path in (_native.PATH_GEMV8, _native.PATH_GEMV):
+    for path in (_native.PATH_STREAM8, _native.PATH_GEMV8, _native.PATH_GEMV):
         c = SemanticCache(capacity=cap, dim=dim)
         o = OracleCache(cap, dim)
         c.ring.set_path(path)
@@ -371,3 +373,49 @@ def test_int8_and_fp16_small_batch_paths_with_pending_appends(dim):
                     assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (path, i)
                     assert r.k == k and _close(r.similarity, sim), (path, i, r, sim)
         c.close()
+
+
+def test_stream8_queue_overflow_falls_back_exactly():
+    """Streamed int8 scan with every row an exact duplicate: each row survives the bound, the
+    per-warp candidate queues overflow, the certificate fails and the exhaustive float64 path
+    answers — the newest duplicate, flagged as a tie."""
+    rng = np.random.default_rng(31)
+    d, n = 1024, 120_000
+    v = rng.standard_normal(d)
+    v /= np.linalg.norm(v)
+    c = SemanticCache(capacity=n, dim=d)
+    block = np.repeat(v[None, :], 10_000, axis=0)
+    for _ in range(n // 10_000):
+        c.ring.append(block)
+    Q = np.stack([v] + [wl_noise(v[None, :], rng)[0] for _ in range(3)])
+    c.ring.set_path(_native.PATH_STREAM8)
+    for B in (1, 2, 3, 4):
+        live, sim, k, flags = c.retrieve_flags(Q[:B], ThresholdTable.default())
+        for b in range(B):
+            assert int(live[b]) == n - 1, (B, b, live[b])
+            assert abs(sim[b] - float(v @ Q[b])) <= 1e-12
+            assert flags[b] & _native.MC_FLAG_TIE and flags[b] & _native.MC_FLAG_FALLBACK, (B, b, flags[b])
+    c.close()
+
+
+@pytest.mark.parametrize("dim", [4, 130, 768])
+def test_stream8_windows_smaller_than_the_grid(dim):
+    """Fewer live rows than CTAs (most CTAs scan nothing), ring wrap at every size, B = 1..4."""
+    rng = np.random.default_rng(dim)
+    cap = 5
+    c = SemanticCache(capacity=cap, dim=dim)
+    o = OracleCache(cap, dim)
+    table, ot = ThresholdTable.default(), OracleTable()
+    c.ring.set_path(_native.PATH_STREAM8)
+    for i in range(12):
+        v = rng.standard_normal(dim)
+        v /= np.linalg.norm(v)
+        c.insert(CacheEntry(f"e{i}", v, "large", i, float(i)))
+        o.insert(OracleEntry(f"e{i}", v, "large", i, float(i)))
+        Q = np.stack([rows_like(o, rng) for _ in range(1 + i % 4)])
+        got = c.retrieve_batch(Q, table) if len(Q) > 1 else [c.retrieve(Q[0], table)]
+        for q, r in zip(Q, got):
+            e, sim, k = o.retrieve_entry(q, ot)
+            assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (dim, i)
+            assert r.k == k and _close(r.similarity, sim), (dim, i, r, sim)
+    c.close()
