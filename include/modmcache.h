@@ -128,6 +128,16 @@ int mc_merge_records(mc_cache* h, const void* dev_records, int32_t G, int32_t B,
 int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int32_t B, int32_t iters,
                      int64_t flush_bytes, double* out_ms, int64_t* out_counts);
 
+/* Measurement hook (bench.py): `iters` back-to-back lookup steps rotating over
+ * nh caches of one shape on one device (together larger than L2, so each step
+ * streams its cache from HBM), timed by a single pair of CUDA events — no
+ * per-step events or flushes inside the timed region.  Step i = [append
+ * rows[i] if rows != NULL] + lookup of queries[i] (B x dim) on hs[i % nh].
+ * out_ms[0] = mean step; out_counts[0] = kernel launches per step,
+ * [1] = answers whose certificate would have needed the exhaustive rescan. */
+int mc_profile_rotate(mc_cache* const* hs, int32_t nh, const double* queries, const double* rows, int32_t B,
+                      int32_t iters, double* out_ms, int64_t* out_counts);
+
 /* Measurement hook, active only when MC_GEMV_TIMING=1 was set before the first
  * lookup: reads (reset = 0) or resets (reset = 1) eight globaltimer stamps of the
  * last small-batch launch(es): [0] first CTA start, [1] last scan end, [2] last

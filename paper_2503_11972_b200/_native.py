@@ -29,7 +29,8 @@ RECORD_DTYPE = np.dtype([("sim", "<f8"), ("second", "<f8"), ("pos", "<i8"), ("fl
 EXPORTED = (
     "mc_create", "mc_destroy", "mc_set_thresholds", "mc_append", "mc_evict_front", "mc_size",
     "mc_retrieve_batch", "mc_set_path", "mc_configure_shard", "mc_retrieve_local_async",
-    "mc_merge_records", "mc_stats", "mc_last_error", "mc_version", "mc_profile_steps", "mc_debug_gemv_timing",
+    "mc_merge_records", "mc_stats", "mc_last_error", "mc_version", "mc_profile_steps", "mc_profile_rotate",
+    "mc_debug_gemv_timing",
 )
 
 
@@ -56,6 +57,7 @@ def _declare(lib):
     lib.mc_merge_records.argtypes = [vp, vp, i32, i32, i64, vp, dp, dp, dp, dp]
     lib.mc_stats.argtypes = [vp, dp]
     lib.mc_profile_steps.argtypes = [vp, dp, dp, i32, i32, i64, dp, dp]
+    lib.mc_profile_rotate.argtypes = [dp, i32, dp, dp, i32, i32, dp, dp]
     lib.mc_debug_gemv_timing.argtypes = [dp, i32]
     lib.mc_last_error.restype = C.c_char_p
     lib.mc_version.restype = C.c_char_p
@@ -223,6 +225,21 @@ class DeviceRing:
                                                    int(flush_bytes), _ptr(ms), _ptr(cnt)))
         return {"step_ms": ms[0], "scan_ms": ms[1], "merge_ms": ms[2], "append_ms": ms[3],
                 "launches_per_step": int(cnt[0]), "would_fallback": int(cnt[1])}
+
+    @staticmethod
+    def profile_rotate(rings, Q: np.ndarray, rows: np.ndarray | None, iters: int):
+        """Back-to-back device-timed steps rotating over `rings` (see mc_profile_rotate).
+        Q: [iters, B, dim]; rows: [iters, dim] or None."""
+        lib = load()
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        B = Q.shape[1]
+        r = None if rows is None else np.ascontiguousarray(rows, dtype=np.float64)
+        hs = (C.c_void_p * len(rings))(*[ring._hv for ring in rings])
+        ms = np.zeros(1, dtype=np.float64)
+        cnt = np.zeros(2, dtype=np.int64)
+        _check(lib, lib.mc_profile_rotate(C.cast(hs, C.c_void_p), len(rings), _ptr(Q), None if r is None else _ptr(r),
+                                          B, int(iters), _ptr(ms), _ptr(cnt)))
+        return {"step_ms": float(ms[0]), "launches_per_step": int(cnt[0]), "would_fallback": int(cnt[1])}
 
     def stats(self) -> dict:
         out = np.zeros(8, dtype=np.int64)

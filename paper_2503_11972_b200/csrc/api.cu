@@ -85,7 +85,11 @@ struct mc_cache {
   mc_record* d_rec = nullptr;
   mc_record* d_scratch = nullptr;
   OutRec* d_out = nullptr;
-  OutRec* h_out = nullptr;  // pinned
+  OutRec* h_out = nullptr;  // pinned, mapped (the streamed scan writes decisions here directly)
+  OutRec* d_outm = nullptr; // device view of h_out
+  unsigned* h_seq = nullptr;  // pinned, mapped: completion word of the zero-copy lookup
+  unsigned* d_seq = nullptr;
+  unsigned seq = 0;
 
   TcPlan* tc = nullptr;           // tensor-core scan plan, created on first batched lookup
   S8Plan* s8 = nullptr;           // TMA-streamed int8 scan plan (tensor maps of ring8 / ringq)
@@ -175,6 +179,7 @@ void free_batch(mc_cache* h) {
   h->d_scratch = nullptr;
   h->d_out = nullptr;
   h->h_out = nullptr;
+  h->d_outm = nullptr;
 }
 
 // Grow the query capacity to >= B (power of two): per-batch buffers and the
@@ -212,7 +217,8 @@ int ensure_batch(mc_cache* h, int B) {
   CU(cudaMalloc(&h->d_rec, (size_t)cap * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_scratch, (size_t)cap * exact_grid(h->sm_count) * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_out, (size_t)cap * sizeof(OutRec)));
-  CU(cudaMallocHost(&h->h_out, (size_t)cap * sizeof(OutRec)));
+  CU(cudaHostAlloc(&h->h_out, (size_t)cap * sizeof(OutRec), cudaHostAllocMapped));
+  CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_outm), h->h_out, 0));
   h->Bcap = cap;
   return MC_OK;
 }
@@ -314,7 +320,8 @@ int ensure_tc(mc_cache* h, int B) {
 // the first GEMV launch, or applied by k_append before a tensor-core scan).
 // t_mid (optional) is recorded between the scan and the standalone merge.
 int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
-               const QPrep* prep, const int8_t* q8, cudaEvent_t t_mid = nullptr) {
+               const QPrep* prep, const int8_t* q8, cudaEvent_t t_mid = nullptr, unsigned* done_seq = nullptr,
+               unsigned seq = 0) {
   if (use_gemm(h, B)) {
     if (app.n > 0) {
       CU(launch_append(app.stage, app.n, app.first_slot, mirror(h), h->D, h->Dp, rbufs(h), h->d_state, h->stream));
@@ -347,7 +354,7 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
     if (s8)
       CU(launch_stream8_scan(h->s8, rbufs(h), st, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0, h->sm_count, h->shard,
                              h->d_counter, h->d_gmax, h->thr, rec, out, a, prep + b0, q8 + (size_t)b0 * h->Dp,
-                             h->stream));
+                             b0 + nb == B ? done_seq : nullptr, seq, h->stream));
     else if (int8)
       CU(launch_gemv8_scan(rbufs(h), st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
                            nb == 1 ? gemv_grid(h->sm_count) : h->sm_count, h->shard, h->d_counter, h->d_gmax, h->thr, rec, out, a, prep + b0,
@@ -368,7 +375,7 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
 // decisions) are enqueued, not complete.  Returns the device query pointer.
 // The caller has run ensure_batch(h, B) (rec / out may be handle buffers).
 int lookup_enqueue(mc_cache* h, const double* queries, int B, mc_record* rec, OutRec* out, bool async_reuse,
-                   const double** q_dev) {
+                   const double** q_dev, unsigned* done_seq = nullptr, unsigned seq = 0) {
   int rc;
   if (h->n_pending > FUSE_APPEND_MAX) {
     rc = flush(h);
@@ -382,7 +389,32 @@ int lookup_enqueue(mc_cache* h, const double* queries, int B, mc_record* rec, Ou
   if (rc) return rc;
   const GemvAppendArgs app = take_pending(h, h->d_env);
   *q_dev = q;
-  return scan_merge(h, q, B, rec, out, app, prep, q8);
+  return scan_merge(h, q, B, rec, out, app, prep, q8, nullptr, done_seq, seq);
+}
+
+// True when a B-query lookup runs on the streamed int8 scan, which can hand
+// its decisions straight to host-mapped memory.
+bool direct_result(const mc_cache* h, int B) {
+  return h->s8 && !use_gemm(h, B) && h->path != MC_PATH_GEMV && h->path != MC_PATH_GEMV8;
+}
+
+// Spin until the streamed scan has published lookup `seq` into host-mapped
+// memory; a failed or silently finished stream is reported, never waited on.
+int wait_seq(mc_cache* h, unsigned seq) {
+  volatile unsigned* f = h->h_seq;
+  for (unsigned spins = 1; *f != seq; ++spins) {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+    if ((spins & 1023u) == 0) {
+      const cudaError_t e = cudaStreamQuery(h->stream);
+      if (e == cudaSuccess && *f != seq) return fail(MC_ERR_STATE, "lookup %u finished without publishing its result", seq);
+      if (e != cudaSuccess && e != cudaErrorNotReady)
+        return fail(MC_ERR_CUDA, "lookup %u: %s", seq, cudaGetErrorString(e));
+    }
+  }
+  __atomic_thread_fence(__ATOMIC_ACQUIRE);
+  return MC_OK;
 }
 
 int copy_out(mc_cache* h, int B, int64_t* out_live, double* out_sim, int32_t* out_k, uint32_t* out_flags) {
@@ -463,6 +495,9 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
     h->s8 = s8_plan_create(h->ring8, h->ringq, h->C, h->Dp, h->P8, err, sizeof err);
     if (!h->s8) return cleanup(fail(MC_ERR_CUDA, "int8 stream scan plan: %s", err));
   }
+  CUC(cudaHostAlloc(&h->h_seq, 64, cudaHostAllocMapped));
+  *h->h_seq = 0u;
+  CUC(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_seq), h->h_seq, 0));
   CUC(cudaMalloc(&h->d_counter, sizeof(unsigned)));
   CUC(cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned), h->stream));
   h->stage_cap = std::max<long long>(1, std::min<long long>(h->C, (16ll << 20) / ((long long)h->Dp * 8)));
@@ -499,6 +534,7 @@ int mc_destroy(mc_cache* h) {
     cudaFree(h->ringq);
     cudaFree(h->d_state);
     cudaFree(h->d_counter);
+    cudaFreeHost(h->h_seq);
     if (h->env_ev) cudaEventDestroy(h->env_ev);
     if (h->stream) cudaStreamDestroy(h->stream);
   }
@@ -605,10 +641,18 @@ int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* ou
   int rc = ensure_batch(h, B);  // may reallocate d_rec / d_out: evaluate them after
   if (rc) return rc;
   const double* q = nullptr;
-  rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_out, false, &q);
-  if (rc) return rc;
-  CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
-  CU(cudaStreamSynchronize(h->stream));
+  if (direct_result(h, B)) {  // decisions land in host-mapped memory; no D2H copy, no stream sync
+    const unsigned seq = ++h->seq;
+    rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_outm, false, &q, h->d_seq, seq);
+    if (rc) return rc;
+    rc = wait_seq(h, seq);
+    if (rc) return rc;
+  } else {
+    rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_out, false, &q);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+  }
   h->env_inflight = false;
   bool need = false;
   for (int b = 0; b < B; ++b) need |= (h->h_out[b].flags & FLAG_NEED_ANY) != 0;
@@ -806,17 +850,144 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
   return MC_OK;
 }
 
+// Measurement hook: `iters` back-to-back steps rotating over nh caches of the
+// same shape (their scan copies together larger than L2, so every step streams
+// its ring from HBM), timed by ONE pair of CUDA events on hs[0]'s stream — no
+// per-step event or flush in the timed region.  Step i = [append rows[i]] +
+// lookup of queries[i] (B x dim) on cache hs[i % nh].
+int mc_profile_rotate(mc_cache* const* hs, int32_t nh, const double* queries, const double* rows, int32_t B,
+                      int32_t iters, double* out_ms, int64_t* out_counts) {
+  if (!hs || nh < 1 || !queries || !out_ms || !out_counts) return fail(MC_ERR_ARG, "NULL argument");
+  if (B < 1 || iters < 1) return fail(MC_ERR_ARG, "need B >= 1 and iters >= 1");
+  mc_cache* h0 = hs[0];
+  for (int k = 0; k < nh; ++k) {
+    if (!hs[k]) return fail(MC_ERR_ARG, "NULL handle %d", k);
+    if (hs[k]->dev != h0->dev || hs[k]->D != h0->D || hs[k]->C != h0->C)
+      return fail(MC_ERR_ARG, "rotation needs caches of one shape on one device");
+    if (hs[k]->count == 0 && !rows) return fail(MC_ERR_STATE, "profile needs non-empty caches");
+  }
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (int k = 0; k < nh; ++k) locks.emplace_back(hs[k]->mu);
+  DeviceGuard guard(h0->dev);
+  for (int k = 0; k < nh; ++k) {
+    int rc = ensure_batch(hs[k], B);
+    if (!rc) rc = flush(hs[k]);
+    if (!rc && use_gemm(hs[k], B)) rc = ensure_tc(hs[k], B);
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(hs[k]->stream));
+  }
+  const int D = h0->D, Dp = h0->Dp;
+  double *d_qall = nullptr, *d_rows = nullptr;
+  OutRec* d_outs = nullptr;
+  QPrep* d_prep = nullptr;
+  int8_t* d_q8 = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaStream_t common = h0->stream;
+  std::vector<cudaStream_t> saved(nh);
+  for (int k = 0; k < nh; ++k) saved[k] = hs[k]->stream;
+  auto release = [&]() {
+    cudaStreamSynchronize(common);
+    for (int k = 0; k < nh; ++k) hs[k]->stream = saved[k];
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaFree(d_qall);
+    cudaFree(d_rows);
+    cudaFree(d_outs);
+    cudaFree(d_prep);
+    cudaFree(d_q8);
+  };
+#define CUR(call)                                                                                      \
+  do {                                                                                                 \
+    cudaError_t e_ = (call);                                                                           \
+    if (e_ != cudaSuccess) {                                                                           \
+      release();                                                                                       \
+      return fail(MC_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_));    \
+    }                                                                                                  \
+  } while (0)
+  const size_t qbytes = (size_t)iters * B * Dp * sizeof(double);
+  CUR(cudaMalloc(&d_qall, qbytes));
+  CUR(cudaMemset(d_qall, 0, qbytes));
+  CUR(cudaMemcpy2D(d_qall, (size_t)Dp * sizeof(double), queries, (size_t)D * sizeof(double), (size_t)D * sizeof(double),
+                   (size_t)iters * B, cudaMemcpyHostToDevice));
+  if (rows) {
+    CUR(cudaMalloc(&d_rows, (size_t)iters * Dp * sizeof(double)));
+    CUR(cudaMemset(d_rows, 0, (size_t)iters * Dp * sizeof(double)));
+    CUR(cudaMemcpy2D(d_rows, (size_t)Dp * sizeof(double), rows, (size_t)D * sizeof(double), (size_t)D * sizeof(double),
+                     (size_t)iters, cudaMemcpyHostToDevice));
+  }
+  CUR(cudaMalloc(&d_outs, (size_t)iters * B * sizeof(OutRec)));
+  {
+    std::vector<QPrep> hp((size_t)iters * B);
+    std::vector<int8_t> h8((size_t)iters * B * Dp);
+    std::vector<double> qrow(Dp, 0.0);
+    for (size_t i = 0; i < hp.size(); ++i) {
+      memcpy(qrow.data(), queries + i * D, D * sizeof(double));
+      quantize_query(qrow.data(), D, Dp, &hp[i], &h8[i * Dp]);
+    }
+    CUR(cudaMalloc(&d_prep, hp.size() * sizeof(QPrep)));
+    CUR(cudaMalloc(&d_q8, h8.size()));
+    CUR(cudaMemcpy(d_prep, hp.data(), hp.size() * sizeof(QPrep), cudaMemcpyHostToDevice));
+    CUR(cudaMemcpy(d_q8, h8.data(), h8.size(), cudaMemcpyHostToDevice));
+  }
+  CUR(cudaEventCreate(&e0));
+  CUR(cudaEventCreate(&e1));
+  for (int k = 0; k < nh; ++k) hs[k]->stream = common;
+  long long launches0 = 0;
+  for (int k = 0; k < nh; ++k) launches0 += hs[k]->stats[7];
+  CUR(cudaEventRecord(e0, common));
+  for (int it = 0; it < iters; ++it) {
+    mc_cache* h = hs[it % nh];
+    GemvAppendArgs app;
+    app.rb = rbufs(h);
+    app.d_state = h->d_state;
+    if (rows) {
+      if (h->count == h->C) {
+        h->head = (h->head + 1) % h->C;
+        h->count--;
+        h->jhead++;
+      }
+      app.stage = d_rows + (size_t)it * Dp;
+      app.n = 1;
+      app.first_slot = (h->head + h->count) % h->C;
+      h->count++;
+      h->appended++;
+    }
+    int rc = scan_merge(h, d_qall + (size_t)it * B * Dp, B, h->d_rec, d_outs + (size_t)it * B, app,
+                        d_prep + (size_t)it * B, d_q8 + (size_t)it * B * Dp);
+    if (rc) {
+      release();
+      return rc;
+    }
+  }
+  CUR(cudaEventRecord(e1, common));
+  CUR(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CUR(cudaEventElapsedTime(&ms, e0, e1));
+  long long launches1 = 0;
+  for (int k = 0; k < nh; ++k) launches1 += hs[k]->stats[7];
+  std::vector<OutRec> outs((size_t)iters * B);
+  CUR(cudaMemcpy(outs.data(), d_outs, outs.size() * sizeof(OutRec), cudaMemcpyDeviceToHost));
+  long long need = 0;
+  for (size_t i = 0; i < outs.size(); ++i) need += (outs[i].flags & FLAG_NEED_ANY) != 0;
+  out_ms[0] = ms / iters;
+  out_counts[0] = (launches1 - launches0) / iters;
+  out_counts[1] = need;
+  release();
+#undef CUR
+  return MC_OK;
+}
+
 // Measurement hook (MC_GEMV_TIMING=1): read (reset=0) or reset (reset=1) the
 // GEMV phase timestamps; 8 x u64 nanoseconds.  Not part of the stable ABI.
 int mc_debug_gemv_timing(unsigned long long* out8, int reset) {
   unsigned long long* t = gemv_timing_buffer();
   if (!t) return fail(MC_ERR_STATE, "set MC_GEMV_TIMING=1 before the first lookup");
   CU(cudaDeviceSynchronize());
-  if (reset == 2) {  // per-CTA stamps of the streamed scan: [cta][8] after the 8 globals
-    CU(cudaMemcpy(out8, t + 8, 8 * 512 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  if (reset == 2) {  // per-CTA stamps of the streamed scan: [cta][8] then [cta][4] after the 8 globals
+    CU(cudaMemcpy(out8, t + 8, 12 * 512 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   } else if (reset) {
     const unsigned long long init8[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
-    CU(cudaMemset(t + 8, 0, 8 * 512 * sizeof(unsigned long long)));
+    CU(cudaMemset(t + 8, 0, 12 * 512 * sizeof(unsigned long long)));
     CU(cudaMemcpy(t, init8, sizeof init8, cudaMemcpyHostToDevice));
   } else {
     CU(cudaMemcpy(out8, t, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));

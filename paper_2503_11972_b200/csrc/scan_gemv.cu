@@ -369,8 +369,8 @@ unsigned long long* gemv_timing_buffer() {
   if (!init) {
     init = true;
     const char* e = getenv("MC_GEMV_TIMING");
-    if (e && atoi(e) && cudaMalloc(&g_timing, (8 + 8 * 512) * sizeof(unsigned long long)) == cudaSuccess) {
-      cudaMemset(g_timing, 0, (8 + 8 * 512) * sizeof(unsigned long long));
+    if (e && atoi(e) && cudaMalloc(&g_timing, (8 + 12 * 512) * sizeof(unsigned long long)) == cudaSuccess) {
+      cudaMemset(g_timing, 0, (8 + 12 * 512) * sizeof(unsigned long long));
       const unsigned long long init8[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
       cudaMemcpy(g_timing, init8, sizeof init8, cudaMemcpyHostToDevice);
     }

@@ -113,6 +113,8 @@ struct S8Args {
   const double* stage;         // pending appends (float64, stride Dp)
   long long n_app;
   RingState* d_state;
+  unsigned* done_seq;          // optional (host-mapped): set to `seq` after `out` is written (zero-copy result)
+  unsigned seq;
 };
 
 // Rows [r0, r1) (live-local) of one CTA, cut into stages of up to `rows`
@@ -145,11 +147,342 @@ struct S8Work {
   }
 };
 
-template <int KB, int NB>
+// Shared state of one CTA (besides the dynamic stage buffers); sized for
+// four queries, declared once at namespace scope so the out-of-line helpers
+// below address it directly.
+constexpr int NB = 4;
+struct S8Smem {
+  uint64_t full[S8_CW], empty[S8_CW];   // stage mbarriers
+  float qu[S8_CW][S8_QCAP];             // candidate queues: upper bound (float, rounded up)
+  long long qp[S8_CW][S8_QCAP];         //   global position << 2 | query
+  int qc[S8_CW][S8_QCAP];               //   pool claim flags
+  int qtail[S8_CW];
+  float ovf[S8_CW][NB];                 // largest bound a full queue dropped
+  unsigned bound[NB];                   // CTA lower bound (order-preserving float key)
+  int done, pool_done;
+  Best2 best[S8_CW + 1][NB];            // float64 best per pool warp
+  unsigned long long t[8];              // measurement stamps (MC_GEMV_TIMING=1)
+  unsigned long long c[4];              // pool cycle counts (MC_GEMV_TIMING=1)
+};
+__shared__ S8Smem g_s8;
+#define S g_s8
+
+// Per-launch constants of the cold paths (pool, pending rows, finish).
+struct S8Ctx {
+  RingBufs rb;
+  RingState st;
+  ShardMap sm;
+  const double* sq64;  // shared memory: [NB][Dp] float64 queries
+  int Dp, nb, ncw;
+  bool timing;
+};
+
+__device__ __forceinline__ void s8_raise(unsigned* bound, int lane, double sc) {
+  // an exact score is a lower bound for everyone (the poller publishes it)
+  if (lane == 0 && !isnan(sc)) atomicMax(bound, s8_key(__double2float_rd(sc)));
+}
+
+// The cold paths below run once per launch.  They are out of line, so their
+// code exists once (shared by the nine pool warps) and the instruction cache
+// holds one copy.
+
+// One out-of-line copy of the exact dot for every rescoring warp of the CTA
+// (the pool, CTA 0's pending rows, the poller's warm-up).
+__device__ __noinline__ double s8_dot(const double* row, const double* q, int n, int lane) {
+  return warp_dot64(row, q, n, lane);
+}
+
+// One best-first pass over the (final) candidate queues, flattened by their
+// prefix sums so the entries spread over the 32 lanes with independent
+// loads.  Returns the queue index (w * S8_QCAP + i) of the live, unclaimed
+// candidate with the largest upper bound, or -1.  `retire` marks candidates
+// whose bound fell below the CTA's lower bound (false: a side-effect-free
+// warm-up pass).  Out of line: one copy for all pool warps and the poller.
+__device__ __noinline__ int s8_pass(int ncw, bool retire) {
+  const int lane = threadIdx.x & 31;
+  int tails = 0;  // lane w < ncw: tail of queue w
+  if (lane < ncw) tails = *(volatile int*)&S.qtail[lane];
+  int start[S8_CW];
+  int total = 0;
+#pragma unroll
+  for (int w = 0; w < S8_CW; ++w) {
+    start[w] = total;
+    total += w < ncw ? __shfl_sync(FULL, tails, w) : 0;
+  }
+  float bu = -INFINITY;
+  int bi = -1;
+  for (int f = lane; f < total; f += 32) {
+    int w = 0, base = 0;
+#pragma unroll
+    for (int k = 1; k < S8_CW; ++k)
+      if (k < ncw && f >= start[k]) {
+        w = k;
+        base = start[k];
+      }
+    const int i = f - base;
+    const float u = *(volatile float*)&S.qu[w][i];
+    const int claimed = *(volatile int*)&S.qc[w][i];
+    const int b = (int)(S.qp[w][i] & 3);
+    const float bnd = s8_val(ld_vol_u32(&S.bound[b]));
+    if (u == -INFINITY || claimed) continue;
+    if ((double)u < (double)bnd - 1e-9) {
+      if (retire) S.qu[w][i] = -INFINITY;  // strictly below a row whose exact score is known to exceed it
+      continue;
+    }
+    if (u > bu) {
+      bu = u;
+      bi = w * S8_QCAP + i;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const float ou = __shfl_xor_sync(FULL, bu, off);
+    const int oi = __shfl_xor_sync(FULL, bi, off);
+    if (ou > bu || (ou == bu && oi > bi)) {
+      bu = ou;
+      bi = oi;
+    }
+  }
+  return bi;
+}
+
+// CTA 0's rescorer: rows appended since the last lookup are not in the int8
+// copy yet — write every ring copy and score them exactly (float64).
+__device__ __forceinline__ void s8_pending(const S8Ctx x, const double* stage, long long n_app,
+                                        long long n_pend, long long n_scan) {
+  const int lane = threadIdx.x & 31;
+  for (long long i = 0; i < n_pend; ++i) {
+    const double* srow = stage + (size_t)(n_app - n_pend + i) * x.Dp;
+    const long long row = n_scan + i;
+    write_row_all(srow, ring_slot(x.st, row), x.rb, x.Dp, lane);
+    for (int b = 0; b < x.nb; ++b) {
+      const double sc = s8_dot(srow, x.sq64 + (size_t)b * x.Dp, x.Dp, lane);
+      if (lane == 0) S.best[S8_CW][b].add(sc, global_pos(x.st, row, x.sm));
+      s8_raise(&S.bound[b], lane, sc);
+    }
+  }
+  __syncwarp();
+}
+
+// Rescoring pool: the rescorer warp and the eight consumer warps, once every
+// consumer is done (a hardware barrier: nothing spins beside the streaming
+// warps).  Lazy: nothing is rescored while the CTA streams (those loads would
+// queue behind the scan's, and the bound keeps rising).  Best-first: claim the
+// live candidate with the largest upper bound and rescore it in float64; its
+// exact score then prunes the rest.  Candidates whose bound fell below the
+// CTA's lower bound are retired unscored.  Result: S.best[wid][*].
+__device__ __forceinline__ void s8_pool(const S8Ctx x, int wid) {
+  const int lane = threadIdx.x & 31;
+  asm volatile("bar.sync 1, %0;" ::"n"((S8_CW + 1) * 32) : "memory");
+  if (x.timing && lane == 0) atomicMax(&S.t[S8T_POOL], s8_timer());
+  const long long c_pool = clock64();
+  bool first_pass = true;
+  while (true) {
+    const int bi = s8_pass(x.ncw, true);
+    if (x.timing && first_pass && lane == 0) atomicMax(&S.c[0], (unsigned long long)(clock64() - c_pool));
+    first_pass = false;
+    if (bi < 0) break;  // nothing live and unclaimed is left (claimed ones finish with their claimer)
+    const int w = bi / S8_QCAP, i = bi % S8_QCAP;
+    int won = 0;
+    if (lane == 0) won = atomicCAS(&S.qc[w][i], 0, 1) == 0;
+    if (__shfl_sync(FULL, won, 0)) {
+      const long long pb = S.qp[w][i];
+      const int b = (int)(pb & 3);
+      const long long p = pb >> 2;
+      const long long slot = ring_slot(x.st, local_row(x.st, p, x.sm));
+      const long long c_dot = clock64();
+      if (x.timing && lane == 0) {
+        atomicMin(&S.t[S8T_R0], s8_timer());
+        atomicMin(&S.c[2], (unsigned long long)(c_dot - c_pool));
+      }
+      const double sc = s8_dot(x.rb.r64 + (size_t)slot * x.Dp, x.sq64 + (size_t)b * x.Dp, x.Dp, lane);
+      if (lane == 0) {
+        S.best[wid][b].add(sc, p);
+        if (x.timing) {
+          atomicMax(&S.t[S8T_R1], s8_timer());
+          atomicMax(&S.c[3], (unsigned long long)(clock64() - c_dot));
+          atomicAdd(&S.t[S8T_RESC], 1ull);
+        }
+      }
+      s8_raise(&S.bound[b], lane, sc);
+      __syncwarp();
+      if (lane == 0) S.qu[w][i] = -INFINITY;
+    }
+    __syncwarp();
+  }
+  if (x.timing && lane == 0) atomicMax(&S.t[S8T_POOLX], s8_timer());
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    atomicAdd(&S.pool_done, 1);
+  }
+}
+
+// The rescorer after the pool: the CTA record, the ticket and, in the last
+// CTA, the merge of every record and the decision (cache.py:255-260,
+// select_k :112-117), then the zero-copy completion word.
+__device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, CtaRec* cta, int b0) {
+  const int lane = threadIdx.x & 31;
+  const int nb = x.nb;
+  if (lane == 0)
+    while (ld_acq_cta(&S.pool_done) != S8_CW + 1) {  // the nine pool warps
+    }
+  __syncwarp();
+  for (int b = 0; b < nb; ++b) {
+    Best2 m;
+    m.init();
+    float ov = -INFINITY;
+    for (int w = 0; w <= S8_CW; ++w) m.merge(S.best[w][b]);
+    for (int w = 0; w < x.ncw; ++w) ov = fmaxf(ov, S.ovf[w][b]);
+    if (lane == 0) {
+      CtaRec r;
+      r.s = m.s;
+      r.s2 = m.s2;
+      r.p = m.p;
+      r.ovf = ov;
+      r.ties = m.ties;
+      cta[(size_t)(b0 + b) * gridDim.x + blockIdx.x] = r;
+    }
+  }
+  if (x.timing && lane == 0) S.t[S8T_REC] = s8_timer();
+  __syncwarp();
+  auto dump = [&]() {  // measurement stamps, written once this CTA is off the critical path
+    if (x.timing && lane < 8) a.timing[8 + 8 * blockIdx.x + lane] = S.t[lane];
+    if (x.timing && lane < 4) a.timing[8 + 8 * 512 + 4 * blockIdx.x + lane] = S.c[lane];
+  };
+  unsigned exotic = 0;  // loaded before the ticket (off the tail's critical path)
+  if (lane < nb) exotic = a.prep[lane].exotic != 0 ? 1u : 0u;
+  unsigned old = 0;
+  if (lane == 0)
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.counter) : "memory");
+  old = __shfl_sync(FULL, old, 0);
+  if (old != gridDim.x - 1) {
+    dump();
+    return;
+  }
+  __threadfence();
+  if (lane == 0 && x.timing) a.timing[4] = s8_timer();
+  // Merge the per-CTA records with independent warp reductions (no chain of
+  // Best2 merges): best = max s; among records at best: max position and the
+  // summed tie counts; runner-up = max over the others' s and everyone's s2
+  // (a second record at the best makes the runner-up equal to it, as in
+  // Best2::merge).  Record similarities are finite here (exotic queries are
+  // flagged for the exhaustive path).
+  for (int b = 0; b < nb; ++b) {
+    const int gb = b0 + b;
+    constexpr int PER = 5;  // records per lane, all loaded before use (grid <= 160: one round trip)
+    double rs[PER], rs2[PER];
+    long long rp[PER];
+    int rt[PER];
+    float ro[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int c = 32 * k + lane;
+      rp[k] = -1;
+      rs[k] = rs2[k] = -INFINITY;
+      rt[k] = 0;
+      ro[k] = -INFINITY;
+      if (c < (int)gridDim.x) {
+        const CtaRec* src = cta + (size_t)gb * gridDim.x + c;
+        rs[k] = __ldcg(&src->s);
+        rs2[k] = __ldcg(&src->s2);
+        rp[k] = __ldcg(&src->p);
+        rt[k] = __ldcg(&src->ties);
+        ro[k] = __ldcg(&src->ovf);
+      }
+    }
+    for (int c0 = 32 * PER; c0 < (int)gridDim.x; c0 += 32) {  // grids beyond 160 CTAs
+      const int c = c0 + lane;
+      if (c < (int)gridDim.x) {
+        const CtaRec* src = cta + (size_t)gb * gridDim.x + c;
+        Best2 m0, mx;
+        m0.init();
+        if (rp[0] >= 0) {
+          m0.s = rs[0];
+          m0.s2 = rs2[0];
+          m0.p = rp[0];
+          m0.ties = rt[0];
+        }
+        mx.s = __ldcg(&src->s);
+        mx.s2 = __ldcg(&src->s2);
+        mx.p = __ldcg(&src->p);
+        mx.ties = __ldcg(&src->ties);
+        ro[0] = fmaxf(ro[0], __ldcg(&src->ovf));
+        if (mx.p >= 0) {  // fold into slot 0 with Best2 semantics
+          m0.merge(mx);
+          rs[0] = m0.s;
+          rs2[0] = m0.s2;
+          rp[0] = m0.p;
+          rt[0] = m0.ties;
+        }
+      }
+    }
+    if (b == 0 && lane == 0 && x.timing) a.timing[5] = s8_timer();
+    double bs = -INFINITY;
+    float ov = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      if (rp[k] >= 0) bs = fmax(bs, rs[k]);
+      ov = fmaxf(ov, ro[k]);
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      bs = fmax(bs, __shfl_xor_sync(FULL, bs, off));
+      ov = fmaxf(ov, __shfl_xor_sync(FULL, ov, off));
+    }
+    long long bp = -1;
+    int nt = 0, neq = 0;
+    double s2 = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      if (rp[k] < 0) continue;
+      if (rs[k] == bs) {
+        bp = max(bp, rp[k]);
+        nt += rt[k];
+        ++neq;
+      } else {
+        s2 = fmax(s2, rs[k]);
+      }
+      s2 = fmax(s2, rs2[k]);
+    }
+    nt = __reduce_add_sync(FULL, (unsigned)nt);
+    neq = __reduce_add_sync(FULL, (unsigned)neq);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      bp = max(bp, __shfl_xor_sync(FULL, bp, off));
+      s2 = fmax(s2, __shfl_xor_sync(FULL, s2, off));
+    }
+    if (neq >= 2) s2 = bs;
+    const bool exo = __shfl_sync(FULL, exotic, b) != 0;
+    if (lane == 0) {
+      const bool fail = bp < 0 || !(ov == -INFINITY || (double)ov + 1e-9 < bs);
+      mc_record r;
+      r.sim = bs;
+      r.second = s2;
+      r.pos = bp;
+      r.flags = (nt >= 2 ? MC_FLAG_TIE : 0u) | (fail ? FLAG_NEED_FALLBACK : 0u) | (exo ? FLAG_NEED_EXHAUSTIVE : 0u);
+      r.reserved = 0;
+      a.rec[gb] = r;
+      if (a.out) a.out[gb] = decide(record_best(r), r.flags & FLAG_NEED_ANY, x.st.jhead, a.thr);
+    }
+    if (lane < S8_GREP) a.gmax[(size_t)gb * S8_GSTRIDE + 32 * lane] = 0u;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (a.done_seq) {  // zero-copy result: the decisions, then the sequence word, over the system fabric
+      __threadfence_system();
+      *(volatile unsigned*)a.done_seq = a.seq;
+    }
+    *a.counter = 0u;
+    if (x.timing) a.timing[3] = s8_timer();
+  }
+  dump();
+}
+
+template <int KB, int NBQ>
 __global__ void __launch_bounds__(S8_THREADS, 1)
-    k_stream8_scan(RingBufs rb, const RingState st,
-                   const double* __restrict__ q64, int nb, CtaRec* __restrict__ cta, int b0, ShardMap sm,
-                   S8Args a, int nst, int Dp) {
+    k_stream8_scan(RingBufs rb, const RingState st, const double* __restrict__ q64, int nb,
+                   CtaRec* __restrict__ cta, int b0, ShardMap sm, S8Args a, int nst, int Dp) {
   constexpr int P8 = KB * 128;                // int8 row stride (Dp rounded up to 128)
   constexpr int R = s8_rows_per_lane(KB);
   constexpr int SROWS = 32 * R;               // rows per stage
@@ -160,20 +493,8 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stages = base;                                            // [nst][SDATA]
   float2* rqs = reinterpret_cast<float2*>(base + (size_t)nst * SDATA);  // [nst][RQS]
-  int8_t* sq8 = reinterpret_cast<int8_t*>(rqs + (size_t)nst * RQS);     // [NB][P8]
-  double* sq64 = reinterpret_cast<double*>(sq8 + NB * P8);              // [NB][Dp] float64 queries
-
-  __shared__ __align__(8) uint64_t full[S8_CW], empty[S8_CW];
-  __shared__ float qu[S8_CW][S8_QCAP];
-  __shared__ long long qp[S8_CW][S8_QCAP];
-  __shared__ int qtail[S8_CW];
-  __shared__ float sh_ovf[S8_CW][NB];
-  __shared__ unsigned sh_bound[NB];
-  __shared__ int sh_done;
-  __shared__ int qc[S8_CW][S8_QCAP];      // claim flags of the rescoring pool
-  __shared__ Best2 sh_best[S8_CW + 1][NB];  // each pool warp's float64 best
-  __shared__ int sh_pool_done;
-  __shared__ unsigned long long sh_t[8];  // measurement stamps (MC_GEMV_TIMING=1)
+  int8_t* sq8 = reinterpret_cast<int8_t*>(rqs + (size_t)nst * RQS);     // [NBQ][P8]
+  double* sq64 = reinterpret_cast<double*>(sq8 + NBQ * P8);              // [NBQ][Dp] float64 queries
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -182,170 +503,83 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
   const long long n_scan = n - n_pend;  // rows [n_scan, n) are scored exactly by CTA 0
   S8Work wk;
   wk.init(st, n_scan, blockIdx.x, gridDim.x, SROWS);
+  const bool timing = a.timing != nullptr;
 
+  // Programmatic dependent launch: the next lookup's grid may be scheduled as
+  // soon as SMs free up; it runs its prologue (this block up to
+  // griddepcontrol.wait) while this grid's last CTA still merges.
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int i = 0; i < nst; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    for (int b = 0; b < NB; ++b) sh_bound[b] = s8_key(-INFINITY);
-    sh_done = 0;
-    sh_pool_done = 0;
-    if (blockIdx.x == 0 && a.d_state) *a.d_state = st;
-    for (int k = 0; k < 8; ++k) sh_t[k] = 0ull;
-    sh_t[S8T_R0] = ~0ull;
-    if (a.timing) atomicMin(a.timing + 0, s8_timer());
+    for (int b = 0; b < NBQ; ++b) S.bound[b] = s8_key(-INFINITY);
+    S.done = 0;
+    S.pool_done = 0;
+    for (int k = 0; k < 8; ++k) S.t[k] = 0ull;
+    S.t[S8T_R0] = ~0ull;
+    for (int k = 0; k < 4; ++k) S.c[k] = k == 2 ? ~0ull : 0ull;
   }
-  if (threadIdx.x < S8_CW) qtail[threadIdx.x] = 0;
-  for (int i = threadIdx.x; i < S8_CW * S8_QCAP; i += blockDim.x) (&qc[0][0])[i] = 0;
-  for (int i = threadIdx.x; i < NB * Dp; i += blockDim.x) sq64[i] = i < nb * Dp ? q64[i] : 0.0;
-  for (int i = threadIdx.x; i < NB * P8 / 16; i += blockDim.x) {  // q̂ (stride Dp) -> [NB][P8], zero-padded
+  if (threadIdx.x < S8_CW) S.qtail[threadIdx.x] = 0;
+  for (int i = threadIdx.x; i < (S8_CW + 1) * NB; i += blockDim.x) (&S.best[0][0])[i].init();
+  for (int i = threadIdx.x; i < S8_CW * S8_QCAP; i += blockDim.x) (&S.qc[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < NBQ * Dp; i += blockDim.x) sq64[i] = i < nb * Dp ? q64[i] : 0.0;
+  for (int i = threadIdx.x; i < NBQ * P8 / 16; i += blockDim.x) {  // q̂ (stride Dp) -> [NBQ][P8], zero-padded
     const int b = i / (P8 / 16), c = i % (P8 / 16);
     reinterpret_cast<uint4*>(sq8)[i] = (b < nb && c < Dp / 16)
                                            ? reinterpret_cast<const uint4*>(a.q8 + (size_t)b * Dp)[c]
                                            : make_uint4(0u, 0u, 0u, 0u);
   }
+  // Everything above reads only this launch's inputs (host-staged queries) and
+  // initialises shared memory; from here on the ring, the counters and the
+  // records the previous grid may still be writing are touched.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) {
+    if (blockIdx.x == 0 && a.d_state) *a.d_state = st;
+    if (timing) atomicMin(a.timing + 0, s8_timer());
+  }
   __syncthreads();
 
   const int ncw = min(nst, S8_CW);
+  const S8Ctx x{rb, st, sm, sq64, Dp, nb, ncw, timing};
   unsigned* const gq = a.gmax + (size_t)b0 * S8_GSTRIDE;  // this launch's queries
-  auto raise = [&](int b, double sc) {  // an exact score is a lower bound for everyone (the poller publishes it)
-    if (lane == 0 && !isnan(sc)) atomicMax(&sh_bound[b], s8_key(__double2float_rd(sc)));
-  };
-  const bool timing = a.timing != nullptr;
-  auto stamp_max = [&](int k) { atomicMax(&sh_t[k], s8_timer()); };  // shared memory only
-  // Rescoring pool (the rescorer warp from the start, each consumer warp once
-  // its stages are done).  Best-first: claim the live candidate with the
-  // largest upper bound and rescore it in float64; its exact score then prunes
-  // the rest.  Candidates whose bound fell below the CTA's lower bound are
-  // retired without rescoring.  The poller also folds the global bound in.
-  // Rescoring pool: the rescorer warp and the consumer warps, once every
-  // consumer is done (a hardware barrier, no spinning beside the streaming
-  // warps).  Lazy: nothing is rescored while the CTA still streams (those
-  // loads would queue behind the scan's, and the bound keeps rising).
-  // Best-first: claim the live candidate with the largest upper bound and
-  // rescore it in float64; its exact score then prunes the rest.  Candidates
-  // whose bound fell below the CTA's lower bound are retired unscored.
-  auto pool = [&](int wid, Best2 (&best)[NB]) {
-    asm volatile("bar.sync 1, %0;" ::"n"((S8_CW + 1) * 32) : "memory");
-    if (timing && lane == 0) stamp_max(S8T_POOL);
-    int tails = 0;  // lane w < ncw: final tail of queue w
-    if (lane < ncw) tails = *(volatile int*)&qtail[lane];
-    while (true) {
-      float bu = -INFINITY;
-      int bi = -1;
-      for (int w = 0; w < ncw; ++w) {
-        const int t = __shfl_sync(FULL, tails, w);
-        for (int i = lane; i < t; i += 32) {
-          const float u = *(volatile float*)&qu[w][i];
-          if (u == -INFINITY || *(volatile int*)&qc[w][i]) continue;
-          const int b = (int)(qp[w][i] & 3);
-          if ((double)u < (double)s8_val(ld_vol_u32(&sh_bound[b])) - 1e-9) {
-            qu[w][i] = -INFINITY;  // retired: strictly below a row whose exact score is known to exceed it
-            continue;
-          }
-          if (u > bu) {
-            bu = u;
-            bi = w * S8_QCAP + i;
-          }
-        }
-      }
-#pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        const float ou = __shfl_xor_sync(FULL, bu, off);
-        const int oi = __shfl_xor_sync(FULL, bi, off);
-        if (ou > bu || (ou == bu && oi > bi)) {
-          bu = ou;
-          bi = oi;
-        }
-      }
-      if (bi < 0) break;  // nothing live and unclaimed is left (claimed ones finish with their claimer)
-      const int w = bi / S8_QCAP, i = bi % S8_QCAP;
-      int won = 0;
-      if (lane == 0) won = atomicCAS(&qc[w][i], 0, 1) == 0;
-      if (__shfl_sync(FULL, won, 0)) {
-        const long long pb = qp[w][i];
-        const int b = (int)(pb & 3);
-        const long long p = pb >> 2;
-        const long long slot = ring_slot(st, local_row(st, p, sm));
-        if (timing && lane == 0) atomicMin(&sh_t[S8T_R0], s8_timer());
-        const double sc = warp_dot64(rb.r64 + (size_t)slot * Dp, sq64 + (size_t)b * Dp, Dp, lane);
-        if (timing && lane == 0) stamp_max(S8T_R1);
-#pragma unroll
-        for (int bb = 0; bb < NB; ++bb)
-          if (bb == b) best[bb].add(sc, p);
-        raise(b, sc);
-        if (timing && lane == 0) atomicAdd(&sh_t[S8T_RESC], 1ull);
-        __syncwarp();
-        if (lane == 0) qu[w][i] = -INFINITY;
-      }
-      __syncwarp();
-    }
-    if (timing && lane == 0) stamp_max(S8T_POOLX);
-#pragma unroll
-    for (int b = 0; b < NB; ++b)
-      if (lane == 0) sh_best[wid][b] = best[b];
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      atomicAdd(&sh_pool_done, 1);
-    }
-  };
 
   if (warp == S8_CW + 2) {
     // ------------------------------------------------------------ bound poller
     // Until the pool is done: carry the CTA's bound to the other CTAs (lane
     // S8_PUB0 + r owns replica r), fold theirs in (replica cta % S8_GREP), and
     // while the CTA streams pull the leading candidate's float64 row into L2
-    // so its rescoring after the scan hits L2.  This warp never synchronises.
+    // so its rescoring after the scan hits L2.  This warp never synchronises
+    // (its global atomics stay off the other warps' fences and barriers).
     int pf = -1;
-    unsigned pub[NB];
+    unsigned pub[NBQ];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) pub[b] = 0u;
-    while (*(volatile int*)&sh_pool_done != S8_CW + 1) {
+    for (int b = 0; b < NBQ; ++b) pub[b] = 0u;
+    while (*(volatile int*)&S.pool_done != S8_CW + 1) {
       unsigned gk = 0;
       if (lane >= S8_PUB0 && lane - S8_PUB0 < nb)
         gk = ld_relaxed_gpu(gq + (lane - S8_PUB0) * S8_GSTRIDE + 32 * (blockIdx.x % S8_GREP));
 #pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const unsigned mine = ld_vol_u32(&sh_bound[b]);
+      for (int b = 0; b < NBQ; ++b) {
+        const unsigned mine = ld_vol_u32(&S.bound[b]);
         if (b < nb && mine > pub[b]) {
           if (lane >= S8_PUB0) atomicMax(gq + b * S8_GSTRIDE + 32 * (lane - S8_PUB0), mine);
           pub[b] = mine;
         }
       }
-      if (*(volatile int*)&sh_done != S8_CW) {
-        float bu = -INFINITY;
-        int bi = -1;
-        for (int w = 0; w < ncw; ++w) {
-          const int t = *(volatile int*)&qtail[w];
-          for (int i = lane; i < t; i += 32) {
-            const float u = *(volatile float*)&qu[w][i];
-            if (u > bu) {
-              bu = u;
-              bi = w * S8_QCAP + i;
-            }
-          }
-        }
-#pragma unroll
-        for (int off = 16; off; off >>= 1) {
-          const float ou = __shfl_xor_sync(FULL, bu, off);
-          const int oi = __shfl_xor_sync(FULL, bi, off);
-          if (ou > bu || (ou == bu && oi > bi)) {
-            bu = ou;
-            bi = oi;
-          }
-        }
+      if (*(volatile int*)&S.done != S8_CW) {
+        const int bi = s8_pass(ncw, false);
         if (bi >= 0 && bi != pf) {
           pf = bi;
-          const long long p = qp[bi / S8_QCAP][bi % S8_QCAP] >> 2;
+          const long long p = S.qp[bi / S8_QCAP][bi % S8_QCAP] >> 2;
           const char* row = reinterpret_cast<const char*>(rb.r64 + (size_t)ring_slot(st, local_row(st, p, sm)) * Dp);
           for (int off = lane * 128; off < Dp * 8; off += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + off));
         }
       }
-      if (gk && gk > ld_vol_u32(&sh_bound[lane - S8_PUB0])) atomicMax(&sh_bound[lane - S8_PUB0], gk);
+      if (gk && gk > ld_vol_u32(&S.bound[lane - S8_PUB0])) atomicMax(&S.bound[lane - S8_PUB0], gk);
       __syncwarp();
     }
     return;
@@ -356,313 +590,147 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     if (lane == 0) {
       for (int i = 0; i < wk.ns; ++i) {
         const int buf = i % nst;
-        mbar_wait(&empty[buf], ((i / nst) & 1) ^ 1);
+        mbar_wait(&S.empty[buf], ((i / nst) & 1) ^ 1);
         long long row0, slot0;
         int nr;
         wk.stage(i, st, row0, nr, slot0);
         const long long q0 = slot0 & ~1ll;    // (s, L1) pairs from a 16-byte aligned slot
         const uint32_t qbytes = (uint32_t)(((slot0 - q0) + nr + 1) / 2 * 16);
         const uint32_t dbytes = (uint32_t)nr * P8;
-        mbar_expect_tx(&full[buf], dbytes + qbytes);
-        bulk_load(stages + (size_t)buf * SDATA, rb.r8 + (size_t)slot0 * P8, dbytes, &full[buf]);
-        bulk_load(rqs + (size_t)buf * RQS, rb.rq + q0, qbytes, &full[buf]);
+        mbar_expect_tx(&S.full[buf], dbytes + qbytes);
+        bulk_load(stages + (size_t)buf * SDATA, rb.r8 + (size_t)slot0 * P8, dbytes, &S.full[buf]);
+        bulk_load(rqs + (size_t)buf * RQS, rb.rq + q0, qbytes, &S.full[buf]);
       }
     }
-  } else if (warp <= S8_CW) {
-    // ------------------------------------------------------------ consumers
-    const int cw = warp - 1;
-    double sq[NB], q1[NB];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const QPrep pq = b < nb ? a.prep[b] : QPrep{0.0, 0.0, 0.0, 0.f, 0};
-      sq[b] = pq.s;
-      q1[b] = pq.q1;
-    }
-    float lo[NB], ovf[NB];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      lo[b] = -INFINITY;
-      ovf[b] = -INFINITY;
-    }
-    int tail = 0;
-    if (cw < ncw) {
-      for (int i = cw; i < wk.ns; i += ncw) {
-        const int buf = i % nst;
-        long long row0, slot0;
-        int nr;
-        wk.stage(i, st, row0, nr, slot0);
-        mbar_wait(&full[buf], (i / nst) & 1);
-        const uint8_t* sb = stages + (size_t)buf * SDATA;
-        int acc[R][NB], acc2[R][NB];  // two chains per dot (exact integers: order is free)
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-#pragma unroll
-          for (int b = 0; b < NB; ++b) acc[r][b] = acc2[r][b] = 0;
-#pragma unroll
-        for (int j = 0; j < NCH; ++j) {
-          int c = j + lane;  // rotated chunk order (conflict-free, see the header)
-          c = c >= NCH ? c - NCH : c;
-          c = c >= NCH ? c - NCH : c;
-          uint4 v[R];
-#pragma unroll
-          for (int r = 0; r < R; ++r) v[r] = *reinterpret_cast<const uint4*>(sb + (r * 32 + lane) * P8 + c * 16);
-#pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            const uint4 qv = *reinterpret_cast<const uint4*>(sq8 + b * P8 + c * 16);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              if (j & 1)
-                acc2[r][b] = dp16x(v[r], qv, acc2[r][b]);
-              else
-                acc[r][b] = dp16x(v[r], qv, acc[r][b]);
-            }
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-#pragma unroll
-          for (int b = 0; b < NB; ++b) acc[r][b] += acc2[r][b];
-        float2 e[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) e[r] = rqs[(size_t)buf * RQS + (slot0 & 1) + r * 32 + lane];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[buf]);
-
-        // bounds: the warp's own, then the CTA's (which carries the global one)
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const bool valid = r * 32 + lane < nr;
-#pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            if (b >= nb) break;
-            const double approx = (double)acc[r][b] * ((double)e[r].x * sq[b]);
-            const double dl = (0.5 * sq[b] * (double)e[r].y + 0.5 * (double)e[r].x * q1[b]) * (1.0 + 1e-9) + 1e-12;
-            float lf = valid ? __double2float_rd(approx - dl) : -INFINITY;
-#pragma unroll
-            for (int off = 16; off; off >>= 1) lf = fmaxf(lf, __shfl_xor_sync(FULL, lf, off));
-            float bnd = s8_val(ld_vol_u32(&sh_bound[b]));
-            if (lf > lo[b]) {
-              lo[b] = lf;
-              if (lf > bnd) {  // publish to the CTA (the poller carries it to the other CTAs)
-                if (lane == 0) atomicMax(&sh_bound[b], s8_key(lf));
-                bnd = lf;
-              }
-            }
-            const double u = approx + dl;
-            const bool keep = valid && u >= (double)bnd - 1e-9;
-            const unsigned m = __ballot_sync(FULL, keep);
-            if (m) {
-              const int idx = tail + __popc(m & ((1u << lane) - 1u));
-              if (keep) {
-                const float uf = __double2float_ru(u);
-                if (idx < S8_QCAP) {
-                  qu[cw][idx] = uf;
-                  qp[cw][idx] = (global_pos(st, row0 + r * 32 + lane, sm) << 2) | b;
-                } else {
-                  ovf[b] = fmaxf(ovf[b], uf);
-                }
-              }
-              if (timing && lane == 0) atomicAdd(&sh_t[S8T_PUSH], (unsigned long long)__popc(m));
-              tail = min(tail + __popc(m), S8_QCAP);
-              __syncwarp();
-              if (lane == 0) st_rel_cta(&qtail[cw], tail);
-            }
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      float o = ovf[b];
-#pragma unroll
-      for (int off = 16; off; off >>= 1) o = fmaxf(o, __shfl_xor_sync(FULL, o, off));
-      if (lane == 0) sh_ovf[cw][b] = o;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      atomicAdd(&sh_done, 1);
-    }
-    if (timing && lane == 0) stamp_max(S8T_SCAN);
-    Best2 best[NB];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) best[b].init();
-    pool(cw, best);
-  } else {
-    // ------------------------------------------------------------ rescorer
-    Best2 best[NB];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) best[b].init();
-    if (blockIdx.x == 0 && n_pend > 0) {  // rows appended since the last lookup
-      for (long long i = 0; i < n_pend; ++i) {
-        const double* srow = a.stage + (size_t)(a.n_app - n_pend + i) * Dp;
-        const long long row = n_scan + i;
-        write_row_all(srow, ring_slot(st, row), rb, Dp, lane);
-#pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          if (b >= nb) break;
-          const double sc = warp_dot64(srow, sq64 + (size_t)b * Dp, Dp, lane);
-          best[b].add(sc, global_pos(st, row, sm));
-          raise(b, sc);
-        }
-      }
-    }
-    pool(S8_CW, best);
-    if (lane == 0)
-      while (ld_acq_cta(&sh_pool_done) != S8_CW + 1) {
-      }
-    __syncwarp();
-#pragma unroll
-    for (int b = 0; b < NB; ++b)
-      for (int w = 0; w < S8_CW; ++w) best[b].merge(sh_best[w][b]);
-    // CTA records
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      if (b >= nb) break;
-      float ov = -INFINITY;
-      for (int w = 0; w < ncw; ++w) ov = fmaxf(ov, sh_ovf[w][b]);
-      if (lane == 0) {
-        CtaRec r;
-        r.s = best[b].s;
-        r.s2 = best[b].s2;
-        r.p = best[b].p;
-        r.ovf = ov;
-        r.ties = best[b].ties;
-        cta[(size_t)(b0 + b) * gridDim.x + blockIdx.x] = r;
-      }
-    }
-    if (timing && lane == 0) sh_t[S8T_REC] = s8_timer();
-    __syncwarp();
-    auto dump = [&]() {  // measurement stamps, written once this CTA is off the critical path
-      if (timing && lane < 8) a.timing[8 + 8 * blockIdx.x + lane] = sh_t[lane];
-    };
-    unsigned exotic = 0;  // loaded before the ticket (off the tail's critical path)
-    if (lane < nb) exotic = a.prep[lane].exotic != 0 ? 1u : 0u;
-    // ticket; the last CTA merges every record and decides
-    unsigned old = 0;
-    if (lane == 0)
-      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.counter) : "memory");
-    old = __shfl_sync(FULL, old, 0);
-    if (old != gridDim.x - 1) {
-      dump();
-      return;
-    }
-    __threadfence();
-    if (lane == 0 && a.timing) a.timing[4] = s8_timer();
-    // Merge the per-CTA records with independent warp reductions (no chain of
-    // Best2 merges): best = max s; among records at best: max position and the
-    // summed tie counts; runner-up = max over the others' s and everyone's s2
-    // (a second record at the best makes the runner-up equal to it, as in
-    // Best2::merge).  Record similarities are finite here (exotic queries are
-    // flagged for the exhaustive path).
-    for (int b = 0; b < nb; ++b) {
-      const int gb = b0 + b;
-      constexpr int PER = 5;  // records per lane, all loaded before use (grid <= 160: one round trip)
-      double rs[PER], rs2[PER];
-      long long rp[PER];
-      int rt[PER];
-      float ro[PER];
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const int c = 32 * k + lane;
-        rp[k] = -1;
-        rs[k] = rs2[k] = -INFINITY;
-        rt[k] = 0;
-        ro[k] = -INFINITY;
-        if (c < (int)gridDim.x) {
-          const CtaRec* src = cta + (size_t)gb * gridDim.x + c;
-          rs[k] = __ldcg(&src->s);
-          rs2[k] = __ldcg(&src->s2);
-          rp[k] = __ldcg(&src->p);
-          rt[k] = __ldcg(&src->ties);
-          ro[k] = __ldcg(&src->ovf);
-        }
-      }
-      for (int c0 = 32 * PER; c0 < (int)gridDim.x; c0 += 32) {  // grids beyond 160 CTAs
-        const int c = c0 + lane;
-        if (c < (int)gridDim.x) {
-          const CtaRec* src = cta + (size_t)gb * gridDim.x + c;
-          const double xs = __ldcg(&src->s), xs2 = __ldcg(&src->s2);
-          const long long xp = __ldcg(&src->p);
-          const int xt = __ldcg(&src->ties);
-          ro[0] = fmaxf(ro[0], __ldcg(&src->ovf));
-          if (xp >= 0) {  // fold into slot 0 with Best2 semantics
-            Best2 m0, mx;
-            m0.init();
-            if (rp[0] >= 0) {
-              m0.s = rs[0];
-              m0.s2 = rs2[0];
-              m0.p = rp[0];
-              m0.ties = rt[0];
-            }
-            mx.s = xs;
-            mx.s2 = xs2;
-            mx.p = xp;
-            mx.ties = xt;
-            m0.merge(mx);
-            rs[0] = m0.s;
-            rs2[0] = m0.s2;
-            rp[0] = m0.p;
-            rt[0] = m0.ties;
-          }
-        }
-      }
-      if (b == 0 && lane == 0 && a.timing) a.timing[5] = s8_timer();
-      double bs = -INFINITY;
-      float ov = -INFINITY;
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        if (rp[k] >= 0) bs = fmax(bs, rs[k]);
-        ov = fmaxf(ov, ro[k]);
-      }
-#pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        bs = fmax(bs, __shfl_xor_sync(FULL, bs, off));
-        ov = fmaxf(ov, __shfl_xor_sync(FULL, ov, off));
-      }
-      long long bp = -1;
-      int nt = 0, neq = 0;
-      double s2 = -INFINITY;
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        if (rp[k] < 0) continue;
-        if (rs[k] == bs) {
-          bp = max(bp, rp[k]);
-          nt += rt[k];
-          ++neq;
-        } else {
-          s2 = fmax(s2, rs[k]);
-        }
-        s2 = fmax(s2, rs2[k]);
-      }
-      nt = __reduce_add_sync(FULL, (unsigned)nt);
-      neq = __reduce_add_sync(FULL, (unsigned)neq);
-#pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        bp = max(bp, __shfl_xor_sync(FULL, bp, off));
-        s2 = fmax(s2, __shfl_xor_sync(FULL, s2, off));
-      }
-      if (neq >= 2) s2 = bs;
-      const bool exo = __shfl_sync(FULL, exotic, b) != 0;
-      if (lane == 0) {
-        const bool fail = bp < 0 || !(ov == -INFINITY || (double)ov + 1e-9 < bs);
-        mc_record r;
-        r.sim = bs;
-        r.second = s2;
-        r.pos = bp;
-        r.flags = (nt >= 2 ? MC_FLAG_TIE : 0u) | (fail ? FLAG_NEED_FALLBACK : 0u) | (exo ? FLAG_NEED_EXHAUSTIVE : 0u);
-        r.reserved = 0;
-        a.rec[gb] = r;
-        if (a.out) a.out[gb] = decide(record_best(r), r.flags & FLAG_NEED_ANY, st.jhead, a.thr);
-      }
-      if (lane < S8_GREP) a.gmax[(size_t)gb * S8_GSTRIDE + 32 * lane] = 0u;
-    }
-    if (lane == 0) {
-      *a.counter = 0u;
-      if (a.timing) a.timing[3] = s8_timer();
-    }
-    dump();
+    return;
   }
+
+  if (warp > S8_CW) {
+    // ------------------------------------------------------------ rescorer
+    if (blockIdx.x == 0 && n_pend > 0) s8_pending(x, a.stage, a.n_app, n_pend, n_scan);
+    s8_pool(x, S8_CW);
+    s8_finish(x, a, cta, b0);
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int cw = warp - 1;
+  double sq[NBQ], q1[NBQ];
+#pragma unroll
+  for (int b = 0; b < NBQ; ++b) {
+    const QPrep pq = b < nb ? a.prep[b] : QPrep{0.0, 0.0, 0.0, 0.f, 0};
+    sq[b] = pq.s;
+    q1[b] = pq.q1;
+  }
+  float lo[NBQ], ovf[NBQ];
+#pragma unroll
+  for (int b = 0; b < NBQ; ++b) {
+    lo[b] = -INFINITY;
+    ovf[b] = -INFINITY;
+  }
+  int tail = 0;
+  if (cw < ncw) {
+    for (int i = cw; i < wk.ns; i += ncw) {
+      const int buf = i % nst;
+      long long row0, slot0;
+      int nr;
+      wk.stage(i, st, row0, nr, slot0);
+      mbar_wait(&S.full[buf], (i / nst) & 1);
+      const uint8_t* sb = stages + (size_t)buf * SDATA;
+      int acc[R][NBQ], acc2[R][NBQ];  // two chains per dot (exact integers: order is free)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int b = 0; b < NBQ; ++b) acc[r][b] = acc2[r][b] = 0;
+      // partially unrolled: each warp runs this loop only a few times per
+      // launch, so a compact body keeps it resident in the instruction cache
+#pragma unroll 8
+      for (int j = 0; j < NCH; ++j) {
+        int c = j + lane;  // rotated chunk order (conflict-free, see the header)
+        c = c >= NCH ? c - NCH : c;
+        c = c >= NCH ? c - NCH : c;
+        uint4 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = *reinterpret_cast<const uint4*>(sb + (r * 32 + lane) * P8 + c * 16);
+#pragma unroll
+        for (int b = 0; b < NBQ; ++b) {
+          const uint4 qv = *reinterpret_cast<const uint4*>(sq8 + b * P8 + c * 16);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (j & 1)
+              acc2[r][b] = dp16x(v[r], qv, acc2[r][b]);
+            else
+              acc[r][b] = dp16x(v[r], qv, acc[r][b]);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int b = 0; b < NBQ; ++b) acc[r][b] += acc2[r][b];
+      float2 e[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) e[r] = rqs[(size_t)buf * RQS + (slot0 & 1) + r * 32 + lane];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[buf]);
+
+      // bounds: the warp's own, then the CTA's (which carries the global one)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const bool valid = r * 32 + lane < nr;
+#pragma unroll
+        for (int b = 0; b < NBQ; ++b) {
+          if (b >= nb) break;
+          const double approx = (double)acc[r][b] * ((double)e[r].x * sq[b]);
+          const double dl = (0.5 * sq[b] * (double)e[r].y + 0.5 * (double)e[r].x * q1[b]) * (1.0 + 1e-9) + 1e-12;
+          float lf = valid ? __double2float_rd(approx - dl) : -INFINITY;
+#pragma unroll
+          for (int off = 16; off; off >>= 1) lf = fmaxf(lf, __shfl_xor_sync(FULL, lf, off));
+          float bnd = s8_val(ld_vol_u32(&S.bound[b]));
+          if (lf > lo[b]) {
+            lo[b] = lf;
+            if (lf > bnd) {  // publish to the CTA (the poller carries it to the other CTAs)
+              if (lane == 0) atomicMax(&S.bound[b], s8_key(lf));
+              bnd = lf;
+            }
+          }
+          const double u = approx + dl;
+          const bool keep = valid && u >= (double)bnd - 1e-9;
+          const unsigned m = __ballot_sync(FULL, keep);
+          if (m) {
+            const int idx = tail + __popc(m & ((1u << lane) - 1u));
+            if (keep) {
+              const float uf = __double2float_ru(u);
+              if (idx < S8_QCAP) {
+                S.qu[cw][idx] = uf;
+                S.qp[cw][idx] = (global_pos(st, row0 + r * 32 + lane, sm) << 2) | b;
+              } else {
+                ovf[b] = fmaxf(ovf[b], uf);
+              }
+            }
+            if (timing && lane == 0) atomicAdd(&S.t[S8T_PUSH], (unsigned long long)__popc(m));
+            tail = min(tail + __popc(m), S8_QCAP);
+            __syncwarp();
+            if (lane == 0) st_rel_cta(&S.qtail[cw], tail);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < NBQ; ++b) {
+    float o = ovf[b];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) o = fmaxf(o, __shfl_xor_sync(FULL, o, off));
+    if (lane == 0) S.ovf[cw][b] = o;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    atomicAdd(&S.done, 1);
+    if (timing) atomicMax(&S.t[S8T_SCAN], s8_timer());
+  }
+  s8_pool(x, cw);
 }
 
 // ---------------------------------------------------------------- host side
@@ -739,21 +807,27 @@ void s8_plan_destroy(S8Plan* p) { delete p; }
 template <int KB>
 static cudaError_t s8_launch(const S8Plan* p, const RingBufs& rb, const RingState& st, const double* q64, int nb,
                              CtaRec* cta, int b0, int grid, ShardMap sm, const S8Args& a, cudaStream_t s) {
-  if (nb == 1)
-    k_stream8_scan<KB, 1><<<grid, S8_THREADS, p->smem[0], s>>>(rb, st, q64, nb, cta, b0, sm, a,
-                                                                p->nst[0], p->Dp);
-  else
-    k_stream8_scan<KB, 4><<<grid, S8_THREADS, p->smem[1], s>>>(rb, st, q64, nb, cta, b0, sm, a,
-                                                                p->nst[1], p->Dp);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(S8_THREADS);
+  cfg.dynamicSmemBytes = nb == 1 ? p->smem[0] : p->smem[1];
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see griddepcontrol in the kernel
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (nb == 1) return cudaLaunchKernelEx(&cfg, k_stream8_scan<KB, 1>, rb, st, q64, nb, cta, b0, sm, a, p->nst[0], p->Dp);
+  return cudaLaunchKernelEx(&cfg, k_stream8_scan<KB, 4>, rb, st, q64, nb, cta, b0, sm, a, p->nst[1], p->Dp);
 }
 
 cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingState& st, const double* q64, int nb,
                                 CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
                                 const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
-                                const QPrep* prep, const int8_t* q8, cudaStream_t s) {
+                                const QPrep* prep, const int8_t* q8, unsigned* done_seq, unsigned seq,
+                                cudaStream_t s) {
   if (!p || nb < 1 || nb > 4) return cudaErrorInvalidValue;
-  S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), prep, q8, app.stage, app.n, app.d_state};
+  S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), prep, q8, app.stage, app.n, app.d_state, done_seq, seq};
   switch (p->P8 / 128) {
     case 1: return s8_launch<1>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
     case 2: return s8_launch<2>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
@@ -767,4 +841,5 @@ cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingS
   }
 }
 
+#undef S
 }  // namespace mc

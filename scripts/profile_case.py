@@ -42,7 +42,7 @@ if os.environ.get("MC_GEMV_TIMING"):
     lib = _native.load()
     lib.mc_debug_gemv_timing.restype = ctypes.c_int
     t = (ctypes.c_ulonglong * 8)()
-    per = (ctypes.c_ulonglong * (8 * 512))()
+    per = (ctypes.c_ulonglong * (12 * 512))()
     for i in range(a.iters):
         lib.mc_debug_gemv_timing(t, 1)  # reset
         ring.retrieve(Q[i])
@@ -64,10 +64,12 @@ if os.environ.get("MC_GEMV_TIMING"):
                                              arr[:, 6].sum(), arr[:, 7].sum()))
         if i == a.iters - 1:
             order = _np.argsort(-rec)
-            print("slowest CTAs: cta scan_end pool_entry resc_start resc_end pool_exit record n_resc (us)")
+            cyc = _np.array(per[8 * 512:8 * 512 + 4 * 148], dtype=_np.float64).reshape(148, 4)
+            print("slowest CTAs: cta scan_end pool_entry resc_start resc_end pool_exit record n_resc (us) | "
+                  "cycles: first_pass second_pass first_dot dot")
             for c in order[:8]:
-                print("   %4d %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f %3d" % (c, rel(scan_end[c]), rel(pool[c]), rel(r0[c]),
-                                                                     rel(r1[c]) if r1[c] else _np.nan, rel(poolx[c]),
-                                                                     rel(rec[c]), arr[c, 7]))
+                print("   %4d %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f %3d | %6d %4d %6d %6d" % (
+                    c, rel(scan_end[c]), rel(pool[c]), rel(r0[c]), rel(r1[c]) if r1[c] else _np.nan, rel(poolx[c]),
+                    rel(rec[c]), arr[c, 7], cyc[c, 0], cyc[c, 1], cyc[c, 2] if cyc[c, 2] < 1e18 else -1, cyc[c, 3]))
             print("median: scan_end %.1f pool_entry %.1f pool_exit %.1f record %.1f" % (
                 rel(_np.median(scan_end)), rel(_np.median(pool)), rel(_np.median(poolx)), rel(_np.median(rec))))
