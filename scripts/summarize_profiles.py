@@ -56,14 +56,15 @@ def to_bytes(v, unit):
     return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
 
 
-summary = {}
+old = DST / "ncu_summary.json"
+summary = json.loads(old.read_text()) if old.exists() else {}
 for rep in sorted(SRC.glob("*.ncu-rep")):
     m, stalls, kname = raw_metrics(rep)
     tot, top = source_top(rep)
     key = rep.stem
     dram = to_bytes(*m["dram__bytes_read.sum"]) + to_bytes(*m["dram__bytes_write.sum"])
-    kshort = ("k_gemv8_scan" if "gemv8" in key else "k_gemv_scan" if "gemv" in key
-              else "k_tc_scan_pair" if "tc_pair" in key else "k_merge")
+    kshort = ("k_stream8_scan" if key.startswith("s8") else "k_gemv8_scan" if "gemv8" in key
+              else "k_gemv_scan" if "gemv" in key else "k_tc_scan_pair" if "tc_pair" in key else "k_merge")
     summary[kshort] = {"capture": f"{tag}_{key}.txt", "dram_bytes_per_launch": dram,
                        "duration_us_under_ncu": float(m["gpu__time_duration.sum"][0]) * (
                            1e-3 if m["gpu__time_duration.sum"][1] == "nsecond" else 1.0)}
@@ -96,7 +97,9 @@ if launch_csv.exists():
     total = sum(sum(v) for v in per.values())
     with open(DST / f"{tag}_launches_bench.txt", "w") as fh:
         fh.write("ncu --metrics gpu__time_duration.sum --clock-control none over "
-                 "`python bench.py --steps 4 --warmup 3 --no-c3` (cold-cache, serialised: compare shares, not absolutes)\n\n")
+                 "`python bench.py --steps 8 --warmup 3 --no-c3` (cold-cache, serialised: compare shares, not absolutes)\n"
+                 "k_append = the bulk preload of the 4 rotation caches (setup); k_l2_flush = the per-step cross-check's "
+                 "L2 flush (outside its events); the timed steps launch only the scan kernel\n\n")
         fh.write(f"{'kernel':40s} {'launches':>8s} {'mean us':>9s} {'share':>7s}\n")
         for name, v in sorted(per.items(), key=lambda x: -sum(x[1])):
             fh.write(f"{name:40s} {len(v):8d} {sum(v) / len(v):9.1f} {100 * sum(v) / total:6.1f}%\n")
