@@ -155,7 +155,7 @@ def cpu_baseline(rows, Q, new_rows, insert: bool, seconds: float = 12.0, batch: 
 
 
 # --------------------------------------------------------------------------- our arm
-def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, device=0, n_rot=4):
+def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, device=0, n_rot=4, dist=None):
     """One BASELINE config on one GPU.
 
     value: `steps` back-to-back lookup steps (B queries + the step's FIFO insert)
@@ -170,9 +170,7 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
     total = warmup + steps
     rows, Q, new_rows = make_workload(dim, n_entries, (2 * total + 8) * B)
     cache = SemanticCache(capacity=n_entries, dim=dim, device=device)
-    cache.ring.append(rows)  # bulk preload (device ring), host metadata alongside
-    cache._store.extend(CacheEntry(f"e{i}", rows[i], "large", i, 0.0) for i in range(n_entries))
-    cache._next_seq = n_entries
+    cache.bulk_load(CacheEntry(f"e{i}", rows[i], "large", i, 0.0) for i in range(n_entries))  # one device append
     table = ThresholdTable.default()
     cache.ring.set_table(table.pairs, table.total_steps)
     extra = []
@@ -186,8 +184,12 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
     qd = Q[: total * B].reshape(total, B, dim)
     rd = new_rows[:total] if insert else None
     _native.DeviceRing.profile_rotate(rings, qd[:warmup], None if rd is None else rd[:warmup], warmup)
+    if dist:
+        dist.barrier()  # every rank enters the timed region together
     with ClockSampler(device) as clk:
         rot = _native.DeviceRing.profile_rotate(rings, qd[warmup:], None if rd is None else rd[warmup:], steps)
+    if dist:  # the job's time is the slowest rank's
+        rot["step_ms"] = dist.max_over_ranks(rot["step_ms"])
     # per-step cross-check: events around each step, L2 flushed between steps
     n_chk = min(steps, 200)
     prof = cache.ring.profile_steps(qd[warmup:warmup + n_chk], None if rd is None else rd[warmup:warmup + n_chk],
@@ -206,7 +208,7 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
                 cache._store.popleft()
     assert len(cache._store) == len(cache.ring)
     step_ms = rot["step_ms"]
-    value = B / (step_ms * 1e-3)
+    value = (dist.world if dist else 1) * B / (step_ms * 1e-3)  # units all ranks processed / the job's time
 
     # e2e: public API from host buffers
     Qe = Q[total * B:].reshape(-1, B, dim)
@@ -217,15 +219,20 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
         (cache.retrieve(Qe[i][0], table) if B == 1 else cache.retrieve_batch(Qe[i], table))
         if insert:
             cache.add(f"w{i}", re[i], "large", t_base + i)
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
     for i in range(warmup, warmup + steps):
         r = cache.retrieve(Qe[i][0], table) if B == 1 else cache.retrieve_batch(Qe[i], table)
         if insert:
             cache.add(f"s{i}", re[i], "large", t_base + i)
     e2e_s = time.perf_counter() - t0
+    if dist:
+        e2e_s = dist.max_over_ranks(e2e_s)
+    n_ranks = dist.world if dist else 1
     e2e_launches = (cache.ring.stats()["kernel_launches"] - launches0) / (warmup + steps)
     e2e = {
-        "value": B * steps / e2e_s, "unit": "lookups/s",
+        "value": n_ranks * B * steps / e2e_s, "unit": "lookups/s",
         "h2d_bytes_per_step": B * dim * 8 + (dim * 8 if insert else 0),
         "d2h_bytes_per_step": B * 24,
         "kernel_launches_per_step": e2e_launches,
@@ -274,6 +281,56 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
     }
     cache.close()
     return out
+
+
+class Dist:
+    """torch.distributed plumbing for N > 1 (one process per GPU, NCCL): barrier and max over ranks."""
+
+    def __init__(self):
+        import torch
+        import torch.distributed as td
+
+        self.torch, self.td = torch, td
+        self.rank = int(os.environ["RANK"])
+        self.world = int(os.environ["WORLD_SIZE"])
+        self.local = int(os.environ.get("LOCAL_RANK", self.rank))
+        torch.cuda.set_device(self.local)
+        td.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        self.td.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device="cuda")
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+
+def run_sharded(dist, dim, per_gpu, steps, warmup):
+    """C4-style: one cache of world x per_gpu entries sharded round-robin across the ranks; every
+    batch-1 lookup scans each shard (certified local scan) and all-gathers 32-byte records over NCCL,
+    then merges on the device.  Timed through the sharded public API (host in the loop), max over ranks."""
+    from paper_2503_11972_b200 import CacheEntry, ThresholdTable
+    from paper_2503_11972_b200.sharded import ShardedSemanticCache
+
+    n = dist.world * per_gpu
+    rows, Q, _ = make_workload(dim, n, steps + warmup + 8)
+    sc = ShardedSemanticCache(capacity=n, dim=dim, device=dist.local)
+    sc.bulk_load([CacheEntry(f"e{i}", rows[i], "large", i, 0.0) for i in range(n)])
+    table = ThresholdTable.default()
+    for i in range(warmup):
+        sc.retrieve(Q[i], table)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(warmup, warmup + steps):
+        sc.retrieve(Q[i], table)
+    dt = dist.max_over_ranks(time.perf_counter() - t0)
+    sc.close()
+    return {"workload": f"C4: {n} entries ({per_gpu} per GPU) sharded round-robin over {dist.world} GPUs, "
+                        f"{dim}-dim, batch-1 lookups, NCCL all-gather of 32-byte records + device merge",
+            "value": steps / dt, "unit": "lookups/s", "ms_per_lookup": 1e3 * dt / steps, "scaling": "weak",
+            "timing": "public sharded API with the host in the loop (H2D, NCCL, merge, D2H), max over ranks"}
 
 
 def traffic_from_profiles(kernel: str):
@@ -347,9 +404,11 @@ def main():
         print(json.dumps(reference_arm(args)))
         return
 
+    dist = Dist() if (world > 1 or os.environ.get("BENCH_DIST")) else None  # BENCH_DIST: exercise N=1 under torchrun
+    device = dist.local if dist else 0
     pk = peaks()
     flush = 256 << 20
-    c2 = run_config("c2", 768, 100_000, 1, args.steps, args.warmup, True, flush, pk)
+    c2 = run_config("c2", 768, 100_000, 1, args.steps, args.warmup, True, flush, pk, device=device, dist=dist)
     line = {
         "metric": METRIC,
         "value": c2["value"], "unit": "lookups/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -364,14 +423,22 @@ def main():
     }
     if not args.no_c3:
         c3 = run_config("c3", 1024, 100_000, 256, min(60, max(20, args.steps // 10)), args.warmup, False, flush, pk,
-                        n_rot=2)
+                        device=device, n_rot=2, dist=dist)
         line["c3"] = {"workload": "C3: 100k entries, 1024-dim, batch-256 lookups", "value": c3["value"],
                       "unit": "lookups/s", "ms_per_step": c3["ms_per_step"], "e2e": c3["e2e"],
                       "roofline": c3["roofline"], "clocks": c3["clocks"], "gpu_launches": c3["gpu_launches"],
                       "profile": c3["profile"]}
+    if dist:  # the path's real exchange step: an entry-sharded cache merged over NCCL
+        try:
+            line["c4"] = run_sharded(dist, 768, 100_000, min(2000, args.steps), args.warmup)
+        except Exception as exc:  # reported, never fatal to the headline line
+            line["c4"] = {"error": f"{type(exc).__name__}: {exc}"}
     if rank == 0:
         line["cpu_baseline"] = cpu_baseline(c2["rows"], c2["Q"], c2["new_rows"], insert=True, seconds=args.cpu_seconds)
         print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.td.destroy_process_group()
 
 
 if __name__ == "__main__":

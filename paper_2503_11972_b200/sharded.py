@@ -158,6 +158,33 @@ class ShardedSemanticCache:
     def add(self, id: str, embedding: np.ndarray, producer: str, inserted_at: float) -> list[CacheEntry]:
         return self.insert(CacheEntry(id, embedding, producer, self._next_seq, inserted_at))
 
+    def bulk_load(self, entries) -> list[CacheEntry]:
+        """insert() for every entry in order (same answers, errors and evictions on every rank),
+        with one device append of this shard's rows; see SemanticCache.bulk_load."""
+        from .cache import _validated_prefix
+
+        entries = list(entries)
+        batch, bad = _validated_prefix(self, entries)
+        if self.max_age_s is not None or len(batch) > self.capacity:  # the per-entry path decides evictions
+            out: list[CacheEntry] = []
+            for e in entries:
+                out.extend(self.insert(e))
+            return out
+        evicted: list[CacheEntry] = []
+        if batch:
+            # capacity evictions first (module doc), then this shard's share of the appends
+            self._evict(len(self._store) + len(batch) - self.capacity, evicted)
+            p0 = self._appended
+            mine = [e.embedding for j, e in enumerate(batch) if (p0 + j) % self.n_shards == self.shard]
+            if mine:
+                self.ring.append(np.stack(mine))
+            self._store.extend(batch)
+            self._appended += len(batch)
+            self._next_seq = max(self._next_seq, batch[-1].seq + 1)
+        if bad is not None:
+            self.insert(bad)  # raises the reference's error for the first invalid entry
+        return evicted
+
     # -- lookups (SPMD: every rank passes the same queries) -----------------------
     def _records(self, Q: np.ndarray):
         """Local records -> all-gathered [G, B] record bytes, on the comm device."""

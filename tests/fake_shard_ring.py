@@ -38,6 +38,10 @@ class FakeShardRing:
         self.pos.append(self.j * self.G + self.g)
         self.j += 1
 
+    def append(self, rows):
+        for r in np.asarray(rows, dtype=np.float64).reshape(-1, self.dim):
+            self.append1(r)
+
     def evict_front(self, n):
         assert 0 <= n <= len(self.rows)
         del self.rows[:n], self.pos[:n]

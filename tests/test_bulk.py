@@ -1,0 +1,103 @@
+"""Bulk preload / snapshot import: SemanticCache.bulk_load and the chunked
+import_jsonl must equal the reference's per-entry insert() replay (cache.py:206-235, 279-302) in
+every observable — stored entries, evictions, next_seq, errors and their messages (CPU, fake ring)."""
+import json
+
+import numpy as np
+import pytest
+
+import paper_2503_11972_b200.cache as cache_mod
+from paper_2503_11972_b200 import CacheEntry, EmbeddingError, SemanticCache, normalize
+from tests.fake_ring import FakeRing
+
+
+@pytest.fixture(autouse=True)
+def fake_ring(monkeypatch):
+    monkeypatch.setattr(cache_mod.SemanticCache, "_ring_factory", staticmethod(FakeRing))
+
+
+def _entries(rng, n, d, seq0=0, small_every=0):
+    out = []
+    for i in range(n):
+        prod = "small" if small_every and i % small_every == 0 else "large"
+        out.append(CacheEntry(f"e{seq0 + i}", normalize(rng.standard_normal(d)), prod, seq0 + i, float(i)))
+    return out
+
+
+def _state(c):
+    return [e.id for e in c.entries()], c.next_seq, [r.tolist() for r in c.ring.rows]
+
+
+@pytest.mark.parametrize("policy", ["all", "large"])
+@pytest.mark.parametrize("cap,n", [(50, 30), (50, 50), (50, 120), (7, 1000)])
+def test_bulk_equals_sequential_inserts(policy, cap, n):
+    rng = np.random.default_rng(cap * 1000 + n)
+    d = 8
+    pre = _entries(rng, 20, d)
+    batch = _entries(rng, n, d, seq0=100, small_every=3)
+    a, b = SemanticCache(cap, d, policy=policy), SemanticCache(cap, d, policy=policy)
+    for e in pre:
+        a.insert(e)
+        b.insert(e)
+    ev_seq = [x.id for e in batch for x in a.insert(e)]
+    ev_bulk = [x.id for x in b.bulk_load(batch)]
+    assert ev_bulk == ev_seq
+    assert _state(a) == _state(b)
+
+
+def test_bulk_stops_at_the_first_invalid_entry_like_insert():
+    rng = np.random.default_rng(5)
+    d = 6
+    good = _entries(rng, 10, d)
+    bad_norm = CacheEntry("bad", 2.0 * good[0].embedding, "large", 10, 0.0)
+    rest = _entries(rng, 5, d, seq0=11)
+    for bad, exc, msg in [(bad_norm, EmbeddingError, "not unit norm"),
+                          (CacheEntry("shape", np.ones(d + 1) / np.sqrt(d + 1), "large", 10, 0.0), EmbeddingError,
+                           "shape"),
+                          (CacheEntry("prod", good[0].embedding, "medium", 10, 0.0), ValueError, "unknown producer"),
+                          (CacheEntry("seq", good[0].embedding, "large", 3, 0.0), ValueError, "seq must increase")]:
+        a, b = SemanticCache(40, d), SemanticCache(40, d)
+        with pytest.raises(exc, match=msg) as e1:
+            for e in good + [bad] + rest:
+                a.insert(e)
+        with pytest.raises(exc, match=msg) as e2:
+            b.bulk_load(good + [bad] + rest)
+        assert str(e1.value) == str(e2.value)
+        assert _state(a) == _state(b)
+
+
+def test_bulk_with_age_limit_matches_inserts():
+    rng = np.random.default_rng(9)
+    d = 4
+    batch = _entries(rng, 60, d)
+    batch = [CacheEntry(e.id, e.embedding, e.producer, e.seq, 10.0 * i) for i, e in enumerate(batch)]
+    a, b = SemanticCache(100, d, max_age_s=95.0), SemanticCache(100, d, max_age_s=95.0)
+    ev_seq = [x.id for e in batch for x in a.insert(e)]
+    assert [x.id for x in b.bulk_load(batch)] == ev_seq
+    assert _state(a) == _state(b)
+
+
+def test_chunked_import_equals_per_line_replay(tmp_path):
+    rng = np.random.default_rng(2)
+    d = 5
+    path = tmp_path / "snap.jsonl"
+    ents = _entries(rng, 9000, d, small_every=4)
+    with open(path, "w") as fh:
+        for e in ents:
+            fh.write(json.dumps({"id": e.id, "seq": e.seq, "inserted_at": e.inserted_at, "producer": e.producer,
+                                 "embedding": e.embedding.tolist()}) + "\n")
+    a = SemanticCache(5000, d, policy="large")
+    ref_acc = 0
+    for e in ents:  # the reference's loop (cache.py:279-302)
+        before = a.next_seq
+        a.insert(e)
+        ref_acc += a.next_seq != before
+    b = SemanticCache(5000, d, policy="large")
+    assert b.import_jsonl(path) == ref_acc
+    assert _state(a) == _state(b)
+    with open(path, "a") as fh:
+        fh.write("{not json\n")
+    c = SemanticCache(5000, d, policy="large")
+    with pytest.raises(ValueError, match=r"snap.jsonl:9001: bad snapshot record"):
+        c.import_jsonl(path)
+    assert _state(c) == _state(a)  # every record before the bad line was stored

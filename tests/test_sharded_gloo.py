@@ -31,10 +31,27 @@ def _worker(rank, world, port, errq):
 
         rng = np.random.default_rng(123)  # same stream on every rank (SPMD)
         d, cap = 24, 37
-        sc = ShardedSemanticCache(cap, d, policy="all", max_age_s=60.0, ring_factory=FakeShardRing)
-        oc = OracleCache(cap, d, max_age_s=60.0)
         table, ot = ThresholdTable.default(), OracleTable()
         centers = rng.standard_normal((5, d))
+        # bulk preload of a capacity-only cache, then churn, against the oracle
+        sb = ShardedSemanticCache(cap, d, policy="large", ring_factory=FakeShardRing)
+        ob = OracleCache(cap, d, policy="large")
+        pre = []
+        for i in range(90):
+            v = centers[i % 5] + 0.7 * rng.standard_normal(d)
+            pre.append(CacheEntry(f"b{i}", v / np.linalg.norm(v), "small" if i % 7 == 0 else "large", i, float(i)))
+        for chunk in (pre[:30], pre[30:]):  # the second chunk evicts part of the first
+            evb = sb.bulk_load(chunk)
+            evo = [x for e in chunk for x in ob.insert(OracleEntry(e.id, e.embedding, e.producer, e.seq, e.inserted_at))]
+            assert [x.id for x in evb] == [x.id for x in evo], rank
+        Qb = centers[rng.integers(0, 5, 6)] + 0.7 * rng.standard_normal((6, d))
+        Qb /= np.linalg.norm(Qb, axis=1, keepdims=True)
+        for q, r in zip(Qb, sb.retrieve_batch(Qb, table)):
+            e, sim, k = ob.retrieve_entry(q, ot)
+            assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), rank
+            assert r.k == k and abs(r.similarity - sim) < 1e-12
+        sc = ShardedSemanticCache(cap, d, policy="all", max_age_s=60.0, ring_factory=FakeShardRing)
+        oc = OracleCache(cap, d, max_age_s=60.0)
         t = 0.0
         for i in range(400):
             t += float(rng.exponential(1.0)) + (80.0 if i in (150, 151, 300) else 0.0)
