@@ -96,6 +96,16 @@ int64_t mc_size(const mc_cache* h);
 int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* out_live,
                       double* out_sim, int32_t* out_k, uint32_t* out_flags);
 
+/* Asynchronous form of mc_retrieve_batch (the serving loop's overlap of host
+ * work with the scan): submit enqueues the lookup against the current cache
+ * state and returns a ticket; wait returns its answers exactly as
+ * mc_retrieve_batch would have.  One lookup may be in flight per handle.
+ * mc_append / mc_evict_front between submit and wait only change what LATER
+ * lookups see (a forced device flush first completes the lookup in flight). */
+int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* out_ticket);
+int mc_retrieve_wait(mc_cache* h, uint32_t ticket, int64_t* out_live, double* out_sim, int32_t* out_k,
+                     uint32_t* out_flags);
+
 /* Force a scan path (tests / benchmarks).  MC_PATH_AUTO picks by batch size. */
 int mc_set_path(mc_cache* h, int32_t path);
 

@@ -30,7 +30,7 @@ EXPORTED = (
     "mc_create", "mc_destroy", "mc_set_thresholds", "mc_append", "mc_evict_front", "mc_size",
     "mc_retrieve_batch", "mc_set_path", "mc_configure_shard", "mc_retrieve_local_async",
     "mc_merge_records", "mc_stats", "mc_last_error", "mc_version", "mc_profile_steps", "mc_profile_rotate",
-    "mc_debug_gemv_timing",
+    "mc_debug_gemv_timing", "mc_retrieve_submit", "mc_retrieve_wait",
 )
 
 
@@ -58,6 +58,8 @@ def _declare(lib):
     lib.mc_stats.argtypes = [vp, dp]
     lib.mc_profile_steps.argtypes = [vp, dp, dp, i32, i32, i64, dp, dp]
     lib.mc_profile_rotate.argtypes = [dp, i32, dp, dp, i32, i32, dp, dp]
+    lib.mc_retrieve_submit.argtypes = [vp, dp, i32, dp]
+    lib.mc_retrieve_wait.argtypes = [vp, C.c_uint32, dp, dp, dp, dp]
     lib.mc_debug_gemv_timing.argtypes = [dp, i32]
     lib.mc_last_error.restype = C.c_char_p
     lib.mc_version.restype = C.c_char_p
@@ -107,6 +109,9 @@ class DeviceRing:
         self._hv = h.value  # plain int handle for the per-call fast paths
         self._append = self.lib.mc_append
         self._retrieve = self.lib.mc_retrieve_batch
+        self._submit = self.lib.mc_retrieve_submit
+        self._wait = self.lib.mc_retrieve_wait
+        self._ticket = np.zeros(1, dtype=np.uint32)
         self._bcap = 0
         self._ensure_out(1)
         self._table_key = None
@@ -186,6 +191,21 @@ class DeviceRing:
         """One query (1-d, length dim) -> (live, sim, k, flags) as Python scalars."""
         self._qbuf[0] = q  # copies and converts; the buffer pointer never changes
         rc = self._retrieve(self._hv, self._qptr, 1, *self._out_ptrs)
+        if rc:
+            _check(self.lib, rc)
+        return int(self._live[0]), float(self._sim[0]), int(self._k[0]), int(self._flags[0])
+
+    def submit1(self, q: np.ndarray) -> int:
+        """Enqueue one lookup (mc_retrieve_submit); returns its ticket."""
+        self._qbuf[0] = q
+        rc = self._submit(self._hv, self._qptr, 1, self._ticket.ctypes.data)
+        if rc:
+            _check(self.lib, rc)
+        return int(self._ticket[0])
+
+    def wait1(self, ticket: int):
+        """The submitted lookup's (live, sim, k, flags) as Python scalars (mc_retrieve_wait)."""
+        rc = self._wait(self._hv, ticket, *self._out_ptrs)
         if rc:
             _check(self.lib, rc)
         return int(self._live[0]), float(self._sim[0]), int(self._k[0]), int(self._flags[0])

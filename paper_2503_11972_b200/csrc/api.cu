@@ -17,7 +17,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -27,6 +29,18 @@
 using namespace mc;
 
 static thread_local std::string g_err;
+
+// MC_HOST_TIMING=1: mean host-side phase times of mc_retrieve_batch, printed at mc_destroy
+// (measurement only): [0] stage + quantise, [1] H2D enqueue, [2] launch, [3] wait for the result.
+struct HostTiming {
+  bool on = getenv("MC_HOST_TIMING") && atoi(getenv("MC_HOST_TIMING"));
+  double acc[4] = {0, 0, 0, 0};
+  long long n = 0;
+};
+static HostTiming g_ht;
+static inline double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -90,6 +104,11 @@ struct mc_cache {
   unsigned* h_seq = nullptr;  // pinned, mapped: completion word of the zero-copy lookup
   unsigned* d_seq = nullptr;
   unsigned seq = 0;
+  // an asynchronous lookup in flight (mc_retrieve_submit): its batch, device query and seq
+  unsigned inflight_seq = 0;
+  int inflight_B = 0;
+  const double* inflight_q = nullptr;
+  bool inflight_ready = false;  // completed (and any fallback applied) while staging appends
 
   TcPlan* tc = nullptr;           // tensor-core scan plan, created on first batched lookup
   S8Plan* s8 = nullptr;           // TMA-streamed int8 scan plan (tensor maps of ring8 / ringq)
@@ -116,6 +135,8 @@ struct DeviceGuard {
 };
 
 RingState mirror(const mc_cache* h) { return RingState{h->head, h->count, h->jhead, h->C}; }
+
+int finish_inflight(mc_cache* h);
 
 RingBufs rbufs(const mc_cache* h) { return RingBufs{h->ring16, h->ring64, h->ring8, h->ringq, h->P8}; }
 
@@ -147,12 +168,18 @@ void quantize_query(const double* q, int D, int Dp, QPrep* p, int8_t* q8) {
     s = (float)(amax / 127.0);
     if ((double)s < amax / 127.0) s = std::nextafter(s, INFINITY);
   }
+  // q̂ = rint(q / s) via one reciprocal: a rounding flip from the multiply moves
+  // |q_i - s q̂_i| past s/2 by ~2^-52 s at most, far inside the bound's slack
+  // (the 1 + 1e-9 factor and the 1e-12 term of the per-row delta)
   double l1 = 0.0;
-  for (int i = 0; i < Dp; ++i) {
-    const int qi = (i < D && s > 0.0f) ? (int)std::nearbyint(q[i] / (double)s) : 0;
+  const double inv = s > 0.0f ? 1.0 / (double)s : 0.0;
+  int i = 0;
+  for (; i < D; ++i) {
+    const int qi = (int)__builtin_rint(q[i] * inv);
     q8[i] = (int8_t)qi;
-    l1 += std::fabs((double)qi);
+    l1 += (double)(qi < 0 ? -qi : qi);
   }
+  for (; i < Dp; ++i) q8[i] = 0;
   p->q1 = l1 * (double)s;
   p->n2 = std::sqrt(a2) * (1.0 + 1e-12);
   p->n1 = a1 * (1.0 + 1e-12);
@@ -261,8 +288,10 @@ int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse,
   int8_t* h8 = reinterpret_cast<int8_t*>(hp + prep_head(B));
   if (quantise)
     for (int b = 0; b < B; ++b) quantize_query(qdst + (size_t)b * h->Dp, h->D, h->Dp, hq + b, h8 + (size_t)b * h->Dp);
+  const double t1 = g_ht.on ? now_us() : 0.0;
   CU(cudaMemcpyAsync(h->d_env, h->h_env, prep_off + (quantise ? prep_bytes(h, B) : 0), cudaMemcpyHostToDevice,
                      h->stream));
+  if (g_ht.on) g_ht.acc[1] += now_us() - t1;
   if (async_reuse) {  // the caller returns before the copy completes
     CU(cudaEventRecord(h->env_ev, h->stream));
     h->env_inflight = true;
@@ -278,7 +307,9 @@ int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse,
 // when the pending batch is too large to ride along with a lookup.
 int flush(mc_cache* h) {
   if (h->n_pending == 0 && !h->state_dirty) return MC_OK;
-  int rc = wait_env(h);
+  int rc = finish_inflight(h);  // an asynchronous lookup must finish on the ring state it scanned
+  if (rc) return rc;
+  rc = wait_env(h);
   if (rc) return rc;
   if (h->n_pending > 0)
     CU(cudaMemcpyAsync(h->d_env, h->h_env, (size_t)h->n_pending * h->Dp * sizeof(double), cudaMemcpyHostToDevice,
@@ -390,6 +421,30 @@ int lookup_enqueue(mc_cache* h, const double* queries, int B, mc_record* rec, Ou
   const GemvAppendArgs app = take_pending(h, h->d_env);
   *q_dev = q;
   return scan_merge(h, q, B, rec, out, app, prep, q8, nullptr, done_seq, seq);
+}
+
+int wait_seq(mc_cache* h, unsigned seq);
+
+// Complete the asynchronous lookup in flight, if any: wait for its decisions
+// and run the exhaustive fallback for the queries whose certificate needs it
+// (while the ring still holds the state that lookup scanned).
+int finish_inflight(mc_cache* h) {
+  if (!h->inflight_seq || h->inflight_ready) return MC_OK;
+  int rc = wait_seq(h, h->inflight_seq);
+  if (rc) return rc;
+  const int B = h->inflight_B;
+  bool need = false;
+  for (int b = 0; b < B; ++b) need |= (h->h_out[b].flags & FLAG_NEED_ANY) != 0;
+  if (need) {
+    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, h->inflight_q, B, h->d_rec, h->d_scratch,
+                           exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
+    CU(launch_finalize(h->d_rec, 1, B, -1, h->d_state, h->thr, h->d_out, h->stream));
+    h->stats[7] += 3;
+    CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+  }
+  h->inflight_ready = true;
+  return MC_OK;
 }
 
 // True when a B-query lookup runs on the streamed int8 scan, which can hand
@@ -519,6 +574,10 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
 
 int mc_destroy(mc_cache* h) {
   if (!h) return MC_OK;
+  if (g_ht.on && g_ht.n)
+    fprintf(stderr, "[modmcache host timing] %lld lookups: H2D enqueue %.2f us, stage+quantise+launch %.2f us, "
+                    "wait for result %.2f us (means)\n", g_ht.n, g_ht.acc[1] / g_ht.n, g_ht.acc[2] / g_ht.n,
+            g_ht.acc[3] / g_ht.n);
   {
     std::lock_guard<std::mutex> lk(h->mu);
     DeviceGuard guard(h->dev);
@@ -628,6 +687,7 @@ int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* ou
   if (B == 0) return MC_OK;
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard guard(h->dev);
+  if (h->inflight_seq) return fail(MC_ERR_STATE, "an asynchronous lookup is in flight: mc_retrieve_wait first");
   if (h->count == 0) {  // cache.py:252-253
     for (int b = 0; b < B; ++b) {
       if (out_live) out_live[b] = -1;
@@ -643,10 +703,19 @@ int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* ou
   const double* q = nullptr;
   if (direct_result(h, B)) {  // decisions land in host-mapped memory; no D2H copy, no stream sync
     const unsigned seq = ++h->seq;
+    const double t0 = g_ht.on ? now_us() : 0.0;
+    const double h2d0 = g_ht.acc[1];
     rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_outm, false, &q, h->d_seq, seq);
     if (rc) return rc;
+    const double t2 = g_ht.on ? now_us() : 0.0;
     rc = wait_seq(h, seq);
     if (rc) return rc;
+    if (g_ht.on) {  // enqueue time minus the H2D call = staging, quantisation and the launch
+      const double t3 = now_us();
+      g_ht.acc[2] += (t2 - t0) - (g_ht.acc[1] - h2d0);
+      g_ht.acc[3] += t3 - t2;
+      g_ht.n++;
+    }
   } else {
     rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_out, false, &q);
     if (rc) return rc;
@@ -664,6 +733,57 @@ int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* ou
     CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
   }
+  return copy_out(h, B, out_live, out_sim, out_k, out_flags);
+}
+
+int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* out_ticket) {
+  if (!h || !out_ticket || (!queries && B > 0)) return fail(MC_ERR_ARG, "NULL argument");
+  if (B < 1) return fail(MC_ERR_ARG, "batch must be positive");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  if (h->inflight_seq) return fail(MC_ERR_STATE, "an asynchronous lookup is already in flight");
+  int rc = ensure_batch(h, B);
+  if (rc) return rc;
+  const unsigned seq = ++h->seq;
+  h->inflight_B = B;
+  h->inflight_q = nullptr;
+  if (h->count == 0) {  // cache.py:252-253: answered now
+    for (int b = 0; b < B; ++b) h->h_out[b] = OutRec{-1, NAN, 0, MC_FLAG_EMPTY};
+    h->inflight_ready = true;
+  } else if (direct_result(h, B)) {  // the kernel publishes into mapped memory; the caller returns now
+    const double* q = nullptr;
+    rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_outm, /*async_reuse=*/true, &q, h->d_seq, seq);
+    if (rc) return rc;
+    h->inflight_q = q;
+    h->inflight_ready = false;
+  } else {  // paths without a zero-copy result complete synchronously
+    const double* q = nullptr;
+    rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_out, false, &q);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    h->env_inflight = false;
+    h->inflight_seq = seq;
+    h->inflight_q = q;
+    h->inflight_ready = false;
+    *h->h_seq = seq;  // already complete: finish_inflight only applies the fallback
+  }
+  h->inflight_seq = seq;
+  *out_ticket = seq;
+  return MC_OK;
+}
+
+int mc_retrieve_wait(mc_cache* h, uint32_t ticket, int64_t* out_live, double* out_sim, int32_t* out_k,
+                     uint32_t* out_flags) {
+  if (!h) return fail(MC_ERR_ARG, "NULL handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  if (!h->inflight_seq || ticket != h->inflight_seq) return fail(MC_ERR_STATE, "no lookup %u in flight", ticket);
+  int rc = finish_inflight(h);
+  if (rc) return rc;
+  const int B = h->inflight_B;
+  h->inflight_seq = 0;
+  h->inflight_ready = false;
   return copy_out(h, B, out_live, out_sim, out_k, out_flags);
 }
 

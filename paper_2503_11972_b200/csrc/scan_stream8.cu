@@ -51,7 +51,8 @@
 namespace mc {
 
 constexpr int S8_CW = 8;                       // consumer warps (max)
-constexpr int S8_THREADS = (S8_CW + 3) * 32;   // producer + consumers + rescorer + bound poller
+constexpr int S8_THREADS = (S8_CW + 4) * 32;   // producer + consumers + rescorer + bound poller + eager rescorer
+constexpr int S8_EAGER = S8_CW + 1;            // S.best slot of the eager rescorer
 constexpr int S8_QCAP = 128;                   // candidate queue entries per consumer warp
 constexpr int S8_GSTRIDE = 256;                // gmax words per query: S8_GREP replicas, 128 B apart
 constexpr int S8_GREP = 8;                     // replicas of the global bound (spreads the hot line)
@@ -160,7 +161,7 @@ struct S8Smem {
   float ovf[S8_CW][NB];                 // largest bound a full queue dropped
   unsigned bound[NB];                   // CTA lower bound (order-preserving float key)
   int done, pool_done;
-  Best2 best[S8_CW + 1][NB];            // float64 best per pool warp
+  Best2 best[S8_CW + 2][NB];            // float64 best per pool warp, then the eager rescorer's
   unsigned long long t[8];              // measurement stamps (MC_GEMV_TIMING=1)
   unsigned long long c[4];              // pool cycle counts (MC_GEMV_TIMING=1)
 };
@@ -325,14 +326,14 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, CtaRec
   const int lane = threadIdx.x & 31;
   const int nb = x.nb;
   if (lane == 0)
-    while (ld_acq_cta(&S.pool_done) != S8_CW + 1) {  // the nine pool warps
+    while (ld_acq_cta(&S.pool_done) != S8_CW + 2) {  // the nine pool warps and the eager rescorer
     }
   __syncwarp();
   for (int b = 0; b < nb; ++b) {
     Best2 m;
     m.init();
     float ov = -INFINITY;
-    for (int w = 0; w <= S8_CW; ++w) m.merge(S.best[w][b]);
+    for (int w = 0; w <= S8_EAGER; ++w) m.merge(S.best[w][b]);
     for (int w = 0; w < x.ncw; ++w) ov = fmaxf(ov, S.ovf[w][b]);
     if (lane == 0) {
       CtaRec r;
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     for (int k = 0; k < 4; ++k) S.c[k] = k == 2 ? ~0ull : 0ull;
   }
   if (threadIdx.x < S8_CW) S.qtail[threadIdx.x] = 0;
-  for (int i = threadIdx.x; i < (S8_CW + 1) * NB; i += blockDim.x) (&S.best[0][0])[i].init();
+  for (int i = threadIdx.x; i < (S8_CW + 2) * NB; i += blockDim.x) (&S.best[0][0])[i].init();
   for (int i = threadIdx.x; i < S8_CW * S8_QCAP; i += blockDim.x) (&S.qc[0][0])[i] = 0;
   for (int i = threadIdx.x; i < NBQ * Dp; i += blockDim.x) sq64[i] = i < nb * Dp ? q64[i] : 0.0;
   for (int i = threadIdx.x; i < NBQ * P8 / 16; i += blockDim.x) {  // q̂ (stride Dp) -> [NBQ][P8], zero-padded
@@ -547,6 +548,46 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
   const S8Ctx x{rb, st, sm, sq64, Dp, nb, ncw, timing};
   unsigned* const gq = a.gmax + (size_t)b0 * S8_GSTRIDE;  // this launch's queries
 
+  if (warp == S8_CW + 3) {
+    // ------------------------------------------------------------ eager rescorer
+    // While the CTA streams, rescore (best-first, one at a time) the live
+    // candidate with the largest upper bound: its exact score raises the bound
+    // early and the pool after the scan mostly finds the CTA's best done.  It
+    // checks `done` before each claim and never waits on global memory, so it
+    // hands over within one exact dot once the scan is over.
+    while (*(volatile int*)&S.done != S8_CW) {
+      const int bi = s8_pass(ncw, false);
+      if (bi < 0 || *(volatile int*)&S.done == S8_CW) {
+        __nanosleep(200);
+        continue;
+      }
+      const int w = bi / S8_QCAP, i = bi % S8_QCAP;
+      int won = 0;
+      if (lane == 0) won = atomicCAS(&S.qc[w][i], 0, 1) == 0;
+      if (__shfl_sync(FULL, won, 0)) {
+        const long long pb = S.qp[w][i];
+        const int b = (int)(pb & 3);
+        const long long p = pb >> 2;
+        const long long slot = ring_slot(st, local_row(st, p, sm));
+        const double sc = s8_dot(rb.r64 + (size_t)slot * Dp, sq64 + (size_t)b * Dp, Dp, lane);
+        if (lane == 0) {
+          S.best[S8_EAGER][b].add(sc, p);
+          if (!isnan(sc)) atomicMax(&S.bound[b], s8_key(__double2float_rd(sc)));
+          if (timing) atomicAdd(&S.t[S8T_RESC], 1ull);
+        }
+        __syncwarp();
+        if (lane == 0) S.qu[w][i] = -INFINITY;
+      }
+      __syncwarp();
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      atomicAdd(&S.pool_done, 1);
+    }
+    return;
+  }
+
   if (warp == S8_CW + 2) {
     // ------------------------------------------------------------ bound poller
     // Until the pool is done: carry the CTA's bound to the other CTAs (lane
@@ -558,7 +599,7 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     unsigned pub[NBQ];
 #pragma unroll
     for (int b = 0; b < NBQ; ++b) pub[b] = 0u;
-    while (*(volatile int*)&S.pool_done != S8_CW + 1) {
+    while (*(volatile int*)&S.pool_done < S8_CW + 2) {
       unsigned gk = 0;
       if (lane >= S8_PUB0 && lane - S8_PUB0 < nb)
         gk = ld_relaxed_gpu(gq + (lane - S8_PUB0) * S8_GSTRIDE + 32 * (blockIdx.x % S8_GREP));

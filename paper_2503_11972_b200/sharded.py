@@ -3,7 +3,7 @@
 Layout.  Global append position p (0, 1, 2, ... over the
 cache's lifetime) decides the owner: shard g of G stores p ≡ g (mod G), as
 local row j = p // G of its device ring (``mc_configure_shard``).  Every rank
-keeps the full metadata deque (the reference's ``_store``, cache.py:164), so
+keeps the full metadata FIFO (the reference's ``_store``, cache.py:164), so
 validation, eviction decisions and the returned ``CacheEntry`` objects are
 identical on all ranks; only the embeddings are divided.
 
@@ -23,11 +23,10 @@ to displace anything on its own.
 from __future__ import annotations
 
 import math
-from collections import deque
 
 import numpy as np
 
-from .cache import _HIT, _EMPTY, _MISS_EMPTY, _unit_norm, _default_device
+from .cache import _HIT, _EMPTY, _MISS_EMPTY, EntryFifo, _unit_norm, _default_device
 from .records import (
     DEFAULT_DIM,
     LARGE,
@@ -80,7 +79,7 @@ class ShardedSemanticCache:
         self.policy = policy
         self.max_age_s = max_age_s
         self.device = _default_device() if device is None else int(device)
-        self._store: deque[CacheEntry] = deque()
+        self._store = EntryFifo()
         self._next_seq = 0
         self._appended = 0  # global append position of the next entry
         if ring_factory is None:

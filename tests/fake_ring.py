@@ -40,6 +40,15 @@ class FakeRing:
         live, sim, k, flags = self.retrieve(np.asarray(q, dtype=np.float64)[None, :])
         return int(live[0]), float(sim[0]), int(k[0]), int(flags[0])
 
+    def submit1(self, q):
+        self._pending = self.retrieve1(q)  # answered against the rows as they are now
+        return 7
+
+    def wait1(self, ticket):
+        assert ticket == 7
+        r, self._pending = self._pending, None
+        return r
+
     def evict_front(self, n):
         assert 0 <= n <= len(self.rows)
         del self.rows[:n]

@@ -101,3 +101,27 @@ def test_chunked_import_equals_per_line_replay(tmp_path):
     with pytest.raises(ValueError, match=r"snap.jsonl:9001: bad snapshot record"):
         c.import_jsonl(path)
     assert _state(c) == _state(a)  # every record before the bad line was stored
+
+
+def test_async_lookup_resolves_against_its_submit_state():
+    """retrieve_async + insert (capacity evictions) + result() == retrieve() before the insert."""
+    rng = np.random.default_rng(17)
+    d, cap = 8, 40
+    a, b = SemanticCache(cap, d), SemanticCache(cap, d)
+    from paper_2503_11972_b200 import ThresholdTable
+
+    table = ThresholdTable.default()
+    ents = _entries(rng, 2000, d)
+    for e in ents[:cap]:
+        a.insert(e)
+        b.insert(e)
+    for i, e in enumerate(ents[cap:]):
+        q = normalize(ents[cap + i - 3].embedding + 0.3 * rng.standard_normal(d))
+        want = a.retrieve(q, table)
+        a.insert(e)
+        pend = b.retrieve_async(q, table)
+        b.insert(e)  # evicts the oldest entry while the lookup is pending
+        got = pend.result()
+        assert got == want, i
+        assert (got.entry is want.entry) or got.entry is None
+    assert _state(a) == _state(b)

@@ -419,3 +419,28 @@ def test_stream8_windows_smaller_than_the_grid(dim):
             assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (dim, i)
             assert r.k == k and _close(r.similarity, sim), (dim, i, r, sim)
     c.close()
+
+
+def test_async_lookup_overlapping_inserts_matches_oracle():
+    """retrieve_async (zero-copy streamed scan) with the request's insert staged while the scan runs:
+    every answer equals the float64 oracle's for the state at submit time, through capacity evictions."""
+    wl = ClusteredWorkload(768, n_clusters=24, seed=77)
+    cap = 3000
+    c = SemanticCache(capacity=cap, dim=768)
+    o = OracleCache(cap, 768)
+    table, ot = ThresholdTable.default(), OracleTable()
+    rows = wl.cache_rows(cap)
+    c.bulk_load(CacheEntry(f"e{i}", v, "large", i, float(i)) for i, v in enumerate(rows))
+    for i, v in enumerate(rows):
+        o.insert(OracleEntry(f"e{i}", v, "large", i, float(i)))
+    Q = wl.queries(400)
+    imgs = wl.images(Q)
+    for i, (q, img) in enumerate(zip(Q, imgs)):
+        e, sim, k = o.retrieve_entry(q, ot)
+        pend = c.retrieve_async(q, table)
+        c.add(f"n{i}", img, "large", float(cap + i))  # evicts the oldest while the lookup is in flight
+        o.insert(OracleEntry(f"n{i}", img, "large", cap + i, float(cap + i)))
+        r = pend.result()
+        assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), i
+        assert r.k == k and _close(r.similarity, sim), (i, r, sim)
+    c.close()
