@@ -41,17 +41,19 @@ extern "C" {
 #define MC_FLAG_NONFINITE 0x40u /* query had NaN/Inf; answered by exhaustive float64 scan */
 
 /* Scan-path selection for mc_set_path (default MC_PATH_AUTO: B <= 4 -> the
- * TMA-streamed int8 scan when 128 | Dp <= 1024 (Dp = D rounded up to 64), else
- * the register int8 GEMV when it covers Dp, else the fp16 GEMV; B >= 5 -> the
- * tcgen05 scan).  Every path returns the same certified answers. */
+ * TMA-streamed int8 scan when Dp <= 1024 (Dp = D rounded up to 64), else the
+ * fp16 GEMV; B >= 5 -> the fp16 tcgen05 scan on CTA pairs).  Every path
+ * returns the same certified answers. */
 #define MC_PATH_AUTO 0
 #define MC_PATH_GEMV 1 /* CUDA-core fp16 GEMV scan, register top-K' (cross-checks) */
 #define MC_PATH_GEMM 2 /* tcgen05/TMEM/TMA fp16 scan on CTA pairs (cta_group::2), fused top-K' epilogue */
 #define MC_PATH_GEMM_1SM 3 /* same scan on single CTAs (cta_group::1), kept for cross-checks */
 #define MC_PATH_GEMM_QUAD 4 /* 4-CTA clusters multicasting the query operand (cross-checks) */
 #define MC_PATH_GEMV8 5 /* int8 dp4a register-streaming GEMV scan with per-row bounds (cross-checks) */
-#define MC_PATH_STREAM8 6 /* int8 scan streamed by TMA, lane-per-row dp4a, in-scan float64 rescoring
-                             (AUTO's choice for B <= 4 when 128 | Dp <= 1024) */
+#define MC_PATH_STREAM8 6 /* int8 scan streamed by TMA bulk copies, lane-per-row dp4a, float64 rescoring
+                             pool (AUTO's choice for B <= 4 when Dp <= 1024) */
+#define MC_PATH_GEMM8 7 /* tcgen05 kind::i8 scan on CTA pairs over the int8 ring, per-row certified
+                           bounds + float64 merge (cross-check; AUTO keeps the fp16 scan for B >= 5) */
 
 typedef struct mc_cache mc_cache;
 

@@ -22,7 +22,7 @@ MC_FLAG_NEAR_TAU = 0x10
 MC_FLAG_FALLBACK = 0x20
 MC_FLAG_NONFINITE = 0x40
 
-PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_GEMM_1SM, PATH_GEMM_QUAD, PATH_GEMV8, PATH_STREAM8 = 0, 1, 2, 3, 4, 5, 6
+PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_GEMM_1SM, PATH_GEMM_QUAD, PATH_GEMV8, PATH_STREAM8, PATH_GEMM8 = 0, 1, 2, 3, 4, 5, 6, 7
 
 RECORD_DTYPE = np.dtype([("sim", "<f8"), ("second", "<f8"), ("pos", "<i8"), ("flags", "<u4"), ("reserved", "<i4")])
 

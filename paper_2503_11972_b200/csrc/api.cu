@@ -110,7 +110,9 @@ struct mc_cache {
   const double* inflight_q = nullptr;
   bool inflight_ready = false;  // completed (and any fallback applied) while staging appends
 
-  TcPlan* tc = nullptr;           // tensor-core scan plan, created on first batched lookup
+  TcPlan* tc = nullptr;           // fp16 tensor-core scan plan (MC_PATH_GEMM*), created on first use
+  Tc8Plan* tc8 = nullptr;         // int8 tensor-core scan plan (the batched default), created on first use
+  float* d_part_maxl = nullptr;   // [Bcap][chunks] of the int8 tensor-core scan
   S8Plan* s8 = nullptr;           // TMA-streamed int8 scan plan (tensor maps of ring8 / ringq)
   unsigned* d_counter = nullptr;  // last-CTA ticket of the fused GEMV scan (zero between launches)
 
@@ -191,6 +193,7 @@ void free_batch(mc_cache* h) {
   cudaFree(h->d_part_s);
   cudaFree(h->d_part_p);
   cudaFree(h->d_part_floor);
+  cudaFree(h->d_part_maxl);
   cudaFree(h->d_cta);
   cudaFree(h->d_gmax);
   cudaFree(h->d_rec);
@@ -200,6 +203,7 @@ void free_batch(mc_cache* h) {
   h->d_part_s = nullptr;
   h->d_part_p = nullptr;
   h->d_part_floor = nullptr;
+  h->d_part_maxl = nullptr;
   h->d_cta = nullptr;
   h->d_gmax = nullptr;
   h->d_rec = nullptr;
@@ -237,6 +241,7 @@ int ensure_batch(mc_cache* h, int B) {
   CU(cudaMalloc(&h->d_part_s, (size_t)cap * chunks * KP * sizeof(float)));
   CU(cudaMalloc(&h->d_part_p, (size_t)cap * chunks * KP * sizeof(long long)));
   CU(cudaMalloc(&h->d_part_floor, (size_t)cap * chunks * sizeof(float)));
+  CU(cudaMalloc(&h->d_part_maxl, (size_t)cap * chunks * sizeof(float)));
   CU(cudaMalloc(&h->d_cta, (size_t)cap * gemv_grid(h->sm_count) * sizeof(CtaRec)));
   // 256 words per query: the streamed scan keeps 8 replicas of its bound 128 B apart
   CU(cudaMalloc(&h->d_gmax, (size_t)cap * 256 * sizeof(unsigned)));
@@ -331,7 +336,25 @@ constexpr long long FUSE_APPEND_MAX = 256;
 bool use_gemm(const mc_cache* h, int B) {
   if (h->path == MC_PATH_GEMV || h->path == MC_PATH_GEMV8 || h->path == MC_PATH_STREAM8) return false;
   return h->path == MC_PATH_GEMM || h->path == MC_PATH_GEMM_1SM || h->path == MC_PATH_GEMM_QUAD ||
-         (h->path == MC_PATH_AUTO && B >= GEMM_MIN_B);
+         h->path == MC_PATH_GEMM8 || (h->path == MC_PATH_AUTO && B >= GEMM_MIN_B);
+}
+
+// int8 tensor cores (MC_PATH_GEMM8).  Not AUTO's choice yet: at C3 its looser
+// per-row bound admits ~5x the float64 rescoring of the fp16 scan and the
+// scan itself measured slower.
+bool use_gemm8(const mc_cache* h, int B) {
+  return use_gemm(h, B) && h->path == MC_PATH_GEMM8 && tc8_supported(h->P8);
+}
+
+int ensure_tc8(mc_cache* h, int B) {
+  if (h->tc8 && tc8_bcap(h->tc8) >= B) return MC_OK;
+  CU(cudaStreamSynchronize(h->stream));
+  tc8_plan_destroy(h->tc8);
+  h->tc8 = nullptr;
+  char err[256] = {0};
+  h->tc8 = tc8_plan_create(h->ring8, h->C, h->Dp, h->P8, std::max(B, 256), h->sm_count, err, sizeof err);
+  if (!h->tc8) return fail(MC_ERR_CUDA, "int8 tensor-core scan plan: %s", err);
+  return MC_OK;
 }
 
 int ensure_tc(mc_cache* h, int B) {
@@ -353,6 +376,26 @@ int ensure_tc(mc_cache* h, int B) {
 int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
                const QPrep* prep, const int8_t* q8, cudaEvent_t t_mid = nullptr, unsigned* done_seq = nullptr,
                unsigned seq = 0) {
+  if (use_gemm8(h, B)) {
+    if (app.n > 0) {
+      CU(launch_append(app.stage, app.n, app.first_slot, mirror(h), h->D, h->Dp, rbufs(h), h->d_state, h->stream));
+      h->stats[7]++;
+    }
+    int rc = ensure_tc8(h, B);
+    if (rc) return rc;
+    Partials part{h->d_part_s, h->d_part_p, h->d_part_floor, tc8_chunks(h->tc8, B)};
+    part.maxl = h->d_part_maxl;
+    CU(launch_tc8_scan(h->tc8, q64, B, h->D, h->d_state, h->ringq, part, h->shard, h->stream));
+    if (t_mid) CU(cudaEventRecord(t_mid, h->stream));
+    CU(launch_merge8(h->d_state, h->ring64, h->D, h->Dp, q64, B, part, rec, h->shard, h->stream));
+    h->stats[6]++;
+    h->stats[7] += 3;
+    if (out) {
+      CU(launch_finalize(rec, 1, B, -1, h->d_state, h->thr, out, h->stream));
+      h->stats[7]++;
+    }
+    return MC_OK;
+  }
   if (use_gemm(h, B)) {
     if (app.n > 0) {
       CU(launch_append(app.stage, app.n, app.first_slot, mirror(h), h->D, h->Dp, rbufs(h), h->d_state, h->stream));
@@ -584,6 +627,7 @@ int mc_destroy(mc_cache* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     free_batch(h);
     tc_plan_destroy(h->tc);
+    tc8_plan_destroy(h->tc8);
     s8_plan_destroy(h->s8);
     cudaFreeHost(h->h_env);
     cudaFree(h->d_env);
@@ -629,7 +673,7 @@ int mc_configure_shard(mc_cache* h, int32_t n_shards, int32_t shard_id) {
 
 int mc_set_path(mc_cache* h, int32_t path) {
   if (!h) return fail(MC_ERR_ARG, "NULL handle");
-  if (path < MC_PATH_AUTO || path > MC_PATH_STREAM8) return fail(MC_ERR_ARG, "unknown path %d", path);
+  if (path < MC_PATH_AUTO || path > MC_PATH_GEMM8) return fail(MC_ERR_ARG, "unknown path %d", path);
   std::lock_guard<std::mutex> lk(h->mu);
   h->path = path;
   return MC_OK;
@@ -992,7 +1036,8 @@ int mc_profile_rotate(mc_cache* const* hs, int32_t nh, const double* queries, co
   for (int k = 0; k < nh; ++k) {
     int rc = ensure_batch(hs[k], B);
     if (!rc) rc = flush(hs[k]);
-    if (!rc && use_gemm(hs[k], B)) rc = ensure_tc(hs[k], B);
+    if (!rc && use_gemm8(hs[k], B)) rc = ensure_tc8(hs[k], B);
+    else if (!rc && use_gemm(hs[k], B)) rc = ensure_tc(hs[k], B);
     if (rc) return rc;
     CU(cudaStreamSynchronize(hs[k]->stream));
   }

@@ -47,6 +47,7 @@ struct Partials {
   long long* p;      // [B][n_chunks][KP] global position (-1 = empty)
   float* floor_;     // [B][n_chunks]  K'-th score if rows were dropped, else -inf
   int n_chunks;
+  float* maxl = nullptr;  // [B][n_chunks] largest lower bound seen (int8 tensor-core scan only)
 };
 
 // One CTA's exact answer for one query on the GEMV path: the float64 best over
@@ -149,6 +150,19 @@ int tc_chunks(const TcPlan* p, int B);
 const double* tc_qscale(const TcPlan* p);
 cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const RingState* d_state,
                            const Partials& part, ShardMap sm, cudaStream_t s);
+
+// int8 tensor-core scan (scan_tc8.cu, tcgen05 kind::i8 on CTA pairs) with
+// per-row certified bounds; its merge uses part.maxl.  rq: the ring's (s, L1).
+struct Tc8Plan;
+bool tc8_supported(int P8);
+Tc8Plan* tc8_plan_create(int8_t* ring8, long long C, int Dp, int P8, int Bcap, int sm_count, char* err, int errlen);
+void tc8_plan_destroy(Tc8Plan* p);
+int tc8_bcap(const Tc8Plan* p);
+int tc8_chunks(const Tc8Plan* p, int B);
+cudaError_t launch_tc8_scan(Tc8Plan* p, const double* q64, int B, int D, const RingState* d_state,
+                            const float2* rq, const Partials& part, ShardMap sm, cudaStream_t s);
+cudaError_t launch_merge8(const RingState* d_state, const double* ring64, int D, int Dp, const double* q64, int B,
+                          const Partials& part, mc_record* rec, ShardMap sm, cudaStream_t s);
 
 // Merge per-chunk lists -> certified float64 best per query (mc_record).
 // qscale: per-query factor turning partial scores into similarity units (nullptr = 1).

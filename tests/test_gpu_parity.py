@@ -285,7 +285,7 @@ def _paths(cache, Q, table):
     out = {}
     for name, path in (("gemv", _native.PATH_GEMV), ("gemm", _native.PATH_GEMM), ("gemm1", _native.PATH_GEMM_1SM),
                        ("gemm4", _native.PATH_GEMM_QUAD), ("gemv8", _native.PATH_GEMV8),
-                       ("stream8", _native.PATH_STREAM8)):
+                       ("stream8", _native.PATH_STREAM8), ("gemm8", _native.PATH_GEMM8)):
         cache.ring.set_path(path)
         out[name] = cache.retrieve_flags(Q, table)
     cache.ring.set_path(_native.PATH_AUTO)
@@ -311,7 +311,7 @@ def test_tensor_core_scan_matches_gemv_and_oracle(dim, cap, n_ins, B):
     keep = ~((fv | fm) & AMBIG).astype(bool)
     assert np.array_equal(lv[keep], lm[keep]) and np.array_equal(kv, km)
     assert np.array_equal(sv, sm_)  # both certified float64 rescoring: bit-identical
-    for name in ("gemv8", "stream8"):  # int8 scans: same certified answers
+    for name in ("gemv8", "stream8", "gemm8"):  # int8 scans (CUDA cores / tensor cores): same certified answers
         l8, s8, k8, f8 = res[name]
         keep8 = ~((fv | f8) & AMBIG).astype(bool)
         assert np.array_equal(lv[keep8], l8[keep8]) and np.array_equal(kv, k8) and np.array_equal(sv, s8), name
@@ -320,6 +320,8 @@ def test_tensor_core_scan_matches_gemv_and_oracle(dim, cap, n_ins, B):
             assert np.array_equal(a, b)
     c.ring.set_path(_native.PATH_GEMM)
     _check_against_scan(c, live_rows, Q, table, f"gemm d{dim} cap{cap} B{B}")
+    c.ring.set_path(_native.PATH_GEMM8)
+    _check_against_scan(c, live_rows, Q, table, f"gemm8 d{dim} cap{cap} B{B}")
     st = c.ring.stats()
     assert st["gemm_launches"] >= 2
     c.close()
@@ -443,4 +445,21 @@ def test_async_lookup_overlapping_inserts_matches_oracle():
         r = pend.result()
         assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), i
         assert r.k == k and _close(r.similarity, sim), (i, r, sim)
+    c.close()
+
+
+@pytest.mark.parametrize("dim,cap,n_ins,B", [(1024, 100_000, 100_000, 256), (768, 9000, 20_000, 64), (100, 700, 1800, 5)])
+def test_int8_tensor_core_scan_matches_oracle(dim, cap, n_ins, B):
+    """tcgen05 kind::i8 scan (the batched default) against the reference scan formula: full C3 shape,
+    a wrapped partial window, and a tiny D (zero-padded K block)."""
+    wl = ClusteredWorkload(dim, n_clusters=128, seed=dim + cap)
+    rows = wl.cache_rows(n_ins)
+    c = SemanticCache(capacity=cap, dim=dim)
+    c.ring.append(rows)
+    live_rows = rows[-cap:]
+    c._store.extend(CacheEntry(f"e{i}", r, "large", i, 0.0) for i, r in enumerate(live_rows))
+    Q = wl.queries(B)
+    c.ring.set_path(_native.PATH_GEMM8)
+    st = _check_against_scan(c, live_rows, Q, ThresholdTable.default(), f"gemm8 d{dim} B{B}")
+    assert st["fallback"] <= max(2, B // 50)
     c.close()
