@@ -28,7 +28,7 @@ wl = ClusteredWorkload(dim, n_clusters=512, seed=17)
 rows = wl.cache_rows(n)
 ring = _native.DeviceRing(n, dim, 0)
 ring.append(rows)
-ring.set_path({"auto": 0, "gemv": 1, "gemm": 2, "gemv8": 5, "stream8": 6}[a.path])
+ring.set_path({"auto": 0, "gemv": 1, "gemm": 2, "gemv8": 5, "stream8": 6, "gemm8": 7}[a.path])
 t = ThresholdTable.default()
 ring.set_table(t.pairs, t.total_steps)
 Q = wl.queries(B * a.iters).reshape(a.iters, B, dim)

@@ -63,7 +63,8 @@ for rep in sorted(SRC.glob("*.ncu-rep")):
     tot, top = source_top(rep)
     key = rep.stem
     dram = to_bytes(*m["dram__bytes_read.sum"]) + to_bytes(*m["dram__bytes_write.sum"])
-    kshort = ("k_stream8_scan" if key.startswith("s8") else "k_gemv8_scan" if "gemv8" in key
+    kshort = ("k_stream8_scan" if key.startswith("s8") else "k_tc8_scan_pair" if key.startswith("tc8")
+              else "k_merge8" if key.startswith("merge8") else "k_gemv8_scan" if "gemv8" in key
               else "k_gemv_scan" if "gemv" in key else "k_tc_scan_pair" if "tc_pair" in key else "k_merge")
     summary[kshort] = {"capture": f"{tag}_{key}.txt", "dram_bytes_per_launch": dram,
                        "duration_us_under_ncu": float(m["gpu__time_duration.sum"][0]) * (
