@@ -32,6 +32,7 @@
 // Algorithmic work per launch: 2 * Bp * n_live * P8 int8 ops; HBM bytes
 // n_live * (P8 + 8) + Bp * P8.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "merge.cuh"
@@ -160,7 +161,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T8_THREADS, 1)
                     const RingState* __restrict__ d_state, const float2* __restrict__ rq,
                     const float* __restrict__ qs, const float* __restrict__ qn1, int n_mp, int B, int n_kb,
                     float* __restrict__ part_s, long long* __restrict__ part_p, float* __restrict__ part_floor,
-                    float* __restrict__ part_maxl, int n_chunks, ShardMap sm) {
+                    float* __restrict__ part_maxl, int n_chunks, ShardMap sm, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -252,7 +253,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T8_THREADS, 1)
             const uint32_t b0 = smem_u32(smB + stage * T8_B_BYTES);
 #pragma unroll
             for (int k = 0; k < T8_BK / T8_UK; ++k)
-              umma_i8_pair(d_tmem, umma_desc_sw128(a0 + k * T8_UK), umma_desc_sw128(b0 + k * T8_UK), idesc,
+              if (!(dbg & 2)) umma_i8_pair(d_tmem, umma_desc_sw128(a0 + k * T8_UK), umma_desc_sw128(b0 + k * T8_UK), idesc,
                            (kb | k) != 0);
             umma_commit_pair(&empty[stage]);
           }
@@ -301,6 +302,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T8_THREADS, 1)
       const bool all_live = (slot0 + T8_BN <= st.cap) && (l0 + T8_BN <= st.count);
 #pragma unroll 1
       for (int c = 0; c < T8_BN / 32; ++c) {
+        if (dbg & 4) break;  // bisection: no epilogue work
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * T8_BN + c * 32), v);
         float uu[32], ll[32];
@@ -471,6 +473,7 @@ __global__ void __launch_bounds__(MERGE_THREADS)
 
 // ---------------------------------------------------------------- host side
 struct Tc8Plan {
+  int dbg = 0;  // MC_TC8_DEBUG bisection switches: 2 no MMA, 4 no epilogue (timing only)
   int8_t* q8 = nullptr;  // [Bcap][P8] quantised queries (the A operand)
   float* qs = nullptr;   // [Bcap] s_q
   float* q1 = nullptr;   // [Bcap] s_q ||q̂||_1
@@ -517,6 +520,7 @@ Tc8Plan* tc8_plan_create(int8_t* ring8, long long C, int Dp, int P8, int Bcap, i
   p->P8 = P8;
   p->Dp = Dp;
   p->sm_count = sm_count;
+  if (const char* e = getenv("MC_TC8_DEBUG")) p->dbg = atoi(e);
   if (cudaMalloc(&p->q8, (size_t)p->Bcap * P8) != cudaSuccess ||
       cudaMalloc(&p->qs, (size_t)p->Bcap * sizeof(float)) != cudaSuccess ||
       cudaMalloc(&p->q1, (size_t)p->Bcap * sizeof(float)) != cudaSuccess) {
@@ -553,7 +557,7 @@ cudaError_t launch_tc8_scan(Tc8Plan* p, const double* q64, int B, int D, const R
   if (e != cudaSuccess) return e;
   k_tc8_scan_pair<<<2 * nm * groups, T8_THREADS, T8_SMEM, s>>>(p->q_map, p->ring_map, d_state, rq, p->qs, p->q1, nm,
                                                                  B, p->P8 / T8_BK, part.s, part.p, part.floor_,
-                                                                 part.maxl, groups, sm);
+                                                                 part.maxl, groups, sm, p->dbg);
   return cudaGetLastError();
 }
 
