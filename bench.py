@@ -422,7 +422,7 @@ def main():
         "metric": METRIC,
         "value": c2["value"], "unit": "lookups/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": c2["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f16 scan / f32 accumulate / f64 rescoring",
+        "dtype": "int8 scan (exact int32 dot, certified per-row bounds) / f64 rescoring",
         "data": DATA,
         "config": dict(C2_CONFIG, l2="inputs larger than L2: steps rotate over 4 caches of this shape (4 x 77.6 MB "
                                      "int8 scan copies), timed back to back",

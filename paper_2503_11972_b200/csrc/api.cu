@@ -18,6 +18,9 @@
 
 #include <algorithm>
 #include <chrono>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -101,6 +104,9 @@ struct mc_cache {
   OutRec* d_out = nullptr;
   OutRec* h_out = nullptr;  // pinned, mapped (the streamed scan writes decisions here directly)
   OutRec* d_outm = nullptr; // device view of h_out
+  uint4* h_outp = nullptr;    // pinned, mapped: packed decisions (16 B each, self-validating sequence tag)
+  uint4* d_outp = nullptr;
+  bool packed = true;         // packed zero-copy results (else: decisions + fence + completion word)
   unsigned* h_seq = nullptr;  // pinned, mapped: completion word of the zero-copy lookup
   unsigned* d_seq = nullptr;
   unsigned seq = 0;
@@ -200,6 +206,7 @@ void free_batch(mc_cache* h) {
   cudaFree(h->d_scratch);
   cudaFree(h->d_out);
   cudaFreeHost(h->h_out);
+  cudaFreeHost(h->h_outp);
   h->d_part_s = nullptr;
   h->d_part_p = nullptr;
   h->d_part_floor = nullptr;
@@ -211,6 +218,8 @@ void free_batch(mc_cache* h) {
   h->d_out = nullptr;
   h->h_out = nullptr;
   h->d_outm = nullptr;
+  h->h_outp = nullptr;
+  h->d_outp = nullptr;
 }
 
 // Grow the query capacity to >= B (power of two): per-batch buffers and the
@@ -251,6 +260,9 @@ int ensure_batch(mc_cache* h, int B) {
   CU(cudaMalloc(&h->d_out, (size_t)cap * sizeof(OutRec)));
   CU(cudaHostAlloc(&h->h_out, (size_t)cap * sizeof(OutRec), cudaHostAllocMapped));
   CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_outm), h->h_out, 0));
+  CU(cudaHostAlloc(&h->h_outp, (size_t)cap * sizeof(uint4), cudaHostAllocMapped));
+  memset(h->h_outp, 0, (size_t)cap * sizeof(uint4));
+  CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_outp), h->h_outp, 0));
   h->Bcap = cap;
   return MC_OK;
 }
@@ -375,7 +387,7 @@ int ensure_tc(mc_cache* h, int B) {
 // t_mid (optional) is recorded between the scan and the standalone merge.
 int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
                const QPrep* prep, const int8_t* q8, cudaEvent_t t_mid = nullptr, unsigned* done_seq = nullptr,
-               unsigned seq = 0) {
+               unsigned seq = 0, uint4* outp = nullptr) {
   if (use_gemm8(h, B)) {
     if (app.n > 0) {
       CU(launch_append(app.stage, app.n, app.first_slot, mirror(h), h->D, h->Dp, rbufs(h), h->d_state, h->stream));
@@ -428,7 +440,7 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
     if (s8)
       CU(launch_stream8_scan(h->s8, rbufs(h), st, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0, h->sm_count, h->shard,
                              h->d_counter, h->d_gmax, h->thr, rec, out, a, prep + b0, q8 + (size_t)b0 * h->Dp,
-                             b0 + nb == B ? done_seq : nullptr, seq, h->stream));
+                             b0 + nb == B ? done_seq : nullptr, seq, outp, h->stream));
     else if (int8)
       CU(launch_gemv8_scan(rbufs(h), st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
                            nb == 1 ? gemv_grid(h->sm_count) : h->sm_count, h->shard, h->d_counter, h->d_gmax, h->thr, rec, out, a, prep + b0,
@@ -449,7 +461,7 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
 // decisions) are enqueued, not complete.  Returns the device query pointer.
 // The caller has run ensure_batch(h, B) (rec / out may be handle buffers).
 int lookup_enqueue(mc_cache* h, const double* queries, int B, mc_record* rec, OutRec* out, bool async_reuse,
-                   const double** q_dev, unsigned* done_seq = nullptr, unsigned seq = 0) {
+                   const double** q_dev, unsigned* done_seq = nullptr, unsigned seq = 0, uint4* outp = nullptr) {
   int rc;
   if (h->n_pending > FUSE_APPEND_MAX) {
     rc = flush(h);
@@ -463,19 +475,34 @@ int lookup_enqueue(mc_cache* h, const double* queries, int B, mc_record* rec, Ou
   if (rc) return rc;
   const GemvAppendArgs app = take_pending(h, h->d_env);
   *q_dev = q;
-  return scan_merge(h, q, B, rec, out, app, prep, q8, nullptr, done_seq, seq);
+  return scan_merge(h, q, B, rec, out, app, prep, q8, nullptr, done_seq, seq, outp);
 }
 
 int wait_seq(mc_cache* h, unsigned seq);
+int wait_packed(mc_cache* h, unsigned seq, int B);
+unsigned seq_tag(unsigned seq);
+bool direct_result(const mc_cache* h, int B);
+
+// Enqueue a zero-copy lookup: packed self-validating decisions (default), or
+// the decisions + a system fence + the completion word.
+int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool async_reuse, const double** q) {
+  if (h->packed) {
+    memset(h->h_outp, 0, (size_t)B * sizeof(uint4));  // no stale record can carry this lookup's tag
+    return lookup_enqueue(h, queries, B, h->d_rec, nullptr, async_reuse, q, nullptr, seq_tag(seq), h->d_outp);
+  }
+  return lookup_enqueue(h, queries, B, h->d_rec, h->d_outm, async_reuse, q, h->d_seq, seq);
+}
+
+int wait_direct(mc_cache* h, unsigned seq, int B) { return h->packed ? wait_packed(h, seq, B) : wait_seq(h, seq); }
 
 // Complete the asynchronous lookup in flight, if any: wait for its decisions
 // and run the exhaustive fallback for the queries whose certificate needs it
 // (while the ring still holds the state that lookup scanned).
 int finish_inflight(mc_cache* h) {
   if (!h->inflight_seq || h->inflight_ready) return MC_OK;
-  int rc = wait_seq(h, h->inflight_seq);
-  if (rc) return rc;
   const int B = h->inflight_B;
+  int rc = h->inflight_q && direct_result(h, B) ? wait_direct(h, h->inflight_seq, B) : wait_seq(h, h->inflight_seq);
+  if (rc) return rc;
   bool need = false;
   for (int b = 0; b < B; ++b) need |= (h->h_out[b].flags & FLAG_NEED_ANY) != 0;
   if (need) {
@@ -494,6 +521,55 @@ int finish_inflight(mc_cache* h) {
 // its decisions straight to host-mapped memory.
 bool direct_result(const mc_cache* h, int B) {
   return h->s8 && !use_gemm(h, B) && h->path != MC_PATH_GEMV && h->path != MC_PATH_GEMV8;
+}
+
+// Packed zero-copy results: tag of lookup `seq` (never 0, so zeroed slots never match).
+unsigned seq_tag(unsigned seq) { return seq % 65535u + 1u; }
+
+// Spin until the B packed decisions of lookup `seq` carry its tag, then unpack
+// them into h_out.  Each record is one 16-byte store on the device side and one
+// 16-byte load here, so a record is seen whole or not at all.
+int wait_packed(mc_cache* h, unsigned seq, int B) {
+  const unsigned tag = seq_tag(seq);
+  for (int b = 0; b < B; ++b) {
+    const uint4* p = h->h_outp + b;
+    uint4 v;
+    for (unsigned spins = 1;; ++spins) {
+#if defined(__x86_64__)
+      const __m128i x = _mm_load_si128(reinterpret_cast<const __m128i*>(p));
+      memcpy(&v, &x, sizeof v);
+#else
+      v = *(volatile const uint4*)p;
+#endif
+      if ((v.w >> 16) == tag) break;
+#if defined(__x86_64__) || defined(__i386__)
+      __builtin_ia32_pause();
+#endif
+      if ((spins & 1023u) == 0) {
+        const cudaError_t e = cudaStreamQuery(h->stream);
+        if (e != cudaSuccess && e != cudaErrorNotReady)
+          return fail(MC_ERR_CUDA, "lookup %u: %s", seq, cudaGetErrorString(e));
+        if (e == cudaSuccess) {  // the stream is idle: one last look, then report
+#if defined(__x86_64__)
+          const __m128i y = _mm_load_si128(reinterpret_cast<const __m128i*>(p));
+          memcpy(&v, &y, sizeof v);
+#else
+          v = *(volatile const uint4*)p;
+#endif
+          if ((v.w >> 16) == tag) break;
+          return fail(MC_ERR_STATE, "lookup %u finished without publishing query %d", seq, b);
+        }
+      }
+    }
+    OutRec& o = h->h_out[b];
+    const unsigned long long sb = (unsigned long long)v.x | ((unsigned long long)v.y << 32);
+    memcpy(&o.sim, &sb, sizeof sb);
+    o.live = (long long)(int)v.z;
+    o.k = (int)(v.w & 0xffu);
+    const unsigned f8 = (v.w >> 8) & 0xffu;
+    o.flags = (f8 & 0x7fu) | ((f8 & 0x80u) ? FLAG_NEED_FALLBACK : 0u);
+  }
+  return MC_OK;
 }
 
 // Spin until the streamed scan has published lookup `seq` into host-mapped
@@ -593,6 +669,8 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
     h->s8 = s8_plan_create(h->ring8, h->ringq, h->C, h->Dp, h->P8, err, sizeof err);
     if (!h->s8) return cleanup(fail(MC_ERR_CUDA, "int8 stream scan plan: %s", err));
   }
+  if (const char* e = getenv("MC_PACKED_RESULT")) h->packed = atoi(e) != 0;
+  if (h->C > 0x7fffffffll) h->packed = false;  // live index must fit the packed int32
   CUC(cudaHostAlloc(&h->h_seq, 64, cudaHostAllocMapped));
   *h->h_seq = 0u;
   CUC(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_seq), h->h_seq, 0));
@@ -652,6 +730,7 @@ int mc_set_thresholds(mc_cache* h, const int32_t* ks, const double* taus, int32_
     if (!(ks[i] > ks[i - 1]) || !(taus[i] > taus[i - 1]))
       return fail(MC_ERR_ARG, "k and tau must be strictly increasing");
   std::lock_guard<std::mutex> lk(h->mu);
+  if (ks[n - 1] > 255) h->packed = false;  // the packed decision carries k in 8 bits
   h->thr.n = n;
   h->thr.total_steps = total_steps;
   for (int i = 0; i < n; ++i) {
@@ -749,10 +828,10 @@ int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* ou
     const unsigned seq = ++h->seq;
     const double t0 = g_ht.on ? now_us() : 0.0;
     const double h2d0 = g_ht.acc[1];
-    rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_outm, false, &q, h->d_seq, seq);
+    rc = enqueue_direct(h, queries, B, seq, false, &q);
     if (rc) return rc;
     const double t2 = g_ht.on ? now_us() : 0.0;
-    rc = wait_seq(h, seq);
+    rc = wait_direct(h, seq, B);
     if (rc) return rc;
     if (g_ht.on) {  // enqueue time minus the H2D call = staging, quantisation and the launch
       const double t3 = now_us();
@@ -796,7 +875,7 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
     h->inflight_ready = true;
   } else if (direct_result(h, B)) {  // the kernel publishes into mapped memory; the caller returns now
     const double* q = nullptr;
-    rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_outm, /*async_reuse=*/true, &q, h->d_seq, seq);
+    rc = enqueue_direct(h, queries, B, seq, /*async_reuse=*/true, &q);
     if (rc) return rc;
     h->inflight_q = q;
     h->inflight_ready = false;

@@ -132,7 +132,7 @@ cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingS
                                 CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
                                 const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
                                 const QPrep* prep, const int8_t* q8, unsigned* done_seq, unsigned seq,
-                                cudaStream_t s);
+                                uint4* outp, cudaStream_t s);
 
 int gemv_grid(int sm_count);
 cudaError_t launch_l2_flush(void* buf, size_t bytes, cudaStream_t s);  // measurement: evict L2 by reading

@@ -116,7 +116,20 @@ struct S8Args {
   RingState* d_state;
   unsigned* done_seq;          // optional (host-mapped): set to `seq` after `out` is written (zero-copy result)
   unsigned seq;
+  uint4* outp;                 // optional (host-mapped): packed decisions, one 16-byte store each (see below)
 };
+
+// A decision packed into one 16-byte store (one PCIe write, read by the host
+// with one 16-byte load): sim | live (int32) | k (8) flags (8: MC_FLAG_* bits
+// 0-6, bit 7 = needs the exhaustive path) seq (16).  The sequence tag makes
+// each record self-validating, so no system-scope fence has to separate the
+// decisions from a completion word.
+__device__ __forceinline__ uint4 pack_out(const OutRec& o, unsigned seq16) {
+  const unsigned long long sb = (unsigned long long)__double_as_longlong(o.sim);
+  const unsigned f8 = (o.flags & 0x7fu) | ((o.flags & FLAG_NEED_ANY) ? 0x80u : 0u);
+  return make_uint4((unsigned)sb, (unsigned)(sb >> 32), (unsigned)o.live,
+                    ((unsigned)o.k & 0xffu) | (f8 << 8) | (seq16 << 16));
+}
 
 // Rows [r0, r1) (live-local) of one CTA, cut into stages of up to `rows`
 // rows that never cross the physical end of the ring.
@@ -464,7 +477,14 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, CtaRec
       r.flags = (nt >= 2 ? MC_FLAG_TIE : 0u) | (fail ? FLAG_NEED_FALLBACK : 0u) | (exo ? FLAG_NEED_EXHAUSTIVE : 0u);
       r.reserved = 0;
       a.rec[gb] = r;
-      if (a.out) a.out[gb] = decide(record_best(r), r.flags & FLAG_NEED_ANY, x.st.jhead, a.thr);
+      const OutRec o = decide(record_best(r), r.flags & FLAG_NEED_ANY, x.st.jhead, a.thr);
+      if (a.out) a.out[gb] = o;
+      if (a.outp) {
+        const uint4 v = pack_out(o, a.seq);
+        asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a.outp + gb), "r"(v.x), "r"(v.y), "r"(v.z),
+                     "r"(v.w)
+                     : "memory");
+      }
     }
     if (lane < S8_GREP) a.gmax[(size_t)gb * S8_GSTRIDE + 32 * lane] = 0u;
   }
@@ -866,9 +886,10 @@ cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingS
                                 CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
                                 const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
                                 const QPrep* prep, const int8_t* q8, unsigned* done_seq, unsigned seq,
-                                cudaStream_t s) {
+                                uint4* outp, cudaStream_t s) {
   if (!p || nb < 1 || nb > 4) return cudaErrorInvalidValue;
-  S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), prep, q8, app.stage, app.n, app.d_state, done_seq, seq};
+  S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), prep, q8, app.stage, app.n, app.d_state, done_seq, seq,
+           outp};
   switch (p->P8 / 128) {
     case 1: return s8_launch<1>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
     case 2: return s8_launch<2>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
