@@ -115,6 +115,10 @@ struct mc_cache {
   int inflight_B = 0;
   const double* inflight_q = nullptr;
   bool inflight_ready = false;  // completed (and any fallback applied) while staging appends
+  bool inflight_direct = false; // its result comes back zero-copy
+  bool param_in = false;        // MC_PARAM_INPUT=1: single-query lookups carry their inputs in the launch
+                                // parameters (measured equal to the pinned-envelope copy on B200)
+  double* h_qkeep = nullptr;    // [Dp] the last parameter-block query (for an exhaustive fallback)
 
   TcPlan* tc = nullptr;           // fp16 tensor-core scan plan (MC_PATH_GEMM*), created on first use
   Tc8Plan* tc8 = nullptr;         // int8 tensor-core scan plan (the batched default), created on first use
@@ -485,7 +489,26 @@ bool direct_result(const mc_cache* h, int B);
 
 // Enqueue a zero-copy lookup: packed self-validating decisions (default), or
 // the decisions + a system fence + the completion word.
+void quantize_query(const double* q, int D, int Dp, QPrep* p, int8_t* q8);
+GemvAppendArgs take_pending(mc_cache* h, const double* dev_rows);
+
 int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool async_reuse, const double** q) {
+  if (h->packed && h->param_in && B == 1 && h->n_pending <= 1 && h->Dp <= 1024) {
+    // the query, its quantisation and the pending row ride in the launch's parameter block:
+    // no host->device copy precedes the kernel
+    const double* stage_row = h->n_pending == 1 ? h->h_env : nullptr;
+    memcpy(h->h_qkeep, queries, (size_t)h->D * sizeof(double));
+    const RingState st = mirror(h);
+    take_pending(h, nullptr);
+    memset(h->h_outp, 0, sizeof(uint4));
+    *q = nullptr;
+    CU(launch_stream8_direct(h->s8, rbufs(h), st, h->D, queries, stage_row, h->d_cta, h->sm_count, h->shard,
+                             h->d_counter, h->d_gmax, h->thr, h->d_rec, nullptr, h->d_state, nullptr, seq_tag(seq),
+                             h->d_outp, quantize_query, h->stream));
+    h->stats[5]++;
+    h->stats[7]++;
+    return MC_OK;
+  }
   if (h->packed) {
     memset(h->h_outp, 0, (size_t)B * sizeof(uint4));  // no stale record can carry this lookup's tag
     return lookup_enqueue(h, queries, B, h->d_rec, nullptr, async_reuse, q, nullptr, seq_tag(seq), h->d_outp);
@@ -495,18 +518,33 @@ int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool
 
 int wait_direct(mc_cache* h, unsigned seq, int B) { return h->packed ? wait_packed(h, seq, B) : wait_seq(h, seq); }
 
+// The device query of a completed lookup, for the exhaustive fallback: a
+// parameter-block lookup has none, so its kept host copy is uploaded now.
+int device_query(mc_cache* h, const double* q, const double** out) {
+  if (q) {
+    *out = q;
+    return MC_OK;
+  }
+  CU(cudaMemcpyAsync(h->d_env, h->h_qkeep, (size_t)h->Dp * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  *out = h->d_env;
+  return MC_OK;
+}
+
 // Complete the asynchronous lookup in flight, if any: wait for its decisions
 // and run the exhaustive fallback for the queries whose certificate needs it
 // (while the ring still holds the state that lookup scanned).
 int finish_inflight(mc_cache* h) {
   if (!h->inflight_seq || h->inflight_ready) return MC_OK;
   const int B = h->inflight_B;
-  int rc = h->inflight_q && direct_result(h, B) ? wait_direct(h, h->inflight_seq, B) : wait_seq(h, h->inflight_seq);
+  int rc = h->inflight_direct ? wait_direct(h, h->inflight_seq, B) : wait_seq(h, h->inflight_seq);
   if (rc) return rc;
   bool need = false;
   for (int b = 0; b < B; ++b) need |= (h->h_out[b].flags & FLAG_NEED_ANY) != 0;
   if (need) {
-    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, h->inflight_q, B, h->d_rec, h->d_scratch,
+    const double* qd = nullptr;
+    rc = device_query(h, h->inflight_q, &qd);
+    if (rc) return rc;
+    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, qd, B, h->d_rec, h->d_scratch,
                            exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
     CU(launch_finalize(h->d_rec, 1, B, -1, h->d_state, h->thr, h->d_out, h->stream));
     h->stats[7] += 3;
@@ -670,6 +708,9 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
     if (!h->s8) return cleanup(fail(MC_ERR_CUDA, "int8 stream scan plan: %s", err));
   }
   if (const char* e = getenv("MC_PACKED_RESULT")) h->packed = atoi(e) != 0;
+  if (const char* e = getenv("MC_PARAM_INPUT")) h->param_in = atoi(e) != 0;
+  CUC(cudaMallocHost(&h->h_qkeep, (size_t)h->Dp * sizeof(double)));
+  memset(h->h_qkeep, 0, (size_t)h->Dp * sizeof(double));
   if (h->C > 0x7fffffffll) h->packed = false;  // live index must fit the packed int32
   CUC(cudaHostAlloc(&h->h_seq, 64, cudaHostAllocMapped));
   *h->h_seq = 0u;
@@ -716,6 +757,7 @@ int mc_destroy(mc_cache* h) {
     cudaFree(h->d_state);
     cudaFree(h->d_counter);
     cudaFreeHost(h->h_seq);
+    cudaFreeHost(h->h_qkeep);
     if (h->env_ev) cudaEventDestroy(h->env_ev);
     if (h->stream) cudaStreamDestroy(h->stream);
   }
@@ -849,6 +891,8 @@ int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* ou
   bool need = false;
   for (int b = 0; b < B; ++b) need |= (h->h_out[b].flags & FLAG_NEED_ANY) != 0;
   if (need) {  // rare: certificate failed or exotic query -> exact rescan, then decide again
+    rc = device_query(h, q, &q);
+    if (rc) return rc;
     CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, q, B, h->d_rec, h->d_scratch,
                            exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
     CU(launch_finalize(h->d_rec, 1, B, -1, h->d_state, h->thr, h->d_out, h->stream));
@@ -879,6 +923,7 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
     if (rc) return rc;
     h->inflight_q = q;
     h->inflight_ready = false;
+    h->inflight_direct = true;
   } else {  // paths without a zero-copy result complete synchronously
     const double* q = nullptr;
     rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_out, false, &q);
@@ -889,6 +934,7 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
     h->inflight_seq = seq;
     h->inflight_q = q;
     h->inflight_ready = false;
+    h->inflight_direct = false;
     *h->h_seq = seq;  // already complete: finish_inflight only applies the fallback
   }
   h->inflight_seq = seq;

@@ -42,8 +42,11 @@
 // from the envelope at kernel start.
 //
 // Algorithmic bytes per launch: count * (P8 + 8) + nb * (9 * Dp + 40), P8 = Dp rounded up to 128.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <type_traits>
 
 #include "merge.cuh"
 #include "sm100.cuh"
@@ -119,6 +122,19 @@ struct S8Args {
   uint4* outp;                 // optional (host-mapped): packed decisions, one 16-byte store each (see below)
 };
 
+// The single-query launch's inputs carried in the kernel parameter block (a
+// __grid_constant__ struct, < 32 KB): the float64 query, its int8
+// quantisation and at most one pending row, all zero-padded to Dp <= 1024.
+struct S8In {
+  QPrep prep;
+  alignas(16) int8_t q8[1024];
+  alignas(16) double q64[1024];
+  alignas(16) double stage[1024];
+};
+struct S8NoIn {
+  int unused;
+};
+
 // A decision packed into one 16-byte store (one PCIe write, read by the host
 // with one 16-byte load): sim | live (int32) | k (8) flags (8: MC_FLAG_* bits
 // 0-6, bit 7 = needs the exhaustive path) seq (16).  The sequence tag makes
@@ -174,6 +190,7 @@ struct S8Smem {
   float ovf[S8_CW][NB];                 // largest bound a full queue dropped
   unsigned bound[NB];                   // CTA lower bound (order-preserving float key)
   int done, pool_done;
+  int q_ready;                          // sq64 (the float64 queries) is filled
   Best2 best[S8_CW + 2][NB];            // float64 best per pool warp, then the eager rescorer's
   unsigned long long t[8];              // measurement stamps (MC_GEMV_TIMING=1)
   unsigned long long c[4];              // pool cycle counts (MC_GEMV_TIMING=1)
@@ -265,6 +282,8 @@ __device__ __noinline__ int s8_pass(int ncw, bool retire) {
 __device__ __forceinline__ void s8_pending(const S8Ctx x, const double* stage, long long n_app,
                                         long long n_pend, long long n_scan) {
   const int lane = threadIdx.x & 31;
+  while (!*(volatile int*)&S.q_ready) {
+  }
   for (long long i = 0; i < n_pend; ++i) {
     const double* srow = stage + (size_t)(n_app - n_pend + i) * x.Dp;
     const long long row = n_scan + i;
@@ -288,6 +307,8 @@ __device__ __forceinline__ void s8_pending(const S8Ctx x, const double* stage, l
 __device__ __forceinline__ void s8_pool(const S8Ctx x, int wid) {
   const int lane = threadIdx.x & 31;
   asm volatile("bar.sync 1, %0;" ::"n"((S8_CW + 1) * 32) : "memory");
+  while (!*(volatile int*)&S.q_ready) {
+  }
   if (x.timing && lane == 0) atomicMax(&S.t[S8T_POOL], s8_timer());
   const long long c_pool = clock64();
   bool first_pass = true;
@@ -335,7 +356,7 @@ __device__ __forceinline__ void s8_pool(const S8Ctx x, int wid) {
 // The rescorer after the pool: the CTA record, the ticket and, in the last
 // CTA, the merge of every record and the decision (cache.py:255-260,
 // select_k :112-117), then the zero-copy completion word.
-__device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, CtaRec* cta, int b0) {
+__device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const QPrep* prep, CtaRec* cta, int b0) {
   const int lane = threadIdx.x & 31;
   const int nb = x.nb;
   if (lane == 0)
@@ -365,7 +386,7 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, CtaRec
     if (x.timing && lane < 4) a.timing[8 + 8 * 512 + 4 * blockIdx.x + lane] = S.c[lane];
   };
   unsigned exotic = 0;  // loaded before the ticket (off the tail's critical path)
-  if (lane < nb) exotic = a.prep[lane].exotic != 0 ? 1u : 0u;
+  if (lane < nb) exotic = prep[lane].exotic != 0 ? 1u : 0u;
   unsigned old = 0;
   if (lane == 0)
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.counter) : "memory");
@@ -500,10 +521,23 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, CtaRec
   dump();
 }
 
-template <int KB, int NBQ>
+template <int KB, int NBQ, bool IN>
 __global__ void __launch_bounds__(S8_THREADS, 1)
-    k_stream8_scan(RingBufs rb, const RingState st, const double* __restrict__ q64, int nb,
-                   CtaRec* __restrict__ cta, int b0, ShardMap sm, S8Args a, int nst, int Dp) {
+    k_stream8_scan(RingBufs rb, const RingState st, const double* __restrict__ q64_dev, int nb,
+                   CtaRec* __restrict__ cta, int b0, ShardMap sm, S8Args a, int nst, int Dp,
+                   const __grid_constant__ std::conditional_t<IN, S8In, S8NoIn> in) {
+  // IN: this lookup's query, its quantisation and its pending row arrive in the
+  // launch's parameter block (no host->device copy before the kernel)
+  const double* q64 = q64_dev;
+  const int8_t* q8p = a.q8;
+  const QPrep* prepp = a.prep;
+  const double* stagep = a.stage;
+  if constexpr (IN) {
+    q64 = in.q64;
+    q8p = in.q8;
+    prepp = &in.prep;
+    stagep = in.stage;
+  }
   constexpr int P8 = KB * 128;                // int8 row stride (Dp rounded up to 128)
   constexpr int R = s8_rows_per_lane(KB);
   constexpr int SROWS = 32 * R;               // rows per stage
@@ -540,6 +574,7 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     for (int b = 0; b < NBQ; ++b) S.bound[b] = s8_key(-INFINITY);
     S.done = 0;
     S.pool_done = 0;
+    S.q_ready = IN ? 0 : 1;
     for (int k = 0; k < 8; ++k) S.t[k] = 0ull;
     S.t[S8T_R0] = ~0ull;
     for (int k = 0; k < 4; ++k) S.c[k] = k == 2 ? ~0ull : 0ull;
@@ -547,11 +582,13 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
   if (threadIdx.x < S8_CW) S.qtail[threadIdx.x] = 0;
   for (int i = threadIdx.x; i < (S8_CW + 2) * NB; i += blockDim.x) (&S.best[0][0])[i].init();
   for (int i = threadIdx.x; i < S8_CW * S8_QCAP; i += blockDim.x) (&S.qc[0][0])[i] = 0;
-  for (int i = threadIdx.x; i < NBQ * Dp; i += blockDim.x) sq64[i] = i < nb * Dp ? q64[i] : 0.0;
+  if constexpr (!IN) {  // a parameter-block query is copied by the poller warp, off the prologue
+    for (int i = threadIdx.x; i < NBQ * Dp; i += blockDim.x) sq64[i] = i < nb * Dp ? q64[i] : 0.0;
+  }
   for (int i = threadIdx.x; i < NBQ * P8 / 16; i += blockDim.x) {  // q̂ (stride Dp) -> [NBQ][P8], zero-padded
     const int b = i / (P8 / 16), c = i % (P8 / 16);
     reinterpret_cast<uint4*>(sq8)[i] = (b < nb && c < Dp / 16)
-                                           ? reinterpret_cast<const uint4*>(a.q8 + (size_t)b * Dp)[c]
+                                           ? reinterpret_cast<const uint4*>(q8p + (size_t)b * Dp)[c]
                                            : make_uint4(0u, 0u, 0u, 0u);
   }
   // Everything above reads only this launch's inputs (host-staged queries) and
@@ -575,6 +612,8 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     // early and the pool after the scan mostly finds the CTA's best done.  It
     // checks `done` before each claim and never waits on global memory, so it
     // hands over within one exact dot once the scan is over.
+    while (!*(volatile int*)&S.q_ready) {
+    }
     while (*(volatile int*)&S.done != S8_CW) {
       const int bi = s8_pass(ncw, false);
       if (bi < 0 || *(volatile int*)&S.done == S8_CW) {
@@ -615,6 +654,14 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     // while the CTA streams pull the leading candidate's float64 row into L2
     // so its rescoring after the scan hits L2.  This warp never synchronises
     // (its global atomics stay off the other warps' fences and barriers).
+    if constexpr (IN) {
+      for (int i = lane; i < NBQ * Dp; i += 32) sq64[i] = i < nb * Dp ? q64[i] : 0.0;
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        *(volatile int*)&S.q_ready = 1;
+      }
+    }
     int pf = -1;
     unsigned pub[NBQ];
 #pragma unroll
@@ -668,9 +715,9 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
 
   if (warp > S8_CW) {
     // ------------------------------------------------------------ rescorer
-    if (blockIdx.x == 0 && n_pend > 0) s8_pending(x, a.stage, a.n_app, n_pend, n_scan);
+    if (blockIdx.x == 0 && n_pend > 0) s8_pending(x, stagep, a.n_app, n_pend, n_scan);
     s8_pool(x, S8_CW);
-    s8_finish(x, a, cta, b0);
+    s8_finish(x, a, prepp, cta, b0);
     return;
   }
 
@@ -679,7 +726,7 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
   double sq[NBQ], q1[NBQ];
 #pragma unroll
   for (int b = 0; b < NBQ; ++b) {
-    const QPrep pq = b < nb ? a.prep[b] : QPrep{0.0, 0.0, 0.0, 0.f, 0};
+    const QPrep pq = b < nb ? prepp[b] : QPrep{0.0, 0.0, 0.0, 0.f, 0};
     sq[b] = pq.s;
     q1[b] = pq.q1;
   }
@@ -821,16 +868,19 @@ static cudaError_t s8_attr(S8Plan* p) {  // sizes the stages, raises the smem li
   cudaGetDevice(&dev);
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e != cudaSuccess) return e;
-  cudaFuncAttributes fa1, fa4;
-  if ((e = cudaFuncGetAttributes(&fa1, k_stream8_scan<KB, 1>)) != cudaSuccess) return e;
-  if ((e = cudaFuncGetAttributes(&fa4, k_stream8_scan<KB, 4>)) != cudaSuccess) return e;
-  p->nst[0] = s8_fit(p->P8, p->Dp, 1, fa1.sharedSizeBytes, (size_t)optin);
+  cudaFuncAttributes fa1, fa4, fai;
+  if ((e = cudaFuncGetAttributes(&fa1, k_stream8_scan<KB, 1, false>)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fa4, k_stream8_scan<KB, 4, false>)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fai, k_stream8_scan<KB, 1, true>)) != cudaSuccess) return e;
+  p->nst[0] = s8_fit(p->P8, p->Dp, 1, std::max(fa1.sharedSizeBytes, fai.sharedSizeBytes), (size_t)optin);
   p->nst[1] = s8_fit(p->P8, p->Dp, 4, fa4.sharedSizeBytes, (size_t)optin);
   p->smem[0] = s8_smem(p->P8, p->Dp, p->nst[0], 1);
   p->smem[1] = s8_smem(p->P8, p->Dp, p->nst[1], 4);
-  e = cudaFuncSetAttribute(k_stream8_scan<KB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem[0]);
+  e = cudaFuncSetAttribute(k_stream8_scan<KB, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem[0]);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_stream8_scan<KB, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem[1]);
+  e = cudaFuncSetAttribute(k_stream8_scan<KB, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem[0]);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_stream8_scan<KB, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem[1]);
 }
 
 S8Plan* s8_plan_create(int8_t* ring8, float2* ringq, long long C, int Dp, int P8, char* err, int errlen) {
@@ -878,8 +928,63 @@ static cudaError_t s8_launch(const S8Plan* p, const RingBufs& rb, const RingStat
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (nb == 1) return cudaLaunchKernelEx(&cfg, k_stream8_scan<KB, 1>, rb, st, q64, nb, cta, b0, sm, a, p->nst[0], p->Dp);
-  return cudaLaunchKernelEx(&cfg, k_stream8_scan<KB, 4>, rb, st, q64, nb, cta, b0, sm, a, p->nst[1], p->Dp);
+  const S8NoIn none{0};
+  if (nb == 1)
+    return cudaLaunchKernelEx(&cfg, k_stream8_scan<KB, 1, false>, rb, st, q64, nb, cta, b0, sm, a, p->nst[0], p->Dp,
+                              none);
+  return cudaLaunchKernelEx(&cfg, k_stream8_scan<KB, 4, false>, rb, st, q64, nb, cta, b0, sm, a, p->nst[1], p->Dp,
+                            none);
+}
+
+template <int KB>
+static cudaError_t s8_launch_in(const S8Plan* p, const RingBufs& rb, const RingState& st, CtaRec* cta, int grid,
+                                ShardMap sm, const S8Args& a, const S8In& in, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(S8_THREADS);
+  cfg.dynamicSmemBytes = p->smem[0];
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_stream8_scan<KB, 1, true>, rb, st, (const double*)nullptr, 1, cta, 0, sm, a,
+                            p->nst[0], p->Dp, in);
+}
+
+size_t s8_in_bytes() { return sizeof(S8In); }
+
+// One query whose float64 row, int8 quantisation and (<= 1) pending row ride
+// in the kernel's parameter block: q64 / stage are HOST rows (D doubles), the
+// quantisation is done here into the block.
+cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const RingState& st, int D, const double* q64,
+                                  const double* stage_row, CtaRec* cta, int grid, ShardMap sm, unsigned* counter,
+                                  unsigned* gmax, const Thresholds& thr, mc_record* rec, OutRec* out,
+                                  RingState* d_state, unsigned* done_seq, unsigned seq, uint4* outp,
+                                  void (*quantise)(const double*, int, int, QPrep*, int8_t*), cudaStream_t s) {
+  if (!p || p->Dp > 1024) return cudaErrorInvalidValue;
+  static thread_local S8In in;
+  const int Dp = p->Dp;
+  memcpy(in.q64, q64, (size_t)D * sizeof(double));
+  memset(in.q64 + D, 0, (size_t)(Dp - D) * sizeof(double));
+  quantise(in.q64, D, Dp, &in.prep, in.q8);
+  if (stage_row) {
+    memcpy(in.stage, stage_row, (size_t)Dp * sizeof(double));  // staged rows are already zero-padded to Dp
+  }
+  S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), nullptr, nullptr, nullptr, stage_row ? 1 : 0, d_state,
+           done_seq, seq, outp};
+  switch (p->P8 / 128) {
+    case 1: return s8_launch_in<1>(p, rb, st, cta, grid, sm, a, in, s);
+    case 2: return s8_launch_in<2>(p, rb, st, cta, grid, sm, a, in, s);
+    case 3: return s8_launch_in<3>(p, rb, st, cta, grid, sm, a, in, s);
+    case 4: return s8_launch_in<4>(p, rb, st, cta, grid, sm, a, in, s);
+    case 5: return s8_launch_in<5>(p, rb, st, cta, grid, sm, a, in, s);
+    case 6: return s8_launch_in<6>(p, rb, st, cta, grid, sm, a, in, s);
+    case 7: return s8_launch_in<7>(p, rb, st, cta, grid, sm, a, in, s);
+    case 8: return s8_launch_in<8>(p, rb, st, cta, grid, sm, a, in, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingState& st, const double* q64, int nb,

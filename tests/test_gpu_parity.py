@@ -463,3 +463,11 @@ def test_int8_tensor_core_scan_matches_oracle(dim, cap, n_ins, B):
     st = _check_against_scan(c, live_rows, Q, ThresholdTable.default(), f"gemm8 d{dim} B{B}")
     assert st["fallback"] <= max(2, B // 50)
     c.close()
+
+
+def test_parameter_block_inputs_match_oracle(monkeypatch):
+    """MC_PARAM_INPUT=1: single-query lookups carry query, quantisation and pending row in the kernel's
+    parameter block (no host->device copy); same answers through inserts, evictions and async lookups."""
+    monkeypatch.setenv("MC_PARAM_INPUT", "1")
+    test_async_lookup_overlapping_inserts_matches_oracle()
+    test_fifo_insert_per_request_matches_oracle_cache()
