@@ -125,3 +125,34 @@ def test_async_lookup_resolves_against_its_submit_state():
         assert got == want, i
         assert (got.entry is want.entry) or got.entry is None
     assert _state(a) == _state(b)
+
+
+def test_serving_decisions_follow_the_reference_rules():
+    """route = hit queue (scheduler.py:80-89), steps = T - k (engine.py:38-45),
+    sigma = noise_reentry_level(k, schedule) (cache.py:305-334), per query, from one batched lookup."""
+    from paper_2503_11972_b200 import ThresholdTable, linear_sigma_schedule, noise_reentry_level
+
+    rng = np.random.default_rng(23)
+    d = 256
+    c = SemanticCache(200, d)
+    ents = _entries(rng, 150, d)
+    c.bulk_load(ents)
+    table = ThresholdTable.default(total_steps=50)
+    sched = linear_sigma_schedule(50)
+    Q = np.stack([normalize(ents[i].embedding + s * rng.standard_normal(d) / np.sqrt(d))
+                  for i, s in zip(rng.integers(0, 150, 64), np.linspace(0.05, 8.0, 64))]
+                 + [normalize(rng.standard_normal(d)) for _ in range(16)])
+    dec = c.serving_decisions(Q, table, sched)
+    for q, row in zip(Q, dec):
+        r = c.retrieve(q, table)
+        assert row["hit"] == r.hit and row["route"] == int(r.hit)
+        assert row["similarity"] == r.similarity
+        assert row["k"] == (r.k or 0) and row["steps"] == 50 - (r.k or 0)
+        if r.hit:
+            assert c.entries()[row["live"]] is r.entry
+            assert row["sigma"] == noise_reentry_level(r.k, sched)
+        else:
+            assert row["live"] == -1 and np.isnan(row["sigma"])
+    assert dec["hit"].any() and (~dec["hit"]).any()
+    empty = SemanticCache(10, d).serving_decisions(Q[:3], table, sched)
+    assert (empty["live"] == -1).all() and (empty["steps"] == 50).all() and not empty["hit"].any()
