@@ -471,3 +471,26 @@ def test_parameter_block_inputs_match_oracle(monkeypatch):
     monkeypatch.setenv("MC_PARAM_INPUT", "1")
     test_async_lookup_overlapping_inserts_matches_oracle()
     test_fifo_insert_per_request_matches_oracle_cache()
+
+
+def test_serving_decisions_on_device_match_sequential_lookups():
+    """SURVEY §8 f3 on the device path: route / steps / sigma from one batched lookup equal the
+    per-query retrieve() results (engine.py:38-45, scheduler.py:80-89, cache.py:305-334)."""
+    from paper_2503_11972_b200 import linear_sigma_schedule, noise_reentry_level
+
+    wl = ClusteredWorkload(768, n_clusters=32, seed=99)
+    c = SemanticCache(capacity=6000, dim=768)
+    c.bulk_load(CacheEntry(f"e{i}", v, "large", i, float(i)) for i, v in enumerate(wl.cache_rows(6000)))
+    table = ThresholdTable.default()
+    sched = linear_sigma_schedule(table.total_steps)
+    Q = np.concatenate([wl.queries(40), np.stack([v / np.linalg.norm(v) for v in
+                                                  np.random.default_rng(1).standard_normal((8, 768))])])
+    dec = c.serving_decisions(Q, table, sched)
+    for q, row in zip(Q, dec):
+        r = c.retrieve(q, table)
+        assert bool(row["hit"]) == r.hit and row["route"] == int(r.hit)
+        assert row["k"] == (r.k or 0) and row["steps"] == table.total_steps - (r.k or 0)
+        assert abs(row["similarity"] - r.similarity) <= 1e-12
+        if r.hit:
+            assert c.entries()[row["live"]] is r.entry and row["sigma"] == noise_reentry_level(r.k, sched)
+    c.close()
