@@ -158,6 +158,10 @@ int mc_profile_rotate(mc_cache* const* hs, int32_t nh, const double* queries, co
  * scripts/profile_case.py. */
 int mc_debug_gemv_timing(unsigned long long* out8, int reset);
 
+/* Debugging hook: copies the float64 master row of live index `live` (0 =
+ * oldest; pending appends are published first) into out[0 .. dim). */
+int mc_debug_read_row(mc_cache* h, int64_t live, double* out);
+
 /* Counters since creation: [0] lookups, [1] certificate fallbacks,
  * [2] non-finite queries, [3] exact ties, [4] candidates rescored,
  * [5] GEMV launches, [6] GEMM launches, [7] kernel launches total. */

@@ -30,7 +30,7 @@ EXPORTED = (
     "mc_create", "mc_destroy", "mc_set_thresholds", "mc_append", "mc_evict_front", "mc_size",
     "mc_retrieve_batch", "mc_set_path", "mc_configure_shard", "mc_retrieve_local_async",
     "mc_merge_records", "mc_stats", "mc_last_error", "mc_version", "mc_profile_steps", "mc_profile_rotate",
-    "mc_debug_gemv_timing", "mc_retrieve_submit", "mc_retrieve_wait",
+    "mc_debug_gemv_timing", "mc_retrieve_submit", "mc_retrieve_wait", "mc_debug_read_row",
 )
 
 
@@ -59,6 +59,7 @@ def _declare(lib):
     lib.mc_profile_steps.argtypes = [vp, dp, dp, i32, i32, i64, dp, dp]
     lib.mc_profile_rotate.argtypes = [dp, i32, dp, dp, i32, i32, dp, dp]
     lib.mc_retrieve_submit.argtypes = [vp, dp, i32, dp]
+    lib.mc_debug_read_row.argtypes = [vp, i64, dp]
     lib.mc_retrieve_wait.argtypes = [vp, C.c_uint32, dp, dp, dp, dp]
     lib.mc_debug_gemv_timing.argtypes = [dp, i32]
     lib.mc_last_error.restype = C.c_char_p
@@ -260,6 +261,12 @@ class DeviceRing:
         _check(lib, lib.mc_profile_rotate(C.cast(hs, C.c_void_p), len(rings), _ptr(Q), None if r is None else _ptr(r),
                                           B, int(iters), _ptr(ms), _ptr(cnt)))
         return {"step_ms": float(ms[0]), "launches_per_step": int(cnt[0]), "would_fallback": int(cnt[1])}
+
+    def debug_read_row(self, live: int) -> np.ndarray:
+        """The device's float64 copy of live row `live` (debugging)."""
+        out = np.empty(3 * self.dim, dtype=np.float64)
+        _check(self.lib, self.lib.mc_debug_read_row(self._h, int(live), _ptr(out)))
+        return out[: self.dim] if not os.environ.get("MC_DEBUG_COPIES") else out.reshape(3, self.dim)
 
     def stats(self) -> dict:
         out = np.zeros(8, dtype=np.int64)

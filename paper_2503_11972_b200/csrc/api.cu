@@ -301,7 +301,10 @@ int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse,
   if (h->D == h->Dp) {
     memcpy(qdst, queries, (size_t)B * row);
   } else {
-    for (int b = 0; b < B; ++b) memcpy(qdst + (size_t)b * h->Dp, queries + (size_t)b * h->D, h->D * sizeof(double));
+    for (int b = 0; b < B; ++b) {  // padding columns may hold an earlier lookup's quantisation bytes
+      memcpy(qdst + (size_t)b * h->Dp, queries + (size_t)b * h->D, h->D * sizeof(double));
+      memset(qdst + (size_t)b * h->Dp + h->D, 0, (size_t)(h->Dp - h->D) * sizeof(double));
+    }
   }
   const size_t prep_off = (size_t)(h->n_pending + B) * row;
   uint8_t* hp = reinterpret_cast<uint8_t*>(h->h_env) + prep_off;
@@ -823,7 +826,10 @@ int mc_append(mc_cache* h, const double* rows, int64_t n) {
     }
     const long long slot = (h->head + h->count) % h->C;
     if (h->n_pending == 0) h->pending_first_slot = slot;
-    memcpy(h->h_env + (size_t)h->n_pending * h->Dp, rows + (size_t)i * h->D, (size_t)h->D * sizeof(double));
+    double* dst = h->h_env + (size_t)h->n_pending * h->Dp;
+    memcpy(dst, rows + (size_t)i * h->D, (size_t)h->D * sizeof(double));
+    // the padding must read as zeros: this envelope row may have held an earlier lookup's quantisation block
+    if (h->Dp > h->D) memset(dst + h->D, 0, (size_t)(h->Dp - h->D) * sizeof(double));
     h->n_pending++;
     h->count++;
     h->appended++;
@@ -1281,6 +1287,34 @@ int mc_debug_gemv_timing(unsigned long long* out8, int reset) {
     CU(cudaMemcpy(t, init8, sizeof init8, cudaMemcpyHostToDevice));
   } else {
     CU(cudaMemcpy(out8, t, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  }
+  return MC_OK;
+}
+
+// Measurement / debugging hook: the float64 master copy of live row `live`
+// (0 = oldest) after every pending append has landed.  Not part of the drop-in.
+int mc_debug_read_row(mc_cache* h, int64_t live, double* out) {
+  if (!h || !out) return fail(MC_ERR_ARG, "NULL argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  if (live < 0 || live >= h->count) return fail(MC_ERR_ARG, "live index %lld outside [0, %lld)", (long long)live,
+                                                (long long)h->count);
+  int rc = flush(h);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(h->stream));
+  const long long slot = (h->head + live) % h->C;
+  CU(cudaMemcpy(out, h->ring64 + (size_t)slot * h->Dp, (size_t)h->D * sizeof(double), cudaMemcpyDeviceToHost));
+  if (getenv("MC_DEBUG_COPIES")) {  // out has room for 3 rows: float64, fp16, int8 x scale
+    std::vector<__half> r16(h->Dp);
+    std::vector<int8_t> r8(h->P8);
+    float2 q;
+    CU(cudaMemcpy(r16.data(), h->ring16 + (size_t)slot * h->Dp, (size_t)h->Dp * sizeof(__half), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(r8.data(), h->ring8 + (size_t)slot * h->P8, (size_t)h->P8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(&q, h->ringq + slot, sizeof q, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < h->D; ++i) {
+      out[h->D + i] = (double)__half2float(r16[i]);
+      out[2 * h->D + i] = (double)r8[i] * q.x;
+    }
   }
   return MC_OK;
 }

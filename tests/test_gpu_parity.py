@@ -494,3 +494,58 @@ def test_serving_decisions_on_device_match_sequential_lookups():
         if r.hit:
             assert c.entries()[row["live"]] is r.entry and row["sigma"] == noise_reentry_level(r.k, sched)
     c.close()
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_operation_sequences_every_path(seed):
+    """Randomised op logs (inserts with policy/age/capacity churn, bulk loads, async and batched
+    lookups of every size) through every scan path against the float64 oracle cache."""
+    rng = np.random.default_rng(1000 + seed)
+    dim = int(rng.choice([8, 96, 200, 512, 768, 1000]))
+    cap = int(rng.integers(50, 3000))
+    age = float(rng.choice([0.0, 400.0]))
+    paths = [_native.PATH_AUTO, _native.PATH_STREAM8, _native.PATH_GEMV8, _native.PATH_GEMV, _native.PATH_GEMM,
+             _native.PATH_GEMM8]
+    c = SemanticCache(capacity=cap, dim=dim, policy="all", max_age_s=age or None)
+    o = OracleCache(cap, dim, max_age_s=age or None)
+    table, ot = ThresholdTable.default(), OracleTable()
+    centers = rng.standard_normal((6, dim))
+    t, seq = 0.0, 0
+
+    def fresh(n):
+        nonlocal t, seq
+        out = []
+        for _ in range(n):
+            v = centers[rng.integers(0, 6)] + 1.2 * rng.standard_normal(dim) / np.sqrt(max(dim, 1)) * 4
+            t += float(rng.exponential(1.0))
+            out.append(CacheEntry(f"e{seq}", v / np.linalg.norm(v), "large" if rng.random() < 0.8 else "small",
+                                  seq, t))
+            seq += 1
+        return out
+
+    for step in range(60):
+        op = rng.random()
+        if op < 0.35:
+            for e in fresh(int(rng.integers(1, 40))):
+                c.insert(e)
+                o.insert(OracleEntry(e.id, e.embedding, e.producer, e.seq, e.inserted_at))
+        elif op < 0.45:
+            batch = fresh(int(rng.integers(1, 400)))
+            c.bulk_load(batch)
+            for e in batch:
+                o.insert(OracleEntry(e.id, e.embedding, e.producer, e.seq, e.inserted_at))
+        else:
+            c.ring.set_path(int(rng.choice(paths)))
+            B = int(rng.choice([1, 1, 2, 3, 4, 5, 17, 130]))
+            Q = centers[rng.integers(0, 6, B)] + 1.2 * rng.standard_normal((B, dim)) / np.sqrt(dim) * 4
+            Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+            if B == 1 and rng.random() < 0.5:
+                got = [c.retrieve_async(Q[0], table).result()]
+            else:
+                got = c.retrieve_batch(Q, table)
+            for q, r in zip(Q, got):
+                e, sim, k = o.retrieve_entry(q, ot)
+                assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (seed, step, dim)
+                assert r.k == k and _close(r.similarity, sim), (seed, step, r, sim)
+    assert len(c) == len(o.meta) == len(c.ring)
+    c.close()
