@@ -347,6 +347,12 @@ constexpr int TP_STAGES = 6;
 constexpr int TP_A_BYTES = 128 * TC_BK * 2;  // 16 KB: this CTA's 128 queries
 constexpr int TP_B_BYTES = 128 * TC_BK * 2;  // 16 KB: this CTA's half of the slot tile
 constexpr int TP_SMEM = TP_STAGES * (TP_A_BYTES + TP_B_BYTES) + 1024 + 256;
+// The pair kernel runs eight epilogue warps (two per TMEM lane quadrant, each
+// owning half of the 256 accumulator columns) so the top-K' filter keeps pace
+// with the MMAs; the column halves' lists meet in shared memory at the end.
+constexpr int TP_THREADS = 320;
+constexpr int TP_X_BYTES = 128 * (2 * KP + 1) * 4;  // half 1's lists: s[KP], slot[KP], drop per query row
+constexpr int TP_SMEM_PAIR = TP_SMEM + TP_X_BYTES;
 
 
 
@@ -364,7 +370,7 @@ __device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t da, uint
 }
 
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
     k_tc_scan_pair(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap ring_map,
                    const RingState* __restrict__ d_state, int n_mp, int B, int n_kb, float* __restrict__ part_s,
                    long long* __restrict__ part_p, float* __restrict__ part_floor, int n_chunks, float margin,
@@ -401,7 +407,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 8);
+      mbar_init(&tempty[i], 16);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -418,14 +424,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
-    if (lane == 0) {
-      const uint32_t leader_full0 = mapa_shared(smem_u32(&full[0]), 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = 0; u < n_units; ++u) {
-        const int t = (win.first + group + u * n_groups) % win.n_total;
-        for (int kb = 0; kb < n_kb; ++kb) {
-          mbar_wait2(&empty[stage], phase ^ 1, dbg & 16);
+    // The whole warp walks the loop and lane 0 issues (no lane parked at the closing
+    // cluster barrier while lane 0 loops).
+    const uint32_t leader_full0 = mapa_shared(smem_u32(&full[0]), 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = 0; u < n_units; ++u) {
+      const int t = (win.first + group + u * n_groups) % win.n_total;
+      for (int kb = 0; kb < n_kb; ++kb) {
+        mbar_wait2(&empty[stage], phase ^ 1, dbg & 16);
+        if (lane == 0) {
           if (rank == 0)
             mbar_expect_tx(&full[stage], (dbg & 1) ? 0 : 2 * (TP_A_BYTES + TP_B_BYTES));
           else
@@ -435,10 +443,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             tma_load_2d_pair(smB + stage * TP_B_BYTES, &ring_map, &full[stage], kb * TC_BK,
                              ((dbg & 8) ? (t & 7) : t) * TC_BN + rank * 128);
           }
-          if (++stage == TP_STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++stage == TP_STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
@@ -483,7 +492,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
+    // Warps 2..9: TMEM lane quadrant = warp % 4, column half = (warp - 2) / 4.
     const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
     const int b = m_pair * 256 + (int)rank * 128 + row;
     const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
@@ -500,7 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       if (l0 < 0) l0 += st.cap;
       const bool all_live = (slot0 + TC_BN <= st.cap) && (l0 + TC_BN <= st.count);
 #pragma unroll 1
-      for (int c = 0; c < TC_BN / 32; ++c) {
+      for (int c = half * (TC_BN / 64); c < (half + 1) * (TC_BN / 64); ++c) {
         float v[32];
         if (dbg & 4) break;
         tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN + c * 32), v);
@@ -519,20 +530,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(leader_tempty0 + acc * 8);
     }
-    if (b < B) {
-      const size_t o = (size_t)b * n_chunks + group;
+    // column half 1 hands its list to half 0 of the same query row
+    float* xs = reinterpret_cast<float*>(bars + 32);  // [KP][128] scores (past the 256-byte barrier block)
+    int* xp = reinterpret_cast<int*>(xs + KP * 128);  // [KP][128] slots
+    float* xd = reinterpret_cast<float*>(xp + KP * 128);  // [128] drop
+    if (half == 1) {
 #pragma unroll
       for (int i = 0; i < KP; ++i) {
-        long long pos = -1;
-        if (top.slot[i] >= 0) {
-          long long l = (long long)top.slot[i] - st.head;
-          if (l < 0) l += st.cap;
-          pos = (st.jhead + l) * (long long)sm.G + sm.g;
-        }
-        part_s[o * KP + i] = top.s[i];
-        part_p[o * KP + i] = pos;
+        xs[i * 128 + row] = top.s[i];
+        xp[i * 128 + row] = top.slot[i];
       }
-      part_floor[o] = top.drop;
+      xd[row] = top.drop;
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (half == 0) {
+      top.drop = fmaxf(top.drop, xd[row]);
+#pragma unroll
+      for (int i = 0; i < KP; ++i) {
+        const float v = xs[i * 128 + row];
+        const int sl = xp[i * 128 + row];
+        if (sl < 0) continue;
+        if (v > top.mn)
+          top.push(v, sl);
+        else
+          top.drop = fmaxf(top.drop, v);
+      }
+      if (b < B) {
+        const size_t o = (size_t)b * n_chunks + group;
+#pragma unroll
+        for (int i = 0; i < KP; ++i) {
+          long long pos = -1;
+          if (top.slot[i] >= 0) {
+            long long l = (long long)top.slot[i] - st.head;
+            if (l < 0) l += st.cap;
+            pos = (st.jhead + l) * (long long)sm.G + sm.g;
+          }
+          part_s[o * KP + i] = top.s[i];
+          part_p[o * KP + i] = pos;
+        }
+        part_floor[o] = top.drop;
+      }
     }
   }
 
@@ -847,7 +884,7 @@ TcPlan* tc_plan_create(__half* ring16, long long C, int Dp, int Bcap, int sm_cou
     return nullptr;
   }
   if (cudaFuncSetAttribute(k_tc_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tc_scan_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, TP_SMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(k_tc_scan_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, TP_SMEM_PAIR) != cudaSuccess ||
       cudaFuncSetAttribute(k_tc_scan_quad, cudaFuncAttributeMaxDynamicSharedMemorySize, TP_SMEM) != cudaSuccess) {
     snprintf(err, errlen, "cannot raise dynamic shared memory to %d bytes", TC_SMEM);
     tc_plan_destroy(p);
@@ -904,7 +941,7 @@ cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const Rin
                                                                       p->Dp / TC_BK, part.s, part.p, part.floor_,
                                                                       groups, margin, sm);
   else if (p->pair)
-    k_tc_scan_pair<<<2 * nm * groups, TC_THREADS, TP_SMEM, s>>>(p->q_map, p->ring_map_half, d_state, nm, B,
+    k_tc_scan_pair<<<2 * nm * groups, TP_THREADS, TP_SMEM_PAIR, s>>>(p->q_map, p->ring_map_half, d_state, nm, B,
                                                                 p->Dp / TC_BK, part.s, part.p, part.floor_, groups,
                                                                 margin, sm, p->dbg);
   else
