@@ -510,11 +510,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
       long long l0 = slot0 - st.head;
       if (l0 < 0) l0 += st.cap;
       const bool all_live = (slot0 + TC_BN <= st.cap) && (l0 + TC_BN <= st.count);
-#pragma unroll 1
-      for (int c = half * (TC_BN / 64); c < (half + 1) * (TC_BN / 64); ++c) {
+      // four 32-column chunks per warp; chunk c+1's TMEM load overlaps chunk c's filter
+      auto filter = [&](uint32_t (&r)[32], int c) {
         float v[32];
-        if (dbg & 4) break;
-        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN + c * 32), v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         if (!all_live) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -525,6 +525,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
           }
         }
         top.scan32(v, (int)(slot0 + c * 32), margin);
+      };
+      if (!(dbg & 4)) {
+        const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN + half * 128);
+        const int c0 = half * 4;
+        uint32_t rc[32], rn[32];
+        tmem_ld32_async(ta, rc);
+        tmem_wait_ld();
+        tmem_pin(rc);
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {  // one copy of the filter code (instruction cache)
+          if (c < 3) tmem_ld32_async(ta + 32 * (c + 1), rn);
+          filter(rc, c0 + c);
+          tmem_wait_ld();
+          tmem_pin(rn);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rc[j] = rn[j];
+        }
       }
       tc_fence_before();
       __syncwarp();
