@@ -428,13 +428,9 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
     CU(launch_tc_scan(h->tc, q64, B, h->D, h->d_state, part, h->shard, h->stream));
     if (t_mid) CU(cudaEventRecord(t_mid, h->stream));
     CU(launch_merge(h->d_state, h->ring64, h->D, h->Dp, q64, B, part, tc_qscale(h->tc), gemm_eps_rel(h->Dp),
-                    eps_abs1(), rec, h->shard, h->stream));
+                    eps_abs1(), rec, h->shard, &h->thr, out, h->stream));  // the decision is fused (G = 1)
     h->stats[6]++;
     h->stats[7] += 3;
-    if (out) {
-      CU(launch_finalize(rec, 1, B, -1, h->d_state, h->thr, out, h->stream));
-      h->stats[7]++;
-    }
     return MC_OK;
   }
   GemvAppendArgs a = app;

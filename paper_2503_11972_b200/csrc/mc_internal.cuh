@@ -174,7 +174,7 @@ cudaError_t launch_merge8(const RingState* d_state, const double* ring64, int D,
 // qscale: per-query factor turning partial scores into similarity units (nullptr = 1).
 cudaError_t launch_merge(const RingState* d_state, const double* ring64, int D, int Dp, const double* q64, int B,
                          const Partials& part, const double* qscale, double eps_rel, double eps_abs1,
-                         mc_record* rec, ShardMap sm, cudaStream_t s);
+                         mc_record* rec, ShardMap sm, const Thresholds* thr, OutRec* out, cudaStream_t s);
 
 // Exhaustive exact rescan for the queries whose record needs it.
 cudaError_t launch_exact_rescan(const __half* ring16, const double* ring64, const RingState* d_state, int D,

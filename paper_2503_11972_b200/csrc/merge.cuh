@@ -202,4 +202,18 @@ __device__ __forceinline__ Best2 record_best(const mc_record& r) {
   return b;
 }
 
+// k_finalize's decision for a single shard's record (G = 1, base = jhead).
+__device__ __forceinline__ OutRec decide_one(const mc_record& r, long long base, const Thresholds& thr) {
+  Best2 best;
+  best.init();
+  unsigned fl = 0;
+  if (r.pos < 0) {
+    if (r.flags != 0xffffffffu) fl |= r.flags & FLAG_NEED_ANY;
+  } else {
+    fl |= r.flags & (MC_FLAG_FALLBACK | MC_FLAG_NONFINITE | FLAG_NEED_ANY);
+    best.merge(record_best(r));
+  }
+  return decide(best, fl, base, thr);
+}
+
 }  // namespace mc

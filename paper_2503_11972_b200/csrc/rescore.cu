@@ -11,7 +11,7 @@ __global__ void __launch_bounds__(MERGE_THREADS)
     k_merge(const RingState* __restrict__ d_state, const double* __restrict__ ring64, int D, int Dp,
             const double* __restrict__ q64, const float* __restrict__ part_s, const long long* __restrict__ part_p,
             const float* __restrict__ part_floor, int n_chunks, const double* __restrict__ qscale, double eps_rel,
-            double eps_a1, mc_record* __restrict__ rec, ShardMap sm) {
+            double eps_a1, mc_record* __restrict__ rec, ShardMap sm, Thresholds thr, OutRec* __restrict__ out) {
   extern __shared__ __align__(16) double sq[];  // [Dp]
   __shared__ MergeScratch ms;
   const int b = blockIdx.x;
@@ -20,19 +20,22 @@ __global__ void __launch_bounds__(MERGE_THREADS)
   const mc_record r = merge_one(st, ring64, D, Dp, sq, part_s + (size_t)b * n_chunks * KP,
                                 part_p + (size_t)b * n_chunks * KP, part_floor + (size_t)b * n_chunks, n_chunks,
                                 qscale ? qscale[b] : 1.0, eps_rel, eps_a1, sm, ms);
-  if (threadIdx.x == 0) rec[b] = r;
+  if (threadIdx.x == 0) {
+    rec[b] = r;
+    if (out) out[b] = decide_one(r, st.jhead, thr);  // single shard: k_finalize's decision, fused
+  }
 }
 
 cudaError_t launch_merge(const RingState* d_state, const double* ring64, int D, int Dp, const double* q64, int B,
                          const Partials& part, const double* qscale, double eps_rel, double eps_a1, mc_record* rec,
-                         ShardMap sm, cudaStream_t s) {
+                         ShardMap sm, const Thresholds* thr, OutRec* out, cudaStream_t s) {
   const size_t smem = (size_t)Dp * sizeof(double);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   k_merge<<<B, MERGE_THREADS, smem, s>>>(d_state, ring64, D, Dp, q64, part.s, part.p, part.floor_, part.n_chunks,
-                                         qscale, eps_rel, eps_a1, rec, sm);
+                                         qscale, eps_rel, eps_a1, rec, sm, out ? *thr : Thresholds{}, out);
   return cudaGetLastError();
 }
 

@@ -421,6 +421,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: everything above overlapped k_tc_prep; the
+  // query operand it writes is read (by TMA) only after this point.  The ring
+  // state was published by kernels that finished before k_tc_prep started.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -813,6 +817,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1)
 // qscale[b] = ||q[b]|| turns a scan score back into query units.
 __global__ void k_tc_prep(const double* __restrict__ q64, int B, int D, int Dp, __half* __restrict__ q16,
                           double* __restrict__ qscale) {
+  // the pair scan (launched as a programmatic dependent) may start its prologue now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ double red[32];
   const int b = blockIdx.x;
   double a = 0.0;
@@ -957,10 +963,20 @@ cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const Rin
     k_tc_scan_quad<<<4 * nm * (groups / 2), TC_THREADS, TP_SMEM, s>>>(p->q_map, p->ring_map_half, d_state, nm, B,
                                                                       p->Dp / TC_BK, part.s, part.p, part.floor_,
                                                                       groups, margin, sm);
-  else if (p->pair)
-    k_tc_scan_pair<<<2 * nm * groups, TP_THREADS, TP_SMEM_PAIR, s>>>(p->q_map, p->ring_map_half, d_state, nm, B,
-                                                                p->Dp / TC_BK, part.s, part.p, part.floor_, groups,
-                                                                margin, sm, p->dbg);
+  else if (p->pair) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * nm * groups);
+    cfg.blockDim = dim3(TP_THREADS);
+    cfg.dynamicSmemBytes = TP_SMEM_PAIR;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see griddepcontrol in both kernels
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_tc_scan_pair, p->q_map, p->ring_map_half, d_state, nm, B, p->Dp / TC_BK,
+                              part.s, part.p, part.floor_, groups, margin, sm, p->dbg);
+  }
   else
     k_tc_scan<<<nm * groups, TC_THREADS, TC_SMEM, s>>>(p->q_map, p->ring_map, d_state, nm, B, p->Dp / TC_BK,
                                                        part.s, part.p, part.floor_, groups, margin, sm);
