@@ -395,7 +395,10 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
     dump();
     return;
   }
-  __threadfence();
+  // No gpu-scope fence: every CTA's ticket is a release after its record store, lane 0's
+  // ticket here is an acquire (acq_rel), and the warp barrier orders the other lanes'
+  // record loads after it.
+  __syncwarp();
   if (lane == 0 && x.timing) a.timing[4] = s8_timer();
   // Merge the per-CTA records with independent warp reductions (no chain of
   // Best2 merges): best = max s; among records at best: max position and the
