@@ -168,12 +168,26 @@ size_t prep_bytes(const mc_cache* h, int B) { return prep_head(B) + (size_t)B * 
 // s >= max|q|/127 rounded up (so |q/s| <= 127), q̂ = rint(q / s), and the
 // norms the certificate and the exhaustive-path decision need.
 void quantize_query(const double* q, int D, int Dp, QPrep* p, int8_t* q8) {
-  double amax = 0.0, a2 = 0.0, a1 = 0.0;
-  for (int i = 0; i < D; ++i) {
-    amax = std::max(amax, std::fabs(q[i]));
-    a2 = std::fma(q[i], q[i], a2);
-    a1 += std::fabs(q[i]);
+  // four independent chains, plain multiply-add (no libm fma call on a generic x86-64
+  // target); the order only moves n2 / n1 by ulps, inside their (1 + 1e-12) slack
+  double mx[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0}, s1[4] = {0.0, 0.0, 0.0, 0.0};
+  int j = 0;
+  for (; j + 4 <= D; j += 4)
+    for (int k = 0; k < 4; ++k) {
+      const double x = q[j + k], ax = std::fabs(x);
+      mx[k] = std::max(mx[k], ax);
+      s2[k] += x * x;
+      s1[k] += ax;
+    }
+  for (; j < D; ++j) {
+    const double x = q[j], ax = std::fabs(x);
+    mx[0] = std::max(mx[0], ax);
+    s2[0] += x * x;
+    s1[0] += ax;
   }
+  const double amax = std::max(std::max(mx[0], mx[1]), std::max(mx[2], mx[3]));
+  const double a2 = (s2[0] + s2[1]) + (s2[2] + s2[3]);
+  const double a1 = (s1[0] + s1[1]) + (s1[2] + s1[3]);
   const bool finite = std::isfinite(a1) && std::isfinite(amax) && amax <= 1e300;
   float s = 0.0f;
   if (finite && amax > 0.0) {
