@@ -45,3 +45,30 @@ for i in range(iters):
     c.add(f"s{i}", imgs[i], "large", 1.0 + i)
 t1 = time.perf_counter()
 print(f"public API retrieve + add: {1e6 * (t1 - t0) / iters:.1f} us")
+# the bench's e2e step: async lookup, the insert while the scan runs, then the result
+t0 = time.perf_counter()
+for i in range(iters):
+    pend = c.retrieve_async(Q[i], t)
+    c.add(f"a{i}", imgs[i], "large", 1.0 + iters + i)
+    pend.result()
+t1 = time.perf_counter()
+print(f"public API retrieve_async + add + result: {1e6 * (t1 - t0) / iters:.1f} us")
+# pieces on the host: submit alone (wait right after), add alone, result alone
+ts = ta = tr = 0.0
+for i in range(iters):
+    a0 = time.perf_counter()
+    pend = c.retrieve_async(Q[i], t)
+    a1 = time.perf_counter()
+    c.add(f"b{i}", imgs[i], "large", 1.0 + 2 * iters + i)
+    a2 = time.perf_counter()
+    time.sleep(0)  # let the scan finish before timing result()
+    while False:
+        pass
+    a3 = time.perf_counter()
+    pend.result()
+    a4 = time.perf_counter()
+    ts += a1 - a0
+    ta += a2 - a1
+    tr += a4 - a3
+print(f"host pieces: retrieve_async {1e6 * ts / iters:.1f} us, add {1e6 * ta / iters:.1f} us, "
+      f"result (incl. waiting) {1e6 * tr / iters:.1f} us")
