@@ -312,14 +312,41 @@ int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse,
   if (rc) return rc;
   const size_t row = (size_t)h->Dp * sizeof(double);
   double* qdst = h->h_env + (size_t)h->n_pending * h->Dp;
-  if (h->D == h->Dp) {
-    memcpy(qdst, queries, (size_t)B * row);
-  } else {
-    for (int b = 0; b < B; ++b) {  // padding columns may hold an earlier lookup's quantisation bytes
-      memcpy(qdst + (size_t)b * h->Dp, queries + (size_t)b * h->D, h->D * sizeof(double));
-      memset(qdst + (size_t)b * h->Dp + h->D, 0, (size_t)(h->Dp - h->D) * sizeof(double));
+  auto stage_rows = [&](int b0, int b1) {
+    if (h->D == h->Dp) {
+      memcpy(qdst + (size_t)b0 * h->Dp, queries + (size_t)b0 * h->D, (size_t)(b1 - b0) * row);
+    } else {
+      for (int b = b0; b < b1; ++b) {  // padding columns may hold an earlier lookup's quantisation bytes
+        memcpy(qdst + (size_t)b * h->Dp, queries + (size_t)b * h->D, h->D * sizeof(double));
+        memset(qdst + (size_t)b * h->Dp + h->D, 0, (size_t)(h->Dp - h->D) * sizeof(double));
+      }
     }
+  };
+  // Large batches: stage and copy in chunks so each chunk's DMA overlaps the next chunk's
+  // host copy (the unquantised large-batch paths only; the int8 paths take B <= 4).
+  constexpr size_t CHUNK_BYTES = 256 << 10;
+  const int chunk = std::max<int>(1, (int)(CHUNK_BYTES / row));
+  if (!quantise && B > 2 * chunk) {
+    const double t1 = g_ht.on ? now_us() : 0.0;
+    const size_t head = (size_t)h->n_pending * row;
+    if (head) CU(cudaMemcpyAsync(h->d_env, h->h_env, head, cudaMemcpyHostToDevice, h->stream));
+    for (int b0 = 0; b0 < B; b0 += chunk) {
+      const int b1 = std::min(B, b0 + chunk);
+      stage_rows(b0, b1);
+      CU(cudaMemcpyAsync(h->d_env + (size_t)(h->n_pending + b0) * h->Dp, qdst + (size_t)b0 * h->Dp,
+                         (size_t)(b1 - b0) * row, cudaMemcpyHostToDevice, h->stream));
+    }
+    if (g_ht.on) g_ht.acc[1] += now_us() - t1;
+    if (async_reuse) {
+      CU(cudaEventRecord(h->env_ev, h->stream));
+      h->env_inflight = true;
+    }
+    *q_dev = h->d_env + (size_t)h->n_pending * h->Dp;
+    *prep_dev = nullptr;
+    *q8_dev = nullptr;
+    return MC_OK;
   }
+  stage_rows(0, B);
   const size_t prep_off = (size_t)(h->n_pending + B) * row;
   uint8_t* hp = reinterpret_cast<uint8_t*>(h->h_env) + prep_off;
   QPrep* hq = reinterpret_cast<QPrep*>(hp);
@@ -898,10 +925,19 @@ int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* ou
       g_ht.n++;
     }
   } else {
+    const double t0 = g_ht.on ? now_us() : 0.0;
+    const double h2d0 = g_ht.acc[1];
     rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_out, false, &q);
     if (rc) return rc;
+    const double t2 = g_ht.on ? now_us() : 0.0;
     CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
+    if (g_ht.on) {
+      const double t3 = now_us();
+      g_ht.acc[2] += (t2 - t0) - (g_ht.acc[1] - h2d0);
+      g_ht.acc[3] += t3 - t2;
+      g_ht.n++;
+    }
   }
   h->env_inflight = false;
   bool need = false;

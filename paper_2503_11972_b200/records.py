@@ -78,6 +78,27 @@ class RetrievalResult:
         return self.entry is not None
 
 
+def _result_factory():
+    """A constructor for RetrievalResult that skips the frozen dataclass's per-field
+    object.__setattr__ calls (about half the cost of a batch's result objects).  The
+    instances are ordinary RetrievalResult objects: same fields, equality, hash and repr."""
+    new = object.__new__
+    cls = RetrievalResult
+
+    def make(entry, similarity, k):
+        r = new(cls)
+        d = r.__dict__
+        d["entry"] = entry
+        d["similarity"] = similarity
+        d["k"] = k
+        return r
+
+    return make
+
+
+make_result = _result_factory()
+
+
 class ThresholdTable:
     """Similarity thresholds tau_k per skippable step count k (cache.py:73-117).
 

@@ -156,3 +156,21 @@ def test_serving_decisions_follow_the_reference_rules():
     assert dec["hit"].any() and (~dec["hit"]).any()
     empty = SemanticCache(10, d).serving_decisions(Q[:3], table, sched)
     assert (empty["live"] == -1).all() and (empty["steps"] == 50).all() and not empty["hit"].any()
+
+
+def test_fast_result_objects_equal_dataclass_ones():
+    """retrieve_batch builds its RetrievalResult objects without the dataclass __init__;
+    they must be indistinguishable from ones built the normal way (and stay frozen)."""
+    import dataclasses
+
+    import pytest
+
+    from paper_2503_11972_b200.records import CacheEntry, RetrievalResult, make_result
+
+    e = CacheEntry("x", np.ones(4) / 2.0, "large", 0, 0.0)
+    for args in ((e, 0.75, 10), (None, 0.125, None)):
+        a, b = make_result(*args), RetrievalResult(*args)
+        assert type(a) is RetrievalResult and a == b and repr(a) == repr(b) and a.hit == b.hit
+        assert (a.entry, a.similarity, a.k) == (b.entry, b.similarity, b.k)
+        with pytest.raises(dataclasses.FrozenInstanceError):
+            a.k = 1
