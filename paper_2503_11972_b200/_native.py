@@ -113,6 +113,9 @@ class DeviceRing:
         self._submit = self.lib.mc_retrieve_submit
         self._wait = self.lib.mc_retrieve_wait
         self._ticket = np.zeros(1, dtype=np.uint32)
+        self._ticket_ptr = self._ticket.ctypes.data  # .ctypes costs ~1 us per access
+        self._rowbuf = np.zeros(self.dim, dtype=np.float64)
+        self._rowptr = self._rowbuf.ctypes.data
         self._bcap = 0
         self._ensure_out(1)
         self._table_key = None
@@ -152,10 +155,10 @@ class DeviceRing:
         _check(self.lib, self.lib.mc_append(self._h, _ptr(rows), n))
 
     def append1(self, row: np.ndarray) -> None:
-        """One float64 row (the per-insert path: no copy for contiguous float64 input)."""
-        if row.dtype != np.float64 or not row.flags.c_contiguous:
-            row = np.ascontiguousarray(row, dtype=np.float64)
-        rc = self._append(self._hv, row.ctypes.data, 1)
+        """One row (the per-insert path): copied into a fixed float64 buffer, whose pointer is
+        computed once (cheaper than a per-call .ctypes on the caller's array)."""
+        self._rowbuf[...] = row
+        rc = self._append(self._hv, self._rowptr, 1)
         if rc:
             _check(self.lib, rc)
 
@@ -199,7 +202,7 @@ class DeviceRing:
     def submit1(self, q: np.ndarray) -> int:
         """Enqueue one lookup (mc_retrieve_submit); returns its ticket."""
         self._qbuf[0] = q
-        rc = self._submit(self._hv, self._qptr, 1, self._ticket.ctypes.data)
+        rc = self._submit(self._hv, self._qptr, 1, self._ticket_ptr)
         if rc:
             _check(self.lib, rc)
         return int(self._ticket[0])

@@ -39,6 +39,7 @@ from .records import (
     EmbeddingError,
     RetrievalResult,
     ThresholdTable,
+    make_result,
 )
 
 RECORD_BYTES = 32  # sizeof(mc_record)
@@ -217,11 +218,11 @@ class ShardedSemanticCache:
         out = []
         for i, f in enumerate(np.asarray(flags).tolist()):
             if f & _HIT:
-                out.append(RetrievalResult(store[int(live[i])], float(sim[i]), int(k[i]) or None))
+                out.append(make_result(store[int(live[i])], float(sim[i]), int(k[i]) or None))
             elif f & _EMPTY:
                 out.append(_MISS_EMPTY)
             else:
-                out.append(RetrievalResult(None, float(sim[i]), None))
+                out.append(make_result(None, float(sim[i]), None))
         return out
 
     def retrieve(self, q: np.ndarray, table: ThresholdTable) -> RetrievalResult:
