@@ -372,6 +372,7 @@ __device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t da, uint
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
     k_tc_scan_pair(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap ring_map,
+                   const __grid_constant__ CUtensorMap ring_map_q,
                    const RingState* __restrict__ d_state, int n_mp, int B, int n_kb, float* __restrict__ part_s,
                    long long* __restrict__ part_p, float* __restrict__ part_floor, int n_chunks, float margin,
                    ShardMap sm, int dbg) {
@@ -396,11 +397,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
   const int m_pair = cid % n_mp;
   const int group = cid / n_mp;
   const int n_groups = n_clusters / n_mp;
-  const int n_units = win.n_live > group ? (win.n_live - group + n_groups - 1) / n_groups : 0;
+  // Slot tiles are dealt round-robin over the pair groups.  When the last round is at most
+  // half full its tiles are split into 128-slot halves (N = 128 MMAs) over twice as many
+  // groups, so no group runs a whole extra tile (C3: 391 tiles over 74 groups).
+  const int n_rounds = win.n_live / n_groups, n_rem = win.n_live % n_groups;
+  const bool split = n_rem > 0 && 2 * n_rem <= n_groups && !(dbg & 128);
+  const int n_full = split ? n_rounds : (win.n_live > group ? (win.n_live - group + n_groups - 1) / n_groups : 0);
+  const int n_units = n_full + ((split && group < 2 * n_rem) ? 1 : 0);
+  // unit u -> physical tile t and half (-1: the whole 256-slot tile)
+  auto unit = [&](int u, int& t, int& hsel) {
+    if (u < n_full) {
+      t = (win.first + group + u * n_groups) % win.n_total;
+      hsel = -1;
+    } else {
+      t = (win.first + n_rounds * n_groups + (group >> 1)) % win.n_total;
+      hsel = group & 1;
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&q_map)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map_q)) : "memory");
     for (int i = 0; i < TP_STAGES; ++i) {
       mbar_init(&full[i], 2);
       mbar_init(&empty[i], 1);
@@ -434,18 +452,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int u = 0; u < n_units; ++u) {
-      const int t = (win.first + group + u * n_groups) % win.n_total;
+      int t, hsel;
+      unit(u, t, hsel);
+      const int bbytes = hsel < 0 ? TP_B_BYTES : TP_B_BYTES / 2;
       for (int kb = 0; kb < n_kb; ++kb) {
         mbar_wait2(&empty[stage], phase ^ 1, dbg & 16);
         if (lane == 0) {
           if (rank == 0)
-            mbar_expect_tx(&full[stage], (dbg & 1) ? 0 : 2 * (TP_A_BYTES + TP_B_BYTES));
+            mbar_expect_tx(&full[stage], (dbg & 1) ? 0 : 2 * (TP_A_BYTES + bbytes));
           else
             mbar_arrive_remote(leader_full0 + stage * 8);
           if (!(dbg & 1)) {
             tma_load_2d_pair(smA + stage * TP_A_BYTES, &q_map, &full[stage], kb * TC_BK, m_pair * 256 + rank * 128);
-            tma_load_2d_pair(smB + stage * TP_B_BYTES, &ring_map, &full[stage], kb * TC_BK,
-                             ((dbg & 8) ? (t & 7) : t) * TC_BN + rank * 128);
+            if (hsel < 0)
+              tma_load_2d_pair(smB + stage * TP_B_BYTES, &ring_map, &full[stage], kb * TC_BK,
+                               ((dbg & 8) ? (t & 7) : t) * TC_BN + rank * 128);
+            else  // this CTA's 64 slots of the half tile
+              tma_load_2d_pair(smB + stage * TP_B_BYTES, &ring_map_q, &full[stage], kb * TC_BK,
+                               t * TC_BN + hsel * 128 + rank * 64);
           }
         }
         __syncwarp();
@@ -458,10 +482,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader only)
     if (rank == 0) {
-      constexpr uint32_t idesc = umma_idesc_f16(256, TC_BN);
+      constexpr uint32_t idesc_full = umma_idesc_f16(256, TC_BN);
+      constexpr uint32_t idesc_half = umma_idesc_f16(256, TC_BN / 2);
       int stage = 0;
       uint32_t phase = 0;
       for (int u = 0; u < n_units; ++u) {
+        int t_unused, hsel;
+        unit(u, t_unused, hsel);
+        const uint32_t idesc = hsel < 0 ? idesc_full : idesc_half;
         const int acc = u & 1;
         const uint32_t acc_phase = (u >> 1) & 1;
         mbar_wait2(&tempty[acc], acc_phase ^ 1, dbg & 16);
@@ -507,14 +535,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
     for (int u = 0; u < n_units; ++u) {
       const int acc = u & 1;
       const uint32_t acc_phase = (u >> 1) & 1;
-      const int t = (win.first + group + u * n_groups) % win.n_total;
-      const long long slot0 = (long long)t * TC_BN;
+      int t, hsel;
+      unit(u, t, hsel);
+      const int width = hsel < 0 ? TC_BN : TC_BN / 2;  // accumulator columns of this unit
+      const int nch = width / 64;                        // 32-column chunks per epilogue warp
+      const long long slot0 = (long long)t * TC_BN + (hsel < 0 ? 0 : hsel * 128);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       long long l0 = slot0 - st.head;
       if (l0 < 0) l0 += st.cap;
-      const bool all_live = (slot0 + TC_BN <= st.cap) && (l0 + TC_BN <= st.count);
-      // four 32-column chunks per warp; chunk c+1's TMEM load overlaps chunk c's filter
+      const bool all_live = (slot0 + width <= st.cap) && (l0 + width <= st.count);
+      // nch (4, or 2 on a half tile) 32-column chunks per warp; chunk c+1's TMEM load overlaps chunk c's filter
       auto filter = [&](uint32_t (&r)[32], int c) {
         float v[32];
 #pragma unroll
@@ -531,15 +562,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
         top.scan32(v, (int)(slot0 + c * 32), margin);
       };
       if (!(dbg & 4)) {
-        const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN + half * 128);
-        const int c0 = half * 4;
+        const int c0 = half * nch;
+        const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN + c0 * 32);
         uint32_t rc[32], rn[32];
         tmem_ld32_async(ta, rc);
         tmem_wait_ld();
         tmem_pin(rc);
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {  // one copy of the filter code (instruction cache)
-          if (c < 3) tmem_ld32_async(ta + 32 * (c + 1), rn);
+        for (int c = 0; c < nch; ++c) {  // one copy of the filter code (instruction cache)
+          if (c + 1 < nch) tmem_ld32_async(ta + 32 * (c + 1), rn);
           filter(rc, c0 + c);
           tmem_wait_ld();
           tmem_pin(rn);
@@ -857,6 +888,7 @@ struct TcPlan {
   CUtensorMap q_map;
   CUtensorMap ring_map;       // 256-slot boxes (single-CTA kernel)
   CUtensorMap ring_map_half;  // 128-slot boxes (CTA-pair kernel)
+  CUtensorMap ring_map_q;     // 64-slot boxes (CTA-pair kernel, half-width tail tiles)
   bool pair = true;
   bool quad = false;  // CTA-quad (query multicast): correct but measured slower than pairs (lockstep)
   int dbg = 0;  // MC_TC_DEBUG bisection switches: 1 no TMA, 2 no MMA, 4 no epilogue (timing only)
@@ -902,7 +934,8 @@ TcPlan* tc_plan_create(__half* ring16, long long C, int Dp, int Bcap, int sm_cou
   }
   if (!encode_2d(&p->q_map, p->q16, p->Bcap, Dp, TC_BM, err, errlen) ||
       !encode_2d(&p->ring_map, ring16, C, Dp, TC_BN, err, errlen) ||
-      !encode_2d(&p->ring_map_half, ring16, C, Dp, 128, err, errlen)) {
+      !encode_2d(&p->ring_map_half, ring16, C, Dp, 128, err, errlen) ||
+      !encode_2d(&p->ring_map_q, ring16, C, Dp, 64, err, errlen)) {
     tc_plan_destroy(p);
     return nullptr;
   }
@@ -974,7 +1007,8 @@ cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const Rin
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_tc_scan_pair, p->q_map, p->ring_map_half, d_state, nm, B, p->Dp / TC_BK,
+    return cudaLaunchKernelEx(&cfg, k_tc_scan_pair, p->q_map, p->ring_map_half, p->ring_map_q, d_state, nm, B,
+                              p->Dp / TC_BK,
                               part.s, part.p, part.floor_, groups, margin, sm, p->dbg);
   }
   else
