@@ -17,6 +17,9 @@ __global__ void __launch_bounds__(MERGE_THREADS)
   const int b = blockIdx.x;
   const RingState st = *d_state;
   load_query(q64 + (size_t)b * Dp, D, Dp, sq);
+  // Programmatic dependent launch: the query and the ring state were written before the
+  // scan's prep kernel started; the candidate lists are read only after the scan is done.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const mc_record r = merge_one(st, ring64, D, Dp, sq, part_s + (size_t)b * n_chunks * KP,
                                 part_p + (size_t)b * n_chunks * KP, part_floor + (size_t)b * n_chunks, n_chunks,
                                 qscale ? qscale[b] : 1.0, eps_rel, eps_a1, sm, ms);
@@ -34,9 +37,19 @@ cudaError_t launch_merge(const RingState* d_state, const double* ring64, int D, 
     cudaError_t e = cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k_merge<<<B, MERGE_THREADS, smem, s>>>(d_state, ring64, D, Dp, q64, part.s, part.p, part.floor_, part.n_chunks,
-                                         qscale, eps_rel, eps_a1, rec, sm, out ? *thr : Thresholds{}, out);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B);
+  cfg.blockDim = dim3(MERGE_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // griddepcontrol.wait in k_merge
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_merge, d_state, ring64, D, Dp, q64, (const float*)part.s, (const long long*)part.p,
+                            (const float*)part.floor_, part.n_chunks, qscale, eps_rel, eps_a1, rec, sm,
+                            out ? *thr : Thresholds{}, out);
 }
 
 // ---------------------------------------------------------------------------

@@ -443,6 +443,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
   // query operand it writes is read (by TMA) only after this point.  The ring
   // state was published by kernels that finished before k_tc_prep started.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // and the merge behind this kernel may be scheduled as CTAs retire (it waits for all of them)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -846,34 +848,31 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1)
 
 // q16[b] = fp16(q[b] / ||q[b]||), zero rows for b >= B and zero padding columns;
 // qscale[b] = ||q[b]|| turns a scan score back into query units.
-__global__ void k_tc_prep(const double* __restrict__ q64, int B, int D, int Dp, __half* __restrict__ q16,
-                          double* __restrict__ qscale) {
+__global__ void __launch_bounds__(256) k_tc_prep(const double* __restrict__ q64, int B, int D, int Dp,
+                                                  __half* __restrict__ q16, double* __restrict__ qscale) {
   // the pair scan (launched as a programmatic dependent) may start its prologue now
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  __shared__ double red[32];
-  const int b = blockIdx.x;
+  // one warp per query row: all of the row's loads in flight at once, a warp reduction
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const double* src = q64 + (size_t)b * Dp;
   double a = 0.0;
   if (b < B)
-    for (int i = threadIdx.x; i < D; i += blockDim.x) {
-      const double x = q64[(size_t)b * Dp + i];
-      a += x * x;
+    for (int i = lane; i < D; i += 32) {
+      const double x = src[i];
+      a = fma(x, x, a);
     }
 #pragma unroll
   for (int off = 16; off; off >>= 1) a += __shfl_xor_sync(FULL, a, off);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    red[0] = sqrt(t);
-  }
-  __syncthreads();
-  const double n = red[0];
+  const double n = sqrt(a);
   const bool ok = b < B && n > 0.0 && isfinite(n);
   const double inv = ok ? 1.0 / n : 0.0;
-  for (int i = threadIdx.x; i < Dp; i += blockDim.x)
-    q16[(size_t)b * Dp + i] = __double2half(ok && i < D ? q64[(size_t)b * Dp + i] * inv : 0.0);
-  if (threadIdx.x == 0 && b < B) qscale[b] = ok ? n : 0.0;
+  for (int i = 2 * lane; i < Dp; i += 64) {  // Dp is a multiple of 64
+    const double x0 = ok && i < D ? src[i] * inv : 0.0;
+    const double x1 = ok && i + 1 < D ? src[i + 1] * inv : 0.0;
+    *reinterpret_cast<__half2*>(q16 + (size_t)b * Dp + i) = __halves2half2(__double2half(x0), __double2half(x1));
+  }
+  if (lane == 0 && b < B) qscale[b] = ok ? n : 0.0;
 }
 
 // ---------------------------------------------------------------- host side
@@ -988,7 +987,7 @@ cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const Rin
   const int groups = tc_chunks(p, B);
   if (groups < 1 || groups > part.n_chunks) return cudaErrorInvalidValue;
   const int rows = nm * (p->pair ? 256 : TC_BM);
-  k_tc_prep<<<rows, 128, 0, s>>>(q64, B, D, p->Dp, p->q16, p->qscale);
+  k_tc_prep<<<(rows + 7) / 8, 256, 0, s>>>(q64, B, D, p->Dp, p->q16, p->qscale);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const float margin = tc_margin(p->Dp);
