@@ -293,10 +293,11 @@ def _paths(cache, Q, table):
 
 
 @pytest.mark.parametrize("dim,cap,n_ins,B", [(768, 20_000, 20_000, 300), (1024, 4096, 4096, 256),
-                                             (64, 300, 1000, 7), (200, 1000, 650, 129)])
+                                             (64, 300, 1000, 7), (200, 1000, 650, 129), (200, 1000, 1300, 300)])
 def test_tensor_core_scan_matches_gemv_and_oracle(dim, cap, n_ins, B):
     """tcgen05 path (forced) vs the GEMV path vs the float64 oracle: B not a multiple of 128,
-    capacity not a multiple of the 256-slot tile, wrapped and partially filled rings."""
+    capacity not a multiple of the 256-slot tile, wrapped and partially filled rings, half-width
+    tail tiles, and batches staged in chunks (B = 300 at a padded dim 200)."""
     wl = ClusteredWorkload(dim, n_clusters=32, seed=dim + B)
     rows = wl.cache_rows(n_ins)
     c = SemanticCache(capacity=cap, dim=dim)
