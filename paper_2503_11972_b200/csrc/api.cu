@@ -98,7 +98,9 @@ struct mc_cache {
   long long* d_part_p = nullptr;
   float* d_part_floor = nullptr;
   CtaRec* d_cta = nullptr;     // [Bcap][gemv grid] per-CTA exact records (GEMV path)
-  unsigned* d_gmax = nullptr;  // [Bcap][256] running max keys of the fused scans (zero between launches)
+  unsigned* d_gmax = nullptr;  // [Bcap][256] running max keys of the fused GEMV scans (zero between launches)
+  unsigned long long* d_gmax8 = nullptr;  // [Bcap][128] epoch-tagged bound replicas of the streamed int8 scan
+  unsigned s8_epoch = 0;                  // the last streamed-scan launch's epoch
   mc_record* d_rec = nullptr;
   mc_record* d_scratch = nullptr;
   OutRec* d_out = nullptr;
@@ -220,6 +222,7 @@ void free_batch(mc_cache* h) {
   cudaFree(h->d_part_maxl);
   cudaFree(h->d_cta);
   cudaFree(h->d_gmax);
+  cudaFree(h->d_gmax8);
   cudaFree(h->d_rec);
   cudaFree(h->d_scratch);
   cudaFree(h->d_out);
@@ -231,6 +234,7 @@ void free_batch(mc_cache* h) {
   h->d_part_maxl = nullptr;
   h->d_cta = nullptr;
   h->d_gmax = nullptr;
+  h->d_gmax8 = nullptr;
   h->d_rec = nullptr;
   h->d_scratch = nullptr;
   h->d_out = nullptr;
@@ -273,6 +277,8 @@ int ensure_batch(mc_cache* h, int B) {
   // 256 words per query: the streamed scan keeps 8 replicas of its bound 128 B apart
   CU(cudaMalloc(&h->d_gmax, (size_t)cap * 256 * sizeof(unsigned)));
   CU(cudaMemsetAsync(h->d_gmax, 0, (size_t)cap * 256 * sizeof(unsigned), h->stream));
+  CU(cudaMalloc(&h->d_gmax8, (size_t)cap * 128 * sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(h->d_gmax8, 0, (size_t)cap * 128 * sizeof(unsigned long long), h->stream));
   CU(cudaMalloc(&h->d_rec, (size_t)cap * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_scratch, (size_t)cap * exact_grid(h->sm_count) * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_out, (size_t)cap * sizeof(OutRec)));
@@ -433,6 +439,16 @@ int ensure_tc(mc_cache* h, int B) {
 // describes appends already on the device that precede the scan (folded into
 // the first GEMV launch, or applied by k_append before a tensor-core scan).
 // t_mid (optional) is recorded between the scan and the standalone merge.
+// Epoch of the next streamed-scan launch (never 0: zeroed words belong to no launch).  On
+// wrap-around the bound words are cleared, so an old epoch can never outrank a new one.
+unsigned s8_epoch(mc_cache* h) {
+  if (++h->s8_epoch == 0) {
+    cudaMemsetAsync(h->d_gmax8, 0, (size_t)h->Bcap * 128 * sizeof(unsigned long long), h->stream);
+    h->s8_epoch = 1;
+  }
+  return h->s8_epoch;
+}
+
 int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
                const QPrep* prep, const int8_t* q8, cudaEvent_t t_mid = nullptr, unsigned* done_seq = nullptr,
                unsigned seq = 0, uint4* outp = nullptr) {
@@ -483,7 +499,7 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
     const int nb = std::min(4, B - b0);
     if (s8)
       CU(launch_stream8_scan(h->s8, rbufs(h), st, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0, h->sm_count, h->shard,
-                             h->d_counter, h->d_gmax, h->thr, rec, out, a, prep + b0, q8 + (size_t)b0 * h->Dp,
+                             h->d_counter, h->d_gmax8, s8_epoch(h), h->thr, rec, out, a, prep + b0, q8 + (size_t)b0 * h->Dp,
                              b0 + nb == B ? done_seq : nullptr, seq, outp, h->stream));
     else if (int8)
       CU(launch_gemv8_scan(rbufs(h), st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
@@ -543,7 +559,8 @@ int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool
     memset(h->h_outp, 0, sizeof(uint4));
     *q = nullptr;
     CU(launch_stream8_direct(h->s8, rbufs(h), st, h->D, queries, stage_row, h->d_cta, h->sm_count, h->shard,
-                             h->d_counter, h->d_gmax, h->thr, h->d_rec, nullptr, h->d_state, nullptr, seq_tag(seq),
+                             h->d_counter, h->d_gmax8, s8_epoch(h), h->thr, h->d_rec, nullptr, h->d_state, nullptr,
+                             seq_tag(seq),
                              h->d_outp, quantize_query, h->stream));
     h->stats[5]++;
     h->stats[7]++;

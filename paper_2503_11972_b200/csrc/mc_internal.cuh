@@ -129,14 +129,16 @@ bool stream8_supported(int Dp);
 // One query (and <= 1 pending row, host pointers) carried in the kernel parameter block.
 cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const RingState& st, int D, const double* q64,
                                   const double* stage_row, CtaRec* cta, int grid, ShardMap sm, unsigned* counter,
-                                  unsigned* gmax, const Thresholds& thr, mc_record* rec, OutRec* out,
+                                  unsigned long long* gmax, unsigned epoch, const Thresholds& thr, mc_record* rec,
+                                  OutRec* out,
                                   RingState* d_state, unsigned* done_seq, unsigned seq, uint4* outp,
                                   void (*quantise)(const double*, int, int, QPrep*, int8_t*), cudaStream_t s);
 S8Plan* s8_plan_create(int8_t* ring8, float2* ringq, long long C, int Dp, int P8, char* err, int errlen);
 void s8_plan_destroy(S8Plan* p);
 cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingState& st, const double* q64, int nb,
-                                CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
-                                const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
+                                CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter,
+                                unsigned long long* gmax, unsigned epoch, const Thresholds& thr, mc_record* rec,
+                                OutRec* out, const GemvAppendArgs& app,
                                 const QPrep* prep, const int8_t* q8, unsigned* done_seq, unsigned seq,
                                 uint4* outp, cudaStream_t s);
 

@@ -57,7 +57,7 @@ constexpr int S8_CW = 8;                       // consumer warps (max)
 constexpr int S8_THREADS = (S8_CW + 4) * 32;   // producer + consumers + rescorer + bound poller + eager rescorer
 constexpr int S8_EAGER = S8_CW + 1;            // S.best slot of the eager rescorer
 constexpr int S8_QCAP = 128;                   // candidate queue entries per consumer warp
-constexpr int S8_GSTRIDE = 256;                // gmax words per query: S8_GREP replicas, 128 B apart
+constexpr int S8_GSTRIDE = 128;                // gmax u64 words per query: S8_GREP replicas, 128 B apart
 constexpr int S8_GREP = 8;                     // replicas of the global bound (spreads the hot line)
 // Only the poller warp touches the global bound: a fence, an acquire/release
 // or a bar.sync waits for the warp's outstanding global operations, and a
@@ -94,9 +94,9 @@ __device__ __forceinline__ void st_rel_cta(int* p, int v) {
   asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned ld_vol_u32(const unsigned* p) { return *(const volatile unsigned*)p; }
-__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ unsigned long long s8_timer() {
@@ -107,7 +107,11 @@ __device__ __forceinline__ unsigned long long s8_timer() {
 
 struct S8Args {
   unsigned* counter;           // last-CTA ticket (zero between launches)
-  unsigned* gmax;              // [(b0 + b) * S8_GSTRIDE + 32 r] global lower-bound key replicas (zero between launches)
+  // [(b0 + b) * S8_GSTRIDE + 16 r] global lower-bound replicas: (epoch << 32) | key.  A value
+  // from an earlier launch's epoch is smaller than any of this launch's and is ignored when
+  // read, so the words are never reset (a late atomic of a finished launch cannot leak into
+  // the next one).
+  unsigned long long* gmax;
   Thresholds thr;
   mc_record* rec;
   OutRec* out;
@@ -120,6 +124,7 @@ struct S8Args {
   unsigned* done_seq;          // optional (host-mapped): set to `seq` after `out` is written (zero-copy result)
   unsigned seq;
   uint4* outp;                 // optional (host-mapped): packed decisions, one 16-byte store each (see below)
+  unsigned epoch;              // this launch's tag on the gmax words (never 0)
 };
 
 // The single-query launch's inputs carried in the kernel parameter block (a
@@ -510,7 +515,6 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
                      : "memory");
       }
     }
-    if (lane < S8_GREP) a.gmax[(size_t)gb * S8_GSTRIDE + 32 * lane] = 0u;
   }
   __syncwarp();
   if (lane == 0) {
@@ -606,7 +610,7 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
 
   const int ncw = min(nst, S8_CW);
   const S8Ctx x{rb, st, sm, sq64, Dp, nb, ncw, timing};
-  unsigned* const gq = a.gmax + (size_t)b0 * S8_GSTRIDE;  // this launch's queries
+  unsigned long long* const gq = a.gmax + (size_t)b0 * S8_GSTRIDE;  // this launch's queries
 
   if (warp == S8_CW + 3) {
     // ------------------------------------------------------------ eager rescorer
@@ -671,13 +675,16 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     for (int b = 0; b < NBQ; ++b) pub[b] = 0u;
     while (*(volatile int*)&S.pool_done < S8_CW + 2) {
       unsigned gk = 0;
-      if (lane >= S8_PUB0 && lane - S8_PUB0 < nb)
-        gk = ld_relaxed_gpu(gq + (lane - S8_PUB0) * S8_GSTRIDE + 32 * (blockIdx.x % S8_GREP));
+      if (lane >= S8_PUB0 && lane - S8_PUB0 < nb) {
+        const unsigned long long g = ld_relaxed_gpu(gq + (lane - S8_PUB0) * S8_GSTRIDE + 16 * (blockIdx.x % S8_GREP));
+        gk = (unsigned)(g >> 32) == a.epoch ? (unsigned)g : 0u;
+      }
 #pragma unroll
       for (int b = 0; b < NBQ; ++b) {
         const unsigned mine = ld_vol_u32(&S.bound[b]);
         if (b < nb && mine > pub[b]) {
-          if (lane >= S8_PUB0) atomicMax(gq + b * S8_GSTRIDE + 32 * (lane - S8_PUB0), mine);
+          if (lane >= S8_PUB0)
+            atomicMax(gq + b * S8_GSTRIDE + 16 * (lane - S8_PUB0), ((unsigned long long)a.epoch << 32) | mine);
           pub[b] = mine;
         }
       }
@@ -963,7 +970,8 @@ size_t s8_in_bytes() { return sizeof(S8In); }
 // quantisation is done here into the block.
 cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const RingState& st, int D, const double* q64,
                                   const double* stage_row, CtaRec* cta, int grid, ShardMap sm, unsigned* counter,
-                                  unsigned* gmax, const Thresholds& thr, mc_record* rec, OutRec* out,
+                                  unsigned long long* gmax, unsigned epoch, const Thresholds& thr, mc_record* rec,
+                                  OutRec* out,
                                   RingState* d_state, unsigned* done_seq, unsigned seq, uint4* outp,
                                   void (*quantise)(const double*, int, int, QPrep*, int8_t*), cudaStream_t s) {
   if (!p || p->Dp > 1024) return cudaErrorInvalidValue;
@@ -976,7 +984,7 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
     memcpy(in.stage, stage_row, (size_t)Dp * sizeof(double));  // staged rows are already zero-padded to Dp
   }
   S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), nullptr, nullptr, nullptr, stage_row ? 1 : 0, d_state,
-           done_seq, seq, outp};
+           done_seq, seq, outp, epoch};
   switch (p->P8 / 128) {
     case 1: return s8_launch_in<1>(p, rb, st, cta, grid, sm, a, in, s);
     case 2: return s8_launch_in<2>(p, rb, st, cta, grid, sm, a, in, s);
@@ -991,13 +999,13 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
 }
 
 cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingState& st, const double* q64, int nb,
-                                CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
-                                const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
+                                CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter,
+                                unsigned long long* gmax, unsigned epoch, const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
                                 const QPrep* prep, const int8_t* q8, unsigned* done_seq, unsigned seq,
                                 uint4* outp, cudaStream_t s) {
   if (!p || nb < 1 || nb > 4) return cudaErrorInvalidValue;
   S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), prep, q8, app.stage, app.n, app.d_state, done_seq, seq,
-           outp};
+           outp, epoch};
   switch (p->P8 / 128) {
     case 1: return s8_launch<1>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
     case 2: return s8_launch<2>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
