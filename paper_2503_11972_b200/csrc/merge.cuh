@@ -109,9 +109,29 @@ static __device__ mc_record merge_one(const RingState& st, const double* __restr
   const bool exotic = !(n1 <= 1e30) || !(n2 >= 1e-30);
   const double delta = eps_rel * n2 + eps_a1 * n1;
 
+  // One pass over the lists (and the floors) into registers: the max, the compaction and
+  // the certificate below reuse them instead of re-reading global memory.
   const int ne = n_chunks * KP;
+  constexpr int PER = 4;  // entries per thread kept in registers; longer lists re-read the rest
+  float es[PER];
+  long long ep[PER];
   float m = -INFINITY;
-  for (int e = threadIdx.x; e < ne; e += blockDim.x)
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int e = threadIdx.x + k * (int)blockDim.x;
+    es[k] = -INFINITY;
+    ep[k] = -1;
+    if (e < ne) {
+      ep[k] = pp[e];
+      es[k] = ps[e];
+    }
+  }
+  float fmx = -INFINITY;  // largest finite-or-inf floor of this thread's chunks (fmaxf skips NaN)
+  for (int c = threadIdx.x; c < n_chunks; c += blockDim.x) fmx = fmaxf(fmx, pf[c]);
+#pragma unroll
+  for (int k = 0; k < PER; ++k)
+    if (ep[k] >= 0) m = fmaxf(m, es[k]);
+  for (int e = threadIdx.x + PER * (int)blockDim.x; e < ne; e += blockDim.x)
     if (pp[e] >= 0) m = fmaxf(m, ps[e]);
   m = block_max(m, ms.shf);
   const double M = (double)m * scale;
@@ -123,16 +143,18 @@ static __device__ mc_record merge_one(const RingState& st, const double* __restr
     ms.fail = 0;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
-    const long long p = pp[e];
-    if (p >= 0 && (double)ps[e] * scale >= thr) {
+  auto admit = [&](long long p, float sc) {
+    if (p >= 0 && (double)sc * scale >= thr) {
       const int i = atomicAdd(&ms.n_cand, 1);
       if (i < MERGE_CAND)
         ms.cand[i] = p;
       else
         ms.fail = 1;
     }
-  }
+  };
+#pragma unroll
+  for (int k = 0; k < PER; ++k) admit(ep[k], es[k]);
+  for (int e = threadIdx.x + PER * (int)blockDim.x; e < ne; e += blockDim.x) admit(pp[e], ps[e]);
   __syncthreads();
   // ... then one warp per candidate computes its float64 similarity.
   const int n_cand = min(ms.n_cand, MERGE_CAND);
@@ -145,12 +167,8 @@ static __device__ mc_record merge_one(const RingState& st, const double* __restr
   }
   best = block_best(best, ms.shb, true);
 
-  int fail = 0;
-  for (int c = threadIdx.x; c < n_chunks; c += blockDim.x) {
-    const float f = pf[c];
-    if (f > -INFINITY && !((double)f * scale + delta < best.s)) fail = 1;
-  }
-  if (fail) atomicOr(&ms.fail, 1);
+  // every chunk's floor must lie below the best (monotone in the floor: test the largest)
+  if (fmx > -INFINITY && !((double)fmx * scale + delta < best.s)) atomicOr(&ms.fail, 1);
   __syncthreads();
   mc_record r;
   r.sim = best.s;
