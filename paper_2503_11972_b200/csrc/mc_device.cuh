@@ -144,13 +144,19 @@ static __device__ __noinline__ float write_row_all(const double* __restrict__ sr
   amax = warp_max_d(amax);
   l1 = warp_sum_d(l1);
   const float s = int8_scale(amax);
+  // row pointers in registers: through the reference every store below could alias rb,
+  // and the compiler would reload its fields from the caller's stack each iteration
+  double* const d64 = rb.r64 + (size_t)slot * Dp;
+  __half* const d16 = rb.r16 + (size_t)slot * Dp;
+  int8_t* const d8 = rb.r8 + (size_t)slot * rb.p8;
+  float2* const dq = rb.rq + slot;
   for (int i = lane; i < Dp; i += 32) {
     const double v = src[i];
-    rb.r64[(size_t)slot * Dp + i] = v;
-    rb.r16[(size_t)slot * Dp + i] = __double2half(v);
-    rb.r8[(size_t)slot * rb.p8 + i] = int8_quant(v, s);
+    d64[i] = v;
+    d16[i] = __double2half(v);
+    d8[i] = int8_quant(v, s);
   }
-  if (lane == 0) rb.rq[slot] = make_float2(s, __double2float_ru(l1 * (1.0 + 1e-12)));
+  if (lane == 0) *dq = make_float2(s, __double2float_ru(l1 * (1.0 + 1e-12)));
   return s;
 }
 
