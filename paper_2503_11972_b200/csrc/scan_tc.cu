@@ -159,16 +159,45 @@ struct TopK {
     runmax = fmaxf(runmax, cmax);
     const float thr = fmaxf(mn, runmax - margin);
     if (cmax > thr) {  // a new or near maximum in this chunk
+      // Elements at or below the chunk-start threshold can never be admitted (the
+      // threshold only rises as pushes raise mn): fold them into drop at once, and walk
+      // only the others, in slot order, through the sequential admission test.  Each lane
+      // loops over its own few candidates instead of the warp predicating all 32 pushes.
+      unsigned mask = 0;
+      float dr = -INFINITY;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        if (v[j] > fmaxf(mn, runmax - margin))
-          push(v[j], slot0 + j);
+        if (v[j] > thr)
+          mask |= 1u << j;
         else
-          drop = fmaxf(drop, v[j]);
+          dr = fmaxf(dr, v[j]);
+      }
+      drop = fmaxf(drop, dr);
+      while (mask) {
+        const int j = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const float x = pick32(v, j);
+        if (x > fmaxf(mn, runmax - margin))
+          push(x, slot0 + j);
+        else
+          drop = fmaxf(drop, x);
       }
     } else {
       drop = fmaxf(drop, cmax);
     }
+  }
+  // v[j] for a runtime j without local memory: a select tree on the bits of j.
+  static __device__ __forceinline__ float pick32(const float (&v)[32], int j) {
+    float a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = (j & 2) ? a[2 * i + 1] : a[2 * i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = (j & 4) ? a[2 * i + 1] : a[2 * i];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) a[i] = (j & 8) ? a[2 * i + 1] : a[2 * i];
+    return (j & 16) ? a[1] : a[0];
   }
 };
 
