@@ -154,7 +154,7 @@ int mc_profile_rotate(mc_cache* const* hs, int32_t nh, const double* queries, co
  * lookup: reads (reset = 0) or resets (reset = 1) eight globaltimer stamps of the
  * last small-batch launch(es): [0] first CTA start, [1] last scan end, [2] last
  * rescoring end, [3] tail end, [4] merge start and [5] records loaded (streamed
- * int8 scan only), [6..7] reserved (ns).  Not needed by the drop-in; used by
+ * int8 scan only), [6] merge reductions done and [7] decision stored (streamed int8 scan only) (ns).  Not needed by the drop-in; used by
  * scripts/profile_case.py. */
 int mc_debug_gemv_timing(unsigned long long* out8, int reset);
 

@@ -497,6 +497,7 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
     }
     if (neq >= 2) s2 = bs;
     const bool exo = __shfl_sync(FULL, exotic, b) != 0;
+    if (b == 0 && lane == 0 && x.timing) a.timing[6] = s8_timer();
     if (lane == 0) {
       const bool fail = bp < 0 || !(ov == -INFINITY || (double)ov + 1e-9 < bs);
       mc_record r;
@@ -514,6 +515,7 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
                      "r"(v.w)
                      : "memory");
       }
+      if (b == 0 && x.timing) a.timing[7] = s8_timer();
     }
   }
   __syncwarp();

@@ -62,6 +62,9 @@ if os.environ.get("MC_GEMV_TIMING"):
               " | pushed %d rescored %d" % (rel(scan_end.max()), rel(rec.max()), (t[4] - rec.max()) / 1e3,
                                              (t[5] - t[4]) / 1e3, (t[3] - t[5]) / 1e3, rel(t[3]),
                                              arr[:, 6].sum(), arr[:, 7].sum()))
+        if t[6] and t[7]:
+            print("   tail detail (us): reductions %.2f | record+decide+result store %.2f | rest %.2f" % (
+                (t[6] - t[5]) / 1e3, (t[7] - t[6]) / 1e3, (t[3] - t[7]) / 1e3))
         if i == a.iters - 1:
             order = _np.argsort(-rec)
             cyc = _np.array(per[8 * 512:8 * 512 + 4 * 148], dtype=_np.float64).reshape(148, 4)
