@@ -765,6 +765,8 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
     if (!h->s8) return cleanup(fail(MC_ERR_CUDA, "int8 stream scan plan: %s", err));
   }
   if (const char* e = getenv("MC_PACKED_RESULT")) h->packed = atoi(e) != 0;
+  // testing hook: start the streamed scan's bound epochs near the 32-bit wrap-around
+  if (const char* e = getenv("MC_S8_EPOCH0")) h->s8_epoch = (unsigned)strtoul(e, nullptr, 0);
   if (const char* e = getenv("MC_PARAM_INPUT")) h->param_in = atoi(e) != 0;
   CUC(cudaMallocHost(&h->h_qkeep, (size_t)h->Dp * sizeof(double)));
   memset(h->h_qkeep, 0, (size_t)h->Dp * sizeof(double));

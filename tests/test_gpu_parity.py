@@ -550,3 +550,21 @@ def test_random_operation_sequences_every_path(seed):
                 assert r.k == k and _close(r.similarity, sim), (seed, step, r, sim)
     assert len(c) == len(o.meta) == len(c.ring)
     c.close()
+
+
+def test_stream8_bound_epochs_across_the_32bit_wrap(monkeypatch):
+    """The streamed scan tags its global-bound words with a per-launch epoch and never resets them.
+    Starting the epochs just below 2^32 runs lookups across the wrap-around (the words are cleared
+    there); every answer must still equal the float64 oracle's."""
+    monkeypatch.setenv("MC_S8_EPOCH0", str(2**32 - 6))
+    wl = ClusteredWorkload(768, n_clusters=16, seed=4321)
+    cap = 5000
+    rows = wl.cache_rows(cap)
+    c = SemanticCache(capacity=cap, dim=768)
+    c.bulk_load(CacheEntry(f"e{i}", v, "large", i, 0.0) for i, v in enumerate(rows))
+    c.ring.set_path(_native.PATH_STREAM8)
+    table = ThresholdTable.default()
+    Q = wl.queries(24)
+    for i in range(0, 24, 2):  # 12 batch-2 launches: epochs 2^32-5 .. 2^32-1, then 1, 2, ...
+        _check_against_scan(c, rows, Q[i:i + 2], table, f"epoch wrap {i}")
+    c.close()
