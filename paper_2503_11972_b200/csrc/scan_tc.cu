@@ -381,7 +381,11 @@ constexpr int TP_SMEM = TP_STAGES * (TP_A_BYTES + TP_B_BYTES) + 1024 + 256;
 // with the MMAs; the column halves' lists meet in shared memory at the end.
 constexpr int TP_THREADS = 320;
 constexpr int TP_X_BYTES = 128 * (2 * KP + 1) * 4;  // half 1's lists: s[KP], slot[KP], drop per query row
-constexpr int TP_SMEM_PAIR = TP_SMEM + TP_X_BYTES;
+// Pair kernel stages: TQ_SUB 64-wide K blocks per stage (fewer barrier round trips per tile),
+// TQ_STAGES deep; TQ_SUB x TQ_STAGES = 6 keeps the bytes in flight of the original 6 x 1.
+constexpr int TQ_SUB = 2;
+constexpr int TQ_STAGES = 3;
+constexpr int TP_SMEM_PAIR = TQ_STAGES * TQ_SUB * (TP_A_BYTES + TP_B_BYTES) + 1024 + 256 + TP_X_BYTES;
 
 
 
@@ -408,11 +412,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
-  uint8_t* smB = smem + TP_STAGES * TP_A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + TP_STAGES * TP_B_BYTES);
+  uint8_t* smB = smem + TQ_STAGES * TQ_SUB * TP_A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + TQ_STAGES * TQ_SUB * TP_B_BYTES);
   uint64_t* full = bars;                   // [S]  leader only: TMA bytes of both CTAs
-  uint64_t* empty = bars + TP_STAGES;      // [S]  MMA commit, multicast to both CTAs
-  uint64_t* tfull = bars + 2 * TP_STAGES;  // [2]  MMA commit, multicast to both CTAs
+  uint64_t* empty = bars + TQ_STAGES;      // [S]  MMA commit, multicast to both CTAs
+  uint64_t* tfull = bars + 2 * TQ_STAGES;  // [2]  MMA commit, multicast to both CTAs
   uint64_t* tempty = tfull + 2;            // [2]  leader only: 4 epilogue warps x 2 CTAs
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -433,6 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
   const bool split = n_rem > 0 && 2 * n_rem <= n_groups && !(dbg & 128);
   const int n_full = split ? n_rounds : (win.n_live > group ? (win.n_live - group + n_groups - 1) / n_groups : 0);
   const int n_units = n_full + ((split && group < 2 * n_rem) ? 1 : 0);
+  const int n_kg = (n_kb + TQ_SUB - 1) / TQ_SUB;  // stages per unit
   // unit u -> physical tile t and half (-1: the whole 256-slot tile)
   auto unit = [&](int u, int& t, int& hsel) {
     if (u < n_full) {
@@ -448,7 +453,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&q_map)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map_q)) : "memory");
-    for (int i = 0; i < TP_STAGES; ++i) {
+    for (int i = 0; i < TQ_STAGES; ++i) {
       mbar_init(&full[i], 2);
       mbar_init(&empty[i], 1);
     }
@@ -486,25 +491,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
       int t, hsel;
       unit(u, t, hsel);
       const int bbytes = hsel < 0 ? TP_B_BYTES : TP_B_BYTES / 2;
-      for (int kb = 0; kb < n_kb; ++kb) {
+      for (int kg = 0; kg < n_kg; ++kg) {
+        const int ns = min(TQ_SUB, n_kb - kg * TQ_SUB);
         mbar_wait2(&empty[stage], phase ^ 1, dbg & 16);
         if (lane == 0) {
           if (rank == 0)
-            mbar_expect_tx(&full[stage], (dbg & 1) ? 0 : 2 * (TP_A_BYTES + bbytes));
+            mbar_expect_tx(&full[stage], (dbg & 1) ? 0 : 2 * ns * (TP_A_BYTES + bbytes));
           else
             mbar_arrive_remote(leader_full0 + stage * 8);
-          if (!(dbg & 1)) {
-            tma_load_2d_pair(smA + stage * TP_A_BYTES, &q_map, &full[stage], kb * TC_BK, m_pair * 256 + rank * 128);
-            if (hsel < 0)
-              tma_load_2d_pair(smB + stage * TP_B_BYTES, &ring_map, &full[stage], kb * TC_BK,
-                               ((dbg & 8) ? (t & 7) : t) * TC_BN + rank * 128);
-            else  // this CTA's 64 slots of the half tile
-              tma_load_2d_pair(smB + stage * TP_B_BYTES, &ring_map_q, &full[stage], kb * TC_BK,
-                               t * TC_BN + hsel * 128 + rank * 64);
-          }
+          if (!(dbg & 1))
+            for (int sb = 0; sb < ns; ++sb) {
+              const int kb = kg * TQ_SUB + sb;
+              uint8_t* da = smA + (stage * TQ_SUB + sb) * TP_A_BYTES;
+              uint8_t* db = smB + (stage * TQ_SUB + sb) * TP_B_BYTES;
+              tma_load_2d_pair(da, &q_map, &full[stage], kb * TC_BK, m_pair * 256 + rank * 128);
+              if (hsel < 0)
+                tma_load_2d_pair(db, &ring_map, &full[stage], kb * TC_BK, ((dbg & 8) ? (t & 7) : t) * TC_BN + rank * 128);
+              else  // this CTA's 64 slots of the half tile
+                tma_load_2d_pair(db, &ring_map_q, &full[stage], kb * TC_BK, t * TC_BN + hsel * 128 + rank * 64);
+            }
         }
         __syncwarp();
-        if (++stage == TP_STAGES) {
+        if (++stage == TQ_STAGES) {
           stage = 0;
           phase ^= 1;
         }
@@ -526,16 +534,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
         mbar_wait2(&tempty[acc], acc_phase ^ 1, dbg & 16);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TC_BN);
-        for (int kb = 0; kb < n_kb; ++kb) {
+        for (int kg = 0; kg < n_kg; ++kg) {
+          const int ns = min(TQ_SUB, n_kb - kg * TQ_SUB);
           mbar_wait2(&full[stage], phase, dbg & 16);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t a0 = smem_u32(smA + stage * TP_A_BYTES);
-            const uint32_t b0 = smem_u32(smB + stage * TP_B_BYTES);
+            for (int sb = 0; sb < ns; ++sb) {
+              const int kb = kg * TQ_SUB + sb;
+              const uint32_t a0 = smem_u32(smA + (stage * TQ_SUB + sb) * TP_A_BYTES);
+              const uint32_t b0 = smem_u32(smB + (stage * TQ_SUB + sb) * TP_B_BYTES);
 #pragma unroll
-            for (int k = 0; k < TC_BK / TC_UK; ++k)
-              if (!(dbg & 2)) umma_f16_pair(d_tmem, umma_desc_sw128(a0 + k * TC_UK * 2), umma_desc_sw128(b0 + k * TC_UK * 2), idesc,
-                            (kb | k) != 0);
+              for (int k = 0; k < TC_BK / TC_UK; ++k)
+                if (!(dbg & 2))
+                  umma_f16_pair(d_tmem, umma_desc_sw128(a0 + k * TC_UK * 2), umma_desc_sw128(b0 + k * TC_UK * 2),
+                                idesc, (kb | k) != 0);
+            }
             if (dbg & 32) {  // bisection only (valid with dbg & 2): plain arrives instead of the commit
               mbar_arrive(&empty[stage]);
               mbar_arrive_remote(mapa_shared(smem_u32(&empty[stage]), 1));
@@ -544,7 +557,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
             }
           }
           __syncwarp();
-          if (++stage == TP_STAGES) {
+          if (++stage == TQ_STAGES) {
             stage = 0;
             phase ^= 1;
           }
