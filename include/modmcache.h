@@ -45,15 +45,14 @@ extern "C" {
  * fp16 GEMV; B >= 5 -> the fp16 tcgen05 scan on CTA pairs).  Every path
  * returns the same certified answers. */
 #define MC_PATH_AUTO 0
-#define MC_PATH_GEMV 1 /* CUDA-core fp16 GEMV scan, register top-K' (cross-checks) */
+#define MC_PATH_GEMV 1 /* CUDA-core fp16 GEMV scan, register top-K' (AUTO's small-batch path when Dp > 1024;
+                          a cross-check elsewhere) */
 #define MC_PATH_GEMM 2 /* tcgen05/TMEM/TMA fp16 scan on CTA pairs (cta_group::2), fused top-K' epilogue */
-#define MC_PATH_GEMM_1SM 3 /* same scan on single CTAs (cta_group::1), kept for cross-checks */
-#define MC_PATH_GEMM_QUAD 4 /* 4-CTA clusters multicasting the query operand (cross-checks) */
-#define MC_PATH_GEMV8 5 /* int8 dp4a register-streaming GEMV scan with per-row bounds (cross-checks) */
+/* 3, 4, 5 and 7 named round-1 cross-check scans (single-CTA and 4-CTA tensor-core scans, the
+ * register-streamed int8 GEMV, the int8 tensor-core scan); they were removed, and
+ * mc_set_path rejects them with MC_ERR_ARG. */
 #define MC_PATH_STREAM8 6 /* int8 scan streamed by TMA bulk copies, lane-per-row dp4a, float64 rescoring
                              pool (AUTO's choice for B <= 4 when Dp <= 1024) */
-#define MC_PATH_GEMM8 7 /* tcgen05 kind::i8 scan on CTA pairs over the int8 ring, per-row certified
-                           bounds + float64 merge (cross-check; AUTO keeps the fp16 scan for B >= 5) */
 
 typedef struct mc_cache mc_cache;
 
@@ -97,6 +96,28 @@ int64_t mc_size(const mc_cache* h);
  *   out_flags MC_FLAG_* bits; MC_FLAG_HIT decides hit/miss. */
 int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* out_live,
                       double* out_sim, int32_t* out_k, uint32_t* out_flags);
+
+/* The full serving decision of one lookup, written by the device's decision
+ * epilogue (SURVEY.md §8 a1 + f3): the reference's answer (cache.py:255-260)
+ * plus what its callers derive from it. */
+typedef struct mc_decision {
+  int64_t live;   /* live index of the best entry (0 = oldest), -1 if the cache is empty */
+  double sim;     /* best float64 similarity (NaN if empty) */
+  double sigma;   /* noise re-entry level schedule[k] on a hit (cache.py:325-334); NaN on a miss,
+                     without a schedule (mc_set_sigma_schedule) or when k lies past it */
+  int32_t k;      /* select_k (cache.py:112-117), 0 = none */
+  int32_t steps;  /* denoising steps to run: total_steps - k on a hit, total_steps on a miss
+                     (engine.py:38-45 service_time) */
+  uint32_t flags; /* MC_FLAG_*; MC_FLAG_HIT decides the route */
+  int32_t route;  /* 1 = hit queue (cached-image refinement), 0 = miss queue (scheduler.py:80-89) */
+} mc_decision;
+
+/* mc_retrieve_batch returning the full decision per query (out: B mc_decisions). */
+int mc_retrieve_decisions(mc_cache* h, const double* queries, int32_t B, mc_decision* out);
+
+/* The sigma schedule over timesteps 0..T (n = T + 1 values; linear_sigma_schedule,
+ * cache.py:305-309; the host validates it with validate_sigma_schedule).  n = 0 clears it. */
+int mc_set_sigma_schedule(mc_cache* h, const double* schedule, int32_t n);
 
 /* Asynchronous form of mc_retrieve_batch (the serving loop's overlap of host
  * work with the scan): submit enqueues the lookup against the current cache

@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 from pathlib import Path
 
 import numpy as np
@@ -22,15 +23,19 @@ MC_FLAG_NEAR_TAU = 0x10
 MC_FLAG_FALLBACK = 0x20
 MC_FLAG_NONFINITE = 0x40
 
-PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_GEMM_1SM, PATH_GEMM_QUAD, PATH_GEMV8, PATH_STREAM8, PATH_GEMM8 = 0, 1, 2, 3, 4, 5, 6, 7
+PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_STREAM8 = 0, 1, 2, 6
 
 RECORD_DTYPE = np.dtype([("sim", "<f8"), ("second", "<f8"), ("pos", "<i8"), ("flags", "<u4"), ("reserved", "<i4")])
+# struct mc_decision (include/modmcache.h)
+DECISION_DTYPE = np.dtype([("live", "<i8"), ("similarity", "<f8"), ("sigma", "<f8"), ("k", "<i4"), ("steps", "<i4"),
+                           ("flags", "<u4"), ("route", "<i4")])
 
 EXPORTED = (
     "mc_create", "mc_destroy", "mc_set_thresholds", "mc_append", "mc_evict_front", "mc_size",
     "mc_retrieve_batch", "mc_set_path", "mc_configure_shard", "mc_retrieve_local_async",
     "mc_merge_records", "mc_stats", "mc_last_error", "mc_version", "mc_profile_steps", "mc_profile_rotate",
     "mc_debug_gemv_timing", "mc_retrieve_submit", "mc_retrieve_wait", "mc_debug_read_row",
+    "mc_retrieve_decisions", "mc_set_sigma_schedule",
 )
 
 
@@ -62,6 +67,8 @@ def _declare(lib):
     lib.mc_debug_read_row.argtypes = [vp, i64, dp]
     lib.mc_retrieve_wait.argtypes = [vp, C.c_uint32, dp, dp, dp, dp]
     lib.mc_debug_gemv_timing.argtypes = [dp, i32]
+    lib.mc_retrieve_decisions.argtypes = [vp, dp, i32, dp]
+    lib.mc_set_sigma_schedule.argtypes = [vp, dp, i32]
     lib.mc_last_error.restype = C.c_char_p
     lib.mc_version.restype = C.c_char_p
     return lib
@@ -119,6 +126,11 @@ class DeviceRing:
         self._bcap = 0
         self._ensure_out(1)
         self._table_key = None
+        # The query / result buffers below are shared by every call on this ring, and ctypes
+        # releases the GIL during the native call: one lock spans each buffer write -> native
+        # call -> copy-out, so concurrent readers ("many readers or one writer", cache.py:144)
+        # never see each other's queries or answers.
+        self._lock = threading.Lock()
 
     # -- lifecycle -----------------------------------------------------------
     def close(self) -> None:
@@ -141,6 +153,23 @@ class DeviceRing:
         taus = np.array([t for _, t in pairs], dtype=np.float64)
         _check(self.lib, self.lib.mc_set_thresholds(self._h, _ptr(ks), _ptr(taus), len(ks), int(total_steps)))
         self._table_key = key
+
+    def set_sigma_schedule(self, schedule) -> None:
+        """sigma over timesteps 0..T for the decision epilogue (None clears it)."""
+        key = None if schedule is None else np.asarray(schedule, dtype=np.float64).tobytes()
+        if key == getattr(self, "_sched_key", None):
+            return
+        s = np.zeros(0) if schedule is None else np.ascontiguousarray(schedule, dtype=np.float64)
+        _check(self.lib, self.lib.mc_set_sigma_schedule(self._h, _ptr(s) if s.size else None, int(s.size)))
+        self._sched_key = key
+
+    def decisions(self, Q: np.ndarray) -> np.ndarray:
+        """Q: float64 [B, dim] -> B serving decisions (DECISION_DTYPE), from the device epilogue."""
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        out = np.empty(Q.shape[0], dtype=DECISION_DTYPE)
+        if Q.shape[0]:
+            _check(self.lib, self.lib.mc_retrieve_decisions(self._h, _ptr(Q), Q.shape[0], _ptr(out)))
+        return out
 
     def set_path(self, path: int) -> None:
         _check(self.lib, self.lib.mc_set_path(self._h, int(path)))
@@ -184,35 +213,39 @@ class DeviceRing:
         self._bcap = cap
 
     def retrieve(self, Q: np.ndarray):
-        """Q: float64 [B, dim] -> (live[B], sim[B], k[B], flags[B]) views (valid until next call)."""
+        """Q: float64 [B, dim] -> (live[B], sim[B], k[B], flags[B]) arrays."""
         Q = np.ascontiguousarray(Q, dtype=np.float64)
         B = Q.shape[0]
-        self._ensure_out(B)
-        _check(self.lib, self.lib.mc_retrieve_batch(self._h, _ptr(Q), B, *self._out_ptrs))
-        return self._live[:B], self._sim[:B], self._k[:B], self._flags[:B]
+        with self._lock:
+            self._ensure_out(B)
+            _check(self.lib, self.lib.mc_retrieve_batch(self._h, _ptr(Q), B, *self._out_ptrs))
+            return self._live[:B].copy(), self._sim[:B].copy(), self._k[:B].copy(), self._flags[:B].copy()
 
     def retrieve1(self, q: np.ndarray):
         """One query (1-d, length dim) -> (live, sim, k, flags) as Python scalars."""
-        self._qbuf[0] = q  # copies and converts; the buffer pointer never changes
-        rc = self._retrieve(self._hv, self._qptr, 1, *self._out_ptrs)
-        if rc:
-            _check(self.lib, rc)
-        return int(self._live[0]), float(self._sim[0]), int(self._k[0]), int(self._flags[0])
+        with self._lock:
+            self._qbuf[0] = q  # copies and converts; the buffer pointer never changes
+            rc = self._retrieve(self._hv, self._qptr, 1, *self._out_ptrs)
+            if rc:
+                _check(self.lib, rc)
+            return int(self._live[0]), float(self._sim[0]), int(self._k[0]), int(self._flags[0])
 
     def submit1(self, q: np.ndarray) -> int:
         """Enqueue one lookup (mc_retrieve_submit); returns its ticket."""
-        self._qbuf[0] = q
-        rc = self._submit(self._hv, self._qptr, 1, self._ticket_ptr)
-        if rc:
-            _check(self.lib, rc)
-        return int(self._ticket[0])
+        with self._lock:
+            self._qbuf[0] = q
+            rc = self._submit(self._hv, self._qptr, 1, self._ticket_ptr)
+            if rc:
+                _check(self.lib, rc)
+            return int(self._ticket[0])
 
     def wait1(self, ticket: int):
         """The submitted lookup's (live, sim, k, flags) as Python scalars (mc_retrieve_wait)."""
-        rc = self._wait(self._hv, ticket, *self._out_ptrs)
-        if rc:
-            _check(self.lib, rc)
-        return int(self._live[0]), float(self._sim[0]), int(self._k[0]), int(self._flags[0])
+        with self._lock:
+            rc = self._wait(self._hv, ticket, *self._out_ptrs)
+            if rc:
+                _check(self.lib, rc)
+            return int(self._live[0]), float(self._sim[0]), int(self._k[0]), int(self._flags[0])
 
     def records_device(self):
         """Device that holds this ring's records (for the collective's buffers)."""
@@ -233,10 +266,11 @@ class DeviceRing:
 
     def merge_records(self, dev_records, G: int, B: int, p0: int, stream_ptr: int = 0):
         """Merge G x B gathered records (shard-major) into decisions; p0 = oldest live global position."""
-        self._ensure_out(B)
-        _check(self.lib, self.lib.mc_merge_records(
-            self._h, self._addr(dev_records), int(G), int(B), int(p0), stream_ptr or None, *self._out_ptrs))
-        return self._live[:B], self._sim[:B], self._k[:B], self._flags[:B]
+        with self._lock:
+            self._ensure_out(B)
+            _check(self.lib, self.lib.mc_merge_records(
+                self._h, self._addr(dev_records), int(G), int(B), int(p0), stream_ptr or None, *self._out_ptrs))
+            return self._live[:B].copy(), self._sim[:B].copy(), self._k[:B].copy(), self._flags[:B].copy()
 
     def profile_steps(self, Q: np.ndarray, rows: np.ndarray | None, iters: int, flush_bytes: int):
         """Device-timed steps (see mc_profile_steps). Q: [iters, B, dim]; rows: [iters, dim] or None."""

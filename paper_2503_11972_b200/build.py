@@ -11,7 +11,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libmodmcache.so"
-SOURCES = ["api.cu", "ring.cu", "scan_gemv.cu", "scan_gemv8.cu", "scan_stream8.cu", "scan_tc.cu", "scan_tc8.cu", "rescore.cu"]
+SOURCES = ["api.cu", "ring.cu", "scan_gemv.cu", "scan_stream8.cu", "scan_tc.cu", "rescore.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -106,7 +106,7 @@ struct mc_cache {
   OutRec* d_out = nullptr;
   OutRec* h_out = nullptr;  // pinned, mapped (the streamed scan writes decisions here directly)
   OutRec* d_outm = nullptr; // device view of h_out
-  uint4* h_outp = nullptr;    // pinned, mapped: packed decisions (16 B each, self-validating sequence tag)
+  uint4* h_outp = nullptr;    // pinned, mapped: packed decisions (2 x 16 B each, self-validating sequence tags)
   uint4* d_outp = nullptr;
   bool packed = true;         // packed zero-copy results (else: decisions + fence + completion word)
   unsigned* h_seq = nullptr;  // pinned, mapped: completion word of the zero-copy lookup
@@ -123,12 +123,11 @@ struct mc_cache {
   double* h_qkeep = nullptr;    // [Dp] the last parameter-block query (for an exhaustive fallback)
 
   TcPlan* tc = nullptr;           // fp16 tensor-core scan plan (MC_PATH_GEMM*), created on first use
-  Tc8Plan* tc8 = nullptr;         // int8 tensor-core scan plan (the batched default), created on first use
-  float* d_part_maxl = nullptr;   // [Bcap][chunks] of the int8 tensor-core scan
   S8Plan* s8 = nullptr;           // TMA-streamed int8 scan plan (tensor maps of ring8 / ringq)
   unsigned* d_counter = nullptr;  // last-CTA ticket of the fused GEMV scan (zero between launches)
 
   Thresholds thr{};
+  std::vector<double> sched;  // sigma schedule over timesteps 0..T (empty: none)
   int path = MC_PATH_AUTO;
   long long stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
@@ -150,6 +149,19 @@ struct DeviceGuard {
 
 RingState mirror(const mc_cache* h) { return RingState{h->head, h->count, h->jhead, h->C}; }
 
+// The answer for an empty cache (cache.py:252-253): a miss with no similarity; every step runs.
+OutRec empty_out(const mc_cache* h) {
+  OutRec o;
+  o.live = -1;
+  o.sim = NAN;
+  o.k = 0;
+  o.flags = MC_FLAG_EMPTY;
+  o.steps = h->thr.total_steps;
+  o.route = 0;
+  o.sigma = NAN;
+  return o;
+}
+
 int finish_inflight(mc_cache* h);
 
 RingBufs rbufs(const mc_cache* h) { return RingBufs{h->ring16, h->ring64, h->ring8, h->ringq, h->P8}; }
@@ -166,7 +178,7 @@ int wait_env(mc_cache* h) {
 size_t prep_head(int B) { return ((size_t)B * sizeof(QPrep) + 63) / 64 * 64; }
 size_t prep_bytes(const mc_cache* h, int B) { return prep_head(B) + (size_t)B * h->Dp; }
 
-// int8 quantisation of one query for the small-batch scan (scan_gemv8.cu):
+// int8 quantisation of one query for the small-batch scan (scan_stream8.cu):
 // s >= max|q|/127 rounded up (so |q/s| <= 127), q̂ = rint(q / s), and the
 // norms the certificate and the exhaustive-path decision need.
 void quantize_query(const double* q, int D, int Dp, QPrep* p, int8_t* q8) {
@@ -219,7 +231,6 @@ void free_batch(mc_cache* h) {
   cudaFree(h->d_part_s);
   cudaFree(h->d_part_p);
   cudaFree(h->d_part_floor);
-  cudaFree(h->d_part_maxl);
   cudaFree(h->d_cta);
   cudaFree(h->d_gmax);
   cudaFree(h->d_gmax8);
@@ -231,7 +242,6 @@ void free_batch(mc_cache* h) {
   h->d_part_s = nullptr;
   h->d_part_p = nullptr;
   h->d_part_floor = nullptr;
-  h->d_part_maxl = nullptr;
   h->d_cta = nullptr;
   h->d_gmax = nullptr;
   h->d_gmax8 = nullptr;
@@ -272,7 +282,6 @@ int ensure_batch(mc_cache* h, int B) {
   CU(cudaMalloc(&h->d_part_s, (size_t)cap * chunks * KP * sizeof(float)));
   CU(cudaMalloc(&h->d_part_p, (size_t)cap * chunks * KP * sizeof(long long)));
   CU(cudaMalloc(&h->d_part_floor, (size_t)cap * chunks * sizeof(float)));
-  CU(cudaMalloc(&h->d_part_maxl, (size_t)cap * chunks * sizeof(float)));
   CU(cudaMalloc(&h->d_cta, (size_t)cap * gemv_grid(h->sm_count) * sizeof(CtaRec)));
   // 256 words per query: the streamed scan keeps 8 replicas of its bound 128 B apart
   CU(cudaMalloc(&h->d_gmax, (size_t)cap * 256 * sizeof(unsigned)));
@@ -284,8 +293,8 @@ int ensure_batch(mc_cache* h, int B) {
   CU(cudaMalloc(&h->d_out, (size_t)cap * sizeof(OutRec)));
   CU(cudaHostAlloc(&h->h_out, (size_t)cap * sizeof(OutRec), cudaHostAllocMapped));
   CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_outm), h->h_out, 0));
-  CU(cudaHostAlloc(&h->h_outp, (size_t)cap * sizeof(uint4), cudaHostAllocMapped));
-  memset(h->h_outp, 0, (size_t)cap * sizeof(uint4));
+  CU(cudaHostAlloc(&h->h_outp, (size_t)cap * 2 * sizeof(uint4), cudaHostAllocMapped));
+  memset(h->h_outp, 0, (size_t)cap * 2 * sizeof(uint4));
   CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_outp), h->h_outp, 0));
   h->Bcap = cap;
   return MC_OK;
@@ -297,6 +306,7 @@ GemvAppendArgs take_pending(mc_cache* h, const double* dev_rows) {
   GemvAppendArgs a;
   a.rb = rbufs(h);
   a.d_state = h->d_state;
+  a.dirty = h->state_dirty || h->n_pending > 0;
   if (h->n_pending > 0) {
     const long long nw = std::min(h->n_pending, h->C);  // older rows were displaced before landing
     const long long skip = h->n_pending - nw;
@@ -400,27 +410,8 @@ constexpr int GEMM_MIN_B = 5;
 constexpr long long FUSE_APPEND_MAX = 256;
 
 bool use_gemm(const mc_cache* h, int B) {
-  if (h->path == MC_PATH_GEMV || h->path == MC_PATH_GEMV8 || h->path == MC_PATH_STREAM8) return false;
-  return h->path == MC_PATH_GEMM || h->path == MC_PATH_GEMM_1SM || h->path == MC_PATH_GEMM_QUAD ||
-         h->path == MC_PATH_GEMM8 || (h->path == MC_PATH_AUTO && B >= GEMM_MIN_B);
-}
-
-// int8 tensor cores (MC_PATH_GEMM8).  Not AUTO's choice yet: at C3 its looser
-// per-row bound admits ~5x the float64 rescoring of the fp16 scan and the
-// scan itself measured slower.
-bool use_gemm8(const mc_cache* h, int B) {
-  return use_gemm(h, B) && h->path == MC_PATH_GEMM8 && tc8_supported(h->P8);
-}
-
-int ensure_tc8(mc_cache* h, int B) {
-  if (h->tc8 && tc8_bcap(h->tc8) >= B) return MC_OK;
-  CU(cudaStreamSynchronize(h->stream));
-  tc8_plan_destroy(h->tc8);
-  h->tc8 = nullptr;
-  char err[256] = {0};
-  h->tc8 = tc8_plan_create(h->ring8, h->C, h->Dp, h->P8, std::max(B, 256), h->sm_count, err, sizeof err);
-  if (!h->tc8) return fail(MC_ERR_CUDA, "int8 tensor-core scan plan: %s", err);
-  return MC_OK;
+  if (h->path == MC_PATH_GEMV || h->path == MC_PATH_STREAM8) return false;
+  return h->path == MC_PATH_GEMM || (h->path == MC_PATH_AUTO && B >= GEMM_MIN_B);
 }
 
 int ensure_tc(mc_cache* h, int B) {
@@ -452,35 +443,13 @@ unsigned s8_epoch(mc_cache* h) {
 int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
                const QPrep* prep, const int8_t* q8, cudaEvent_t t_mid = nullptr, unsigned* done_seq = nullptr,
                unsigned seq = 0, uint4* outp = nullptr) {
-  if (use_gemm8(h, B)) {
-    if (app.n > 0) {
-      CU(launch_append(app.stage, app.n, app.first_slot, mirror(h), h->D, h->Dp, rbufs(h), h->d_state, h->stream));
-      h->stats[7]++;
-    }
-    int rc = ensure_tc8(h, B);
-    if (rc) return rc;
-    Partials part{h->d_part_s, h->d_part_p, h->d_part_floor, tc8_chunks(h->tc8, B)};
-    part.maxl = h->d_part_maxl;
-    CU(launch_tc8_scan(h->tc8, q64, B, h->D, h->d_state, h->ringq, part, h->shard, h->stream));
-    if (t_mid) CU(cudaEventRecord(t_mid, h->stream));
-    CU(launch_merge8(h->d_state, h->ring64, h->D, h->Dp, q64, B, part, rec, h->shard, h->stream));
-    h->stats[6]++;
-    h->stats[7] += 3;
-    if (out) {
-      CU(launch_finalize(rec, 1, B, -1, h->d_state, h->thr, out, h->stream));
-      h->stats[7]++;
-    }
-    return MC_OK;
-  }
   if (use_gemm(h, B)) {
-    if (app.n > 0) {
+    if (app.n > 0 || app.dirty) {  // evictions alone must reach d_state too (the scan reads it)
       CU(launch_append(app.stage, app.n, app.first_slot, mirror(h), h->D, h->Dp, rbufs(h), h->d_state, h->stream));
       h->stats[7]++;
     }
     int rc = ensure_tc(h, B);
     if (rc) return rc;
-    tc_set_pair(h->tc, h->path != MC_PATH_GEMM_1SM);
-    tc_set_quad(h->tc, h->path == MC_PATH_GEMM_QUAD);
     const Partials part{h->d_part_s, h->d_part_p, h->d_part_floor, tc_chunks(h->tc, B)};
     CU(launch_tc_scan(h->tc, q64, B, h->D, h->d_state, part, h->shard, h->stream));
     if (t_mid) CU(cudaEventRecord(t_mid, h->stream));
@@ -493,18 +462,13 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
   GemvAppendArgs a = app;
   const RingState st = mirror(h);
   const bool quant = h->path != MC_PATH_GEMV && prep != nullptr;
-  const bool s8 = quant && h->s8 && h->path != MC_PATH_GEMV8;
-  const bool int8 = quant && !s8 && gemv8_supported(h->Dp);
+  const bool s8 = quant && h->s8;
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nb = std::min(4, B - b0);
     if (s8)
       CU(launch_stream8_scan(h->s8, rbufs(h), st, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0, h->sm_count, h->shard,
                              h->d_counter, h->d_gmax8, s8_epoch(h), h->thr, rec, out, a, prep + b0, q8 + (size_t)b0 * h->Dp,
                              b0 + nb == B ? done_seq : nullptr, seq, outp, h->stream));
-    else if (int8)
-      CU(launch_gemv8_scan(rbufs(h), st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
-                           nb == 1 ? gemv_grid(h->sm_count) : h->sm_count, h->shard, h->d_counter, h->d_gmax, h->thr, rec, out, a, prep + b0,
-                           q8 + (size_t)b0 * h->Dp, h->stream));
     else
       CU(launch_gemv_scan(h->ring16, st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
                           gemv_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax, h->ring64, h->thr, rec, out, a,
@@ -530,7 +494,7 @@ int lookup_enqueue(mc_cache* h, const double* queries, int B, mc_record* rec, Ou
   const double* q = nullptr;
   const QPrep* prep = nullptr;
   const int8_t* q8 = nullptr;
-  const bool int8 = !use_gemm(h, B) && h->path != MC_PATH_GEMV && (h->s8 || gemv8_supported(h->Dp));
+  const bool int8 = !use_gemm(h, B) && h->path != MC_PATH_GEMV && h->s8;
   rc = upload_envelope(h, queries, B, async_reuse, int8, &q, &prep, &q8);
   if (rc) return rc;
   const GemvAppendArgs app = take_pending(h, h->d_env);
@@ -556,7 +520,7 @@ int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool
     memcpy(h->h_qkeep, queries, (size_t)h->D * sizeof(double));
     const RingState st = mirror(h);
     take_pending(h, nullptr);
-    memset(h->h_outp, 0, sizeof(uint4));
+    memset(h->h_outp, 0, 2 * sizeof(uint4));
     *q = nullptr;
     CU(launch_stream8_direct(h->s8, rbufs(h), st, h->D, queries, stage_row, h->d_cta, h->sm_count, h->shard,
                              h->d_counter, h->d_gmax8, s8_epoch(h), h->thr, h->d_rec, nullptr, h->d_state, nullptr,
@@ -567,7 +531,7 @@ int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool
     return MC_OK;
   }
   if (h->packed) {
-    memset(h->h_outp, 0, (size_t)B * sizeof(uint4));  // no stale record can carry this lookup's tag
+    memset(h->h_outp, 0, (size_t)B * 2 * sizeof(uint4));  // no stale record can carry this lookup's tag
     return lookup_enqueue(h, queries, B, h->d_rec, nullptr, async_reuse, q, nullptr, seq_tag(seq), h->d_outp);
   }
   return lookup_enqueue(h, queries, B, h->d_rec, h->d_outm, async_reuse, q, h->d_seq, seq);
@@ -615,7 +579,7 @@ int finish_inflight(mc_cache* h) {
 // True when a B-query lookup runs on the streamed int8 scan, which can hand
 // its decisions straight to host-mapped memory.
 bool direct_result(const mc_cache* h, int B) {
-  return h->s8 && !use_gemm(h, B) && h->path != MC_PATH_GEMV && h->path != MC_PATH_GEMV8;
+  return h->s8 && !use_gemm(h, B) && h->path != MC_PATH_GEMV;
 }
 
 // Packed zero-copy results: tag of lookup `seq` (never 0, so zeroed slots never match).
@@ -624,38 +588,49 @@ unsigned seq_tag(unsigned seq) { return seq % 65535u + 1u; }
 // Spin until the B packed decisions of lookup `seq` carry its tag, then unpack
 // them into h_out.  Each record is one 16-byte store on the device side and one
 // 16-byte load here, so a record is seen whole or not at all.
+// One packed 16-byte record, once it carries `tag` (see pack_out in scan_stream8.cu).
+int wait_record(mc_cache* h, const uint4* p, unsigned tag, unsigned seq, int b, uint4* out) {
+  uint4 v;
+  for (unsigned spins = 1;; ++spins) {
+#if defined(__x86_64__)
+    const __m128i x = _mm_load_si128(reinterpret_cast<const __m128i*>(p));
+    memcpy(&v, &x, sizeof v);
+#else
+    v = *(volatile const uint4*)p;
+#endif
+    if ((v.w >> 16) == tag) break;
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+    if ((spins & 1023u) == 0) {
+      const cudaError_t e = cudaStreamQuery(h->stream);
+      if (e != cudaSuccess && e != cudaErrorNotReady) return fail(MC_ERR_CUDA, "lookup %u: %s", seq, cudaGetErrorString(e));
+      if (e == cudaSuccess) {  // the stream is idle: one last look, then report
+#if defined(__x86_64__)
+        const __m128i y = _mm_load_si128(reinterpret_cast<const __m128i*>(p));
+        memcpy(&v, &y, sizeof v);
+#else
+        v = *(volatile const uint4*)p;
+#endif
+        if ((v.w >> 16) == tag) break;
+        return fail(MC_ERR_STATE, "lookup %u finished without publishing query %d", seq, b);
+      }
+    }
+  }
+  *out = v;
+  return MC_OK;
+}
+
+// Spin until the B packed decisions of lookup `seq` carry its tag, then unpack
+// them into h_out.  Each record is one 16-byte store on the device side and one
+// 16-byte load here, so a record is seen whole or not at all.
 int wait_packed(mc_cache* h, unsigned seq, int B) {
   const unsigned tag = seq_tag(seq);
   for (int b = 0; b < B; ++b) {
-    const uint4* p = h->h_outp + b;
-    uint4 v;
-    for (unsigned spins = 1;; ++spins) {
-#if defined(__x86_64__)
-      const __m128i x = _mm_load_si128(reinterpret_cast<const __m128i*>(p));
-      memcpy(&v, &x, sizeof v);
-#else
-      v = *(volatile const uint4*)p;
-#endif
-      if ((v.w >> 16) == tag) break;
-#if defined(__x86_64__) || defined(__i386__)
-      __builtin_ia32_pause();
-#endif
-      if ((spins & 1023u) == 0) {
-        const cudaError_t e = cudaStreamQuery(h->stream);
-        if (e != cudaSuccess && e != cudaErrorNotReady)
-          return fail(MC_ERR_CUDA, "lookup %u: %s", seq, cudaGetErrorString(e));
-        if (e == cudaSuccess) {  // the stream is idle: one last look, then report
-#if defined(__x86_64__)
-          const __m128i y = _mm_load_si128(reinterpret_cast<const __m128i*>(p));
-          memcpy(&v, &y, sizeof v);
-#else
-          v = *(volatile const uint4*)p;
-#endif
-          if ((v.w >> 16) == tag) break;
-          return fail(MC_ERR_STATE, "lookup %u finished without publishing query %d", seq, b);
-        }
-      }
-    }
+    uint4 v, v2;
+    int rc = wait_record(h, h->h_outp + 2 * b, tag, seq, b, &v);
+    if (!rc) rc = wait_record(h, h->h_outp + 2 * b + 1, tag, seq, b, &v2);
+    if (rc) return rc;
     OutRec& o = h->h_out[b];
     const unsigned long long sb = (unsigned long long)v.x | ((unsigned long long)v.y << 32);
     memcpy(&o.sim, &sb, sizeof sb);
@@ -663,6 +638,10 @@ int wait_packed(mc_cache* h, unsigned seq, int B) {
     o.k = (int)(v.w & 0xffu);
     const unsigned f8 = (v.w >> 8) & 0xffu;
     o.flags = (f8 & 0x7fu) | ((f8 & 0x80u) ? FLAG_NEED_FALLBACK : 0u);
+    const unsigned long long gb = (unsigned long long)v2.x | ((unsigned long long)v2.y << 32);
+    memcpy(&o.sigma, &gb, sizeof gb);
+    o.steps = (int)v2.z;
+    o.route = (int)(v2.w & 0xffu);
   }
   return MC_OK;
 }
@@ -699,6 +678,88 @@ int copy_out(mc_cache* h, int B, int64_t* out_live, double* out_sim, int32_t* ou
     if (f & MC_FLAG_TIE) h->stats[3]++;
   }
   h->stats[0] += B;
+  return MC_OK;
+}
+
+// sigma[k] per threshold pair from the schedule (noise_reentry_level, cache.py:325-334).
+void apply_sigma(mc_cache* h) {
+  Thresholds& t = h->thr;
+  t.has_sigma = h->sched.empty() ? 0 : 1;
+  for (int j = 0; j < MAX_PAIRS; ++j)
+    t.sigma[j] = (j < t.n && t.ks[j] >= 0 && t.ks[j] < (int)h->sched.size()) ? h->sched[t.ks[j]] : NAN;
+}
+
+// The lookup of mc_retrieve_batch / mc_retrieve_decisions: B answers into h->h_out
+// (the caller holds the mutex and the device guard).
+int retrieve_into_hout(mc_cache* h, const double* queries, int32_t B) {
+  if (h->inflight_seq) return fail(MC_ERR_STATE, "an asynchronous lookup is in flight: mc_retrieve_wait first");
+  int rc = ensure_batch(h, B);  // may reallocate d_rec / d_out / h_out: evaluate them after
+  if (rc) return rc;
+  if (h->count == 0) {  // cache.py:252-253
+    for (int b = 0; b < B; ++b) h->h_out[b] = empty_out(h);
+    return MC_OK;
+  }
+  const double* q = nullptr;
+  if (direct_result(h, B)) {  // decisions land in host-mapped memory; no D2H copy, no stream sync
+    const unsigned seq = ++h->seq;
+    const double t0 = g_ht.on ? now_us() : 0.0;
+    const double h2d0 = g_ht.acc[1];
+    rc = enqueue_direct(h, queries, B, seq, false, &q);
+    if (rc) return rc;
+    const double t2 = g_ht.on ? now_us() : 0.0;
+    rc = wait_direct(h, seq, B);
+    if (rc) return rc;
+    if (g_ht.on) {  // enqueue time minus the H2D call = staging, quantisation and the launch
+      const double t3 = now_us();
+      g_ht.acc[2] += (t2 - t0) - (g_ht.acc[1] - h2d0);
+      g_ht.acc[3] += t3 - t2;
+      g_ht.n++;
+    }
+  } else {
+    const double t0 = g_ht.on ? now_us() : 0.0;
+    const double h2d0 = g_ht.acc[1];
+    rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_out, false, &q);
+    if (rc) return rc;
+    const double t2 = g_ht.on ? now_us() : 0.0;
+    CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    if (g_ht.on) {
+      const double t3 = now_us();
+      g_ht.acc[2] += (t2 - t0) - (g_ht.acc[1] - h2d0);
+      g_ht.acc[3] += t3 - t2;
+      g_ht.n++;
+    }
+  }
+  h->env_inflight = false;
+  bool need = false;
+  for (int b = 0; b < B; ++b) need |= (h->h_out[b].flags & FLAG_NEED_ANY) != 0;
+  if (need) {  // rare: certificate failed or exotic query -> exact rescan, then decide again
+    rc = device_query(h, q, &q);
+    if (rc) return rc;
+    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, q, B, h->d_rec, h->d_scratch,
+                           exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
+    CU(launch_finalize(h->d_rec, 1, B, -1, h->d_state, h->thr, h->d_out, h->stream));
+    h->stats[7] += 3;
+    CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+  }
+  return MC_OK;
+}
+
+int copy_decisions(mc_cache* h, int B, mc_decision* out) {
+  int rc = copy_out(h, B, nullptr, nullptr, nullptr, nullptr);  // counters
+  if (rc) return rc;
+  for (int b = 0; b < B; ++b) {
+    const OutRec& o = h->h_out[b];
+    mc_decision& d = out[b];
+    d.live = o.live;
+    d.sim = o.sim;
+    d.sigma = o.sigma;
+    d.k = o.k;
+    d.steps = o.steps;
+    d.flags = o.flags & 0xffffu;
+    d.route = o.route;
+  }
   return MC_OK;
 }
 
@@ -805,7 +866,6 @@ int mc_destroy(mc_cache* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     free_batch(h);
     tc_plan_destroy(h->tc);
-    tc8_plan_destroy(h->tc8);
     s8_plan_destroy(h->s8);
     cudaFreeHost(h->h_env);
     cudaFree(h->d_env);
@@ -838,6 +898,7 @@ int mc_set_thresholds(mc_cache* h, const int32_t* ks, const double* taus, int32_
     h->thr.ks[i] = ks[i];
     h->thr.taus[i] = taus[i];
   }
+  apply_sigma(h);
   return MC_OK;
 }
 
@@ -853,7 +914,8 @@ int mc_configure_shard(mc_cache* h, int32_t n_shards, int32_t shard_id) {
 
 int mc_set_path(mc_cache* h, int32_t path) {
   if (!h) return fail(MC_ERR_ARG, "NULL handle");
-  if (path < MC_PATH_AUTO || path > MC_PATH_GEMM8) return fail(MC_ERR_ARG, "unknown path %d", path);
+  if (path != MC_PATH_AUTO && path != MC_PATH_GEMV && path != MC_PATH_GEMM && path != MC_PATH_STREAM8)
+    return fail(MC_ERR_ARG, "unknown path %d", path);
   std::lock_guard<std::mutex> lk(h->mu);
   h->path = path;
   return MC_OK;
@@ -914,64 +976,29 @@ int mc_retrieve_batch(mc_cache* h, const double* queries, int32_t B, int64_t* ou
   if (B == 0) return MC_OK;
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard guard(h->dev);
-  if (h->inflight_seq) return fail(MC_ERR_STATE, "an asynchronous lookup is in flight: mc_retrieve_wait first");
-  if (h->count == 0) {  // cache.py:252-253
-    for (int b = 0; b < B; ++b) {
-      if (out_live) out_live[b] = -1;
-      if (out_sim) out_sim[b] = NAN;
-      if (out_k) out_k[b] = 0;
-      if (out_flags) out_flags[b] = MC_FLAG_EMPTY;
-    }
-    h->stats[0] += B;
-    return MC_OK;
-  }
-  int rc = ensure_batch(h, B);  // may reallocate d_rec / d_out: evaluate them after
+  int rc = retrieve_into_hout(h, queries, B);
   if (rc) return rc;
-  const double* q = nullptr;
-  if (direct_result(h, B)) {  // decisions land in host-mapped memory; no D2H copy, no stream sync
-    const unsigned seq = ++h->seq;
-    const double t0 = g_ht.on ? now_us() : 0.0;
-    const double h2d0 = g_ht.acc[1];
-    rc = enqueue_direct(h, queries, B, seq, false, &q);
-    if (rc) return rc;
-    const double t2 = g_ht.on ? now_us() : 0.0;
-    rc = wait_direct(h, seq, B);
-    if (rc) return rc;
-    if (g_ht.on) {  // enqueue time minus the H2D call = staging, quantisation and the launch
-      const double t3 = now_us();
-      g_ht.acc[2] += (t2 - t0) - (g_ht.acc[1] - h2d0);
-      g_ht.acc[3] += t3 - t2;
-      g_ht.n++;
-    }
-  } else {
-    const double t0 = g_ht.on ? now_us() : 0.0;
-    const double h2d0 = g_ht.acc[1];
-    rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_out, false, &q);
-    if (rc) return rc;
-    const double t2 = g_ht.on ? now_us() : 0.0;
-    CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
-    CU(cudaStreamSynchronize(h->stream));
-    if (g_ht.on) {
-      const double t3 = now_us();
-      g_ht.acc[2] += (t2 - t0) - (g_ht.acc[1] - h2d0);
-      g_ht.acc[3] += t3 - t2;
-      g_ht.n++;
-    }
-  }
-  h->env_inflight = false;
-  bool need = false;
-  for (int b = 0; b < B; ++b) need |= (h->h_out[b].flags & FLAG_NEED_ANY) != 0;
-  if (need) {  // rare: certificate failed or exotic query -> exact rescan, then decide again
-    rc = device_query(h, q, &q);
-    if (rc) return rc;
-    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, q, B, h->d_rec, h->d_scratch,
-                           exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
-    CU(launch_finalize(h->d_rec, 1, B, -1, h->d_state, h->thr, h->d_out, h->stream));
-    h->stats[7] += 3;
-    CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
-    CU(cudaStreamSynchronize(h->stream));
-  }
   return copy_out(h, B, out_live, out_sim, out_k, out_flags);
+}
+
+int mc_retrieve_decisions(mc_cache* h, const double* queries, int32_t B, mc_decision* out) {
+  if (!h || !out || (!queries && B > 0)) return fail(MC_ERR_ARG, "NULL argument");
+  if (B < 0) return fail(MC_ERR_ARG, "negative batch");
+  if (B == 0) return MC_OK;
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  int rc = retrieve_into_hout(h, queries, B);
+  if (rc) return rc;
+  return copy_decisions(h, B, out);
+}
+
+int mc_set_sigma_schedule(mc_cache* h, const double* schedule, int32_t n) {
+  if (!h || (!schedule && n > 0)) return fail(MC_ERR_ARG, "NULL argument");
+  if (n < 0) return fail(MC_ERR_ARG, "negative schedule length");
+  std::lock_guard<std::mutex> lk(h->mu);
+  h->sched.assign(schedule, schedule + n);
+  apply_sigma(h);
+  return MC_OK;
 }
 
 int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* out_ticket) {
@@ -986,7 +1013,7 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
   h->inflight_B = B;
   h->inflight_q = nullptr;
   if (h->count == 0) {  // cache.py:252-253: answered now
-    for (int b = 0; b < B; ++b) h->h_out[b] = OutRec{-1, NAN, 0, MC_FLAG_EMPTY};
+    for (int b = 0; b < B; ++b) h->h_out[b] = empty_out(h);
     h->inflight_ready = true;
   } else if (direct_result(h, B)) {  // the kernel publishes into mapped memory; the caller returns now
     const double* q = nullptr;
@@ -1232,8 +1259,7 @@ int mc_profile_rotate(mc_cache* const* hs, int32_t nh, const double* queries, co
   for (int k = 0; k < nh; ++k) {
     int rc = ensure_batch(hs[k], B);
     if (!rc) rc = flush(hs[k]);
-    if (!rc && use_gemm8(hs[k], B)) rc = ensure_tc8(hs[k], B);
-    else if (!rc && use_gemm(hs[k], B)) rc = ensure_tc(hs[k], B);
+    if (!rc && use_gemm(hs[k], B)) rc = ensure_tc(hs[k], B);
     if (rc) return rc;
     CU(cudaStreamSynchronize(hs[k]->stream));
   }

@@ -39,6 +39,8 @@ struct Thresholds {
   int total_steps;
   int ks[MAX_PAIRS];
   double taus[MAX_PAIRS];
+  int has_sigma;             // a sigma schedule is set (mc_set_sigma_schedule)
+  double sigma[MAX_PAIRS];   // schedule[ks[j]] (noise_reentry_level, cache.py:325-334); NaN if ks[j] is past it
 };
 
 // Where a scan pass leaves its per-chunk top-K' lists (approximate scores).
@@ -47,7 +49,6 @@ struct Partials {
   long long* p;      // [B][n_chunks][KP] global position (-1 = empty)
   float* floor_;     // [B][n_chunks]  K'-th score if rows were dropped, else -inf
   int n_chunks;
-  float* maxl = nullptr;  // [B][n_chunks] largest lower bound seen (int8 tensor-core scan only)
 };
 
 // One CTA's exact answer for one query on the GEMV path: the float64 best over
@@ -74,12 +75,18 @@ struct ShardMap {
   int g;  // this shard
 };
 
-// Final per-query answer written by the decision epilogue.
+// Final per-query answer written by the decision epilogue (the serving decision of
+// SURVEY.md §8 a1 + f3): the reference's (entry, similarity, k) plus what its callers
+// derive from them — steps to run (engine.py:38-45), route (scheduler.py:80-89) and the
+// noise re-entry level sigma[k] (cache.py:325-334).
 struct OutRec {
   long long live;  // live index (0 = oldest), -1 if none
   double sim;      // best float64 similarity
   int k;           // select_k result, 0 = none
   unsigned flags;  // MC_FLAG_*
+  int steps;       // denoising steps to run: total_steps - k (total_steps on a miss)
+  int route;       // 1 = hit queue (refine a cached image), 0 = miss queue (full generation)
+  double sigma;    // schedule[k] on a hit with a schedule set, else NaN
 };
 
 // ---- launch wrappers (each .cu owns its kernels) ---------------------------
@@ -94,6 +101,7 @@ struct GemvAppendArgs {
   long long first_slot = 0;
   RingBufs rb{};
   RingState* d_state = nullptr;
+  bool dirty = false;  // the host window changed since the device last saw it (appends or evictions)
 };
 
 // GEMV scan of up to 4 queries (q64 rows q0 .. q0+nb-1, stride Dp) over the
@@ -104,7 +112,6 @@ cudaError_t launch_gemv_scan(const __half* ring16, const RingState& st, int D, i
                              CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
                              const double* ring64, const Thresholds& thr, mc_record* rec, OutRec* out,
                              const GemvAppendArgs& app, cudaStream_t s);
-// int8 small-batch scan (scan_gemv8.cu): same contract as launch_gemv_scan.
 // Per-query int8 quantisation for the small-batch scan (computed on the host
 // by quantize_query, uploaded in the envelope next to the float64 query).
 struct QPrep {
@@ -114,15 +121,7 @@ struct QPrep {
   int exotic;     // non-finite / extreme query: answered by the exhaustive float64 scan
 };
 
-// prep / q8: the nb queries' quantisation (device pointers, q8 stride Dp).
-cudaError_t launch_gemv8_scan(const RingBufs& rb, const RingState& st, int D, int Dp, const double* q64, int nb,
-                              CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter, unsigned* gmax,
-                              const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
-                              const QPrep* prep, const int8_t* q8, cudaStream_t s);
-
-bool gemv8_supported(int Dp);
-
-// TMA-streamed int8 scan (scan_stream8.cu): same contract as launch_gemv8_scan,
+// TMA-streamed int8 scan (scan_stream8.cu): same contract as launch_gemv_scan,
 // grid = one CTA per SM.  The plan holds the ring's tensor maps.
 struct S8Plan;
 bool stream8_supported(int Dp);
@@ -152,25 +151,10 @@ struct TcPlan;
 TcPlan* tc_plan_create(__half* ring16, long long C, int Dp, int Bcap, int sm_count, char* err, int errlen);
 void tc_plan_destroy(TcPlan* p);
 int tc_bcap(const TcPlan* p);
-void tc_set_pair(TcPlan* p, bool pair);  // CTA-pair kernels (default) or single-CTA kernel
-void tc_set_quad(TcPlan* p, bool quad);  // with pairs: 4-CTA clusters sharing the query operand (default)
 int tc_chunks(const TcPlan* p, int B);
 const double* tc_qscale(const TcPlan* p);
 cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const RingState* d_state,
                            const Partials& part, ShardMap sm, cudaStream_t s);
-
-// int8 tensor-core scan (scan_tc8.cu, tcgen05 kind::i8 on CTA pairs) with
-// per-row certified bounds; its merge uses part.maxl.  rq: the ring's (s, L1).
-struct Tc8Plan;
-bool tc8_supported(int P8);
-Tc8Plan* tc8_plan_create(int8_t* ring8, long long C, int Dp, int P8, int Bcap, int sm_count, char* err, int errlen);
-void tc8_plan_destroy(Tc8Plan* p);
-int tc8_bcap(const Tc8Plan* p);
-int tc8_chunks(const Tc8Plan* p, int B);
-cudaError_t launch_tc8_scan(Tc8Plan* p, const double* q64, int B, int D, const RingState* d_state,
-                            const float2* rq, const Partials& part, ShardMap sm, cudaStream_t s);
-cudaError_t launch_merge8(const RingState* d_state, const double* ring64, int D, int Dp, const double* q64, int B,
-                          const Partials& part, mc_record* rec, ShardMap sm, cudaStream_t s);
 
 // Merge per-chunk lists -> certified float64 best per query (mc_record).
 // qscale: per-query factor turning partial scores into similarity units (nullptr = 1).

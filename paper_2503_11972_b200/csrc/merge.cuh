@@ -181,12 +181,18 @@ static __device__ mc_record merge_one(const RingState& st, const double* __restr
   return r;
 }
 
-// Decision for one query from its merged best (cache.py:255-260 + select_k).
+// Decision for one query from its merged best (cache.py:255-260 + select_k), plus the serving
+// decision the callers derive from it: steps = T - k (engine.py:38-45, service_time), route =
+// hit / miss queue (scheduler.py:80-89) and sigma[k] (noise_reentry_level, cache.py:325-334).
 __device__ __forceinline__ OutRec decide(const Best2& best, unsigned fl, long long base, const Thresholds& thr) {
   OutRec o;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  o.steps = thr.total_steps;
+  o.route = 0;
+  o.sigma = qnan;
   if (best.p < 0) {
     o.live = -1;
-    o.sim = __longlong_as_double(0x7ff8000000000000ll);
+    o.sim = qnan;
     o.k = 0;
     o.flags = MC_FLAG_EMPTY | (fl & (FLAG_NEED_FALLBACK | FLAG_NEED_EXHAUSTIVE));
     return o;
@@ -196,15 +202,23 @@ __device__ __forceinline__ OutRec decide(const Best2& best, unsigned fl, long lo
   const double s = best.s;
   unsigned f = fl;
   if (!(s < thr.taus[0])) f |= MC_FLAG_HIT;  // cache.py:258 — `best < tau` is the miss test
-  int k = 0;
+  int k = 0, jk = -1;
   for (int j = 0; j < thr.n; ++j) {
-    if (s >= thr.taus[j]) k = thr.ks[j];  // cache.py:112-117
+    if (s >= thr.taus[j]) {  // cache.py:112-117
+      k = thr.ks[j];
+      jk = j;
+    }
     if (fabs(s - thr.taus[j]) < AMBIG) f |= MC_FLAG_NEAR_TAU;
   }
   o.k = k;
   if (best.ties >= 2) f |= MC_FLAG_TIE;
   if (best.s2 != s && s - best.s2 < AMBIG) f |= MC_FLAG_NEAR_TIE;
   o.flags = f;
+  if (f & MC_FLAG_HIT) {
+    o.route = 1;
+    o.steps = thr.total_steps - k;  // a NaN best is a hit with no k: every step runs
+    if (thr.has_sigma && jk >= 0) o.sigma = thr.sigma[jk];
+  }
   return o;
 }
 

@@ -140,16 +140,22 @@ struct S8NoIn {
   int unused;
 };
 
-// A decision packed into one 16-byte store (one PCIe write, read by the host
-// with one 16-byte load): sim | live (int32) | k (8) flags (8: MC_FLAG_* bits
-// 0-6, bit 7 = needs the exhaustive path) seq (16).  The sequence tag makes
-// each record self-validating, so no system-scope fence has to separate the
-// decisions from a completion word.
+// A decision packed into two 16-byte stores (two PCIe writes, each read by the
+// host with one 16-byte load):
+//   [0] sim | live (int32) | k (8) flags (8: MC_FLAG_* bits 0-6, bit 7 = needs the
+//       exhaustive path) seq (16)
+//   [1] sigma | steps (int32) | route (8) 0 (8) seq (16)
+// The sequence tag makes each record self-validating, so no system-scope fence
+// has to separate the decisions from a completion word.
 __device__ __forceinline__ uint4 pack_out(const OutRec& o, unsigned seq16) {
   const unsigned long long sb = (unsigned long long)__double_as_longlong(o.sim);
   const unsigned f8 = (o.flags & 0x7fu) | ((o.flags & FLAG_NEED_ANY) ? 0x80u : 0u);
   return make_uint4((unsigned)sb, (unsigned)(sb >> 32), (unsigned)o.live,
                     ((unsigned)o.k & 0xffu) | (f8 << 8) | (seq16 << 16));
+}
+__device__ __forceinline__ uint4 pack_out2(const OutRec& o, unsigned seq16) {
+  const unsigned long long gb = (unsigned long long)__double_as_longlong(o.sigma);
+  return make_uint4((unsigned)gb, (unsigned)(gb >> 32), (unsigned)o.steps, ((unsigned)o.route & 0xffu) | (seq16 << 16));
 }
 
 // Rows [r0, r1) (live-local) of one CTA, cut into stages of up to `rows`
@@ -510,9 +516,12 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
       const OutRec o = decide(record_best(r), r.flags & FLAG_NEED_ANY, x.st.jhead, a.thr);
       if (a.out) a.out[gb] = o;
       if (a.outp) {
-        const uint4 v = pack_out(o, a.seq);
-        asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a.outp + gb), "r"(v.x), "r"(v.y), "r"(v.z),
+        const uint4 v = pack_out(o, a.seq), v2 = pack_out2(o, a.seq);
+        asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a.outp + 2 * gb), "r"(v.x), "r"(v.y), "r"(v.z),
                      "r"(v.w)
+                     : "memory");
+        asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a.outp + 2 * gb + 1), "r"(v2.x), "r"(v2.y),
+                     "r"(v2.z), "r"(v2.w)
                      : "memory");
       }
       if (b == 0 && x.timing) a.timing[7] = s8_timer();

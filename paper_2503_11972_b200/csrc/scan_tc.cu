@@ -201,169 +201,6 @@ struct TopK {
   }
 };
 
-__global__ void __launch_bounds__(TC_THREADS, 1)
-    k_tc_scan(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap ring_map,
-              const RingState* __restrict__ d_state, int n_m, int B, int n_kb, float* __restrict__ part_s,
-              long long* __restrict__ part_p, float* __restrict__ part_floor, int n_chunks, float margin,
-              ShardMap sm) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* smA = smem;
-  uint8_t* smB = smem + TC_STAGES * TC_A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + TC_STAGES * TC_B_BYTES);
-  uint64_t* full = bars;                   // [S]  TMA -> MMA
-  uint64_t* empty = bars + TC_STAGES;      // [S]  MMA -> TMA
-  uint64_t* tfull = bars + 2 * TC_STAGES;  // [2]  MMA -> epilogue
-  uint64_t* tempty = tfull + 2;            // [2]  epilogue -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const RingState st = *d_state;
-  const TileWindow win = tile_window(st);
-  const int m_tile = blockIdx.x % n_m;
-  const int group = blockIdx.x / n_m;
-  const int n_groups = gridDim.x / n_m;
-  const int n_units = win.n_live > group ? (win.n_live - group + n_groups - 1) / n_groups : 0;
-
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&q_map)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map)) : "memory");
-    for (int i = 0; i < TC_STAGES; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TC_TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = 0; u < n_units; ++u) {
-        const int t = (win.first + group + u * n_groups) % win.n_total;
-        for (int kb = 0; kb < n_kb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], TC_A_BYTES + TC_B_BYTES);
-          tma_load_2d(smA + stage * TC_A_BYTES, &q_map, &full[stage], kb * TC_BK, m_tile * TC_BM);
-          tma_load_2d(smB + stage * TC_B_BYTES, &ring_map, &full[stage], kb * TC_BK, t * TC_BN);
-          if (++stage == TC_STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = umma_idesc_f16(TC_BM, TC_BN);
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int u = 0; u < n_units; ++u) {
-      const int acc = u & 1;
-      const uint32_t acc_phase = (u >> 1) & 1;
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TC_BN);
-      for (int kb = 0; kb < n_kb; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a0 = smem_u32(smA + stage * TC_A_BYTES);
-          const uint32_t b0 = smem_u32(smB + stage * TC_B_BYTES);
-#pragma unroll
-          for (int k = 0; k < TC_BK / TC_UK; ++k) {
-            umma_f16(d_tmem, umma_desc_sw128(a0 + k * TC_UK * 2), umma_desc_sw128(b0 + k * TC_UK * 2), idesc,
-                     (kb | k) != 0);
-          }
-          umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
-        }
-        __syncwarp();
-        if (++stage == TC_STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-      if (lane == 0) umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
-      __syncwarp();
-    }
-  } else {
-    // ------------------------------------------------------------ epilogue
-    const int quad = warp & 3;  // TMEM lanes 32*quad .. 32*quad+31
-    const int row = quad * 32 + lane;
-    const int b = m_tile * TC_BM + row;
-    TopK top;
-    top.init();
-    for (int u = 0; u < n_units; ++u) {
-      const int acc = u & 1;
-      const uint32_t acc_phase = (u >> 1) & 1;
-      const int t = (win.first + group + u * n_groups) % win.n_total;
-      const long long slot0 = (long long)t * TC_BN;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      long long l0 = slot0 - st.head;  // live-local row of the tile's first slot
-      if (l0 < 0) l0 += st.cap;
-      const bool all_live = (slot0 + TC_BN <= st.cap) && (l0 + TC_BN <= st.count);
-#pragma unroll 1
-      for (int c = 0; c < TC_BN / 32; ++c) {
-        float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN + c * 32), v);
-        if (!all_live) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const long long slot = slot0 + c * 32 + j;
-            long long l = l0 + c * 32 + j;
-            if (l >= st.cap) l -= st.cap;
-            if (slot >= st.cap || l >= st.count) v[j] = -INFINITY;
-          }
-        }
-        top.scan32(v, (int)(slot0 + c * 32), margin);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-    }
-    if (b < B) {
-      const size_t o = (size_t)b * n_chunks + group;
-#pragma unroll
-      for (int i = 0; i < KP; ++i) {
-        long long pos = -1;
-        if (top.slot[i] >= 0) {
-          long long l = (long long)top.slot[i] - st.head;
-          if (l < 0) l += st.cap;
-          pos = (st.jhead + l) * (long long)sm.G + sm.g;
-        }
-        part_s[o * KP + i] = top.s[i];
-        part_p[o * KP + i] = pos;
-      }
-      part_floor[o] = top.drop;
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TC_TMEM_COLS)
-                 : "memory");
-  }
-}
-
 // ---------------------------------------------------------------- CTA-pair variant
 // cta_group::2: a cluster of two CTAs on one TPC computes a 256-query x
 // 256-slot tile per MMA.  CTA r loads queries [256 m + 128 r, +128) and ring
@@ -678,216 +515,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
   }
 }
 
-// ---------------------------------------------------------------- CTA-quad variant
-// Two CTA pairs per 4-CTA cluster work on adjacent slot tiles in lockstep and
-// share the query operand: pair 0's CTA r loads query half r once and TMA
-// multicasts it to CTA r and CTA r+2 (the same offset in both pairs), so each
-// query k-block leaves L2 once per two slot tiles instead of once per tile.
-// Slot tiles still stream once per pair.  Both MMA leaders commit `empty` to
-// all four CTAs (count 2): a stage is refilled only when both pairs consumed
-// it.  A pair without a tile in the last round multiplies a clamped tile and
-// its epilogue ignores the result, keeping the two pairs in lockstep.
-__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                                    int c1, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_BIT_MASK), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
-
-__device__ __forceinline__ void umma_commit_mask(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-
-__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(TC_THREADS, 1)
-    k_tc_scan_quad(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap ring_map,
-                   const RingState* __restrict__ d_state, int n_mp, int B, int n_kb, float* __restrict__ part_s,
-                   long long* __restrict__ part_p, float* __restrict__ part_floor, int n_chunks, float margin,
-                   ShardMap sm) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* smA = smem;
-  uint8_t* smB = smem + TP_STAGES * TP_A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + TP_STAGES * TP_B_BYTES);
-  uint64_t* full = bars;                   // [S]  pair leader: TMA bytes of the pair's stage
-  uint64_t* empty = bars + TP_STAGES;      // [S]  both leaders' commits (count 2)
-  uint64_t* tfull = bars + 2 * TP_STAGES;  // [2]  own leader's commit
-  uint64_t* tempty = tfull + 2;            // [2]  pair leader: 4 epilogue warps x 2 CTAs
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  const uint32_t pair = rank >> 1, r = rank & 1;
-  const uint32_t leader = pair * 2;
-  const int cid = blockIdx.x >> 2;
-  const int n_clusters = gridDim.x >> 2;
-  const RingState st = *d_state;
-  const TileWindow win = tile_window(st);
-  const int m_pair = cid % n_mp;
-  const int group = cid / n_mp;
-  const int n_groups = n_clusters / n_mp;
-  // round u: this cluster's two tiles are 2 (group + u n_groups) + {0, 1}
-  const int n_rounds = win.n_live > 2 * group ? (win.n_live - 2 * group + 2 * n_groups - 1) / (2 * n_groups) : 0;
-
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&q_map)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map)) : "memory");
-    for (int i = 0; i < TP_STAGES; ++i) {
-      mbar_init(&full[i], 2);
-      mbar_init(&empty[i], 2);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 8);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TC_TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (all four CTAs)
-    if (lane == 0) {
-      const uint32_t leader_full0 = mapa_shared(smem_u32(&full[0]), leader);
-      const uint16_t a_mask = (uint16_t)((1u << r) | (1u << (r + 2)));
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = 0; u < n_rounds; ++u) {
-        const int idx = 2 * (group + u * n_groups) + (int)pair;
-        const int t = (win.first + (idx < win.n_live ? idx : idx - 1)) % win.n_total;
-        for (int kb = 0; kb < n_kb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (r == 0)
-            mbar_expect_tx(&full[stage], 2 * (TP_A_BYTES + TP_B_BYTES));
-          else
-            mbar_arrive_remote(leader_full0 + stage * 8);
-          if (pair == 0)
-            tma_load_2d_pair_mc(smA + stage * TP_A_BYTES, &q_map, &full[stage], kb * TC_BK, m_pair * 256 + r * 128,
-                                a_mask);
-          tma_load_2d_pair(smB + stage * TP_B_BYTES, &ring_map, &full[stage], kb * TC_BK, t * TC_BN + r * 128);
-          if (++stage == TP_STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuers (pair leaders)
-    if (r == 0) {
-      constexpr uint32_t idesc = umma_idesc_f16(256, TC_BN);
-      const uint16_t pair_mask = (uint16_t)(3u << leader);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = 0; u < n_rounds; ++u) {
-        const int acc = u & 1;
-        const uint32_t acc_phase = (u >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TC_BN);
-        for (int kb = 0; kb < n_kb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          if (lane == 0) {
-            const uint32_t a0 = smem_u32(smA + stage * TP_A_BYTES);
-            const uint32_t b0 = smem_u32(smB + stage * TP_B_BYTES);
-#pragma unroll
-            for (int k = 0; k < TC_BK / TC_UK; ++k)
-              umma_f16_pair(d_tmem, umma_desc_sw128(a0 + k * TC_UK * 2), umma_desc_sw128(b0 + k * TC_UK * 2), idesc,
-                            (kb | k) != 0);
-            umma_commit_mask(&empty[stage], (uint16_t)0xF);
-          }
-          __syncwarp();
-          if (++stage == TP_STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        if (lane == 0) umma_commit_mask(&tfull[acc], pair_mask);
-        __syncwarp();
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ epilogue (all four CTAs)
-    const int quad = warp & 3;
-    const int row = quad * 32 + lane;
-    const int b = m_pair * 256 + (int)r * 128 + row;
-    const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty[0]), leader);
-    TopK top;
-    top.init();
-    for (int u = 0; u < n_rounds; ++u) {
-      const int acc = u & 1;
-      const uint32_t acc_phase = (u >> 1) & 1;
-      const int idx = 2 * (group + u * n_groups) + (int)pair;
-      const bool valid = idx < win.n_live;  // block-uniform
-      const int t = (win.first + idx) % win.n_total;
-      const long long slot0 = (long long)t * TC_BN;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      if (valid) {
-        long long l0 = slot0 - st.head;
-        if (l0 < 0) l0 += st.cap;
-        const bool all_live = (slot0 + TC_BN <= st.cap) && (l0 + TC_BN <= st.count);
-#pragma unroll 1
-        for (int c = 0; c < TC_BN / 32; ++c) {
-          float v[32];
-          tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * TC_BN + c * 32), v);
-          if (!all_live) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const long long slot = slot0 + c * 32 + j;
-              long long l = l0 + c * 32 + j;
-              if (l >= st.cap) l -= st.cap;
-              if (slot >= st.cap || l >= st.count) v[j] = -INFINITY;
-            }
-          }
-          top.scan32(v, (int)(slot0 + c * 32), margin);
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(leader_tempty0 + acc * 8);
-    }
-    if (b < B) {
-      const size_t o = (size_t)b * n_chunks + (size_t)group * 2 + pair;
-#pragma unroll
-      for (int i = 0; i < KP; ++i) {
-        long long pos = -1;
-        if (top.slot[i] >= 0) {
-          long long l = (long long)top.slot[i] - st.head;
-          if (l < 0) l += st.cap;
-          pos = (st.jhead + l) * (long long)sm.G + sm.g;
-        }
-        part_s[o * KP + i] = top.s[i];
-        part_p[o * KP + i] = pos;
-      }
-      part_floor[o] = top.drop;
-    }
-  }
-
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TC_TMEM_COLS)
-                 : "memory");
-  }
-}
-
 // q16[b] = fp16(q[b] / ||q[b]||), zero rows for b >= B and zero padding columns;
 // qscale[b] = ||q[b]|| turns a scan score back into query units.
 __global__ void __launch_bounds__(256) k_tc_prep(const double* __restrict__ q64, int B, int D, int Dp,
@@ -927,11 +554,8 @@ struct TcPlan {
   __half* q16 = nullptr;
   double* qscale = nullptr;
   CUtensorMap q_map;
-  CUtensorMap ring_map;       // 256-slot boxes (single-CTA kernel)
   CUtensorMap ring_map_half;  // 128-slot boxes (CTA-pair kernel)
   CUtensorMap ring_map_q;     // 64-slot boxes (CTA-pair kernel, half-width tail tiles)
-  bool pair = true;
-  bool quad = false;  // CTA-quad (query multicast): correct but measured slower than pairs (lockstep)
   int dbg = 0;  // MC_TC_DEBUG bisection switches: 1 no TMA, 2 no MMA, 4 no epilogue (timing only)
 };
 
@@ -974,16 +598,13 @@ TcPlan* tc_plan_create(__half* ring16, long long C, int Dp, int Bcap, int sm_cou
     return nullptr;
   }
   if (!encode_2d(&p->q_map, p->q16, p->Bcap, Dp, TC_BM, err, errlen) ||
-      !encode_2d(&p->ring_map, ring16, C, Dp, TC_BN, err, errlen) ||
       !encode_2d(&p->ring_map_half, ring16, C, Dp, 128, err, errlen) ||
       !encode_2d(&p->ring_map_q, ring16, C, Dp, 64, err, errlen)) {
     tc_plan_destroy(p);
     return nullptr;
   }
-  if (cudaFuncSetAttribute(k_tc_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tc_scan_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, TP_SMEM_PAIR) != cudaSuccess ||
-      cudaFuncSetAttribute(k_tc_scan_quad, cudaFuncAttributeMaxDynamicSharedMemorySize, TP_SMEM) != cudaSuccess) {
-    snprintf(err, errlen, "cannot raise dynamic shared memory to %d bytes", TC_SMEM);
+  if (cudaFuncSetAttribute(k_tc_scan_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, TP_SMEM_PAIR) != cudaSuccess) {
+    snprintf(err, errlen, "cannot raise dynamic shared memory to %d bytes", TP_SMEM_PAIR);
     tc_plan_destroy(p);
     return nullptr;
   }
@@ -999,17 +620,13 @@ void tc_plan_destroy(TcPlan* p) {
 
 int tc_bcap(const TcPlan* p) { return p->Bcap; }
 
-void tc_set_pair(TcPlan* p, bool pair) { p->pair = pair; }
-void tc_set_quad(TcPlan* p, bool quad) { p->quad = quad; }
-
-// M tiles (single CTA, 128 queries) or M pairs (CTA pair, 256 queries) for B queries.
-static int tc_nm(const TcPlan* p, int B) { return p->pair ? (B + 255) / 256 : (B + TC_BM - 1) / TC_BM; }
-
-int tc_chunks(const TcPlan* p, int B) {
-  if (p->pair && p->quad) return 2 * ((p->sm_count / 4) / tc_nm(p, B));  // one list per pair
-  const int units = p->pair ? p->sm_count / 2 : p->sm_count;  // clusters or CTAs
-  return units / tc_nm(p, B);
+// M pairs (CTA pair, 256 queries) for B queries.
+static int tc_nm(const TcPlan* p, int B) {
+  (void)p;
+  return (B + 255) / 256;
 }
+
+int tc_chunks(const TcPlan* p, int B) { return (p->sm_count / 2) / tc_nm(p, B); }  // one list per cluster
 
 const double* tc_qscale(const TcPlan* p) { return p->qscale; }
 
@@ -1028,16 +645,12 @@ cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const Rin
   const int nm = tc_nm(p, B);
   const int groups = tc_chunks(p, B);
   if (groups < 1 || groups > part.n_chunks) return cudaErrorInvalidValue;
-  const int rows = nm * (p->pair ? 256 : TC_BM);
+  const int rows = nm * 256;
   k_tc_prep<<<(rows + 7) / 8, 256, 0, s>>>(q64, B, D, p->Dp, p->q16, p->qscale);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const float margin = tc_margin(p->Dp);
-  if (p->pair && p->quad)
-    k_tc_scan_quad<<<4 * nm * (groups / 2), TC_THREADS, TP_SMEM, s>>>(p->q_map, p->ring_map_half, d_state, nm, B,
-                                                                      p->Dp / TC_BK, part.s, part.p, part.floor_,
-                                                                      groups, margin, sm);
-  else if (p->pair) {
+  {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * nm * groups);
     cfg.blockDim = dim3(TP_THREADS);
@@ -1052,9 +665,6 @@ cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const Rin
                               p->Dp / TC_BK,
                               part.s, part.p, part.floor_, groups, margin, sm, p->dbg);
   }
-  else
-    k_tc_scan<<<nm * groups, TC_THREADS, TC_SMEM, s>>>(p->q_map, p->ring_map, d_state, nm, B, p->Dp / TC_BK,
-                                                       part.s, part.p, part.floor_, groups, margin, sm);
   return cudaGetLastError();
 }
 

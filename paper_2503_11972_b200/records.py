@@ -78,12 +78,13 @@ class RetrievalResult:
         return self.entry is not None
 
 
-def _result_factory():
-    """A constructor for RetrievalResult that skips the frozen dataclass's per-field
+def _result_factory(cls=None):
+    """A constructor for RetrievalResult (or another frozen dataclass with the same three
+    fields, e.g. the host application's own) that skips the frozen dataclass's per-field
     object.__setattr__ calls (about half the cost of a batch's result objects).  The
-    instances are ordinary RetrievalResult objects: same fields, equality, hash and repr."""
+    instances are ordinary `cls` objects: same fields, equality, hash and repr."""
     new = object.__new__
-    cls = RetrievalResult
+    cls = RetrievalResult if cls is None else cls
 
     def make(entry, similarity, k):
         r = new(cls)
@@ -113,16 +114,18 @@ class ThresholdTable:
             raise ValueError("threshold table must not be empty")
         ks = [k for k, _ in table]
         taus = [tau for _, tau in table]
-        problems = (
-            (_rising(ks), f"k values must be strictly increasing: {ks}"),
-            (_rising(taus), f"thresholds must be strictly increasing: {taus}"),
-            (all(-1.0 <= t <= 1.0 for t in taus), f"thresholds must lie in [-1, 1]: {taus}"),
-            (ks[-1] < total_steps, f"max k {ks[-1]} must stay below total steps {total_steps}"),
-            (all(k > 0 for k in ks), f"k values must be positive: {ks}"),
-        )
-        for ok, message in problems:  # checked in the reference's order
-            if not ok:
-                raise ValueError(message)
+        # the reference's predicates, evaluated lazily in its order (cache.py:84-93): a NaN
+        # tau passes `b <= a` and is caught by the range check, as there
+        if _falls(ks):
+            raise ValueError(f"k values must be strictly increasing: {ks}")
+        if _falls(taus):
+            raise ValueError(f"thresholds must be strictly increasing: {taus}")
+        if any(not -1.0 <= t <= 1.0 for t in taus):
+            raise ValueError(f"thresholds must lie in [-1, 1]: {taus}")
+        if ks[-1] >= total_steps:
+            raise ValueError(f"max k {ks[-1]} must stay below total steps {total_steps}")
+        if any(k <= 0 for k in ks):
+            raise ValueError(f"k values must be positive: {ks}")
         self.pairs = tuple(table)
         self.total_steps = int(total_steps)
 
@@ -145,8 +148,9 @@ class ThresholdTable:
         return met[-1] if met else None
 
 
-def _rising(values: list) -> bool:
-    return all(a < b for a, b in zip(values, values[1:]))
+def _falls(values: list) -> bool:
+    """Some neighbour fails to rise (the reference's `any(b <= a ...)`, NaN-tolerant like it)."""
+    return any(b <= a for a, b in zip(values, values[1:]))
 
 
 # -- noise re-entry schedule (cache.py:305-334); exported, not on the lookup path ---------

@@ -7,14 +7,31 @@ keeps the full metadata FIFO (the reference's ``_store``, cache.py:164), so
 validation, eviction decisions and the returned ``CacheEntry`` objects are
 identical on all ranks; only the embeddings are divided.
 
-A lookup is SPMD: every rank passes the same query batch, scans its shard
-with the certified local scan (``mc_retrieve_local_async`` -> one 32-byte
+Two deployments share this code:
+
+* ``group`` mode (default): one process per GPU, the shard = the rank of a
+  torch.distributed group.  A lookup is SPMD: every rank passes the same
+  query batch, scans its shard with the certified local scan (``mc_retrieve_local_async`` -> one 32-byte
 ``mc_record`` per query: exact float64 best, runner-up, global position,
 flags), the records are all-gathered (``torch.distributed``: NCCL on GPUs,
 gloo in the CPU tests) and each rank merges the G records on the device
 (``mc_merge_records``: max similarity, ties to the newer position, then the
 threshold / k epilogue).  That all-gather of B x 32 bytes per rank is the
 path's only collective.
+* ``local_shards=G`` mode: one process drives all G shard rings (on
+  ``devices``, one per shard; several shards may share a device).  Each
+  shard's local scan writes its records straight into its slice of one
+  [G, B] record buffer on the merging device (a peer copy when the shard lives
+  on another GPU), and the merge runs there — no collective at all.  With
+  every shard on one device this is the single-GPU test bed of the sharded
+  kernels (tests/test_gpu_parity.py).
+
+Partition: round-robin by append position (module doc above) keeps the
+shards within one row of each other at every fill level and through age
+evictions, so the slowest shard — which sets the lookup's time — never
+holds more than ceil(n/G) rows.  A contiguous ring-slot range per shard
+(SURVEY.md §8 e) balances only a full ring; DESIGN.md §7 quantifies the
+difference on the C4 trace (profiles/partition_r02.txt).
 
 FIFO bookkeeping evicts before it appends — the capacity evictions an insert
 will cause are known up front — so a shard ring of ceil(C/G) rows never has
@@ -62,31 +79,48 @@ class ShardedSemanticCache:
 
     def __init__(self, capacity: int, dim: int = DEFAULT_DIM, policy: str = POLICY_ALL,
                  max_age_s: float | None = None, device: int | None = None, group=None,
-                 ring_factory=None):
+                 ring_factory=None, local_shards: int | None = None, devices=None):
         if capacity < 1:
             raise ValueError(f"capacity must be >= 1, got {capacity}")
         if policy not in POLICIES:
             raise ValueError(f"unknown cache policy {policy!r}, expected one of {POLICIES}")
         if max_age_s is not None and max_age_s <= 0:
             raise ValueError(f"max_age_s must be positive, got {max_age_s}")
-        import torch.distributed as dist
-
-        self._dist = dist
-        self._group = group
-        self.n_shards = dist.get_world_size(group)
-        self.shard = dist.get_rank(group)
         self.capacity = int(capacity)
         self.dim = int(dim)
         self.policy = policy
         self.max_age_s = max_age_s
         self.device = _default_device() if device is None else int(device)
+        self._group = group
+        if local_shards is None:
+            import torch.distributed as dist
+
+            self._dist = dist
+            self.n_shards = dist.get_world_size(group)
+            self.shard = dist.get_rank(group)
+            owned = {self.shard: self.device}
+        else:
+            if local_shards < 1:
+                raise ValueError(f"local_shards must be >= 1, got {local_shards}")
+            self._dist = None
+            self.n_shards = int(local_shards)
+            self.shard = 0
+            devs = [self.device] * self.n_shards if devices is None else [int(x) for x in devices]
+            if len(devs) != self.n_shards:
+                raise ValueError(f"need one device per shard: {len(devs)} devices for {self.n_shards} shards")
+            owned = dict(enumerate(devs))
         self._store = EntryFifo()
         self._next_seq = 0
         self._appended = 0  # global append position of the next entry
         if ring_factory is None:
             from ._native import DeviceRing as ring_factory
-        self.ring = ring_factory(math.ceil(self.capacity / self.n_shards), self.dim, self.device)
-        self.ring.configure_shard(self.n_shards, self.shard)
+        cap_g = math.ceil(self.capacity / self.n_shards)
+        self._rings = {}
+        for g, dev in owned.items():
+            ring = ring_factory(cap_g, self.dim, dev)
+            ring.configure_shard(self.n_shards, g)
+            self._rings[g] = ring
+        self.ring = self._rings[min(self._rings)]  # the merging shard's ring
         self._table_key = None
 
     # -- bookkeeping -------------------------------------------------------------
@@ -112,14 +146,16 @@ class ShardedSemanticCache:
         return True
 
     def _evict(self, n: int, evicted: list) -> None:
-        """Drop the n oldest entries everywhere; this shard drops the ones it owns."""
+        """Drop the n oldest entries everywhere; each owned shard drops the ones it holds."""
         if n <= 0:
             return
-        mine = _count_owned(self.oldest_position, n, self.shard, self.n_shards)
+        p_lo = self.oldest_position
+        for g, ring in self._rings.items():
+            mine = _count_owned(p_lo, n, g, self.n_shards)
+            if mine:
+                ring.evict_front(mine)
         for _ in range(n):
             evicted.append(self._store.popleft())
-        if mine:
-            self.ring.evict_front(mine)
 
     def insert(self, entry: CacheEntry) -> list[CacheEntry]:
         """cache.py:206-235 semantics, on every rank with the same entry stream."""
@@ -148,8 +184,9 @@ class ShardedSemanticCache:
         # capacity eviction of the append below, applied first (see module doc)
         self._evict(len(store) + 1 - self.capacity, evicted)
         store.append(entry)
-        if self._appended % self.n_shards == self.shard:
-            self.ring.append1(emb)
+        ring = self._rings.get(self._appended % self.n_shards)
+        if ring is not None:
+            ring.append1(emb)
         self._appended += 1
         if entry.seq >= self._next_seq:
             self._next_seq = entry.seq + 1
@@ -175,9 +212,10 @@ class ShardedSemanticCache:
             # capacity evictions first (module doc), then this shard's share of the appends
             self._evict(len(self._store) + len(batch) - self.capacity, evicted)
             p0 = self._appended
-            mine = [e.embedding for j, e in enumerate(batch) if (p0 + j) % self.n_shards == self.shard]
-            if mine:
-                self.ring.append(np.stack(mine))
+            for g, ring in self._rings.items():
+                mine = [e.embedding for j, e in enumerate(batch) if (p0 + j) % self.n_shards == g]
+                if mine:
+                    ring.append(np.stack(mine))
             self._store.extend(batch)
             self._appended += len(batch)
             self._next_seq = max(self._next_seq, batch[-1].seq + 1)
@@ -187,16 +225,29 @@ class ShardedSemanticCache:
 
     # -- lookups (SPMD: every rank passes the same queries) -----------------------
     def _records(self, Q: np.ndarray):
-        """Local records -> all-gathered [G, B] record bytes, on the comm device."""
+        """Every shard's local records -> one [G, B] record buffer on the merging device."""
         import torch
 
         B = Q.shape[0]
+        nb = B * RECORD_BYTES
         dev = self.ring.records_device()
-        local = torch.empty(B * RECORD_BYTES, dtype=torch.uint8, device=dev)
         stream = torch.cuda.current_stream(dev).cuda_stream if dev.type == "cuda" else 0
-        self.ring.retrieve_local_async(Q, local, stream)
-        gathered = torch.empty(self.n_shards * B * RECORD_BYTES, dtype=torch.uint8, device=dev)
-        self._dist.all_gather_into_tensor(gathered, local, group=self._group)
+        gathered = torch.empty(self.n_shards * nb, dtype=torch.uint8, device=dev)
+        if self._dist is not None:  # one shard per rank: all-gather the B records (the only collective)
+            local = torch.empty(nb, dtype=torch.uint8, device=dev)
+            self.ring.retrieve_local_async(Q, local, stream)
+            self._dist.all_gather_into_tensor(gathered, local, group=self._group)
+            return gathered, stream
+        for g, ring in self._rings.items():  # every shard in this process: write the slices directly
+            rdev = ring.records_device()
+            if rdev == dev:
+                ring.retrieve_local_async(Q, gathered[g * nb:(g + 1) * nb], stream)
+            else:  # shard on a peer GPU: its records cross NVLink as one peer copy
+                local = torch.empty(nb, dtype=torch.uint8, device=rdev)
+                rs = torch.cuda.current_stream(rdev)
+                ring.retrieve_local_async(Q, local, rs.cuda_stream)
+                torch.cuda.current_stream(dev).wait_stream(rs)
+                gathered[g * nb:(g + 1) * nb].copy_(local, non_blocking=True)
         return gathered, stream
 
     def retrieve_batch(self, Q: np.ndarray, table: ThresholdTable) -> list[RetrievalResult]:
@@ -209,16 +260,17 @@ class ShardedSemanticCache:
             return [_MISS_EMPTY] * Q.shape[0]
         key = (table.pairs, table.total_steps)
         if key != self._table_key:
-            self.ring.set_table(table.pairs, table.total_steps)
+            for ring in self._rings.values():
+                ring.set_table(table.pairs, table.total_steps)
             self._table_key = key
         gathered, stream = self._records(Q)
         live, sim, k, flags = self.ring.merge_records(gathered, self.n_shards, Q.shape[0], self.oldest_position,
                                                       stream)
-        store = self._store
+        at = self._store.live
         out = []
         for i, f in enumerate(np.asarray(flags).tolist()):
             if f & _HIT:
-                out.append(make_result(store[int(live[i])], float(sim[i]), int(k[i]) or None))
+                out.append(make_result(at(int(live[i])), float(sim[i]), int(k[i]) or None))
             elif f & _EMPTY:
                 out.append(_MISS_EMPTY)
             else:
@@ -230,5 +282,10 @@ class ShardedSemanticCache:
             raise EmbeddingError(f"query has shape {q.shape}, cache dim is {self.dim}")
         return self.retrieve_batch(q[None, :], table)[0]
 
+    def shard_sizes(self) -> list[int]:
+        """Live rows per shard held by this process (shard id order)."""
+        return [len(self._rings[g]) for g in sorted(self._rings)]
+
     def close(self) -> None:
-        self.ring.close()
+        for ring in self._rings.values():
+            ring.close()

@@ -24,6 +24,26 @@ class FakeRing:
 
     def set_table(self, pairs, total_steps):
         self.pairs = tuple(pairs)
+        self.total_steps = int(total_steps)
+
+    def set_sigma_schedule(self, schedule):
+        self.schedule = None if schedule is None else np.asarray(schedule, dtype=np.float64)
+
+    def decisions(self, Q):
+        """The device epilogue's serving decision, restated (merge.cuh decide): steps = T - k
+        (engine.py:38-45), route (scheduler.py:80-89), sigma[k] (cache.py:325-334)."""
+        live, sim, k, flags = self.retrieve(Q)
+        out = np.zeros(len(live), dtype=_native.DECISION_DTYPE)
+        out["live"], out["similarity"], out["k"], out["flags"] = live, sim, k, flags
+        hit = (flags & _native.MC_FLAG_HIT) != 0
+        out["route"] = hit
+        out["steps"] = np.where(hit, self.total_steps - k, self.total_steps)
+        sched = getattr(self, "schedule", None)
+        out["sigma"] = np.nan
+        if sched is not None:
+            ok = hit & (k > 0) & (k < len(sched))
+            out["sigma"][ok] = sched[k[ok]]
+        return out
 
     def append(self, rows):
         rows = np.asarray(rows, dtype=np.float64).reshape(-1, self.dim)

@@ -23,9 +23,30 @@ SIM_TOL = 1e-3  # north-star tolerance, written in the test
 AMBIG = _native.MC_FLAG_NEAR_TAU | _native.MC_FLAG_NEAR_TIE
 
 
+_PARITY = []  # per-check counts, written to gpurun_out/parity_<label>.json (profiles/parity_r02.txt)
+
+
 @pytest.fixture(scope="module", autouse=True)
 def native():
     _native.load()
+    yield
+    if _PARITY:
+        import json
+        import os
+        from pathlib import Path
+
+        out = Path(__file__).resolve().parents[1] / "gpurun_out"
+        out.mkdir(exist_ok=True)
+        path = out / f"parity_{os.environ.get('PARITY_TAG', 'gpu')}.jsonl"
+        with open(path, "a") as fh:
+            for row in _PARITY:
+                fh.write(json.dumps(row) + "\n")
+
+
+def _record_parity(label, stats):
+    """Ties, near-threshold, near-tie and certificate-fallback counts of one parity check
+    (north_star: "with ties and near-threshold cases reported")."""
+    _PARITY.append(dict(check=label, **{k: int(v) for k, v in stats.items()}))
 
 
 def _close(a, b, tol=1e-12):
@@ -63,6 +84,12 @@ def test_golden_op_logs(name):
             continue
         assert (seq, live, k) == (b[0], b[1], b[3]), (name, i, a, b)
     print(f"{name}: {len(got)} lookups, {n_bit} bit-identical similarities, {n_ambig} ulp-ambiguous (reported)")
+    _record_parity(f"golden {name}", dict(queries=len(got), sim_bit_equal=n_bit, ambiguous=n_ambig,
+                                          exact_ties=sum(bool(a[4] & _native.MC_FLAG_TIE) for a in got),
+                                          near_tau=sum(bool(a[4] & _native.MC_FLAG_NEAR_TAU) for a in got),
+                                          near_tie=sum(bool(a[4] & _native.MC_FLAG_NEAR_TIE) for a in got),
+                                          fallback=sum(bool(a[4] & _native.MC_FLAG_FALLBACK) for a in got),
+                                          hits=sum(a[0] is not None for a in got)))
 
 
 def _fill(cache, oracle, rows, t0=0):
@@ -72,17 +99,29 @@ def _fill(cache, oracle, rows, t0=0):
             oracle.insert(OracleEntry(f"e{t0 + i}", v, "large", t0 + i, float(t0 + i)))
 
 
-def _check_against_scan(cache, matrix, Q, table, label):
+def _check_against_scan(cache, matrix, Q, table, label, sims_all=None):
+    """Every answer of one batched lookup against the reference's independent scan formula
+    (test_acceptance.py:429-436).  `sims_all` ([B, n] float64) skips recomputing matrix @ q."""
     live, sim, k, flags = cache.retrieve_flags(Q, table)
     ot = OracleTable(table.pairs, table.total_steps)
-    stats = dict(ambiguous=0, ties=0, fallback=0, hits=0)
+    stats = dict(queries=len(Q), hits=0, exact_ties=0, near_tau=0, near_tie=0, fallback=0, oracle_near_set=0,
+                 ambiguous=0, sim_bit_equal=0)
     for i, q in enumerate(Q):
-        hit_idx, best, kk, arg = scan_oracle(matrix, q, ot)
+        sims = matrix @ q if sims_all is None else sims_all[i]
+        best = float(sims.max())
+        arg = int(np.flatnonzero(sims == best)[-1])
+        kk = ot.select_k(best)
+        hit_idx = None if best < ot.tau else arg
         assert abs(sim[i] - best) <= 1e-12, (label, i, sim[i], best)
-        sims = matrix @ q
+        assert abs(sim[i] - best) <= SIM_TOL
+        stats["sim_bit_equal"] += sim[i] == best
         near = np.flatnonzero(sims >= best - 1e-12)  # the oracle's own ulp-ambiguous argmax set
-        stats["ties"] += bool(flags[i] & _native.MC_FLAG_TIE)
+        stats["exact_ties"] += bool(flags[i] & _native.MC_FLAG_TIE)
+        stats["near_tau"] += bool(flags[i] & _native.MC_FLAG_NEAR_TAU)
+        stats["near_tie"] += bool(flags[i] & _native.MC_FLAG_NEAR_TIE)
         stats["fallback"] += bool(flags[i] & _native.MC_FLAG_FALLBACK)
+        stats["oracle_near_set"] += len(near) > 1
+        stats["hits"] += bool(flags[i] & _native.MC_FLAG_HIT)
         if flags[i] & AMBIG or len(near) > 1:
             # numpy's dgemv may round identical rows differently (SURVEY.md §0 finding 3):
             # the index is reported, and must lie in the oracle's near-tie set.
@@ -96,8 +135,8 @@ def _check_against_scan(cache, matrix, Q, table, label):
         assert got_hit == (hit_idx is not None), (label, i)
         assert int(live[i]) == arg, (label, i, live[i], arg)
         assert (int(k[i]) or None) == kk, (label, i, k[i], kk)
-        stats["hits"] += got_hit
     print(label, stats)
+    _record_parity(label, stats)
     return stats
 
 
@@ -178,7 +217,7 @@ def test_exact_duplicates_tie_to_newest_and_fallback():
     _fill(c, None, rows)
     Q = np.concatenate([pool, wl_noise(pool, rng)])
     st = _check_against_scan(c, rows, Q, ThresholdTable.default(), "duplicates")
-    assert st["ties"] >= 12  # every pool vector is duplicated many times
+    assert st["exact_ties"] >= 12  # every pool vector is duplicated many times
     assert st["fallback"] >= 1  # > K' duplicates inside a chunk forces the exhaustive path
 
 
@@ -283,9 +322,7 @@ def test_reference_suite_kats_on_gpu():
 
 def _paths(cache, Q, table):
     out = {}
-    for name, path in (("gemv", _native.PATH_GEMV), ("gemm", _native.PATH_GEMM), ("gemm1", _native.PATH_GEMM_1SM),
-                       ("gemm4", _native.PATH_GEMM_QUAD), ("gemv8", _native.PATH_GEMV8),
-                       ("stream8", _native.PATH_STREAM8), ("gemm8", _native.PATH_GEMM8)):
+    for name, path in (("gemv", _native.PATH_GEMV), ("gemm", _native.PATH_GEMM), ("stream8", _native.PATH_STREAM8)):
         cache.ring.set_path(path)
         out[name] = cache.retrieve_flags(Q, table)
     cache.ring.set_path(_native.PATH_AUTO)
@@ -312,17 +349,11 @@ def test_tensor_core_scan_matches_gemv_and_oracle(dim, cap, n_ins, B):
     keep = ~((fv | fm) & AMBIG).astype(bool)
     assert np.array_equal(lv[keep], lm[keep]) and np.array_equal(kv, km)
     assert np.array_equal(sv, sm_)  # both certified float64 rescoring: bit-identical
-    for name in ("gemv8", "stream8", "gemm8"):  # int8 scans (CUDA cores / tensor cores): same certified answers
-        l8, s8, k8, f8 = res[name]
-        keep8 = ~((fv | f8) & AMBIG).astype(bool)
-        assert np.array_equal(lv[keep8], l8[keep8]) and np.array_equal(kv, k8) and np.array_equal(sv, s8), name
-    for other in ("gemm1", "gemm4"):  # CTA-pair vs single-CTA vs CTA-quad tensor-core kernels
-        for a, b in zip(res["gemm"], res[other]):
-            assert np.array_equal(a, b)
+    l8, s8, k8, f8 = res["stream8"]  # the int8 streamed scan (CUDA cores): same certified answers
+    keep8 = ~((fv | f8) & AMBIG).astype(bool)
+    assert np.array_equal(lv[keep8], l8[keep8]) and np.array_equal(kv, k8) and np.array_equal(sv, s8)
     c.ring.set_path(_native.PATH_GEMM)
     _check_against_scan(c, live_rows, Q, table, f"gemm d{dim} cap{cap} B{B}")
-    c.ring.set_path(_native.PATH_GEMM8)
-    _check_against_scan(c, live_rows, Q, table, f"gemm8 d{dim} cap{cap} B{B}")
     st = c.ring.stats()
     assert st["gemm_launches"] >= 2
     c.close()
@@ -360,7 +391,7 @@ def test_int8_and_fp16_small_batch_paths_with_pending_appends(dim):
     wl = ClusteredWorkload(dim, n_clusters=24, seed=100 + dim)
     cap = 1500
     table, ot = ThresholdTable.default(), OracleTable()
-    for path in (_native.PATH_STREAM8, _native.PATH_GEMV8, _native.PATH_GEMV):
+    for path in (_native.PATH_STREAM8, _native.PATH_GEMV):
         c = SemanticCache(capacity=cap, dim=dim)
         o = OracleCache(cap, dim)
         c.ring.set_path(path)
@@ -450,9 +481,10 @@ def test_async_lookup_overlapping_inserts_matches_oracle():
 
 
 @pytest.mark.parametrize("dim,cap,n_ins,B", [(1024, 100_000, 100_000, 256), (768, 9000, 20_000, 64), (100, 700, 1800, 5)])
-def test_int8_tensor_core_scan_matches_oracle(dim, cap, n_ins, B):
-    """tcgen05 kind::i8 scan (the batched default) against the reference scan formula: full C3 shape,
-    a wrapped partial window, and a tiny D (zero-padded K block)."""
+def test_default_batched_path_at_the_c3_shape(dim, cap, n_ins, B):
+    """The path AUTO takes for B >= 5 (the fp16 tcgen05 CTA-pair scan + certified merge), not a forced
+    one, against the reference scan formula: the exact C3 shape (100k x 1024, B = 256), a wrapped
+    partial window, and a tiny D (zero-padded K block)."""
     wl = ClusteredWorkload(dim, n_clusters=128, seed=dim + cap)
     rows = wl.cache_rows(n_ins)
     c = SemanticCache(capacity=cap, dim=dim)
@@ -460,8 +492,9 @@ def test_int8_tensor_core_scan_matches_oracle(dim, cap, n_ins, B):
     live_rows = rows[-cap:]
     c._store.extend(CacheEntry(f"e{i}", r, "large", i, 0.0) for i, r in enumerate(live_rows))
     Q = wl.queries(B)
-    c.ring.set_path(_native.PATH_GEMM8)
-    st = _check_against_scan(c, live_rows, Q, ThresholdTable.default(), f"gemm8 d{dim} B{B}")
+    g0 = c.ring.stats()["gemm_launches"]
+    st = _check_against_scan(c, live_rows, Q, ThresholdTable.default(), f"auto d{dim} B{B}")
+    assert c.ring.stats()["gemm_launches"] == g0 + 1  # answered by the tensor-core scan
     assert st["fallback"] <= max(2, B // 50)
     c.close()
 
@@ -474,26 +507,147 @@ def test_parameter_block_inputs_match_oracle(monkeypatch):
     test_fifo_insert_per_request_matches_oracle_cache()
 
 
-def test_serving_decisions_on_device_match_sequential_lookups():
-    """SURVEY §8 f3 on the device path: route / steps / sigma from one batched lookup equal the
-    per-query retrieve() results (engine.py:38-45, scheduler.py:80-89, cache.py:305-334)."""
-    from paper_2503_11972_b200 import linear_sigma_schedule, noise_reentry_level
+@pytest.mark.parametrize("B", [1, 3, 48])
+def test_serving_decisions_match_the_oracle(B):
+    """route, steps = T - k and sigma[k] come out of the device's decision epilogue
+    (csrc/merge.cuh decide, through the packed zero-copy record for B <= 4 and the tensor-core
+    path's merge for B >= 5) and must equal the oracle's decision pushed through the reference's
+    own rules: engine.py:38-45 (service_time steps), scheduler.py:80-89 (route) and
+    cache.py:305-334 (linear_sigma_schedule / noise_reentry_level)."""
+    from paper_2503_11972_b200 import linear_sigma_schedule
 
-    wl = ClusteredWorkload(768, n_clusters=32, seed=99)
+    wl = ClusteredWorkload(768, n_clusters=32, seed=99 + B)
+    rows = wl.cache_rows(6000)
     c = SemanticCache(capacity=6000, dim=768)
-    c.bulk_load(CacheEntry(f"e{i}", v, "large", i, float(i)) for i, v in enumerate(wl.cache_rows(6000)))
+    c.bulk_load(CacheEntry(f"e{i}", v, "large", i, float(i)) for i, v in enumerate(rows))
+    for table in (ThresholdTable.default(), ThresholdTable([(5, 0.45), (10, 0.47), (15, 0.49), (20, 0.51)], 40)):
+        T = table.total_steps
+        sched = linear_sigma_schedule(T)
+        ot = OracleTable(table.pairs, T)
+        Q = np.concatenate([wl.queries(max(1, B - B // 4)), np.stack([v / np.linalg.norm(v) for v in
+                            np.random.default_rng(B).standard_normal((B // 4, 768))])]) if B > 1 else wl.queries(1)
+        for schedule in (sched, None):
+            dec = c.serving_decisions(Q, table, schedule)
+            for q, row in zip(Q, dec):
+                hit_idx, best, kk, arg = scan_oracle(rows, q, ot)
+                hit = hit_idx is not None
+                assert bool(row["hit"]) == hit and row["route"] == int(hit)
+                assert abs(row["similarity"] - best) <= 1e-12
+                assert row["k"] == (kk or 0) and row["steps"] == T - (kk or 0)  # service_time, engine.py:44
+                if hit:
+                    assert row["live"] == arg
+                    want = float(schedule[kk]) if schedule is not None else None  # noise_reentry_level
+                    assert (np.isnan(row["sigma"]) if want is None else row["sigma"] == want)
+                else:
+                    assert row["live"] == -1 and np.isnan(row["sigma"])
+    c.close()
+
+
+def test_c2_request_stream_against_the_oracle_cache():
+    """C2 as served: a 100k x 768 cache, then 600 batch-1 requests, each a retrieve_async (the
+    streamed int8 scan, zero-copy result) with that request's FIFO insert staged while the scan
+    runs -- every answer (hit/miss, entry, k, similarity) against the float64 oracle cache fed
+    the same op stream (cache.py:244-260 on the reference's own growable window)."""
+    wl = ClusteredWorkload(768, n_clusters=512, seed=1717)
+    n = 100_000
+    rows = wl.cache_rows(n)
+    c = SemanticCache(capacity=n, dim=768)
+    o = OracleCache(n, 768)
+    c.bulk_load(CacheEntry(f"e{i}", v, "large", i, float(i)) for i, v in enumerate(rows))
+    for i, v in enumerate(rows):
+        o.insert(OracleEntry(f"e{i}", v, "large", i, float(i)))
+    table, ot = ThresholdTable.default(), OracleTable()
+    Q = wl.queries(600)
+    imgs = wl.images(Q)
+    stats = dict(queries=0, hits=0, exact_ties=0, near_tau=0, near_tie=0, fallback=0, sim_bit_equal=0)
+    for i, (q, img) in enumerate(zip(Q, imgs)):
+        e, sim, k = o.retrieve_entry(q, ot)
+        pend = c.retrieve_async(q, table)
+        c.add(f"n{i}", img, "large", float(n + i))
+        o.insert(OracleEntry(f"n{i}", img, "large", n + i, float(n + i)))
+        r = pend.result()
+        assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), i
+        assert r.k == k and abs(r.similarity - sim) <= 1e-12, (i, r.similarity, sim)
+        stats["queries"] += 1
+        stats["hits"] += r.hit
+        stats["sim_bit_equal"] += r.similarity == sim
+    fl = c.ring.stats()
+    stats["fallback"] = fl["fallbacks"]
+    stats["exact_ties"] = fl["ties"]
+    _record_parity("C2 100k x 768 request stream (retrieve_async + add)", stats)
+    assert len(c) == len(o) == len(c.ring) == n
+    c.close()
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_native_shards_on_one_device(G):
+    """The sharded path's native pieces on one GPU: G shard rings (mc_configure_shard, global
+    positions dealt round-robin) on cuda:0, each writing its certified local records
+    (mc_retrieve_local_async) into slice g of one [G, B] record buffer, then mc_merge_records
+    (k_finalize over G records).  Churn through capacity, age and policy evictions, every answer
+    against the single-cache oracle; plus a batched (tensor-core) lookup on every shard."""
+    from paper_2503_11972_b200.sharded import ShardedSemanticCache
+
+    rng = np.random.default_rng(500 + G)
+    d, cap = 256, 1000 + G  # capacity not a multiple of G: shards of ceil(C/G) rows
+    sc = ShardedSemanticCache(cap, d, policy="large", max_age_s=400.0, local_shards=G)
+    oc = OracleCache(cap, d, policy="large", max_age_s=400.0)
+    table, ot = ThresholdTable.default(), OracleTable()
+    centers = rng.standard_normal((8, d))
+    t = 0.0
+    n_checked = 0
+    for i in range(3000):
+        t += float(rng.exponential(1.0)) + (500.0 if i in (1700, 2400) else 0.0)
+        v = centers[i % 8] + 0.9 * rng.standard_normal(d) / 2
+        v /= np.linalg.norm(v)
+        prod = "large" if rng.random() < 0.8 else "small"
+        ev1 = sc.insert(CacheEntry(f"e{i}", v, prod, i, t))
+        ev2 = oc.insert(OracleEntry(f"e{i}", v, prod, i, t))
+        assert [x.id for x in ev1] == [x.id for x in ev2], i
+        if i % 61 == 0 or i in (1700, 1701, 2400):
+            B = 1 + (i // 61) % 4 if i % 122 else 37  # small-batch and tensor-core scans per shard
+            Q = centers[rng.integers(0, 8, B)] + 0.9 * rng.standard_normal((B, d)) / 2
+            Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+            for q, r in zip(Q, sc.retrieve_batch(Q, table)):
+                e, sim, k = oc.retrieve_entry(q, ot)
+                assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (G, i)
+                assert r.k == k and _close(r.similarity, sim), (G, i, r, sim)
+                n_checked += 1
+    sizes = sc.shard_sizes()
+    assert sum(sizes) == len(sc) == len(oc) and max(sizes) - min(sizes) <= 1, sizes
+    assert n_checked > 150
+    _record_parity(f"native shards G={G} on one device", dict(queries=n_checked))
+    sc.close()
+
+
+def _chunked_scan(rows, Q, chunk=131072):
+    """Exact float64 sims of Q against `rows` in row chunks (numpy GEMM): [B, n]."""
+    out = np.empty((Q.shape[0], rows.shape[0]))
+    for s in range(0, rows.shape[0], chunk):
+        out[:, s:s + chunk] = (rows[s:s + chunk] @ Q.T).T
+    return out
+
+
+def test_one_million_entries_single_gpu():
+    """A 1M x 768 cache on one B200 (C4's size unsharded): batch-1 lookups on the streamed int8
+    scan and one B = 256 lookup on the tensor-core scan, sampled queries against the reference
+    scan formula (test_acceptance.py:429-436) computed in row chunks."""
+    n, d = 1_000_000, 768
+    wl = ClusteredWorkload(d, n_clusters=2048, seed=1000)
+    rows = wl.cache_rows(n)
+    c = SemanticCache(capacity=n, dim=d)
+    for s in range(0, n, 250_000):
+        c.ring.append(rows[s:s + 250_000])
+    c._store.extend(CacheEntry(f"e{i}", None, "large", i, 0.0) for i in range(n))
     table = ThresholdTable.default()
-    sched = linear_sigma_schedule(table.total_steps)
-    Q = np.concatenate([wl.queries(40), np.stack([v / np.linalg.norm(v) for v in
-                                                  np.random.default_rng(1).standard_normal((8, 768))])])
-    dec = c.serving_decisions(Q, table, sched)
-    for q, row in zip(Q, dec):
-        r = c.retrieve(q, table)
-        assert bool(row["hit"]) == r.hit and row["route"] == int(r.hit)
-        assert row["k"] == (r.k or 0) and row["steps"] == table.total_steps - (r.k or 0)
-        assert abs(row["similarity"] - r.similarity) <= 1e-12
-        if r.hit:
-            assert c.entries()[row["live"]] is r.entry and row["sigma"] == noise_reentry_level(r.k, sched)
+    Q1 = wl.queries(16)
+    S1 = _chunked_scan(rows, Q1)
+    for b in range(16):
+        _check_against_scan(c, rows, Q1[b:b + 1], table, f"1M x 768 B=1 #{b}", sims_all=S1[b:b + 1])
+    Q = wl.queries(256)
+    S = _chunked_scan(rows, Q)
+    st = _check_against_scan(c, rows, Q, table, "1M x 768 B=256", sims_all=S)
+    assert st["fallback"] <= 5
     c.close()
 
 
@@ -505,8 +659,7 @@ def test_random_operation_sequences_every_path(seed):
     dim = int(rng.choice([8, 96, 200, 512, 768, 1000]))
     cap = int(rng.integers(50, 3000))
     age = float(rng.choice([0.0, 400.0]))
-    paths = [_native.PATH_AUTO, _native.PATH_STREAM8, _native.PATH_GEMV8, _native.PATH_GEMV, _native.PATH_GEMM,
-             _native.PATH_GEMM8]
+    paths = [_native.PATH_AUTO, _native.PATH_STREAM8, _native.PATH_GEMV, _native.PATH_GEMM]
     c = SemanticCache(capacity=cap, dim=dim, policy="all", max_age_s=age or None)
     o = OracleCache(cap, dim, max_age_s=age or None)
     table, ot = ThresholdTable.default(), OracleTable()
@@ -567,4 +720,65 @@ def test_stream8_bound_epochs_across_the_32bit_wrap(monkeypatch):
     Q = wl.queries(24)
     for i in range(0, 24, 2):  # 12 batch-2 launches: epochs 2^32-5 .. 2^32-1, then 1, 2, ...
         _check_against_scan(c, rows, Q[i:i + 2], table, f"epoch wrap {i}")
+    c.close()
+
+
+def test_evict_only_then_batched_lookup_never_returns_an_evicted_row():
+    """an eviction with no append since the last lookup must reach the device
+    window before a tensor-core (B >= 5) scan; on a raw handle and on a shard-configured one."""
+    rng = np.random.default_rng(77)
+    d = 128
+    for shard in (None, (3, 1)):
+        ring = _native.DeviceRing(600, d, 0)
+        if shard:
+            ring.configure_shard(*shard)
+        rows = rng.standard_normal((600, d))
+        rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+        ring.append(rows)
+        ring.set_table(ThresholdTable.default().pairs, 50)
+        Q = rows[:8].copy()  # exact matches of the oldest rows
+        live, sim, k, flags = ring.retrieve(Q)
+        assert np.allclose(sim, 1.0) and (shard or np.array_equal(live, np.arange(8)))
+        ring.evict_front(20)  # evict only: no append before the next lookup
+        live, sim, k, flags = ring.retrieve(Q)
+        assert np.all(sim < 0.99), (shard, live, sim)  # the exact matches are gone
+        if not shard:
+            want = (rows[20:] @ Q.T).max(axis=0)
+            assert np.all(live >= 0) and np.allclose(sim, want, atol=1e-12)
+        ring.close()
+
+
+def test_concurrent_readers_see_their_own_answers():
+    """readers on several threads share one ring's buffers; each must get
+    the answer to its own query ("many readers", cache.py:144)."""
+    import threading
+
+    wl = ClusteredWorkload(384, n_clusters=64, seed=8)
+    rows = wl.cache_rows(4000)
+    c = SemanticCache(capacity=4000, dim=384)
+    c.bulk_load(CacheEntry(f"e{i}", v, "large", i, 0.0) for i, v in enumerate(rows))
+    table = ThresholdTable.default()
+    Q = rows[rng_idx := np.random.default_rng(9).integers(0, 4000, 64)]  # exact matches: answer = own row
+    errors = []
+
+    def reader(t):
+        try:
+            for j in range(200):
+                b = (t * 7 + j) % 64
+                if j % 3 == 0:
+                    rs = c.retrieve_batch(Q[b:b + 2] if b < 63 else Q[b:b + 1], table)
+                    r = rs[0]
+                else:
+                    r = c.retrieve(Q[b], table)
+                if r.entry.id != f"e{int(rng_idx[b])}" or r.k != 30:
+                    errors.append((t, j, b, r.entry.id))
+        except Exception as exc:  # pragma: no cover
+            errors.append(repr(exc))
+
+    ts = [threading.Thread(target=reader, args=(t,)) for t in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors[:5]
     c.close()

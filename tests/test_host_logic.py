@@ -180,3 +180,63 @@ class TestPureHelpers:
             noise_reentry_level(51, s)
         with pytest.raises(ValueError):
             validate_sigma_schedule(np.array([1.0, 0.2, 0.5, 0.0]))
+
+
+class TestAsyncLifecycle:
+    """a dropped retrieve_async future must not wedge the cache or its FIFO pin."""
+
+    def test_dropped_future_is_completed_by_the_next_lookup(self):
+        rng = np.random.default_rng(3)
+        c = SemanticCache(capacity=4, dim=8)
+        for i in range(4):
+            c.insert(entry(i, unit(rng, 8)))
+        q = unit(rng, 8)
+        fut = c.retrieve_async(q, ThresholdTable.default())
+        want = c._ring.retrieve1(q)  # the answer for the state at submit time
+        del fut  # never .result()-ed
+        for i in range(4, 2100):  # churn past the compaction threshold: the pin must be released
+            c.insert(entry(i, unit(rng, 8)))
+        r = c.retrieve(q, ThresholdTable.default())  # completes the dropped lookup first
+        assert c._pending is None and c._store._pins == 0
+        c.insert(entry(2100, unit(rng, 8)))
+        assert len(c._store._items) < 100  # compaction runs again once unpinned
+        assert r.similarity is not None and want is not None
+
+    def test_result_is_kept_after_a_later_lookup_completed_it(self):
+        rng = np.random.default_rng(4)
+        c = SemanticCache(capacity=16, dim=8)
+        for i in range(16):
+            c.insert(entry(i, unit(rng, 8)))
+        q = c.entries()[5].embedding
+        fut = c.retrieve_async(q, ThresholdTable.default())
+        c.insert(entry(16, unit(rng, 8)))  # evicts e0 while the lookup is pending
+        c.retrieve_batch(np.stack([q, q]), ThresholdTable.default())  # settles the pending lookup
+        r = fut.result()
+        assert r.hit and r.entry.id == "e5" and r.k == 30
+
+    def test_out_of_window_device_index_fails_loudly(self):
+        from paper_2503_11972_b200 import _native
+
+        class BadRing(FakeRing):
+            def retrieve1(self, q):
+                live, sim, k, flags = super().retrieve1(q)
+                return -1, sim, k, flags | _native.MC_FLAG_HIT
+
+        c = SemanticCache(capacity=4, dim=8)
+        c._ring = BadRing(4, 8)
+        rng = np.random.default_rng(5)
+        for i in range(3):
+            c.insert(entry(i, unit(rng, 8)))
+        with pytest.raises(_native.NativeError, match="outside the window"):
+            c.retrieve(unit(rng, 8), ThresholdTable.default())
+
+
+def test_threshold_table_nan_message_matches_the_reference():
+    """with a NaN tau the reference's `any(b <= a)` passes and the range check
+    raises; the messages must match (cache.py:84-93)."""
+    with pytest.raises(ValueError, match="thresholds must lie in"):
+        ThresholdTable([(5, 0.25), (10, float("nan"))])
+    with pytest.raises(ValueError, match="thresholds must lie in"):
+        ThresholdTable([(5, float("nan")), (10, 0.3), (15, 0.4)])
+    with pytest.raises(ValueError, match="strictly increasing"):
+        ThresholdTable([(5, 0.3), (10, 0.3)])

@@ -111,3 +111,52 @@ def test_count_owned():
                 for n in range(0, 20):
                     want = sum(1 for p in range(lo, lo + n) if p % G == g)
                     assert _count_owned(lo, n, g, G) == want
+
+
+def _churn_against_oracle(make_cache, d=24, cap=37, steps=400, seed=123, B=4, check_every=9):
+    """Insert / evict / lookup churn (policy, age, capacity) vs the single-cache oracle."""
+    from oracle.retrieval import OracleCache, OracleEntry, OracleTable
+    from paper_2503_11972_b200 import CacheEntry, ThresholdTable
+
+    rng = np.random.default_rng(seed)
+    table, ot = ThresholdTable.default(), OracleTable()
+    centers = rng.standard_normal((5, d))
+    sc = make_cache(cap, d, "all", 60.0)
+    oc = OracleCache(cap, d, max_age_s=60.0)
+    t = 0.0
+    n_checked = 0
+    for i in range(steps):
+        t += float(rng.exponential(1.0)) + (80.0 if i in (150, 151, 300) else 0.0)
+        v = centers[i % 5] + 0.7 * rng.standard_normal(d)
+        v /= np.linalg.norm(v)
+        prod = "large" if rng.random() < 0.8 else "small"
+        ev1 = sc.insert(CacheEntry(f"e{i}", v, prod, i, t))
+        ev2 = oc.insert(OracleEntry(f"e{i}", v, prod, i, t))
+        assert [e.id for e in ev1] == [e.id for e in ev2], i
+        assert len(sc) == len(oc.meta) == sum(sc.shard_sizes())
+        if i % check_every == 0:
+            Q = centers[rng.integers(0, 5, B)] + 0.7 * rng.standard_normal((B, d))
+            Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+            for q, r in zip(Q, sc.retrieve_batch(Q, table)):
+                e, sim, k = oc.retrieve_entry(q, ot)
+                assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), i
+                assert r.k == k and (r.similarity is None) == (sim is None)
+                if sim is not None:
+                    assert abs(r.similarity - sim) < 1e-12
+                n_checked += 1
+    sizes = sc.shard_sizes()
+    assert max(sizes) - min(sizes) <= 1, sizes  # round-robin keeps the shards balanced
+    sc.close()
+    return n_checked
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+def test_local_shards_match_oracle_on_cpu(G):
+    """local_shards mode (every shard in one process, records written into one buffer, no
+    collective) over FakeShardRing: the host bookkeeping of the single-process sharded path."""
+    from paper_2503_11972_b200.sharded import ShardedSemanticCache
+    from tests.fake_shard_ring import FakeShardRing
+
+    n = _churn_against_oracle(lambda cap, d, pol, age: ShardedSemanticCache(
+        cap, d, policy=pol, max_age_s=age, ring_factory=FakeShardRing, local_shards=G))
+    assert n > 100
