@@ -91,6 +91,7 @@ struct mc_cache {
   long long n_pending = 0;
   long long pending_first_slot = 0;
   cudaEvent_t env_ev = nullptr;  // last async upload of the envelope (async paths only)
+  cudaEvent_t rec_ev = nullptr;  // a shard's local records are complete (mc_retrieve_local_async)
   bool env_inflight = false;
 
   // per-batch device buffers
@@ -804,6 +805,7 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   } while (0)
   CUC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   CUC(cudaEventCreateWithFlags(&h->env_ev, cudaEventDisableTiming));
+  CUC(cudaEventCreateWithFlags(&h->rec_ev, cudaEventDisableTiming));
   const size_t n16 = (size_t)h->C * h->Dp * sizeof(__half);
   const size_t n64 = (size_t)h->C * h->Dp * sizeof(double);
   const size_t n8 = (size_t)h->C * h->P8;
@@ -878,6 +880,7 @@ int mc_destroy(mc_cache* h) {
     cudaFreeHost(h->h_seq);
     cudaFreeHost(h->h_qkeep);
     if (h->env_ev) cudaEventDestroy(h->env_ev);
+    if (h->rec_ev) cudaEventDestroy(h->rec_ev);
     if (h->stream) cudaStreamDestroy(h->stream);
   }
   delete h;
@@ -1074,12 +1077,9 @@ int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void*
                            exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
     h->stats[7] += 2;
   }
-  if (stream && stream != h->stream) {
-    cudaEvent_t ev;
-    CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    CU(cudaEventRecord(ev, h->stream));
-    CU(cudaStreamWaitEvent((cudaStream_t)stream, ev, 0));
-    CU(cudaEventDestroy(ev));
+  if (stream && stream != h->stream) {  // order the caller's stream (the exchange) after this shard's scan
+    CU(cudaEventRecord(h->rec_ev, h->stream));
+    CU(cudaStreamWaitEvent((cudaStream_t)stream, h->rec_ev, 0));
   }
   h->stats[0] += B;
   return MC_OK;

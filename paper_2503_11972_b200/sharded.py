@@ -224,31 +224,51 @@ class ShardedSemanticCache:
         return evicted
 
     # -- lookups (SPMD: every rank passes the same queries) -----------------------
+    def _comm_stream(self, dev):
+        """A dedicated (non-default) stream for the record exchange and the merge: every
+        shard's scan is ordered before it by an event (mc_retrieve_local_async), which a
+        legacy default stream (handle 0, i.e. "the ring's own stream" to the C ABI) would not
+        get."""
+        import torch
+
+        st = getattr(self, "_streams", None)
+        if st is None:
+            st = self._streams = {}
+        if dev not in st:
+            st[dev] = torch.cuda.Stream(dev) if dev.type == "cuda" else None
+        return st[dev]
+
     def _records(self, Q: np.ndarray):
         """Every shard's local records -> one [G, B] record buffer on the merging device."""
+        import contextlib
+
         import torch
 
         B = Q.shape[0]
         nb = B * RECORD_BYTES
         dev = self.ring.records_device()
-        stream = torch.cuda.current_stream(dev).cuda_stream if dev.type == "cuda" else 0
-        gathered = torch.empty(self.n_shards * nb, dtype=torch.uint8, device=dev)
-        if self._dist is not None:  # one shard per rank: all-gather the B records (the only collective)
-            local = torch.empty(nb, dtype=torch.uint8, device=dev)
-            self.ring.retrieve_local_async(Q, local, stream)
-            self._dist.all_gather_into_tensor(gathered, local, group=self._group)
-            return gathered, stream
-        for g, ring in self._rings.items():  # every shard in this process: write the slices directly
-            rdev = ring.records_device()
-            if rdev == dev:
-                ring.retrieve_local_async(Q, gathered[g * nb:(g + 1) * nb], stream)
-            else:  # shard on a peer GPU: its records cross NVLink as one peer copy
-                local = torch.empty(nb, dtype=torch.uint8, device=rdev)
-                rs = torch.cuda.current_stream(rdev)
-                ring.retrieve_local_async(Q, local, rs.cuda_stream)
-                torch.cuda.current_stream(dev).wait_stream(rs)
-                gathered[g * nb:(g + 1) * nb].copy_(local, non_blocking=True)
-        return gathered, stream
+        cs = self._comm_stream(dev)
+        ctx = torch.cuda.stream(cs) if cs is not None else contextlib.nullcontext()
+        sp = cs.cuda_stream if cs is not None else 0
+        with ctx:
+            gathered = torch.empty(self.n_shards * nb, dtype=torch.uint8, device=dev)
+            if self._dist is not None:  # one shard per rank: all-gather the B records (the only collective)
+                local = torch.empty(nb, dtype=torch.uint8, device=dev)
+                self.ring.retrieve_local_async(Q, local, sp)
+                self._dist.all_gather_into_tensor(gathered, local, group=self._group)
+                return gathered, sp
+            for g, ring in self._rings.items():  # every shard in this process: write the slices directly
+                rdev = ring.records_device()
+                if rdev == dev:
+                    ring.retrieve_local_async(Q, gathered[g * nb:(g + 1) * nb], sp)
+                else:  # shard on a peer GPU: its records cross NVLink as one peer copy
+                    rs = self._comm_stream(rdev)
+                    local = torch.empty(nb, dtype=torch.uint8, device=rdev)
+                    ring.retrieve_local_async(Q, local, rs.cuda_stream)
+                    cs.wait_stream(rs)
+                    gathered[g * nb:(g + 1) * nb].copy_(local, non_blocking=True)
+                    local.record_stream(cs)
+        return gathered, sp
 
     def retrieve_batch(self, Q: np.ndarray, table: ThresholdTable) -> list[RetrievalResult]:
         Q = np.ascontiguousarray(Q, dtype=np.float64)

@@ -1,6 +1,9 @@
 """Drive one BASELINE config through the native ring for ncu / timing (no oracle, no host metadata).
 
-    python scripts/profile_case.py c2|c3 [--iters N] [--path auto|gemv|gemm|gemv8|stream8]
+    python scripts/profile_case.py c2|c3 [--iters N] [--path auto|gemv|gemm|stream8] [--rotate K]
+
+--rotate K: K rings with the same contents, lookup i on ring i % K (K x the scan copy > L2: cold HBM
+reads every lookup, as in bench.py's rotation).
 """
 import argparse
 import sys
@@ -20,20 +23,25 @@ ap.add_argument("--iters", type=int, default=6)
 ap.add_argument("--path", default="auto")
 ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--entries", type=int, default=0)
+ap.add_argument("--rotate", type=int, default=1)
 a = ap.parse_args()
 n, dim, B = CASES[a.case]
 B = a.batch or B
 n = a.entries or n
 wl = ClusteredWorkload(dim, n_clusters=512, seed=17)
 rows = wl.cache_rows(n)
-ring = _native.DeviceRing(n, dim, 0)
-ring.append(rows)
-ring.set_path({"auto": 0, "gemv": 1, "gemm": 2, "gemv8": 5, "stream8": 6, "gemm8": 7}[a.path])
+rings = []
 t = ThresholdTable.default()
-ring.set_table(t.pairs, t.total_steps)
+for _ in range(a.rotate):
+    ring = _native.DeviceRing(n, dim, 0)
+    ring.append(rows)
+    ring.set_path({"auto": 0, "gemv": 1, "gemm": 2, "stream8": 6}[a.path])
+    ring.set_table(t.pairs, t.total_steps)
+    rings.append(ring)
+ring = rings[0]
 Q = wl.queries(B * a.iters).reshape(a.iters, B, dim)
 for i in range(a.iters):
-    live, sim, k, flags = ring.retrieve(Q[i])
+    live, sim, k, flags = rings[i % a.rotate].retrieve(Q[i])
 print(a.case, "ok", ring.stats())
 
 import os  # noqa: E402
@@ -45,6 +53,7 @@ if os.environ.get("MC_GEMV_TIMING"):
     per = (ctypes.c_ulonglong * (12 * 512))()
     for i in range(a.iters):
         lib.mc_debug_gemv_timing(t, 1)  # reset
+        ring = rings[i % a.rotate]
         ring.retrieve(Q[i])
         lib.mc_debug_gemv_timing(t, 0)
         if not t[4]:  # register GEMV kernels: four global stamps

@@ -524,8 +524,10 @@ def test_serving_decisions_match_the_oracle(B):
         T = table.total_steps
         sched = linear_sigma_schedule(T)
         ot = OracleTable(table.pairs, T)
-        Q = np.concatenate([wl.queries(max(1, B - B // 4)), np.stack([v / np.linalg.norm(v) for v in
-                            np.random.default_rng(B).standard_normal((B // 4, 768))])]) if B > 1 else wl.queries(1)
+        Q = wl.queries(B - B // 4)
+        if B // 4:  # plus unrelated unit vectors (misses)
+            R = np.random.default_rng(B).standard_normal((B // 4, 768))
+            Q = np.concatenate([Q, R / np.linalg.norm(R, axis=1, keepdims=True)])
         for schedule in (sched, None):
             dec = c.serving_decisions(Q, table, schedule)
             for q, row in zip(Q, dec):
