@@ -766,6 +766,7 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
       wk.stage(i, st, row0, nr, slot0);
       mbar_wait(&S.full[buf], (i / nst) & 1);
       const uint8_t* sb = stages + (size_t)buf * SDATA;
+      const int lrot = lane % NCH;    // first chunk of this lane (NCH may be 8 < 32 lanes)
       int acc[R][NBQ], acc2[R][NBQ];  // two chains per dot (exact integers: order is free)
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -775,8 +776,7 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
       // launch, so a compact body keeps it resident in the instruction cache
 #pragma unroll 8
       for (int j = 0; j < NCH; ++j) {
-        int c = j + lane;  // rotated chunk order (conflict-free, see the header)
-        c = c >= NCH ? c - NCH : c;
+        int c = j + lrot;  // rotated chunk order (conflict-free, see the header)
         c = c >= NCH ? c - NCH : c;
         uint4 v[R];
 #pragma unroll

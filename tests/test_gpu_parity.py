@@ -409,6 +409,45 @@ def test_int8_and_fp16_small_batch_paths_with_pending_appends(dim):
         c.close()
 
 
+@pytest.mark.parametrize("dim", [32, 64, 100, 128, 160, 256, 384])
+def test_iid_rows_every_small_batch_path(dim):
+    """test_acceptance.py:411-443's workload shape: 10k i.i.d. unit rows (no cluster structure, so
+    many rows sit near the best) — every int8 row width (P8 = 128 ... 384, rows per lane 4/2/1)
+    and every small-batch path against the exact float64 argmax, on every query."""
+    rng = np.random.default_rng(4242)
+    n, nq = 10_000, 200
+    M = rng.standard_normal((n, dim))
+    M /= np.linalg.norm(M, axis=1, keepdims=True)
+    Q = rng.standard_normal((nq, dim))
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    c = SemanticCache(capacity=n, dim=dim)
+    c.bulk_load(CacheEntry(f"e{i}", M[i], "large", i, float(i)) for i in range(n))
+    table, ot = ThresholdTable.default(), OracleTable()
+    stats = {"queries": 0, "ties": 0, "near_tau": 0, "near_tie": 0, "fallback": 0}
+    for path in (_native.PATH_AUTO, _native.PATH_STREAM8, _native.PATH_GEMV):
+        c.ring.set_path(path)
+        for t in range(nq):
+            i, best, kk, arg = scan_oracle(M, Q[t], ot)
+            r = c.retrieve(Q[t], table) if path == _native.PATH_AUTO else None
+            live, sim, k, flags = c.retrieve_flags(Q[t][None], table)
+            f = int(flags[0])
+            stats["queries"] += 1
+            stats["ties"] += bool(f & _native.MC_FLAG_TIE)
+            stats["near_tau"] += bool(f & _native.MC_FLAG_NEAR_TAU)
+            stats["near_tie"] += bool(f & _native.MC_FLAG_NEAR_TIE)
+            stats["fallback"] += bool(f & _native.MC_FLAG_FALLBACK)
+            assert abs(sim[0] - best) <= 1e-12, (path, t, sim[0], best)
+            if f & _native.MC_FLAG_HIT:
+                assert int(live[0]) == arg and int(k[0]) == kk, (path, t, live[0], arg)
+            else:
+                assert kk is None or kk == 0, (path, t)
+            if r is not None:
+                assert abs(r.similarity - best) <= 1e-12, (t, r.similarity, best)
+                assert (r.entry.seq if r.hit else None) == (arg if kk else None), (t, r, arg)
+    _record_parity(f"iid_{dim}", stats)
+    c.close()
+
+
 def test_stream8_queue_overflow_falls_back_exactly():
     """Streamed int8 scan with every row an exact duplicate: each row survives the bound, the
     per-warp candidate queues overflow, the certificate fails and the exhaustive float64 path
