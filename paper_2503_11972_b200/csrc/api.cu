@@ -284,6 +284,8 @@ int ensure_batch(mc_cache* h, int B) {
   CU(cudaMalloc(&h->d_part_p, (size_t)cap * chunks * KP * sizeof(long long)));
   CU(cudaMalloc(&h->d_part_floor, (size_t)cap * chunks * sizeof(float)));
   CU(cudaMalloc(&h->d_cta, (size_t)cap * gemv_grid(h->sm_count) * sizeof(CtaRec)));
+  // the streamed scan's records are epoch-tagged: zero words belong to no launch
+  CU(cudaMemsetAsync(h->d_cta, 0, (size_t)cap * gemv_grid(h->sm_count) * sizeof(CtaRec), h->stream));
   // 256 words per query: the streamed scan keeps 8 replicas of its bound 128 B apart
   CU(cudaMalloc(&h->d_gmax, (size_t)cap * 256 * sizeof(unsigned)));
   CU(cudaMemsetAsync(h->d_gmax, 0, (size_t)cap * 256 * sizeof(unsigned), h->stream));
@@ -436,6 +438,7 @@ int ensure_tc(mc_cache* h, int B) {
 unsigned s8_epoch(mc_cache* h) {
   if (++h->s8_epoch == 0) {
     cudaMemsetAsync(h->d_gmax8, 0, (size_t)h->Bcap * 128 * sizeof(unsigned long long), h->stream);
+    cudaMemsetAsync(h->d_cta, 0, (size_t)h->Bcap * gemv_grid(h->sm_count) * sizeof(CtaRec), h->stream);
     h->s8_epoch = 1;
   }
   return h->s8_epoch;
@@ -822,7 +825,7 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
     RingState z{0, 0, 0, h->C};
     CUC(cudaMemcpyAsync(h->d_state, &z, sizeof z, cudaMemcpyHostToDevice, h->stream));
   }
-  if (stream8_supported(h->Dp)) {
+  if (stream8_supported(h->Dp) && h->C < (1ll << 30)) {  // 30-bit row offsets in its records
     char err[256] = {0};
     h->s8 = s8_plan_create(h->ring8, h->ringq, h->C, h->Dp, h->P8, err, sizeof err);
     if (!h->s8) return cleanup(fail(MC_ERR_CUDA, "int8 stream scan plan: %s", err));
@@ -911,6 +914,8 @@ int mc_configure_shard(mc_cache* h, int32_t n_shards, int32_t shard_id) {
     return fail(MC_ERR_ARG, "bad shard %d of %d", shard_id, n_shards);
   std::lock_guard<std::mutex> lk(h->mu);
   if (h->appended != 0) return fail(MC_ERR_STATE, "configure the shard before the first append");
+  if ((long long)h->C * n_shards >= (1ll << 30))  // the streamed scan's records carry 30-bit row offsets
+    return fail(MC_ERR_ARG, "capacity %lld x %d shards exceeds 2^30 rows", (long long)h->C, n_shards);
   h->shard = ShardMap{n_shards, shard_id};
   return MC_OK;
 }

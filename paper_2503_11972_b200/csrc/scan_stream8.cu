@@ -364,12 +364,35 @@ __device__ __forceinline__ void s8_pool(const S8Ctx x, int wid) {
   }
 }
 
-// The rescorer after the pool: the CTA record, the ticket and, in the last
-// CTA, the merge of every record and the decision (cache.py:255-260,
-// select_k :112-117), then the zero-copy completion word.
-__device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const QPrep* prep, CtaRec* cta, int b0) {
+// Per-CTA record of the streamed scan: two self-validating 16-byte words (each
+// stored and loaded as one 16-byte access), tagged with the launch epoch:
+//   [0] s (float64) | off (bits 0-29: global position - position of live row 0;
+//       0x3fffffff = no candidate) + min(ties, 3) << 30 | epoch
+//   [1] s2 (float64) | ovf (float bits) | epoch
+// No ticket: one merger (CTA 0's rescorer) polls the records until every one
+// carries this launch's epoch.  A word from an earlier launch never matches.
+constexpr unsigned S8_NOOFF = 0x3fffffffu;
+__device__ __forceinline__ uint4 ld_relaxed_v4(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_v4(uint4* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// The rescorer after the pool: the CTA record and, in CTA 0, the merge of
+// every CTA's record and the decision (cache.py:255-260, select_k :112-117),
+// then the zero-copy result.
+__device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const QPrep* prep, uint4* crec, int b0) {
   const int lane = threadIdx.x & 31;
   const int nb = x.nb;
+  const unsigned tag = a.epoch;
+  const long long pbase = global_pos(x.st, 0, x.sm);
   if (lane == 0)
     while (ld_acq_cta(&S.pool_done) != S8_CW + 2) {  // the nine pool warps and the eager rescorer
     }
@@ -381,13 +404,12 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
     for (int w = 0; w <= S8_EAGER; ++w) m.merge(S.best[w][b]);
     for (int w = 0; w < x.ncw; ++w) ov = fmaxf(ov, S.ovf[w][b]);
     if (lane == 0) {
-      CtaRec r;
-      r.s = m.s;
-      r.s2 = m.s2;
-      r.p = m.p;
-      r.ovf = ov;
-      r.ties = m.ties;
-      cta[(size_t)(b0 + b) * gridDim.x + blockIdx.x] = r;
+      const unsigned long long sb = (unsigned long long)__double_as_longlong(m.s);
+      const unsigned long long s2b = (unsigned long long)__double_as_longlong(m.s2);
+      const unsigned off = m.p < 0 ? S8_NOOFF : (unsigned)(m.p - pbase) | ((unsigned)min(m.ties, 3) << 30);
+      uint4* dst = crec + ((size_t)(b0 + b) * gridDim.x + blockIdx.x) * 2;
+      st_v4(dst, make_uint4((unsigned)sb, (unsigned)(sb >> 32), off, tag));
+      st_v4(dst + 1, make_uint4((unsigned)s2b, (unsigned)(s2b >> 32), __float_as_uint(ov), tag));
     }
   }
   if (x.timing && lane == 0) S.t[S8T_REC] = s8_timer();
@@ -396,77 +418,55 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
     if (x.timing && lane < 8) a.timing[8 + 8 * blockIdx.x + lane] = S.t[lane];
     if (x.timing && lane < 4) a.timing[8 + 8 * 512 + 4 * blockIdx.x + lane] = S.c[lane];
   };
-  unsigned exotic = 0;  // loaded before the ticket (off the tail's critical path)
-  if (lane < nb) exotic = prep[lane].exotic != 0 ? 1u : 0u;
-  unsigned old = 0;
-  if (lane == 0)
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.counter) : "memory");
-  old = __shfl_sync(FULL, old, 0);
-  if (old != gridDim.x - 1) {
+  if (blockIdx.x != 0) {
     dump();
     return;
   }
-  // No gpu-scope fence: every CTA's ticket is a release after its record store, lane 0's
-  // ticket here is an acquire (acq_rel), and the warp barrier orders the other lanes'
-  // record loads after it.
-  __syncwarp();
-  if (lane == 0 && x.timing) a.timing[4] = s8_timer();
+  unsigned exotic = 0;
+  if (lane < nb) exotic = prep[lane].exotic != 0 ? 1u : 0u;
   // Merge the per-CTA records with independent warp reductions (no chain of
   // Best2 merges): best = max s; among records at best: max position and the
   // summed tie counts; runner-up = max over the others' s and everyone's s2
   // (a second record at the best makes the runner-up equal to it, as in
   // Best2::merge).  Record similarities are finite here (exotic queries are
   // flagged for the exhaustive path).
+  constexpr int PER = 8;  // records per lane: grid <= 256 (the host clamps it)
   for (int b = 0; b < nb; ++b) {
     const int gb = b0 + b;
-    constexpr int PER = 5;  // records per lane, all loaded before use (grid <= 160: one round trip)
+    const uint4* src = crec + (size_t)gb * gridDim.x * 2;
+    uint4 ra[PER], rb2[PER];
+    unsigned ok = 0;  // bit k: record 32 k + lane seen
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (32 * k + lane >= (int)gridDim.x) ok |= 1u << k;
+    while (true) {
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        if (!(ok >> k & 1u)) {
+          const int c = 32 * k + lane;
+          ra[k] = ld_relaxed_v4(src + 2 * c);
+          rb2[k] = ld_relaxed_v4(src + 2 * c + 1);
+          if (ra[k].w == tag && rb2[k].w == tag) ok |= 1u << k;
+        }
+      }
+      if (__all_sync(FULL, ok == (1u << PER) - 1u)) break;
+    }
+    if (b == 0 && lane == 0 && x.timing) a.timing[4] = a.timing[5] = s8_timer();
     double rs[PER], rs2[PER];
     long long rp[PER];
     int rt[PER];
     float ro[PER];
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
-      const int c = 32 * k + lane;
-      rp[k] = -1;
-      rs[k] = rs2[k] = -INFINITY;
-      rt[k] = 0;
-      ro[k] = -INFINITY;
-      if (c < (int)gridDim.x) {
-        const CtaRec* src = cta + (size_t)gb * gridDim.x + c;
-        rs[k] = __ldcg(&src->s);
-        rs2[k] = __ldcg(&src->s2);
-        rp[k] = __ldcg(&src->p);
-        rt[k] = __ldcg(&src->ties);
-        ro[k] = __ldcg(&src->ovf);
-      }
+      const bool in = 32 * k + lane < (int)gridDim.x;
+      const unsigned off = in ? ra[k].z : S8_NOOFF;
+      rs[k] = __longlong_as_double((long long)(((unsigned long long)ra[k].y << 32) | ra[k].x));
+      rs2[k] = __longlong_as_double((long long)(((unsigned long long)rb2[k].y << 32) | rb2[k].x));
+      ro[k] = in ? __uint_as_float(rb2[k].z) : -INFINITY;
+      rp[k] = off == S8_NOOFF ? -1 : pbase + (long long)(off & S8_NOOFF);
+      rt[k] = (int)(off >> 30);
+      if (rp[k] < 0) rs[k] = rs2[k] = -INFINITY;
     }
-    for (int c0 = 32 * PER; c0 < (int)gridDim.x; c0 += 32) {  // grids beyond 160 CTAs
-      const int c = c0 + lane;
-      if (c < (int)gridDim.x) {
-        const CtaRec* src = cta + (size_t)gb * gridDim.x + c;
-        Best2 m0, mx;
-        m0.init();
-        if (rp[0] >= 0) {
-          m0.s = rs[0];
-          m0.s2 = rs2[0];
-          m0.p = rp[0];
-          m0.ties = rt[0];
-        }
-        mx.s = __ldcg(&src->s);
-        mx.s2 = __ldcg(&src->s2);
-        mx.p = __ldcg(&src->p);
-        mx.ties = __ldcg(&src->ties);
-        ro[0] = fmaxf(ro[0], __ldcg(&src->ovf));
-        if (mx.p >= 0) {  // fold into slot 0 with Best2 semantics
-          m0.merge(mx);
-          rs[0] = m0.s;
-          rs2[0] = m0.s2;
-          rp[0] = m0.p;
-          rt[0] = m0.ties;
-        }
-      }
-    }
-    if (b == 0 && lane == 0 && x.timing) a.timing[5] = s8_timer();
     double bs = -INFINITY;
     float ov = -INFINITY;
 #pragma unroll
@@ -516,13 +516,8 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
       const OutRec o = decide(record_best(r), r.flags & FLAG_NEED_ANY, x.st.jhead, a.thr);
       if (a.out) a.out[gb] = o;
       if (a.outp) {
-        const uint4 v = pack_out(o, a.seq), v2 = pack_out2(o, a.seq);
-        asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a.outp + 2 * gb), "r"(v.x), "r"(v.y), "r"(v.z),
-                     "r"(v.w)
-                     : "memory");
-        asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a.outp + 2 * gb + 1), "r"(v2.x), "r"(v2.y),
-                     "r"(v2.z), "r"(v2.w)
-                     : "memory");
+        st_v4(a.outp + 2 * gb, pack_out(o, a.seq));
+        st_v4(a.outp + 2 * gb + 1, pack_out2(o, a.seq));
       }
       if (b == 0 && x.timing) a.timing[7] = s8_timer();
     }
@@ -533,7 +528,6 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
       __threadfence_system();
       *(volatile unsigned*)a.done_seq = a.seq;
     }
-    *a.counter = 0u;
     if (x.timing) a.timing[3] = s8_timer();
   }
   dump();
@@ -717,6 +711,7 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
       for (int i = 0; i < wk.ns; ++i) {
         const int buf = i % nst;
         mbar_wait(&S.empty[buf], ((i / nst) & 1) ^ 1);
@@ -727,8 +722,8 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
         const uint32_t qbytes = (uint32_t)(((slot0 - q0) + nr + 1) / 2 * 16);
         const uint32_t dbytes = (uint32_t)nr * P8;
         mbar_expect_tx(&S.full[buf], dbytes + qbytes);
-        bulk_load(stages + (size_t)buf * SDATA, rb.r8 + (size_t)slot0 * P8, dbytes, &S.full[buf]);
-        bulk_load(rqs + (size_t)buf * RQS, rb.rq + q0, qbytes, &S.full[buf]);
+        bulk_load_hint(stages + (size_t)buf * SDATA, rb.r8 + (size_t)slot0 * P8, dbytes, &S.full[buf], pol);
+        bulk_load_hint(rqs + (size_t)buf * RQS, rb.rq + q0, qbytes, &S.full[buf], pol);
       }
     }
     return;
@@ -738,7 +733,7 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     // ------------------------------------------------------------ rescorer
     if (blockIdx.x == 0 && n_pend > 0) s8_pending(x, stagep, a.n_app, n_pend, n_scan);
     s8_pool(x, S8_CW);
-    s8_finish(x, a, prepp, cta, b0);
+    s8_finish(x, a, prepp, reinterpret_cast<uint4*>(cta), b0);
     return;
   }
 
@@ -985,7 +980,7 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
                                   OutRec* out,
                                   RingState* d_state, unsigned* done_seq, unsigned seq, uint4* outp,
                                   void (*quantise)(const double*, int, int, QPrep*, int8_t*), cudaStream_t s) {
-  if (!p || p->Dp > 1024) return cudaErrorInvalidValue;
+  if (!p || p->Dp > 1024 || grid > 256) return cudaErrorInvalidValue;
   static thread_local S8In in;
   const int Dp = p->Dp;
   memcpy(in.q64, q64, (size_t)D * sizeof(double));
@@ -1014,7 +1009,7 @@ cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingS
                                 unsigned long long* gmax, unsigned epoch, const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
                                 const QPrep* prep, const int8_t* q8, unsigned* done_seq, unsigned seq,
                                 uint4* outp, cudaStream_t s) {
-  if (!p || nb < 1 || nb > 4) return cudaErrorInvalidValue;
+  if (!p || nb < 1 || nb > 4 || grid > 256) return cudaErrorInvalidValue;  // grid <= 256: the merger's records
   S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), prep, q8, app.stage, app.n, app.d_state, done_seq, seq,
            outp, epoch};
   switch (p->P8 / 128) {
