@@ -79,7 +79,8 @@ def load(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # MODMCACHE_LIB: an alternative build of the same library (A/B kernel measurements only)
+    p = Path(path) if path else Path(os.environ.get("MODMCACHE_LIB") or LIB_PATH)
     if not p.exists():
         raise NativeError(
             f"{p} is missing: build it with `python -m paper_2503_11972_b200.build` "

@@ -30,14 +30,16 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+    """Compile every source into libmodmcache.so (or `out`, with extra -D `defines`: A/B variants)."""
+    lib = Path(out) if out else LIB
+    if not out and not force and not needs_build():
         return LIB
-    objdir = PKG / "_build"
+    objdir = PKG / ("_build" if not out else "_build_" + lib.stem)
     objdir.mkdir(exist_ok=True)
     common = [
         "-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-O2", "-I", str(ROOT / "include"),
-        "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
+        "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3", *[f"-D{d}" for d in defines],
     ]
     jobs = []
     for src in SOURCES:  # one nvcc per translation unit, in parallel
@@ -52,14 +54,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose:
             print(err, file=sys.stderr)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_2503_11972_b200.build [--force] [-v] [--out PATH -DNAME=VALUE ...]
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else None
+    print(build(force="--force" in args, verbose="-v" in args, out=out,
+                defines=[a[2:] for a in args if a.startswith("-D")]))

@@ -239,8 +239,8 @@ __device__ __noinline__ double s8_dot(const double* row, const double* q, int n,
 // loads.  Returns the queue index (w * S8_QCAP + i) of the live, unclaimed
 // candidate with the largest upper bound, or -1.  `retire` marks candidates
 // whose bound fell below the CTA's lower bound (false: a side-effect-free
-// warm-up pass).  Out of line: one copy for all pool warps and the poller.
-__device__ __noinline__ int s8_pass(int ncw, bool retire) {
+// warm-up pass).  Inlined: an out-of-line call costs more here (measured, scripts/ab_c2.sh).
+__device__ __forceinline__ int s8_pass(int ncw, bool retire) {
   const int lane = threadIdx.x & 31;
   int tails = 0;  // lane w < ncw: tail of queue w
   if (lane < ncw) tails = *(volatile int*)&S.qtail[lane];
