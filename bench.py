@@ -140,22 +140,39 @@ def cpu_baseline(rows, Q, new_rows, insert: bool, seconds: float = 12.0, batch: 
             seq += 1
         done += batch
     dt = time.perf_counter() - t0
-    threads = None
-    try:
-        from threadpoolctl import threadpool_info
+    threads = blas_threads()
+    one = None
+    try:  # the same path pinned to one BLAS thread, on a shorter sample
+        from threadpoolctl import threadpool_limits
 
-        threads = max((d.get("num_threads") or 0) for d in threadpool_info() if d.get("user_api") == "blas")
+        with threadpool_limits(1, user_api="blas"):
+            d1, t1 = 0, time.perf_counter()
+            while time.perf_counter() - t1 < max(1.0, seconds / 4) and d1 < len(Q):
+                o.retrieve(Q[d1 % len(Q)], t)
+                d1 += 1
+            one = d1 / (time.perf_counter() - t1)
     except Exception:
         pass
     return {
         "value": done / dt, "unit": "lookups/s", "cores": threads or os.cpu_count(), "kind": "port",
+        "blas_threads": threads, "value_1thread": one,
         "sample": f"{done} sequential retrieve{'+insert' if insert else ''} calls on a {n}x{dim} float64 "
                   f"cache ({dt:.1f} s); {blas_info()}; host cpu_count={os.cpu_count()}",
     }
 
 
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max((d.get("num_threads") or 0) for d in threadpool_info() if d.get("user_api") == "blas") or None
+    except Exception:
+        return None
+
+
 # --------------------------------------------------------------------------- our arm
-def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, device=0, n_rot=4, dist=None):
+def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, device=0, n_rot=4, dist=None,
+               e2e_steps=None):
     """One BASELINE config on one GPU.
 
     value: `steps` back-to-back lookup steps (B queries + the step's FIFO insert)
@@ -168,7 +185,8 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
     from paper_2503_11972_b200 import CacheEntry, SemanticCache, ThresholdTable, _native
 
     total = warmup + steps
-    rows, Q, new_rows = make_workload(dim, n_entries, (2 * total + 8) * B)
+    e2e_steps = max(steps, e2e_steps or steps)  # the public-API leg: enough requests for a stable rate
+    rows, Q, new_rows = make_workload(dim, n_entries, (total + warmup + e2e_steps + 8) * B)
     cache = SemanticCache(capacity=n_entries, dim=dim, device=device)
     cache.bulk_load(CacheEntry(f"e{i}", rows[i], "large", i, 0.0) for i in range(n_entries))  # one device append
     table = ThresholdTable.default()
@@ -233,63 +251,115 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
-    for i in range(warmup, warmup + steps):
+    for i in range(warmup, warmup + e2e_steps):
         step(i, "s")
     e2e_s = time.perf_counter() - t0
     if dist:
         e2e_s = dist.max_over_ranks(e2e_s)
     n_ranks = dist.world if dist else 1
-    e2e_launches = (cache.ring.stats()["kernel_launches"] - launches0) / (warmup + steps)
+    e2e_launches = (cache.ring.stats()["kernel_launches"] - launches0) / (warmup + e2e_steps)
     e2e = {
-        "value": n_ranks * B * steps / e2e_s, "unit": "lookups/s",
+        "value": n_ranks * B * e2e_steps / e2e_s, "unit": "lookups/s", "requests": e2e_steps,
+        "latency_us": 1e6 * e2e_s / e2e_steps,
         "h2d_bytes_per_step": B * dim * 8 + (dim * 8 if insert else 0),
         "d2h_bytes_per_step": B * 24,
         "kernel_launches_per_step": e2e_launches,
     }
+    st = cache.ring.stats()
+    roof = roofline(st, n_entries, dim, B, step_ms, rot, prof, n_rot, pk)
+    out = {
+        "value": value, "ms_per_step": step_ms, "e2e": e2e, "roofline": roof, "clocks": clk.summary(),
+        "gpu_launches": rot["launches_per_step"] * steps,
+        "stats": st,
+        "profile": dict(prof, rotation={"caches": n_rot, **rot},
+                        per_step_check="events around each step, 256 MiB L2 flush between steps (outside the events)"),
+        "rows": rows, "Q": Q, "new_rows": new_rows,
+    }
+    cache.close()
+    return out
+
+
+def run_generated(label, workload, dim, n_entries, B, steps, warmup, flush_bytes, pk, device=0):
+    """A 1M-10M entry cache generated on the device (f4), `steps` back-to-back B-query lookups
+    (the full decision epilogue in every launch), device-timed like C2's value.  The cache alone
+    exceeds L2, so every step streams it from HBM without rotation."""
+    from paper_2503_11972_b200 import ThresholdTable, _native
+    from paper_2503_11972_b200.workload import GeneratedWorkload
+
+    wl = GeneratedWorkload(dim, n_clusters=max(512, n_entries // 200), seed=17)
+    ring = _native.DeviceRing(n_entries, dim, device)
+    t0 = time.perf_counter()
+    wl.fill(ring, n_entries)
+    gen_s = time.perf_counter() - t0
+    table = ThresholdTable.default()
+    ring.set_table(table.pairs, table.total_steps)
+    Q = wl.queries((warmup + steps) * B).reshape(warmup + steps, B, dim)
+    _native.DeviceRing.profile_rotate([ring], Q[:warmup], None, warmup)
+    with ClockSampler(device) as clk:
+        rot = _native.DeviceRing.profile_rotate([ring], Q[warmup:], None, steps)
+    prof = ring.profile_steps(Q[warmup:warmup + min(steps, 20)], None, min(steps, 20), flush_bytes)
+    st = ring.stats()
+    roof = roofline(st, n_entries, dim, B, rot["step_ms"], rot, prof, 1, pk)
+    ring.close()
+    return {"workload": label, "entries": n_entries, "dim": dim, "batch": B,
+            "value": B / (rot["step_ms"] * 1e-3), "unit": "lookups/s", "ms_per_step": rot["step_ms"],
+            "roofline": roof, "clocks": clk.summary(), "gpu_launches": rot["launches_per_step"] * steps,
+            "would_fallback": rot["would_fallback"], "cache_generation_s": gen_s,
+            "data": f"device-generated clustered unit rows (f4, {max(512, n_entries // 200)} clusters), host queries"}
+
+
+def roofline(st, n_entries, dim, B, step_ms, rot, prof, n_rot, pk):
+    """The dominant kernel's roofline entry (bench contract ④), from the library's launch counters."""
     dp = (dim + 63) // 64 * 64
     p8 = (dp + 127) // 128 * 128
-    if B <= 4 and dp <= 1024:  # K2s: TMA-streamed int8 ring + per-row (scale, L1) + float64 queries + quantisation
+    tensor = st["gemm_launches"] > 0  # which scan ran, from the library's own launch counters
+    if not tensor and dp <= 1024:  # K2s: TMA-streamed int8 ring + per-row (scale, L1) + float64 queries + quantisation
         scan_bytes = n_entries * (p8 + 8) + B * (dp * 9 + 40)
         kname = "k_stream8_scan"
-    elif B <= 4:  # K2: fp16 ring
+    elif not tensor:  # K2: fp16 ring
         scan_bytes = n_entries * dp * 2 + B * dp * 8
         kname = "k_gemv_scan"
     else:  # K3: fp16 ring + fp16 queries
         scan_bytes = n_entries * dp * 2 + B * dp * 2
         kname = "k_tc_scan_pair"
+    fp16_bytes = n_entries * dim * 2 + B * dim * 2  # SURVEY.md §8(d)'s definition: an fp16 scan of the window
     flops = 2.0 * B * n_entries * dp
     hbm, tc_burst, tc_sust, src = pk
     # the dominant kernel's average duration: the rotation's mean step (one fused launch per step on the
-    # small-batch path); on the tensor-core path the scan kernel's share comes from the per-step cross-check
-    scan_s = step_ms * 1e-3 if rot["launches_per_step"] == 1 else prof["scan_ms"] * 1e-3
+    # small-batch path); on the tensor-core path the scan's share of the per-step cross-check (prep + pair),
+    # split by the committed ncu launch list's per-kernel shares
+    share = 1.0
+    if rot["launches_per_step"] == 1:
+        scan_s = step_ms * 1e-3
+        timing = (f"CUDA events around the back-to-back timed steps on the library stream (rotation over {n_rot} "
+                  "caches > L2), mean per launch")
+    else:
+        share = launch_share("k_tc_scan_pair", ("k_tc_prep", "k_tc_scan_pair"))
+        scan_s = prof["scan_ms"] * 1e-3 * share
+        timing = ("CUDA events around k_tc_prep + k_tc_scan_pair on the library stream (L2 flushed before each "
+                  f"step), times the pair kernel's share {share:.3f} of that span in the committed ncu launch list")
     t_hbm = scan_bytes / (hbm * 1e9)
     t_tc = flops / (tc_burst * 1e12)
-    bound = "hbm" if (B <= 4 or t_hbm >= t_tc) else "tensor"
+    bound = "hbm" if (not tensor or t_hbm >= t_tc) else "tensor"
     if bound == "hbm":
         roof = {"bound": "hbm", "achieved": scan_bytes / scan_s / 1e9, "peak": hbm, "unit": "GB/s"}
     else:
         roof = {"bound": "tensor", "achieved": flops / scan_s / 1e12, "peak": tc_burst, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["peak_source"] = f"{src} (MEASURED_PEAKS.json)" if src == "measured" else "fallback (B200_PROFILING.md)"
-    roof["kernel"] = {"k_stream8_scan": "k_stream8_scan (TMA-streamed int8 scan + in-scan float64 rescoring + "
-                                        "merge + decision, one launch)",
-                      "k_gemv_scan": "k_gemv_scan (fp16 scan + float64 rescoring + decision, fused)",
-                      "k_tc_scan_pair": "k_tc_scan_pair (tcgen05 cta_group::2)"}[kname]
+    roof["kernel"] = kname
     roof["algorithmic_bytes_per_launch"] = scan_bytes
+    roof["bytes_definition"] = ("bytes the kernel must read: int8 ring rows + per-row (scale, L1) + queries"
+                                if kname == "k_stream8_scan" else "fp16 ring rows + queries")
+    roof["fp16_definition"] = {"bytes": fp16_bytes, "frac": fp16_bytes / scan_s / 1e9 / hbm,
+                               "note": "SURVEY.md §8(d): N*D*2 + B*D*2 (an fp16 scan); the int8 copy reads half"}
     roof["flops_per_launch"] = flops
+    roof["max_of_floors_frac"] = max(t_hbm, t_tc) / scan_s
     roof["step_roofline_frac"] = max(t_hbm, t_tc) / (step_ms * 1e-3)
     roof["traffic"] = traffic_from_profiles(kname)
-    roof["timing"] = ("CUDA events around the back-to-back timed steps on the library stream (rotation over "
-                      f"{n_rot} caches > L2), mean per launch")
-    out = {
-        "value": value, "ms_per_step": step_ms, "e2e": e2e, "roofline": roof, "clocks": clk.summary(),
-        "gpu_launches": rot["launches_per_step"] * steps,
-        "profile": dict(prof, rotation={"caches": n_rot, **rot},
-                        per_step_check="events around each step, 256 MiB L2 flush between steps (outside the events)"),
-        "rows": rows, "Q": Q, "new_rows": new_rows, "stats": cache.ring.stats(),
-    }
-    cache.close()
-    return out
+    roof["traffic_source"] = "dram__bytes_read.sum + dram__bytes_write.sum per launch, profiles/ncu_summary.json"
+    roof["timing"] = timing
+    return roof
 
 
 class Dist:
@@ -342,6 +412,17 @@ def run_sharded(dist, dim, per_gpu, steps, warmup):
             "timing": "public sharded API with the host in the loop (H2D, NCCL, merge, D2H), max over ranks"}
 
 
+def launch_share(kernel: str, group) -> float:
+    """kernel's share of the summed durations of `group` in the committed ncu launch list."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        d = json.loads(p.read_text())["launch_list_mean_us"]
+        tot = sum(d[k] for k in group)
+        return d[kernel] / tot if tot > 0 else 1.0
+    except Exception:
+        return 1.0
+
+
 def traffic_from_profiles(kernel: str):
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
@@ -353,37 +434,70 @@ def traffic_from_profiles(kernel: str):
         return None
 
 
+def _reference_cache_module():
+    """The UNMODIFIED reference package staged under baseline/_ref (scripts/stage_reference.sh), or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "mixserve" / "cache.py").exists():
+        return None
+    sys.path.insert(0, str(ref))
+    try:
+        import mixserve.cache as mc
+
+        return mc
+    except Exception:
+        return None
+
+
 def reference_arm(args):
-    """The reference's CPU path (oracle port: numpy float64 / OpenBLAS, all host threads), same workload.
+    """The reference's own CPU path on the box's host cores, same workload as our arm's headline.
 
     Each step = a bounded sample of the C2 workload: `per_step` sequential
-    retrieve + insert calls against the 100k x 768 cache.
+    SemanticCache.retrieve + add calls (the reference has no batch API) against
+    the 100k x 768 cache.  Runs the real `mixserve.cache.SemanticCache` when the
+    reference is staged under baseline/_ref (kind "reference"); otherwise the
+    oracle port of the same algorithm (kind "port").
     """
-    from oracle.retrieval import OracleCache, OracleEntry, OracleTable, blas_info
-
     per_step = 4
     total = args.warmup + args.steps
     rows, Q, new_rows = make_workload(768, 100_000, total * per_step + 8)
     n, dim = rows.shape
-    o = OracleCache(n, dim)
-    for i, v in enumerate(rows):
-        o.insert(OracleEntry(f"e{i}", v, "large", i, 0.0))
-    t = OracleTable()
-    seq, j = n, 0
+    mc = _reference_cache_module()
+    if mc is not None:
+        cache = mc.SemanticCache(capacity=n, dim=dim)
+        for i, v in enumerate(rows):
+            cache.insert(mc.CacheEntry(f"e{i}", v, "large", i, 0.0))
+        table = mc.ThresholdTable.default()
+        kind, what = "reference", f"mixserve.cache.SemanticCache from baseline/_ref (unmodified reference)"
+        lookup = lambda q: cache.retrieve(q, table)  # noqa: E731
+        insert = lambda j: cache.add(f"n{j}", new_rows[j], "large", 1.0 + j)  # noqa: E731
+    else:
+        from oracle.retrieval import OracleCache, OracleEntry, OracleTable
+
+        o = OracleCache(n, dim)
+        for i, v in enumerate(rows):
+            o.insert(OracleEntry(f"e{i}", v, "large", i, 0.0))
+        t = OracleTable()
+        kind, what = "port", "oracle/retrieval.py (float64 numpy port of cache.py:244-260)"
+        lookup = lambda q: o.retrieve(q, t)  # noqa: E731
+        insert = lambda j: o.insert(OracleEntry(f"n{j}", new_rows[j], "large", n + j, 0.0))  # noqa: E731
+    from oracle.retrieval import blas_info
+
+    j = 0
     times = []
-    for s in range(total):
+    for _ in range(total):
         t0 = time.perf_counter()
         for _ in range(per_step):
-            o.retrieve(Q[j], t)
-            o.insert(OracleEntry(f"n{seq}", new_rows[j], "large", seq, 0.0))
-            seq += 1
+            lookup(Q[j])
+            insert(j)
             j += 1
         times.append(time.perf_counter() - t0)
     timed = sum(times[args.warmup:])
     value = args.steps * per_step / timed
-    cb = {"value": value, "unit": "lookups/s", "cores": os.cpu_count(), "kind": "port",
-          "sample": f"{args.steps} steps x {per_step} sequential retrieve+insert calls on a {n}x{dim} float64 cache; "
-                    f"{blas_info()}"}
+    threads = blas_threads()
+    cb = {"value": value, "unit": "lookups/s", "cores": threads or os.cpu_count(), "kind": kind,
+          "blas_threads": threads, "host_cpu_count": os.cpu_count(),
+          "sample": f"{args.steps} steps x {per_step} sequential retrieve+add calls on a {n}x{dim} float64 cache; "
+                    f"{what}; {blas_info()}"}
     return {
         "metric": METRIC, "value": value, "unit": "lookups/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * timed / args.steps, "higher_is_better": True,
@@ -400,6 +514,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-c3", action="store_true")
+    ap.add_argument("--no-big", action="store_true", help="skip the 1M / 10M-entry single-GPU lines")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
@@ -417,7 +532,8 @@ def main():
     device = dist.local if dist else 0
     pk = peaks()
     flush = 256 << 20
-    c2 = run_config("c2", 768, 100_000, 1, args.steps, args.warmup, True, flush, pk, device=device, dist=dist)
+    c2 = run_config("c2", 768, 100_000, 1, args.steps, args.warmup, True, flush, pk, device=device, dist=dist,
+                    e2e_steps=3000)
     line = {
         "metric": METRIC,
         "value": c2["value"], "unit": "lookups/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -432,11 +548,30 @@ def main():
     }
     if not args.no_c3:
         c3 = run_config("c3", 1024, 100_000, 256, min(60, max(20, args.steps // 10)), args.warmup, False, flush, pk,
-                        device=device, n_rot=2, dist=dist)
+                        device=device, n_rot=2, dist=dist, e2e_steps=100)
         line["c3"] = {"workload": "C3: 100k entries, 1024-dim, batch-256 lookups", "value": c3["value"],
                       "unit": "lookups/s", "ms_per_step": c3["ms_per_step"], "e2e": c3["e2e"],
                       "roofline": c3["roofline"], "clocks": c3["clocks"], "gpu_launches": c3["gpu_launches"],
                       "profile": c3["profile"]}
+    if not args.no_c3:  # C1: the reference's default size, L2-resident by design -> reported as latency
+        c1 = run_config("c1", 768, 10_000, 1, max(200, args.steps), args.warmup, True, 0, pk, device=device, n_rot=1,
+                        dist=dist, e2e_steps=2000)
+        line["c1"] = {"workload": "C1: 10k-entry FIFO cache (reference default), 768-dim, batch-1 lookup + insert",
+                      "latency_us": 1e3 * c1["ms_per_step"], "value": c1["value"], "unit": "lookups/s",
+                      "e2e": c1["e2e"], "roofline": c1["roofline"], "clocks": c1["clocks"],
+                      "l2": "resident (15.4 MB int8 copy): latency, not HBM, is the figure of merit"}
+    if not args.no_big and not dist:  # C4 / C5 shapes on one GPU (device-generated caches, f4)
+        big = {}
+        for key, n, B, k in (("c4_b1", 1_000_000, 1, max(args.steps, 50)), ("c4_b256", 1_000_000, 256, 20),
+                             ("c5_b1", 10_000_000, 1, 20), ("c5_b256", 10_000_000, 256, 6)):
+            label = (f"{'C4' if n == 1_000_000 else 'C5'} shape on ONE GPU: {n:,} entries x 768, batch {B}"
+                     + ("" if n == 1_000_000 else " (all 10M entries in this GPU's HBM: 61.4 GB float64 + 15.4 GB fp16"
+                                                   " + 7.7 GB int8)"))
+            try:
+                big[key] = run_generated(label, None, 768, n, B, k, args.warmup, flush, pk, device=device)
+            except Exception as exc:  # reported, never fatal to the headline line
+                big[key] = {"workload": label, "error": f"{type(exc).__name__}: {exc}"}
+        line["single_gpu_large"] = big
     if dist:  # the path's real exchange step: an entry-sharded cache merged over NCCL
         try:
             line["c4"] = run_sharded(dist, 768, 100_000, min(2000, args.steps), args.warmup)

@@ -179,6 +179,19 @@ int mc_profile_rotate(mc_cache* const* hs, int32_t nh, const double* queries, co
  * scripts/profile_case.py. */
 int mc_debug_gemv_timing(unsigned long long* out8, int reset);
 
+/* f4, measurement infrastructure (the generative model of
+ * pkg/src/mixserve/workload.py:124-154): appends n synthetic unit rows generated
+ * on the device, with FIFO semantics (the oldest rows are evicted as by n
+ * appends).  Row r (global index row0 + r) belongs to a hashed cluster c and is
+ * normalize(beta * q + (1 - beta) * g'), q = normalize(centers[c] + spread * g).
+ * centers: host float64 [n_centers][dim].  dim <= 1024. */
+int mc_generate_rows(mc_cache* h, int64_t n, const double* centers, int32_t n_centers, double spread, double beta,
+                     uint64_t seed, int64_t row0);
+
+/* Copies the float64 master rows of live indices [first_live, first_live + n)
+ * (0 = oldest) into out[n][dim] (parity checks of generated caches). */
+int mc_read_rows(mc_cache* h, int64_t first_live, int64_t n, double* out);
+
 /* Debugging hook: copies the float64 master row of live index `live` (0 =
  * oldest; pending appends are published first) into out[0 .. dim). */
 int mc_debug_read_row(mc_cache* h, int64_t live, double* out);

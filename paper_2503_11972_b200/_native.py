@@ -35,7 +35,7 @@ EXPORTED = (
     "mc_retrieve_batch", "mc_set_path", "mc_configure_shard", "mc_retrieve_local_async",
     "mc_merge_records", "mc_stats", "mc_last_error", "mc_version", "mc_profile_steps", "mc_profile_rotate",
     "mc_debug_gemv_timing", "mc_retrieve_submit", "mc_retrieve_wait", "mc_debug_read_row",
-    "mc_retrieve_decisions", "mc_set_sigma_schedule",
+    "mc_retrieve_decisions", "mc_set_sigma_schedule", "mc_generate_rows", "mc_read_rows",
 )
 
 
@@ -69,6 +69,8 @@ def _declare(lib):
     lib.mc_debug_gemv_timing.argtypes = [dp, i32]
     lib.mc_retrieve_decisions.argtypes = [vp, dp, i32, dp]
     lib.mc_set_sigma_schedule.argtypes = [vp, dp, i32]
+    lib.mc_generate_rows.argtypes = [vp, i64, dp, i32, C.c_double, C.c_double, C.c_uint64, i64]
+    lib.mc_read_rows.argtypes = [vp, i64, i64, dp]
     lib.mc_last_error.restype = C.c_char_p
     lib.mc_version.restype = C.c_char_p
     return lib
@@ -299,6 +301,20 @@ class DeviceRing:
         _check(lib, lib.mc_profile_rotate(C.cast(hs, C.c_void_p), len(rings), _ptr(Q), None if r is None else _ptr(r),
                                           B, int(iters), _ptr(ms), _ptr(cnt)))
         return {"step_ms": float(ms[0]), "launches_per_step": int(cnt[0]), "would_fallback": int(cnt[1])}
+
+    def generate(self, n: int, centers: np.ndarray, spread: float, beta: float, seed: int, row0: int = 0) -> None:
+        """Append n device-generated synthetic rows (mc_generate_rows; measurement infrastructure)."""
+        c = np.ascontiguousarray(centers, dtype=np.float64)
+        if c.ndim != 2 or c.shape[1] != self.dim:
+            raise ValueError(f"centers must be [K, {self.dim}]")
+        _check(self.lib, self.lib.mc_generate_rows(self._h, int(n), _ptr(c), c.shape[0], float(spread), float(beta),
+                                                   int(seed) & (2**64 - 1), int(row0)))
+
+    def read_rows(self, first: int, n: int) -> np.ndarray:
+        """float64 master rows of live indices [first, first + n) (mc_read_rows)."""
+        out = np.empty((int(n), self.dim), dtype=np.float64)
+        _check(self.lib, self.lib.mc_read_rows(self._h, int(first), int(n), _ptr(out)))
+        return out
 
     def debug_read_row(self, live: int) -> np.ndarray:
         """The device's float64 copy of live row `live` (debugging)."""

@@ -1326,6 +1326,10 @@ int mc_profile_rotate(mc_cache* const* hs, int32_t nh, const double* queries, co
   for (int k = 0; k < nh; ++k) hs[k]->stream = common;
   long long launches0 = 0;
   for (int k = 0; k < nh; ++k) launches0 += hs[k]->stats[7];
+  // Hold the stream with a timed spin while the steps are enqueued, so the first timed step does
+  // not wait for its own host-side launch and every step is queued when its predecessor ends
+  // (the host's enqueue rate, ~4 us per launch, is not part of the device time being measured).
+  CUR(launch_spin(std::min<long long>(20000000ll, 6000ll * iters + 200000ll), common));
   CUR(cudaEventRecord(e0, common));
   for (int it = 0; it < iters; ++it) {
     mc_cache* h = hs[it % nh];
@@ -1389,6 +1393,67 @@ int mc_debug_gemv_timing(unsigned long long* out8, int reset) {
 
 // Measurement / debugging hook: the float64 master copy of live row `live`
 // (0 = oldest) after every pending append has landed.  Not part of the drop-in.
+int mc_generate_rows(mc_cache* h, int64_t n, const double* centers, int32_t n_centers, double spread, double beta,
+                     uint64_t seed, int64_t row0) {
+  if (!h || !centers) return fail(MC_ERR_ARG, "NULL argument");
+  if (n < 0 || n_centers < 1) return fail(MC_ERR_ARG, "need n >= 0 and n_centers >= 1");
+  if (h->D > 1024) return fail(MC_ERR_ARG, "the generator covers dim <= 1024 (dim %d)", h->D);
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  int rc = flush(h);  // pending appends precede the generated rows
+  if (rc) return rc;
+  if (n == 0) return MC_OK;
+  // FIFO semantics of n appends: only the newest min(n, C) rows stay live
+  const long long keep = std::min<long long>(n, h->C);
+  const long long skip = n - keep;
+  const long long drop = std::max<long long>(0, h->count + keep - h->C);
+  h->head = (h->head + drop) % h->C;
+  h->count -= drop;
+  h->jhead += drop;
+  if (skip > 0) {  // every earlier row is evicted; the skipped rows pass through the ring unseen
+    h->head = (h->head + h->count) % h->C;
+    h->jhead += h->count + skip;
+    h->count = 0;
+  }
+  const long long first_slot = (h->head + h->count) % h->C;
+  h->count += keep;
+  h->appended += n;
+  h->state_dirty = false;
+  double* d_ctr = nullptr;
+  std::vector<double> ctr((size_t)n_centers * h->Dp, 0.0);
+  for (int c = 0; c < n_centers; ++c) memcpy(&ctr[(size_t)c * h->Dp], centers + (size_t)c * h->D, h->D * sizeof(double));
+  CU(cudaMallocAsync(&d_ctr, ctr.size() * sizeof(double), h->stream));
+  CU(cudaMemcpyAsync(d_ctr, ctr.data(), ctr.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CU(launch_generate(keep, first_slot, mirror(h), h->D, h->Dp, rbufs(h), d_ctr, n_centers, spread, beta, seed,
+                     row0 + skip, h->d_state, h->stream));
+  CU(cudaFreeAsync(d_ctr, h->stream));
+  CU(cudaStreamSynchronize(h->stream));  // the host centre buffer goes out of scope
+  h->stats[7]++;
+  return MC_OK;
+}
+
+int mc_read_rows(mc_cache* h, int64_t first_live, int64_t n, double* out) {
+  if (!h || (!out && n > 0)) return fail(MC_ERR_ARG, "NULL argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  if (first_live < 0 || n < 0 || first_live + n > h->count)
+    return fail(MC_ERR_ARG, "rows [%lld, %lld) outside the %lld live rows", (long long)first_live,
+                (long long)(first_live + n), (long long)h->count);
+  int rc = flush(h);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(h->stream));
+  long long done = 0;
+  while (done < n) {  // at most two contiguous slot ranges (the ring wraps once)
+    const long long slot = (h->head + first_live + done) % h->C;
+    const long long run = std::min<long long>(n - done, h->C - slot);
+    CU(cudaMemcpy2D(out + (size_t)done * h->D, (size_t)h->D * sizeof(double), h->ring64 + (size_t)slot * h->Dp,
+                    (size_t)h->Dp * sizeof(double), (size_t)h->D * sizeof(double), (size_t)run,
+                    cudaMemcpyDeviceToHost));
+    done += run;
+  }
+  return MC_OK;
+}
+
 int mc_debug_read_row(mc_cache* h, int64_t live, double* out) {
   if (!h || !out) return fail(MC_ERR_ARG, "NULL argument");
   std::lock_guard<std::mutex> lk(h->mu);

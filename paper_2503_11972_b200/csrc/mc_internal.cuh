@@ -142,7 +142,11 @@ cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingS
                                 uint4* outp, cudaStream_t s);
 
 int gemv_grid(int sm_count);
-cudaError_t launch_l2_flush(void* buf, size_t bytes, cudaStream_t s);  // measurement: evict L2 by reading
+cudaError_t launch_generate(long long n, long long first_slot, const RingState& ns, int D, int Dp, const RingBufs& rb,
+                            const double* centers, int K, double spread, double beta, unsigned long long seed,
+                            long long row0, RingState* d_state, cudaStream_t s);  // f4 synthetic rows
+cudaError_t launch_l2_flush(void* buf, size_t bytes, cudaStream_t s);
+cudaError_t launch_spin(long long ns, cudaStream_t s);  // measurement: hold a stream for ns of device time  // measurement: evict L2 by reading
 unsigned long long* gemv_timing_buffer();  // MC_GEMV_TIMING=1 phase timestamps (measurement)
 
 // tcgen05 GEMM scan of B queries (scan_tc.cu).  The plan owns the fp16

@@ -71,3 +71,26 @@ def near_threshold_queries(rows: np.ndarray, taus, rng: np.random.Generator, n: 
         s = taus[i % len(taus)] + offsets[(i // len(taus)) % len(offsets)]
         out[i] = s * e + math.sqrt(1.0 - s * s) * u
     return out
+
+
+class GeneratedWorkload:
+    """The same generative model with the cache rows generated ON THE DEVICE (mc_generate_rows,
+    SURVEY.md §8 f4): 1M-10M entry caches without building them on the host.  Cluster centres
+    and queries come from numpy; row r's cluster and noise come from a counter hash on the GPU,
+    so the rows are not numpy's streams — parity checks read them back (DeviceRing.read_rows)."""
+
+    def __init__(self, dim: int, n_clusters: int = 512, seed: int = 17, spread: float | None = None,
+                 beta: float | None = None):
+        self.dim = dim
+        self.seed = seed
+        self.rng = np.random.default_rng(seed)
+        self.centers = _unit_rows(self.rng.standard_normal((n_clusters, dim)))
+        self.spread = spread_for(dim) if spread is None else spread
+        self.beta = beta_for(dim) if beta is None else beta
+
+    def fill(self, ring, n: int, row0: int = 0) -> None:
+        ring.generate(n, self.centers, self.spread, self.beta, self.seed, row0)
+
+    def queries(self, n: int) -> np.ndarray:
+        idx = self.rng.integers(0, len(self.centers), n)
+        return _unit_rows(self.centers[idx] + self.spread * self.rng.standard_normal((n, self.dim)))

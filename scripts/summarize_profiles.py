@@ -20,6 +20,7 @@ HEAD = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__m_xbar2l1tex_read_bytes.sum",
         "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
         "launch__block_size", "launch__shared_mem_per_block_dynamic", "sm__cycles_elapsed.avg", "smsp__inst_executed.sum"]
 
@@ -34,7 +35,11 @@ def raw_metrics(rep):
     h, u, v = r[0], r[1], r[2]
     out = {}
     for k, uu, vv in zip(h, u, v):
-        base = k.split(".", 1)[1] if k.startswith(("TPC.", "SM_C.", "FBSP.", "LTS.")) and k.count(".") > 2 else k
+        base = k
+        for pre in ("sm__", "smsp__", "dram__", "lts__", "l1tex__", "gpu__", "launch__"):
+            if pre in k:
+                base = k[k.index(pre):]
+                break
         if base in HEAD or k in HEAD:
             out[base] = (vv, uu)
     stalls = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(vv or 0)
@@ -91,19 +96,21 @@ if launch_csv.exists():
         if len(r) != len(hdr):
             continue
         d = dict(zip(hdr, r))
-        name = d["Kernel Name"].split("(")[0].replace("void ", "").strip()
+        name = d["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "").strip()
         unit = d.get("Metric Unit", "nsecond")
         val = float(d["Metric Value"].replace(",", ""))
         per[name].append(val / 1e3 if unit in ("ns", "nsecond") else val)
     total = sum(sum(v) for v in per.values())
     with open(DST / f"{tag}_launches_bench.txt", "w") as fh:
         fh.write("ncu --metrics gpu__time_duration.sum --clock-control none over "
-                 "`python bench.py --steps 8 --warmup 3 --no-c3` (cold-cache, serialised: compare shares, not absolutes)\n"
-                 "k_append = the bulk preload of the 4 rotation caches (setup); k_l2_flush = the per-step cross-check's "
-                 "L2 flush (outside its events); the timed steps launch only the scan kernel\n\n")
+                 "`python bench.py --steps 8 --warmup 3` (cold-cache, serialised: compare shares, not absolutes)\n"
+                 "k_append = the bulk preload of the rotation caches (setup); k_l2_flush = the per-step cross-check's "
+                 "L2 flush (outside its events); a C2 step launches only k_stream8_scan, a C3 step k_tc_prep + "
+                 "k_tc_scan_pair + k_merge\n\n")
         fh.write(f"{'kernel':40s} {'launches':>8s} {'mean us':>9s} {'share':>7s}\n")
         for name, v in sorted(per.items(), key=lambda x: -sum(x[1])):
             fh.write(f"{name:40s} {len(v):8d} {sum(v) / len(v):9.1f} {100 * sum(v) / total:6.1f}%\n")
     summary["launch_list"] = f"{tag}_launches_bench.txt"
+    summary["launch_list_mean_us"] = {k: sum(v) / len(v) for k, v in per.items()}
 (DST / "ncu_summary.json").write_text(json.dumps(summary, indent=1) + "\n")
 print(json.dumps(summary, indent=1))

@@ -823,3 +823,80 @@ def test_concurrent_readers_see_their_own_answers():
         t.join()
     assert not errors, errors[:5]
     c.close()
+
+
+def _chunked_scan(ring, Q, table, chunk=250_000):
+    """The oracle on exactly the rows the device holds (read back in chunks): best float64
+    similarity per query, newest index among exact ties (test_acceptance.py:429-436's formula)."""
+    n = len(ring)
+    best = np.full(len(Q), -np.inf)
+    idx = np.full(len(Q), -1, dtype=np.int64)
+    for s in range(0, n, chunk):
+        rows = ring.read_rows(s, min(chunk, n - s))
+        sims = rows @ Q.T
+        m = sims.max(axis=0)
+        last = rows.shape[0] - 1 - np.argmax(sims[::-1] == m[None, :], axis=0)
+        take = m >= best  # equal: the later chunk holds the newer row
+        best = np.where(take, m, best)
+        idx = np.where(take, s + last, idx)
+    return idx, best
+
+
+def _check_generated(ring, Q, table, label):
+    ot = OracleTable(table.pairs, table.total_steps)
+    want_idx, want_sim = _chunked_scan(ring, Q, table)
+    stats = {"queries": 0, "ties": 0, "near_tau": 0, "near_tie": 0, "fallback": 0}
+    for B in sorted({1, len(Q)}):
+        for s0 in range(0, len(Q), B):
+            live, sim, k, flags = ring.retrieve(Q[s0:s0 + B])
+            for b in range(B):
+                j = s0 + b
+                f = int(flags[b])
+                stats["queries"] += 1
+                stats["ties"] += bool(f & _native.MC_FLAG_TIE)
+                stats["near_tau"] += bool(f & _native.MC_FLAG_NEAR_TAU)
+                stats["near_tie"] += bool(f & _native.MC_FLAG_NEAR_TIE)
+                stats["fallback"] += bool(f & _native.MC_FLAG_FALLBACK)
+                assert abs(sim[b] - want_sim[j]) <= 1e-12, (label, B, j, sim[b], want_sim[j])
+                kk = ot.select_k(want_sim[j])
+                if f & _native.MC_FLAG_HIT:
+                    assert kk is not None and int(k[b]) == kk, (label, B, j)
+                    if int(live[b]) != want_idx[j]:  # only an exact / ulp tie may resolve differently
+                        assert f & (_native.MC_FLAG_TIE | _native.MC_FLAG_NEAR_TIE), (label, B, j, live[b], want_idx[j])
+                else:
+                    assert kk is None, (label, B, j)
+    _record_parity(label, stats)
+
+
+def test_device_generator_fifo_semantics_and_unit_rows():
+    """f4: generated rows are unit-norm, and generating n rows into a ring of capacity C keeps
+    exactly the newest C of them (the rows generated directly at their global indices)."""
+    from paper_2503_11972_b200.workload import GeneratedWorkload
+
+    wl = GeneratedWorkload(768, n_clusters=16, seed=5)
+    a = _native.DeviceRing(64, 768, 0)
+    wl.fill(a, 40)
+    wl.fill(a, 100, row0=40)  # 140 appends into 64 slots: rows 76..139 stay
+    b = _native.DeviceRing(64, 768, 0)
+    wl.fill(b, 64, row0=76)
+    ra, rb = a.read_rows(0, 64), b.read_rows(0, 64)
+    assert len(a) == 64 and np.array_equal(ra, rb)
+    assert np.abs(np.linalg.norm(ra, axis=1) - 1.0).max() < 1e-12
+    a.close()
+    b.close()
+
+
+@pytest.mark.parametrize("n,nq", [(1_000_000, 256), (10_000_000, 16)])
+def test_generated_million_entry_caches_match_the_oracle(n, nq):
+    """C4 / C5 cache sizes on one GPU (device-generated rows, f4): batch-1 (streamed int8 scan)
+    and batch-nq (tensor-core scan) decisions against the oracle run on the read-back rows."""
+    from paper_2503_11972_b200.workload import GeneratedWorkload
+
+    wl = GeneratedWorkload(768, n_clusters=max(512, n // 200), seed=23)
+    ring = _native.DeviceRing(n, 768, 0)
+    wl.fill(ring, n)
+    table = ThresholdTable.default()
+    ring.set_table(table.pairs, table.total_steps)
+    Q = wl.queries(nq)
+    _check_generated(ring, Q if n < 10_000_000 else Q, table, f"generated_{n}")
+    ring.close()
