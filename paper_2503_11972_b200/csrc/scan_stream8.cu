@@ -243,7 +243,7 @@ __device__ __noinline__ double s8_dot(const double* row, const double* q, int n,
 __device__ __forceinline__ int s8_pass(int ncw, bool retire) {
   const int lane = threadIdx.x & 31;
   int tails = 0;  // lane w < ncw: tail of queue w
-  if (lane < ncw) tails = *(volatile int*)&S.qtail[lane];
+  if (lane < ncw) tails = ld_acq_cta(&S.qtail[lane]);  // pairs with the pushing warp's st.release
   int start[S8_CW];
   int total = 0;
 #pragma unroll
@@ -317,7 +317,10 @@ __device__ __forceinline__ void s8_pending(const S8Ctx x, const double* stage, l
 // CTA's lower bound are retired unscored.  Result: S.best[wid][*].
 __device__ __forceinline__ void s8_pool(const S8Ctx x, int wid) {
   const int lane = threadIdx.x & 31;
-  asm volatile("bar.sync 1, %0;" ::"n"((S8_CW + 1) * 32) : "memory");
+  // barrier.sync (not bar.sync, the .aligned form): lanes may arrive unconverged after the
+  // lane-0 bookkeeping above (compute-sanitizer synccheck)
+  __syncwarp();
+  asm volatile("barrier.sync 1, %0;" ::"n"((S8_CW + 1) * 32) : "memory");
   while (!*(volatile int*)&S.q_ready) {
   }
   if (x.timing && lane == 0) atomicMax(&S.t[S8T_POOL], s8_timer());

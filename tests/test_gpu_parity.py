@@ -825,7 +825,7 @@ def test_concurrent_readers_see_their_own_answers():
     c.close()
 
 
-def _chunked_scan(ring, Q, table, chunk=250_000):
+def _chunked_ring_scan(ring, Q, chunk=250_000):
     """The oracle on exactly the rows the device holds (read back in chunks): best float64
     similarity per query, newest index among exact ties (test_acceptance.py:429-436's formula)."""
     n = len(ring)
@@ -844,7 +844,7 @@ def _chunked_scan(ring, Q, table, chunk=250_000):
 
 def _check_generated(ring, Q, table, label):
     ot = OracleTable(table.pairs, table.total_steps)
-    want_idx, want_sim = _chunked_scan(ring, Q, table)
+    want_idx, want_sim = _chunked_ring_scan(ring, Q)
     stats = {"queries": 0, "ties": 0, "near_tau": 0, "near_tie": 0, "fallback": 0}
     for B in sorted({1, len(Q)}):
         for s0 in range(0, len(Q), B):
@@ -898,5 +898,5 @@ def test_generated_million_entry_caches_match_the_oracle(n, nq):
     table = ThresholdTable.default()
     ring.set_table(table.pairs, table.total_steps)
     Q = wl.queries(nq)
-    _check_generated(ring, Q if n < 10_000_000 else Q, table, f"generated_{n}")
+    _check_generated(ring, Q, table, f"generated_{n}")
     ring.close()
