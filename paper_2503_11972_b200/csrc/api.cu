@@ -121,7 +121,10 @@ struct mc_cache {
   bool inflight_direct = false; // its result comes back zero-copy
   bool param_in = false;        // MC_PARAM_INPUT=1: single-query lookups carry their inputs in the launch
                                 // parameters (measured equal to the pinned-envelope copy on B200)
-  double* h_qkeep = nullptr;    // [Dp] the last parameter-block query (for an exhaustive fallback)
+  double* h_qkeep = nullptr;    // pinned, mapped [Dp]: the single-query launch's float64 query (read by the kernel)
+  double* h_stage1 = nullptr;   // pinned, mapped [Dp]: its pending row
+  double* d_gq64 = nullptr;     // [Dp] the kernel's L2 relay of h_qkeep
+  unsigned* d_gq_flag = nullptr;
 
   TcPlan* tc = nullptr;           // fp16 tensor-core scan plan (MC_PATH_GEMM*), created on first use
   S8Plan* s8 = nullptr;           // TMA-streamed int8 scan plan (tensor maps of ring8 / ringq)
@@ -439,6 +442,7 @@ unsigned s8_epoch(mc_cache* h) {
   if (++h->s8_epoch == 0) {
     cudaMemsetAsync(h->d_gmax8, 0, (size_t)h->Bcap * 128 * sizeof(unsigned long long), h->stream);
     cudaMemsetAsync(h->d_cta, 0, (size_t)h->Bcap * gemv_grid(h->sm_count) * sizeof(CtaRec), h->stream);
+    cudaMemsetAsync(h->d_gq_flag, 0, sizeof(unsigned), h->stream);
     h->s8_epoch = 1;
   }
   return h->s8_epoch;
@@ -518,18 +522,23 @@ GemvAppendArgs take_pending(mc_cache* h, const double* dev_rows);
 
 int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool async_reuse, const double** q) {
   if (h->packed && h->param_in && B == 1 && h->n_pending <= 1 && h->Dp <= 1024) {
-    // the query, its quantisation and the pending row ride in the launch's parameter block:
-    // no host->device copy precedes the kernel
-    const double* stage_row = h->n_pending == 1 ? h->h_env : nullptr;
-    memcpy(h->h_qkeep, queries, (size_t)h->D * sizeof(double));
+    // no host->device copy precedes the kernel: the quantisation rides in the parameter block,
+    // the query and the pending row are read from mapped host memory (scan_stream8.cu, S8In).
+    // One lookup is in flight per handle, so these buffers are free again once it completes.
+    const double* stage_row = nullptr;
+    if (h->n_pending == 1) {
+      memcpy(h->h_stage1, h->h_env, (size_t)h->Dp * sizeof(double));  // staged rows are zero-padded to Dp
+      stage_row = h->h_stage1;
+    }
+    memcpy(h->h_qkeep, queries, (size_t)h->D * sizeof(double));  // padding columns stay zero
     const RingState st = mirror(h);
     take_pending(h, nullptr);
     memset(h->h_outp, 0, 2 * sizeof(uint4));
     *q = nullptr;
-    CU(launch_stream8_direct(h->s8, rbufs(h), st, h->D, queries, stage_row, h->d_cta, h->sm_count, h->shard,
+    CU(launch_stream8_direct(h->s8, rbufs(h), st, h->D, h->h_qkeep, stage_row, h->d_cta, h->sm_count, h->shard,
                              h->d_counter, h->d_gmax8, s8_epoch(h), h->thr, h->d_rec, nullptr, h->d_state, nullptr,
                              seq_tag(seq),
-                             h->d_outp, quantize_query, h->stream));
+                             h->d_outp, quantize_query, h->d_gq64, h->d_gq_flag, h->stream));
     h->stats[5]++;
     h->stats[7]++;
     return MC_OK;
@@ -834,8 +843,13 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   // testing hook: start the streamed scan's bound epochs near the 32-bit wrap-around
   if (const char* e = getenv("MC_S8_EPOCH0")) h->s8_epoch = (unsigned)strtoul(e, nullptr, 0);
   if (const char* e = getenv("MC_PARAM_INPUT")) h->param_in = atoi(e) != 0;
-  CUC(cudaMallocHost(&h->h_qkeep, (size_t)h->Dp * sizeof(double)));
+  CUC(cudaHostAlloc(&h->h_qkeep, (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
   memset(h->h_qkeep, 0, (size_t)h->Dp * sizeof(double));
+  CUC(cudaHostAlloc(&h->h_stage1, (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
+  memset(h->h_stage1, 0, (size_t)h->Dp * sizeof(double));
+  CUC(cudaMalloc(&h->d_gq64, 2 * (size_t)h->Dp * sizeof(double)));  // query, then the pending row
+  CUC(cudaMalloc(&h->d_gq_flag, sizeof(unsigned)));
+  CUC(cudaMemsetAsync(h->d_gq_flag, 0, sizeof(unsigned), h->stream));
   if (h->C > 0x7fffffffll) h->packed = false;  // live index must fit the packed int32
   CUC(cudaHostAlloc(&h->h_seq, 64, cudaHostAllocMapped));
   *h->h_seq = 0u;
@@ -882,6 +896,9 @@ int mc_destroy(mc_cache* h) {
     cudaFree(h->d_counter);
     cudaFreeHost(h->h_seq);
     cudaFreeHost(h->h_qkeep);
+    cudaFreeHost(h->h_stage1);
+    cudaFree(h->d_gq64);
+    cudaFree(h->d_gq_flag);
     if (h->env_ev) cudaEventDestroy(h->env_ev);
     if (h->rec_ev) cudaEventDestroy(h->rec_ev);
     if (h->stream) cudaStreamDestroy(h->stream);

@@ -125,16 +125,21 @@ struct S8Args {
   unsigned seq;
   uint4* outp;                 // optional (host-mapped): packed decisions, one 16-byte store each (see below)
   unsigned epoch;              // this launch's tag on the gmax words (never 0)
+  double* gq64;                // [Dp] relay of a host-mapped query (single-query launches)
+  unsigned* gq_flag;           // = epoch once gq64 holds this launch's query
 };
 
-// The single-query launch's inputs carried in the kernel parameter block (a
-// __grid_constant__ struct, < 32 KB): the float64 query, its int8
-// quantisation and at most one pending row, all zero-padded to Dp <= 1024.
+// The single-query launch's inputs (no host->device copy before the kernel):
+// the int8 quantisation rides in the kernel parameter block (~1 KB, every CTA
+// needs it at once); the float64 query and the pending row stay in mapped
+// host memory.  CTA 0's poller reads the query over PCIe once and relays it
+// through L2 (an epoch-tagged flag), so the other CTAs never touch host
+// memory; only CTA 0 (which writes the pending row) reads that row.
 struct S8In {
   QPrep prep;
   alignas(16) int8_t q8[1024];
-  alignas(16) double q64[1024];
-  alignas(16) double stage[1024];
+  const double* hq64;    // host-mapped float64 query (zero-padded to Dp): CTA 0 relays it through L2
+  const double* hstage;  // host-mapped pending row (zero-padded to Dp), or nullptr
 };
 struct S8NoIn {
   int unused;
@@ -548,10 +553,10 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
   const QPrep* prepp = a.prep;
   const double* stagep = a.stage;
   if constexpr (IN) {
-    q64 = in.q64;
+    q64 = in.hq64;
     q8p = in.q8;
     prepp = &in.prep;
-    stagep = in.stage;
+    stagep = in.hstage;  // the poller reads it once; CTA 0's rescorer then uses the relay (below)
   }
   constexpr int P8 = KB * 128;                // int8 row stride (Dp rounded up to 128)
   constexpr int R = s8_rows_per_lane(KB);
@@ -670,7 +675,49 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     // so its rescoring after the scan hits L2.  This warp never synchronises
     // (its global atomics stay off the other warps' fences and barriers).
     if constexpr (IN) {
-      for (int i = lane; i < NBQ * Dp; i += 32) sq64[i] = i < nb * Dp ? q64[i] : 0.0;
+      if (blockIdx.x == 0) {  // the one PCIe read of the query (and pending row), relayed through L2
+        // all loads in flight at once (16 x 16 B per lane covers Dp <= 1024): one PCIe round trip
+        const double2* hq = reinterpret_cast<const double2*>(q64);
+        const double2* hs = reinterpret_cast<const double2*>(stagep);
+        double2 vq[16], vs[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int i = lane + 32 * k;
+          vq[k] = 2 * i < Dp ? hq[i] : make_double2(0.0, 0.0);
+          vs[k] = (stagep && 2 * i < Dp) ? hs[i] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int i = lane + 32 * k;
+          if (2 * i < Dp) {
+            reinterpret_cast<double2*>(sq64)[i] = vq[k];
+            reinterpret_cast<double2*>(a.gq64)[i] = vq[k];
+            if (stagep) reinterpret_cast<double2*>(a.gq64 + Dp)[i] = vs[k];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.gq_flag), "r"(a.epoch) : "memory");
+        }
+      } else {
+        if (lane == 0) {
+          unsigned f;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.gq_flag) : "memory");
+          } while (f != a.epoch);
+        }
+        __syncwarp();
+        double2 vq[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int i = lane + 32 * k;
+          vq[k] = 2 * i < Dp ? __ldcg(reinterpret_cast<const double2*>(a.gq64) + i) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (2 * (lane + 32 * k) < Dp) reinterpret_cast<double2*>(sq64)[lane + 32 * k] = vq[k];
+      }
       __syncwarp();
       if (lane == 0) {
         __threadfence_block();
@@ -734,7 +781,7 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
 
   if (warp > S8_CW) {
     // ------------------------------------------------------------ rescorer
-    if (blockIdx.x == 0 && n_pend > 0) s8_pending(x, stagep, a.n_app, n_pend, n_scan);
+    if (blockIdx.x == 0 && n_pend > 0) s8_pending(x, IN ? a.gq64 + Dp : stagep, a.n_app, n_pend, n_scan);
     s8_pool(x, S8_CW);
     s8_finish(x, a, prepp, reinterpret_cast<uint4*>(cta), b0);
     return;
@@ -982,18 +1029,16 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
                                   unsigned long long* gmax, unsigned epoch, const Thresholds& thr, mc_record* rec,
                                   OutRec* out,
                                   RingState* d_state, unsigned* done_seq, unsigned seq, uint4* outp,
-                                  void (*quantise)(const double*, int, int, QPrep*, int8_t*), cudaStream_t s) {
+                                  void (*quantise)(const double*, int, int, QPrep*, int8_t*), double* gq64,
+                                  unsigned* gq_flag, cudaStream_t s) {
   if (!p || p->Dp > 1024 || grid > 256) return cudaErrorInvalidValue;
   static thread_local S8In in;
   const int Dp = p->Dp;
-  memcpy(in.q64, q64, (size_t)D * sizeof(double));
-  memset(in.q64 + D, 0, (size_t)(Dp - D) * sizeof(double));
-  quantise(in.q64, D, Dp, &in.prep, in.q8);
-  if (stage_row) {
-    memcpy(in.stage, stage_row, (size_t)Dp * sizeof(double));  // staged rows are already zero-padded to Dp
-  }
+  quantise(q64, D, Dp, &in.prep, in.q8);  // q64: mapped host row, zero-padded to Dp
+  in.hq64 = q64;
+  in.hstage = stage_row;
   S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), nullptr, nullptr, nullptr, stage_row ? 1 : 0, d_state,
-           done_seq, seq, outp, epoch};
+           done_seq, seq, outp, epoch, gq64, gq_flag};
   switch (p->P8 / 128) {
     case 1: return s8_launch_in<1>(p, rb, st, cta, grid, sm, a, in, s);
     case 2: return s8_launch_in<2>(p, rb, st, cta, grid, sm, a, in, s);
