@@ -38,7 +38,7 @@
 // poller folds the global value back into the CTA's).
 //
 // Pending appends (rows added since the last lookup) are not in the int8
-// copy yet: CTA 0's rescorer writes every ring copy and scores them exactly
+// copy yet: CTA 0's eager warp writes every ring copy and scores them exactly
 // from the envelope at kernel start.
 //
 // Algorithmic bytes per launch: count * (P8 + 8) + nb * (9 * Dp + 40), P8 = Dp rounded up to 128.
@@ -293,7 +293,7 @@ __device__ __forceinline__ int s8_pass(int ncw, bool retire) {
   return bi;
 }
 
-// CTA 0's rescorer: rows appended since the last lookup are not in the int8
+// CTA 0's eager warp: rows appended since the last lookup are not in the int8
 // copy yet — write every ring copy and score them exactly (float64).
 __device__ __forceinline__ void s8_pending(const S8Ctx x, const double* stage, long long n_app,
                                         long long n_pend, long long n_scan) {
@@ -306,7 +306,7 @@ __device__ __forceinline__ void s8_pending(const S8Ctx x, const double* stage, l
     write_row_all(srow, ring_slot(x.st, row), x.rb, x.Dp, lane);
     for (int b = 0; b < x.nb; ++b) {
       const double sc = s8_dot(srow, x.sq64 + (size_t)b * x.Dp, x.Dp, lane);
-      if (lane == 0) S.best[S8_CW][b].add(sc, global_pos(x.st, row, x.sm));
+      if (lane == 0) S.best[S8_EAGER][b].add(sc, global_pos(x.st, row, x.sm));
       s8_raise(&S.bound[b], lane, sc);
     }
   }
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     q64 = in.hq64;
     q8p = in.q8;
     prepp = &in.prep;
-    stagep = in.hstage;  // the poller reads it once; CTA 0's rescorer then uses the relay (below)
+    stagep = in.hstage;  // the poller reads it once; CTA 0's eager warp then uses the relay (below)
   }
   constexpr int P8 = KB * 128;                // int8 row stride (Dp rounded up to 128)
   constexpr int R = s8_rows_per_lane(KB);
@@ -632,6 +632,9 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     // early and the pool after the scan mostly finds the CTA's best done.  It
     // checks `done` before each claim and never waits on global memory, so it
     // hands over within one exact dot once the scan is over.
+    // CTA 0's eager warp first writes and scores the rows appended since the last lookup: off the
+    // rescorer, whose pool barrier (and CTA 0's record, which the merge waits for) it would delay
+    if (blockIdx.x == 0 && n_pend > 0) s8_pending(x, IN ? a.gq64 + Dp : stagep, a.n_app, n_pend, n_scan);
     while (!*(volatile int*)&S.q_ready) {
     }
     while (*(volatile int*)&S.done != S8_CW) {
@@ -781,7 +784,6 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
 
   if (warp > S8_CW) {
     // ------------------------------------------------------------ rescorer
-    if (blockIdx.x == 0 && n_pend > 0) s8_pending(x, IN ? a.gq64 + Dp : stagep, a.n_app, n_pend, n_scan);
     s8_pool(x, S8_CW);
     s8_finish(x, a, prepp, reinterpret_cast<uint4*>(cta), b0);
     return;
