@@ -62,12 +62,17 @@ static int fail(int code, const char* fmt, ...) {
       return fail(MC_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
   } while (0)
 
+// Physical ring slots beyond the logical capacity (see mc_cache::Cp).
+constexpr long long PIPE_SLACK = 8;
+
 struct mc_cache {
   std::mutex mu;
   int dev = 0;
   int sm_count = 148;
   cudaStream_t stream = nullptr;
-  long long C = 0;
+  long long C = 0;   // logical capacity: live rows never exceed it
+  long long Cp = 0;  // physical ring slots = C + PIPE_SLACK: rows an in-flight lookup scanned stay
+                     // intact until PIPE_SLACK more rows have been appended (pipelined lookups)
   int D = 0, Dp = 0;
   int P8 = 0;  // int8 ring row stride (Dp rounded up to 128)
   ShardMap shard{1, 0};
@@ -151,7 +156,10 @@ struct DeviceGuard {
   }
 };
 
-RingState mirror(const mc_cache* h) { return RingState{h->head, h->count, h->jhead, h->C}; }
+// Spare physical slots beyond the capacity.  A pipelined lookup's window must stay readable
+// (its exhaustive fallback may run after the next lookup has written appended rows): the
+// next rows land in these slots instead of over the rows it scanned.
+RingState mirror(const mc_cache* h) { return RingState{h->head, h->count, h->jhead, h->Cp}; }
 
 // The answer for an empty cache (cache.py:252-253): a miss with no similarity; every step runs.
 OutRec empty_out(const mc_cache* h) {
@@ -318,7 +326,7 @@ GemvAppendArgs take_pending(mc_cache* h, const double* dev_rows) {
     const long long skip = h->n_pending - nw;
     a.stage = dev_rows + (size_t)skip * h->Dp;
     a.n = nw;
-    a.first_slot = (h->pending_first_slot + skip) % h->C;
+    a.first_slot = (h->pending_first_slot + skip) % h->Cp;
   }
   h->n_pending = 0;
   h->state_dirty = false;
@@ -426,7 +434,7 @@ int ensure_tc(mc_cache* h, int B) {
   tc_plan_destroy(h->tc);
   h->tc = nullptr;
   char err[256] = {0};
-  h->tc = tc_plan_create(h->ring16, h->C, h->Dp, std::max(B, 128), h->sm_count, err, sizeof err);
+  h->tc = tc_plan_create(h->ring16, h->Cp, h->Dp, std::max(B, 128), h->sm_count, err, sizeof err);
   if (!h->tc) return fail(MC_ERR_CUDA, "tensor-core scan plan: %s", err);
   return MC_OK;
 }
@@ -801,6 +809,7 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   h->dev = device;
   h->sm_count = prop.multiProcessorCount;
   h->C = capacity;
+  h->Cp = capacity + PIPE_SLACK;
   h->D = dim;
   h->Dp = (dim + 63) / 64 * 64;
   h->P8 = (h->Dp + 127) / 128 * 128;
@@ -818,25 +827,25 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   CUC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   CUC(cudaEventCreateWithFlags(&h->env_ev, cudaEventDisableTiming));
   CUC(cudaEventCreateWithFlags(&h->rec_ev, cudaEventDisableTiming));
-  const size_t n16 = (size_t)h->C * h->Dp * sizeof(__half);
-  const size_t n64 = (size_t)h->C * h->Dp * sizeof(double);
-  const size_t n8 = (size_t)h->C * h->P8;
+  const size_t n16 = (size_t)h->Cp * h->Dp * sizeof(__half);
+  const size_t n64 = (size_t)h->Cp * h->Dp * sizeof(double);
+  const size_t n8 = (size_t)h->Cp * h->P8;
   CUC(cudaMalloc(&h->ring16, n16));
   CUC(cudaMalloc(&h->ring64, n64));
   CUC(cudaMalloc(&h->ring8, n8));
-  CUC(cudaMalloc(&h->ringq, (size_t)(h->C + 2) * sizeof(float2)));  // +2: 16-byte aligned bulk copies
+  CUC(cudaMalloc(&h->ringq, (size_t)(h->Cp + 2) * sizeof(float2)));  // +2: 16-byte aligned bulk copies
   CUC(cudaMemsetAsync(h->ring16, 0, n16, h->stream));
   CUC(cudaMemsetAsync(h->ring64, 0, n64, h->stream));
   CUC(cudaMemsetAsync(h->ring8, 0, n8, h->stream));
-  CUC(cudaMemsetAsync(h->ringq, 0, (size_t)(h->C + 2) * sizeof(float2), h->stream));
+  CUC(cudaMemsetAsync(h->ringq, 0, (size_t)(h->Cp + 2) * sizeof(float2), h->stream));
   CUC(cudaMalloc(&h->d_state, sizeof(RingState)));
   {
-    RingState z{0, 0, 0, h->C};
+    RingState z{0, 0, 0, h->Cp};
     CUC(cudaMemcpyAsync(h->d_state, &z, sizeof z, cudaMemcpyHostToDevice, h->stream));
   }
-  if (stream8_supported(h->Dp) && h->C < (1ll << 30)) {  // 30-bit row offsets in its records
+  if (stream8_supported(h->Dp) && h->Cp < (1ll << 30)) {  // 30-bit row offsets in its records
     char err[256] = {0};
-    h->s8 = s8_plan_create(h->ring8, h->ringq, h->C, h->Dp, h->P8, err, sizeof err);
+    h->s8 = s8_plan_create(h->ring8, h->ringq, h->Cp, h->Dp, h->P8, err, sizeof err);
     if (!h->s8) return cleanup(fail(MC_ERR_CUDA, "int8 stream scan plan: %s", err));
   }
   if (const char* e = getenv("MC_PACKED_RESULT")) h->packed = atoi(e) != 0;
@@ -931,7 +940,7 @@ int mc_configure_shard(mc_cache* h, int32_t n_shards, int32_t shard_id) {
     return fail(MC_ERR_ARG, "bad shard %d of %d", shard_id, n_shards);
   std::lock_guard<std::mutex> lk(h->mu);
   if (h->appended != 0) return fail(MC_ERR_STATE, "configure the shard before the first append");
-  if ((long long)h->C * n_shards >= (1ll << 30))  // the streamed scan's records carry 30-bit row offsets
+  if ((long long)h->Cp * n_shards >= (1ll << 30))  // the streamed scan's records carry 30-bit row offsets
     return fail(MC_ERR_ARG, "capacity %lld x %d shards exceeds 2^30 rows", (long long)h->C, n_shards);
   h->shard = ShardMap{n_shards, shard_id};
   return MC_OK;
@@ -963,11 +972,11 @@ int mc_append(mc_cache* h, const double* rows, int64_t n) {
       if (rc) return rc;
     }
     if (h->count == h->C) {  // append-then-evict of cache.py:230-233, evicting first
-      h->head = (h->head + 1) % h->C;
+      h->head = (h->head + 1) % h->Cp;
       h->count--;
       h->jhead++;
     }
-    const long long slot = (h->head + h->count) % h->C;
+    const long long slot = (h->head + h->count) % h->Cp;
     if (h->n_pending == 0) h->pending_first_slot = slot;
     double* dst = h->h_env + (size_t)h->n_pending * h->Dp;
     memcpy(dst, rows + (size_t)i * h->D, (size_t)h->D * sizeof(double));
@@ -987,7 +996,7 @@ int mc_evict_front(mc_cache* h, int64_t n) {
   if (n < 0 || n > h->count) return fail(MC_ERR_STATE, "cannot evict %lld of %lld live rows", (long long)n,
                                          (long long)h->count);
   if (n == 0) return MC_OK;
-  h->head = (h->head + n) % h->C;
+  h->head = (h->head + n) % h->Cp;
   h->count -= n;
   h->jhead += n;
   h->state_dirty = true;
@@ -1207,13 +1216,13 @@ int mc_profile_steps(mc_cache* h, const double* queries, const double* rows, int
     app.d_state = h->d_state;
     if (rows) {  // one FIFO insert per step, already resident on the device
       if (h->count == h->C) {
-        h->head = (h->head + 1) % h->C;
+        h->head = (h->head + 1) % h->Cp;
         h->count--;
         h->jhead++;
       }
       app.stage = d_rows + (size_t)it * h->Dp;
       app.n = 1;
-      app.first_slot = (h->head + h->count) % h->C;
+      app.first_slot = (h->head + h->count) % h->Cp;
       h->count++;
       h->appended++;
     }
@@ -1355,13 +1364,13 @@ int mc_profile_rotate(mc_cache* const* hs, int32_t nh, const double* queries, co
     app.d_state = h->d_state;
     if (rows) {
       if (h->count == h->C) {
-        h->head = (h->head + 1) % h->C;
+        h->head = (h->head + 1) % h->Cp;
         h->count--;
         h->jhead++;
       }
       app.stage = d_rows + (size_t)it * Dp;
       app.n = 1;
-      app.first_slot = (h->head + h->count) % h->C;
+      app.first_slot = (h->head + h->count) % h->Cp;
       h->count++;
       h->appended++;
     }
@@ -1424,15 +1433,15 @@ int mc_generate_rows(mc_cache* h, int64_t n, const double* centers, int32_t n_ce
   const long long keep = std::min<long long>(n, h->C);
   const long long skip = n - keep;
   const long long drop = std::max<long long>(0, h->count + keep - h->C);
-  h->head = (h->head + drop) % h->C;
+  h->head = (h->head + drop) % h->Cp;
   h->count -= drop;
   h->jhead += drop;
   if (skip > 0) {  // every earlier row is evicted; the skipped rows pass through the ring unseen
-    h->head = (h->head + h->count) % h->C;
+    h->head = (h->head + h->count) % h->Cp;
     h->jhead += h->count + skip;
     h->count = 0;
   }
-  const long long first_slot = (h->head + h->count) % h->C;
+  const long long first_slot = (h->head + h->count) % h->Cp;
   h->count += keep;
   h->appended += n;
   h->state_dirty = false;
@@ -1461,8 +1470,8 @@ int mc_read_rows(mc_cache* h, int64_t first_live, int64_t n, double* out) {
   CU(cudaStreamSynchronize(h->stream));
   long long done = 0;
   while (done < n) {  // at most two contiguous slot ranges (the ring wraps once)
-    const long long slot = (h->head + first_live + done) % h->C;
-    const long long run = std::min<long long>(n - done, h->C - slot);
+    const long long slot = (h->head + first_live + done) % h->Cp;
+    const long long run = std::min<long long>(n - done, h->Cp - slot);
     CU(cudaMemcpy2D(out + (size_t)done * h->D, (size_t)h->D * sizeof(double), h->ring64 + (size_t)slot * h->Dp,
                     (size_t)h->Dp * sizeof(double), (size_t)h->D * sizeof(double), (size_t)run,
                     cudaMemcpyDeviceToHost));
@@ -1480,7 +1489,7 @@ int mc_debug_read_row(mc_cache* h, int64_t live, double* out) {
   int rc = flush(h);
   if (rc) return rc;
   CU(cudaStreamSynchronize(h->stream));
-  const long long slot = (h->head + live) % h->C;
+  const long long slot = (h->head + live) % h->Cp;
   CU(cudaMemcpy(out, h->ring64 + (size_t)slot * h->Dp, (size_t)h->D * sizeof(double), cudaMemcpyDeviceToHost));
   if (getenv("MC_DEBUG_COPIES")) {  // out has room for 3 rows: float64, fp16, int8 x scale
     std::vector<__half> r16(h->Dp);

@@ -35,3 +35,12 @@ for i in range(40):
 r = np.median(np.array(res[5:]), axis=0)
 print("median over lookups (us from first CTA start): last scan end %.1f | median scan end %.1f | last record %.1f | "
       "decision %.1f | CTA0 record %.1f" % tuple(r))
+order = np.argsort(-arr[:, 5])
+print("slowest CTAs of the last lookup (us): cta scan_end pool_entry resc_start resc_end pool_exit record n_resc")
+for c in order[:10]:
+    v = arr[c]
+    f = lambda x: (x - t0) / 1e3 if 0 < x < 1.8e19 else float("nan")  # noqa: E731
+    print("   %4d %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f %3d" % (c, f(v[0]), f(v[1]), f(v[2]), f(v[3]), f(v[4]), f(v[5]), v[7]))
+print("records landed by (us): p50 %.1f p90 %.1f max %.1f; rescored per CTA: mean %.2f max %d" % (
+    (np.median(arr[:, 5]) - t0) / 1e3, (np.percentile(arr[:, 5], 90) - t0) / 1e3, (arr[:, 5].max() - t0) / 1e3,
+    arr[:, 7].mean(), arr[:, 7].max()))
