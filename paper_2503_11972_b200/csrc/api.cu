@@ -124,10 +124,25 @@ struct mc_cache {
   const double* inflight_q = nullptr;
   bool inflight_ready = false;  // completed (and any fallback applied) while staging appends
   bool inflight_direct = false; // its result comes back zero-copy
+  int inflight_slot = 0;        // its result slot: h_outp + 2 slot, d_rec + slot (single-query lookups)
+  RingState inflight_st{};      // the window it scans
+  // Pipelined single-query lookups: a second mc_retrieve_submit while one is in flight moves
+  // that one here.  Its window stays intact (PIPE_SLACK spare slots) while the newer launch
+  // writes the rows appended in between, so its exhaustive fallback, if needed, can still run
+  // on exactly what it scanned.
+  unsigned old_seq = 0;         // 0: none
+  bool old_ready = false;       // answered (and any fallback applied); waiting for its mc_retrieve_wait
+  int old_slot = 0;
+  RingState old_st{};
+  OutRec old_out{};
+  long long old_written = 0;    // rows launches after it have written into the ring
+  double* h_qslot[2] = {nullptr, nullptr};  // pinned [Dp]: the single-query lookups' queries (fallback uploads)
+  double* d_qfb = nullptr;      // [Dp] fallback query
+  RingState* d_state_fb = nullptr;  // the fallback's window
   bool param_in = false;        // MC_PARAM_INPUT=1: single-query lookups carry their inputs in the launch
                                 // parameters (measured equal to the pinned-envelope copy on B200)
   double* h_qkeep = nullptr;    // pinned, mapped [Dp]: the single-query launch's float64 query (read by the kernel)
-  double* h_stage1 = nullptr;   // pinned, mapped [Dp]: its pending row
+  double* h_stage1[2] = {nullptr, nullptr};  // pinned, mapped [Dp] per result slot: its pending row
   double* d_gq64 = nullptr;     // [Dp] the kernel's L2 relay of h_qkeep
   unsigned* d_gq_flag = nullptr;
 
@@ -519,7 +534,7 @@ int lookup_enqueue(mc_cache* h, const double* queries, int B, mc_record* rec, Ou
 }
 
 int wait_seq(mc_cache* h, unsigned seq);
-int wait_packed(mc_cache* h, unsigned seq, int B);
+int wait_packed(mc_cache* h, unsigned seq, int B, int slot = 0, OutRec* dst = nullptr);
 unsigned seq_tag(unsigned seq);
 bool direct_result(const mc_cache* h, int B);
 
@@ -528,37 +543,45 @@ bool direct_result(const mc_cache* h, int B);
 void quantize_query(const double* q, int D, int Dp, QPrep* p, int8_t* q8);
 GemvAppendArgs take_pending(mc_cache* h, const double* dev_rows);
 
-int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool async_reuse, const double** q) {
-  if (h->packed && h->param_in && B == 1 && h->n_pending <= 1 && h->Dp <= 1024) {
+int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool async_reuse, const double** q,
+                   int slot = 0, bool param = false) {
+  if (h->packed && (h->param_in || param) && B == 1 && h->n_pending <= 1 && h->Dp <= 1024) {
     // no host->device copy precedes the kernel: the quantisation rides in the parameter block,
     // the query and the pending row are read from mapped host memory (scan_stream8.cu, S8In).
     // One lookup is in flight per handle, so these buffers are free again once it completes.
+    // Per result slot, so a pipelined lookup never overwrites what the one before it reads.
     const double* stage_row = nullptr;
     if (h->n_pending == 1) {
-      memcpy(h->h_stage1, h->h_env, (size_t)h->Dp * sizeof(double));  // staged rows are zero-padded to Dp
-      stage_row = h->h_stage1;
+      memcpy(h->h_stage1[slot], h->h_env, (size_t)h->Dp * sizeof(double));  // staged rows are zero-padded to Dp
+      stage_row = h->h_stage1[slot];
     }
-    memcpy(h->h_qkeep, queries, (size_t)h->D * sizeof(double));  // padding columns stay zero
+    double* hq = h->h_qslot[slot];
+    memcpy(hq, queries, (size_t)h->D * sizeof(double));  // padding columns stay zero
+    memcpy(h->h_qkeep, queries, (size_t)h->D * sizeof(double));
     const RingState st = mirror(h);
     take_pending(h, nullptr);
-    memset(h->h_outp, 0, 2 * sizeof(uint4));
+    memset(h->h_outp + 2 * slot, 0, 2 * sizeof(uint4));
     *q = nullptr;
-    CU(launch_stream8_direct(h->s8, rbufs(h), st, h->D, h->h_qkeep, stage_row, h->d_cta, h->sm_count, h->shard,
-                             h->d_counter, h->d_gmax8, s8_epoch(h), h->thr, h->d_rec, nullptr, h->d_state, nullptr,
-                             seq_tag(seq),
-                             h->d_outp, quantize_query, h->d_gq64, h->d_gq_flag, h->stream));
+    CU(launch_stream8_direct(h->s8, rbufs(h), st, h->D, hq, stage_row, h->d_cta, h->sm_count, h->shard,
+                             h->d_counter, h->d_gmax8, s8_epoch(h), h->thr, h->d_rec + slot, nullptr, h->d_state,
+                             nullptr, seq_tag(seq), h->d_outp + 2 * slot, quantize_query, h->d_gq64, h->d_gq_flag,
+                             h->stream));
     h->stats[5]++;
     h->stats[7]++;
     return MC_OK;
   }
   if (h->packed) {
-    memset(h->h_outp, 0, (size_t)B * 2 * sizeof(uint4));  // no stale record can carry this lookup's tag
-    return lookup_enqueue(h, queries, B, h->d_rec, nullptr, async_reuse, q, nullptr, seq_tag(seq), h->d_outp);
+    memset(h->h_outp + 2 * slot, 0, (size_t)B * 2 * sizeof(uint4));  // no stale record can carry this tag
+    if (B == 1) memcpy(h->h_qslot[slot], queries, (size_t)h->D * sizeof(double));  // for a late fallback
+    return lookup_enqueue(h, queries, B, h->d_rec + slot, nullptr, async_reuse, q, nullptr, seq_tag(seq),
+                          h->d_outp + 2 * slot);
   }
   return lookup_enqueue(h, queries, B, h->d_rec, h->d_outm, async_reuse, q, h->d_seq, seq);
 }
 
-int wait_direct(mc_cache* h, unsigned seq, int B) { return h->packed ? wait_packed(h, seq, B) : wait_seq(h, seq); }
+int wait_direct(mc_cache* h, unsigned seq, int B, int slot = 0) {
+  return h->packed ? wait_packed(h, seq, B, slot) : wait_seq(h, seq);
+}
 
 // The device query of a completed lookup, for the exhaustive fallback: a
 // parameter-block lookup has none, so its kept host copy is uploaded now.
@@ -572,17 +595,49 @@ int device_query(mc_cache* h, const double* q, const double** out) {
   return MC_OK;
 }
 
-// Complete the asynchronous lookup in flight, if any: wait for its decisions
+// Exhaustive fallback of one single-query lookup from its kept query, on the window it
+// scanned (explicit state: later launches may have moved the live window since).
+int fallback_single(mc_cache* h, int slot, const RingState& st, OutRec* dst) {
+  CU(cudaMemcpyAsync(h->d_qfb, h->h_qslot[slot], (size_t)h->Dp * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(h->d_state_fb, &st, sizeof st, cudaMemcpyHostToDevice, h->stream));
+  CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state_fb, h->D, h->Dp, h->d_qfb, 1, h->d_rec + slot, h->d_scratch,
+                         exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
+  CU(launch_finalize(h->d_rec + slot, 1, 1, -1, h->d_state_fb, h->thr, h->d_out, h->stream));
+  h->stats[7] += 3;
+  CU(cudaMemcpyAsync(dst, h->d_out, sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return MC_OK;
+}
+
+// Complete the older pipelined lookup, if any (its answer stays in old_out for mc_retrieve_wait).
+int finish_old(mc_cache* h) {
+  if (!h->old_seq || h->old_ready) return MC_OK;
+  int rc = wait_packed(h, h->old_seq, 1, h->old_slot, &h->old_out);
+  if (rc) return rc;
+  if (h->old_out.flags & FLAG_NEED_ANY) {
+    rc = fallback_single(h, h->old_slot, h->old_st, &h->old_out);
+    if (rc) return rc;
+  }
+  h->old_ready = true;
+  return MC_OK;
+}
+
+// Complete the asynchronous lookups in flight, if any: wait for their decisions
 // and run the exhaustive fallback for the queries whose certificate needs it
 // (while the ring still holds the state that lookup scanned).
 int finish_inflight(mc_cache* h) {
+  int rc0 = finish_old(h);
+  if (rc0) return rc0;
   if (!h->inflight_seq || h->inflight_ready) return MC_OK;
   const int B = h->inflight_B;
-  int rc = h->inflight_direct ? wait_direct(h, h->inflight_seq, B) : wait_seq(h, h->inflight_seq);
+  int rc = h->inflight_direct ? wait_direct(h, h->inflight_seq, B, h->inflight_slot) : wait_seq(h, h->inflight_seq);
   if (rc) return rc;
   bool need = false;
   for (int b = 0; b < B; ++b) need |= (h->h_out[b].flags & FLAG_NEED_ANY) != 0;
-  if (need) {
+  if (need && h->inflight_direct && B == 1 && h->packed) {
+    rc = fallback_single(h, h->inflight_slot, h->inflight_st, h->h_out);
+    if (rc) return rc;
+  } else if (need) {
     const double* qd = nullptr;
     rc = device_query(h, h->inflight_q, &qd);
     if (rc) return rc;
@@ -645,14 +700,15 @@ int wait_record(mc_cache* h, const uint4* p, unsigned tag, unsigned seq, int b, 
 // Spin until the B packed decisions of lookup `seq` carry its tag, then unpack
 // them into h_out.  Each record is one 16-byte store on the device side and one
 // 16-byte load here, so a record is seen whole or not at all.
-int wait_packed(mc_cache* h, unsigned seq, int B) {
+int wait_packed(mc_cache* h, unsigned seq, int B, int slot, OutRec* dst) {
   const unsigned tag = seq_tag(seq);
+  const uint4* src = h->h_outp + 2 * slot;
   for (int b = 0; b < B; ++b) {
     uint4 v, v2;
-    int rc = wait_record(h, h->h_outp + 2 * b, tag, seq, b, &v);
-    if (!rc) rc = wait_record(h, h->h_outp + 2 * b + 1, tag, seq, b, &v2);
+    int rc = wait_record(h, src + 2 * b, tag, seq, b, &v);
+    if (!rc) rc = wait_record(h, src + 2 * b + 1, tag, seq, b, &v2);
     if (rc) return rc;
-    OutRec& o = h->h_out[b];
+    OutRec& o = dst ? dst[b] : h->h_out[b];
     const unsigned long long sb = (unsigned long long)v.x | ((unsigned long long)v.y << 32);
     memcpy(&o.sim, &sb, sizeof sb);
     o.live = (long long)(int)v.z;
@@ -713,7 +769,8 @@ void apply_sigma(mc_cache* h) {
 // The lookup of mc_retrieve_batch / mc_retrieve_decisions: B answers into h->h_out
 // (the caller holds the mutex and the device guard).
 int retrieve_into_hout(mc_cache* h, const double* queries, int32_t B) {
-  if (h->inflight_seq) return fail(MC_ERR_STATE, "an asynchronous lookup is in flight: mc_retrieve_wait first");
+  if (h->inflight_seq || h->old_seq)
+    return fail(MC_ERR_STATE, "an asynchronous lookup is in flight: mc_retrieve_wait first");
   int rc = ensure_batch(h, B);  // may reallocate d_rec / d_out / h_out: evaluate them after
   if (rc) return rc;
   if (h->count == 0) {  // cache.py:252-253
@@ -854,8 +911,16 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   if (const char* e = getenv("MC_PARAM_INPUT")) h->param_in = atoi(e) != 0;
   CUC(cudaHostAlloc(&h->h_qkeep, (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
   memset(h->h_qkeep, 0, (size_t)h->Dp * sizeof(double));
-  CUC(cudaHostAlloc(&h->h_stage1, (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
-  memset(h->h_stage1, 0, (size_t)h->Dp * sizeof(double));
+  for (int k = 0; k < 2; ++k) {  // mapped: the parameter-block launches read the query from here
+    CUC(cudaHostAlloc(&h->h_qslot[k], (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
+    memset(h->h_qslot[k], 0, (size_t)h->Dp * sizeof(double));
+  }
+  CUC(cudaMalloc(&h->d_qfb, (size_t)h->Dp * sizeof(double)));
+  CUC(cudaMalloc(&h->d_state_fb, sizeof(RingState)));
+  for (int k = 0; k < 2; ++k) {
+    CUC(cudaHostAlloc(&h->h_stage1[k], (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
+    memset(h->h_stage1[k], 0, (size_t)h->Dp * sizeof(double));
+  }
   CUC(cudaMalloc(&h->d_gq64, 2 * (size_t)h->Dp * sizeof(double)));  // query, then the pending row
   CUC(cudaMalloc(&h->d_gq_flag, sizeof(unsigned)));
   CUC(cudaMemsetAsync(h->d_gq_flag, 0, sizeof(unsigned), h->stream));
@@ -905,7 +970,12 @@ int mc_destroy(mc_cache* h) {
     cudaFree(h->d_counter);
     cudaFreeHost(h->h_seq);
     cudaFreeHost(h->h_qkeep);
-    cudaFreeHost(h->h_stage1);
+    cudaFreeHost(h->h_stage1[0]);
+    cudaFreeHost(h->h_stage1[1]);
+    cudaFreeHost(h->h_qslot[0]);
+    cudaFreeHost(h->h_qslot[1]);
+    cudaFree(h->d_qfb);
+    cudaFree(h->d_state_fb);
     cudaFree(h->d_gq64);
     cudaFree(h->d_gq_flag);
     if (h->env_ev) cudaEventDestroy(h->env_ev);
@@ -1040,18 +1110,49 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
   if (B < 1) return fail(MC_ERR_ARG, "batch must be positive");
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard guard(h->dev);
-  if (h->inflight_seq) return fail(MC_ERR_STATE, "an asynchronous lookup is already in flight");
+  // Pipelining: a single-query lookup may be submitted while one other single-query lookup
+  // is still in flight (its answer is collected later by its own mc_retrieve_wait).
+  const bool pipe = B == 1 && h->count > 0 && h->packed && direct_result(h, 1) && h->n_pending <= PIPE_SLACK;
+  if (h->inflight_seq && h->old_seq) return fail(MC_ERR_STATE, "two lookups are in flight: mc_retrieve_wait first");
+  if (h->inflight_seq) {
+    if (h->inflight_B != 1) return fail(MC_ERR_STATE, "an asynchronous lookup is already in flight");
+    if (!pipe || !h->inflight_direct) {  // cannot run beside it: answer it now (kept for its wait)
+      int rc = finish_inflight(h);
+      if (rc) return rc;
+    }
+    h->old_seq = h->inflight_seq;  // it becomes the older of the two
+    h->old_ready = h->inflight_ready;
+    h->old_slot = h->inflight_slot;
+    h->old_st = h->inflight_st;
+    if (h->old_ready) h->old_out = h->h_out[0];
+    h->old_written = 0;
+    h->inflight_seq = 0;
+  }
+  if (h->old_seq && !pipe) {  // the new lookup cannot run beside it: answer the older one first
+    int rc = finish_old(h);
+    if (rc) return rc;
+  }
+  if (h->old_seq && !h->old_ready && h->old_written + h->n_pending > PIPE_SLACK) {
+    int rc = finish_old(h);  // the rows this launch writes would reach the older lookup's window
+    if (rc) return rc;
+  }
   int rc = ensure_batch(h, B);
   if (rc) return rc;
   const unsigned seq = ++h->seq;
   h->inflight_B = B;
   h->inflight_q = nullptr;
+  h->inflight_slot = h->old_seq ? 1 - h->old_slot : 0;
+  h->inflight_st = mirror(h);
   if (h->count == 0) {  // cache.py:252-253: answered now
     for (int b = 0; b < B; ++b) h->h_out[b] = empty_out(h);
     h->inflight_ready = true;
+    h->inflight_direct = false;
   } else if (direct_result(h, B)) {  // the kernel publishes into mapped memory; the caller returns now
     const double* q = nullptr;
-    rc = enqueue_direct(h, queries, B, seq, /*async_reuse=*/true, &q);
+    if (h->old_seq) h->old_written += std::min(h->n_pending, h->C);
+    // beside an older lookup: inputs in the launch (no envelope copy in the stream, which would
+    // serialise behind the older kernel and hold back the host's next append)
+    rc = enqueue_direct(h, queries, B, seq, /*async_reuse=*/true, &q, h->inflight_slot, h->old_seq != 0);
     if (rc) return rc;
     h->inflight_q = q;
     h->inflight_ready = false;
@@ -1079,6 +1180,18 @@ int mc_retrieve_wait(mc_cache* h, uint32_t ticket, int64_t* out_live, double* ou
   if (!h) return fail(MC_ERR_ARG, "NULL handle");
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard guard(h->dev);
+  if (ticket && ticket == h->old_seq) {
+    int rc = finish_old(h);
+    if (rc) return rc;
+    h->old_seq = 0;
+    h->old_ready = false;
+    OutRec* keep = h->h_out;  // copy_out reads h_out[0]: hand it the older answer, leave the newer's alone
+    const OutRec saved = keep[0];
+    keep[0] = h->old_out;
+    rc = copy_out(h, 1, out_live, out_sim, out_k, out_flags);
+    keep[0] = saved;
+    return rc;
+  }
   if (!h->inflight_seq || ticket != h->inflight_seq) return fail(MC_ERR_STATE, "no lookup %u in flight", ticket);
   int rc = finish_inflight(h);
   if (rc) return rc;

@@ -61,13 +61,15 @@ class FakeRing:
         return int(live[0]), float(sim[0]), int(k[0]), int(flags[0])
 
     def submit1(self, q):
-        self._pending = self.retrieve1(q)  # answered against the rows as they are now
-        return 7
+        # answered against the rows as they are now; like the native ring, at most two in flight
+        pend = self.__dict__.setdefault("_inflight", {})
+        assert len(pend) < 2, "a third lookup submitted while two are in flight"
+        self._ticket = getattr(self, "_ticket", 6) + 1
+        pend[self._ticket] = self.retrieve1(q)
+        return self._ticket
 
     def wait1(self, ticket):
-        assert ticket == 7
-        r, self._pending = self._pending, None
-        return r
+        return self._inflight.pop(ticket)
 
     def evict_front(self, n):
         assert 0 <= n <= len(self.rows)

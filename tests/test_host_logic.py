@@ -197,7 +197,7 @@ class TestAsyncLifecycle:
         for i in range(4, 2100):  # churn past the compaction threshold: the pin must be released
             c.insert(entry(i, unit(rng, 8)))
         r = c.retrieve(q, ThresholdTable.default())  # completes the dropped lookup first
-        assert c._pending is None and c._store._pins == 0
+        assert not c._pending and c._store._pins == 0
         c.insert(entry(2100, unit(rng, 8)))
         assert len(c._store._items) < 100  # compaction runs again once unpinned
         assert r.similarity is not None and want is not None
