@@ -130,16 +130,15 @@ struct S8Args {
 };
 
 // The single-query launch's inputs (no host->device copy before the kernel):
-// the int8 quantisation rides in the kernel parameter block (~1 KB, every CTA
-// needs it at once); the float64 query and the pending row stay in mapped
-// host memory.  CTA 0's poller reads the query over PCIe once and relays it
-// through L2 (an epoch-tagged flag), so the other CTAs never touch host
-// memory; only CTA 0 (which writes the pending row) reads that row.
+// the query and its int8 quantisation ride in the kernel parameter block
+// (~9 KB; every CTA needs them); the pending row stays in mapped host memory
+// and only CTA 0, which writes it into the ring, reads it (over PCIe, once,
+// with every load in flight) into an L2 relay buffer.
 struct S8In {
   QPrep prep;
   alignas(16) int8_t q8[1024];
-  const double* hq64;    // host-mapped float64 query (zero-padded to Dp): CTA 0 relays it through L2
-  const double* hstage;  // host-mapped pending row (zero-padded to Dp), or nullptr
+  alignas(16) double q64[1024];  // the float64 query, zero-padded to Dp
+  const double* hstage;          // host-mapped pending row (zero-padded to Dp), or nullptr
 };
 struct S8NoIn {
   int unused;
@@ -553,10 +552,10 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
   const QPrep* prepp = a.prep;
   const double* stagep = a.stage;
   if constexpr (IN) {
-    q64 = in.hq64;
+    q64 = in.q64;
     q8p = in.q8;
     prepp = &in.prep;
-    stagep = in.hstage;  // the poller reads it once; CTA 0's eager warp then uses the relay (below)
+    stagep = in.hstage;  // CTA 0's poller reads it once; its eager warp then uses the relay (below)
   }
   constexpr int P8 = KB * 128;                // int8 row stride (Dp rounded up to 128)
   constexpr int R = s8_rows_per_lane(KB);
@@ -634,7 +633,7 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     // hands over within one exact dot once the scan is over.
     // CTA 0's eager warp first writes and scores the rows appended since the last lookup: off the
     // rescorer, whose pool barrier (and CTA 0's record, which the merge waits for) it would delay
-    if (blockIdx.x == 0 && n_pend > 0) s8_pending(x, IN ? a.gq64 + Dp : stagep, a.n_app, n_pend, n_scan);
+    if (blockIdx.x == 0 && n_pend > 0) s8_pending(x, IN ? a.gq64 : stagep, a.n_app, n_pend, n_scan);
     while (!*(volatile int*)&S.q_ready) {
     }
     while (*(volatile int*)&S.done != S8_CW) {
@@ -678,48 +677,20 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     // so its rescoring after the scan hits L2.  This warp never synchronises
     // (its global atomics stay off the other warps' fences and barriers).
     if constexpr (IN) {
-      if (blockIdx.x == 0) {  // the one PCIe read of the query (and pending row), relayed through L2
-        // all loads in flight at once (16 x 16 B per lane covers Dp <= 1024): one PCIe round trip
-        const double2* hq = reinterpret_cast<const double2*>(q64);
+#pragma unroll 4
+      for (int i = lane; 2 * i < Dp; i += 32)  // the query, from the parameter block
+        reinterpret_cast<double2*>(sq64)[i] = reinterpret_cast<const double2*>(q64)[i];
+      if (blockIdx.x == 0 && stagep) {  // the pending row: one PCIe round trip (16 x 16 B per lane, Dp <= 1024)
         const double2* hs = reinterpret_cast<const double2*>(stagep);
-        double2 vq[16], vs[16];
+        double2 vs[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const int i = lane + 32 * k;
-          vq[k] = 2 * i < Dp ? hq[i] : make_double2(0.0, 0.0);
-          vs[k] = (stagep && 2 * i < Dp) ? hs[i] : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int i = lane + 32 * k;
-          if (2 * i < Dp) {
-            reinterpret_cast<double2*>(sq64)[i] = vq[k];
-            reinterpret_cast<double2*>(a.gq64)[i] = vq[k];
-            if (stagep) reinterpret_cast<double2*>(a.gq64 + Dp)[i] = vs[k];
-          }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.gq_flag), "r"(a.epoch) : "memory");
-        }
-      } else {
-        if (lane == 0) {
-          unsigned f;
-          do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.gq_flag) : "memory");
-          } while (f != a.epoch);
-        }
-        __syncwarp();
-        double2 vq[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int i = lane + 32 * k;
-          vq[k] = 2 * i < Dp ? __ldcg(reinterpret_cast<const double2*>(a.gq64) + i) : make_double2(0.0, 0.0);
+          vs[k] = 2 * i < Dp ? hs[i] : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          if (2 * (lane + 32 * k) < Dp) reinterpret_cast<double2*>(sq64)[lane + 32 * k] = vq[k];
+          if (2 * (lane + 32 * k) < Dp) reinterpret_cast<double2*>(a.gq64)[lane + 32 * k] = vs[k];
       }
       __syncwarp();
       if (lane == 0) {
@@ -1036,8 +1007,9 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
   if (!p || p->Dp > 1024 || grid > 256) return cudaErrorInvalidValue;
   static thread_local S8In in;
   const int Dp = p->Dp;
-  quantise(q64, D, Dp, &in.prep, in.q8);  // q64: mapped host row, zero-padded to Dp
-  in.hq64 = q64;
+  memcpy(in.q64, q64, (size_t)D * sizeof(double));
+  memset(in.q64 + D, 0, (size_t)(Dp - D) * sizeof(double));
+  quantise(in.q64, D, Dp, &in.prep, in.q8);
   in.hstage = stage_row;
   S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), nullptr, nullptr, nullptr, stage_row ? 1 : 0, d_state,
            done_seq, seq, outp, epoch, gq64, gq_flag};
