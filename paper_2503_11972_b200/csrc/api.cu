@@ -143,8 +143,7 @@ struct mc_cache {
                                 // parameters (measured equal to the pinned-envelope copy on B200)
   double* h_qkeep = nullptr;    // pinned, mapped [Dp]: the single-query launch's float64 query (read by the kernel)
   double* h_stage1[2] = {nullptr, nullptr};  // pinned, mapped [Dp] per result slot: its pending row
-  double* d_gq64 = nullptr;     // [Dp] the kernel's L2 relay of h_qkeep
-  unsigned* d_gq_flag = nullptr;
+  double* d_gq64 = nullptr;     // [Dp] the kernel's L2 relay of the pending row
 
   TcPlan* tc = nullptr;           // fp16 tensor-core scan plan (MC_PATH_GEMM*), created on first use
   S8Plan* s8 = nullptr;           // TMA-streamed int8 scan plan (tensor maps of ring8 / ringq)
@@ -465,7 +464,6 @@ unsigned s8_epoch(mc_cache* h) {
   if (++h->s8_epoch == 0) {
     cudaMemsetAsync(h->d_gmax8, 0, (size_t)h->Bcap * 128 * sizeof(unsigned long long), h->stream);
     cudaMemsetAsync(h->d_cta, 0, (size_t)h->Bcap * gemv_grid(h->sm_count) * sizeof(CtaRec), h->stream);
-    cudaMemsetAsync(h->d_gq_flag, 0, sizeof(unsigned), h->stream);
     h->s8_epoch = 1;
   }
   return h->s8_epoch;
@@ -564,8 +562,7 @@ int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool
     *q = nullptr;
     CU(launch_stream8_direct(h->s8, rbufs(h), st, h->D, hq, stage_row, h->d_cta, h->sm_count, h->shard,
                              h->d_counter, h->d_gmax8, s8_epoch(h), h->thr, h->d_rec + slot, nullptr, h->d_state,
-                             nullptr, seq_tag(seq), h->d_outp + 2 * slot, quantize_query, h->d_gq64, h->d_gq_flag,
-                             h->stream));
+                             nullptr, seq_tag(seq), h->d_outp + 2 * slot, quantize_query, h->d_gq64, h->stream));
     h->stats[5]++;
     h->stats[7]++;
     return MC_OK;
@@ -921,9 +918,7 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
     CUC(cudaHostAlloc(&h->h_stage1[k], (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
     memset(h->h_stage1[k], 0, (size_t)h->Dp * sizeof(double));
   }
-  CUC(cudaMalloc(&h->d_gq64, 2 * (size_t)h->Dp * sizeof(double)));  // query, then the pending row
-  CUC(cudaMalloc(&h->d_gq_flag, sizeof(unsigned)));
-  CUC(cudaMemsetAsync(h->d_gq_flag, 0, sizeof(unsigned), h->stream));
+  CUC(cudaMalloc(&h->d_gq64, (size_t)h->Dp * sizeof(double)));
   if (h->C > 0x7fffffffll) h->packed = false;  // live index must fit the packed int32
   CUC(cudaHostAlloc(&h->h_seq, 64, cudaHostAllocMapped));
   *h->h_seq = 0u;
@@ -977,7 +972,6 @@ int mc_destroy(mc_cache* h) {
     cudaFree(h->d_qfb);
     cudaFree(h->d_state_fb);
     cudaFree(h->d_gq64);
-    cudaFree(h->d_gq_flag);
     if (h->env_ev) cudaEventDestroy(h->env_ev);
     if (h->rec_ev) cudaEventDestroy(h->rec_ev);
     if (h->stream) cudaStreamDestroy(h->stream);

@@ -125,8 +125,7 @@ struct S8Args {
   unsigned seq;
   uint4* outp;                 // optional (host-mapped): packed decisions, one 16-byte store each (see below)
   unsigned epoch;              // this launch's tag on the gmax words (never 0)
-  double* gq64;                // [Dp] relay of a host-mapped query (single-query launches)
-  unsigned* gq_flag;           // = epoch once gq64 holds this launch's query
+  double* gq64;                // [Dp] L2 relay of the pending row (single-query launches, CTA 0)
 };
 
 // The single-query launch's inputs (no host->device copy before the kernel):
@@ -1003,7 +1002,7 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
                                   OutRec* out,
                                   RingState* d_state, unsigned* done_seq, unsigned seq, uint4* outp,
                                   void (*quantise)(const double*, int, int, QPrep*, int8_t*), double* gq64,
-                                  unsigned* gq_flag, cudaStream_t s) {
+                                  cudaStream_t s) {
   if (!p || p->Dp > 1024 || grid > 256) return cudaErrorInvalidValue;
   static thread_local S8In in;
   const int Dp = p->Dp;
@@ -1012,7 +1011,7 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
   quantise(in.q64, D, Dp, &in.prep, in.q8);
   in.hstage = stage_row;
   S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), nullptr, nullptr, nullptr, stage_row ? 1 : 0, d_state,
-           done_seq, seq, outp, epoch, gq64, gq_flag};
+           done_seq, seq, outp, epoch, gq64};
   switch (p->P8 / 128) {
     case 1: return s8_launch_in<1>(p, rb, st, cta, grid, sm, a, in, s);
     case 2: return s8_launch_in<2>(p, rb, st, cta, grid, sm, a, in, s);
