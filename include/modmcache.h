@@ -192,6 +192,13 @@ int mc_generate_rows(mc_cache* h, int64_t n, const double* centers, int32_t n_ce
  * (0 = oldest) into out[n][dim] (parity checks of generated caches). */
 int mc_read_rows(mc_cache* h, int64_t first_live, int64_t n, double* out);
 
+/* Registers (page-locks) a caller's host buffer for the process: batched lookups whose
+ * query block lies inside a registered buffer are copied to the device by one DMA straight
+ * from it, without staging (cudaHostRegister).  Unregister before freeing the memory.  The
+ * reference has no counterpart (its retrieve reads the query in place, cache.py:254). */
+int mc_register_host(void* ptr, int64_t bytes);
+int mc_unregister_host(void* ptr);
+
 /* Debugging hook: copies the float64 master row of live index `live` (0 =
  * oldest; pending appends are published first) into out[0 .. dim). */
 int mc_debug_read_row(mc_cache* h, int64_t live, double* out);

@@ -16,6 +16,7 @@ from .records import (
     STEP_CHOICES,
     CacheEntry,
     EmbeddingError,
+    RetrievalBatch,
     RetrievalResult,
     ThresholdTable,
     cosine,

@@ -35,7 +35,8 @@ EXPORTED = (
     "mc_retrieve_batch", "mc_set_path", "mc_configure_shard", "mc_retrieve_local_async",
     "mc_merge_records", "mc_stats", "mc_last_error", "mc_version", "mc_profile_steps", "mc_profile_rotate",
     "mc_debug_gemv_timing", "mc_retrieve_submit", "mc_retrieve_wait", "mc_debug_read_row",
-    "mc_retrieve_decisions", "mc_set_sigma_schedule", "mc_generate_rows", "mc_read_rows",
+    "mc_retrieve_decisions", "mc_set_sigma_schedule", "mc_generate_rows", "mc_read_rows", "mc_register_host",
+    "mc_unregister_host",
 )
 
 
@@ -71,6 +72,8 @@ def _declare(lib):
     lib.mc_set_sigma_schedule.argtypes = [vp, dp, i32]
     lib.mc_generate_rows.argtypes = [vp, i64, dp, i32, C.c_double, C.c_double, C.c_uint64, i64]
     lib.mc_read_rows.argtypes = [vp, i64, i64, dp]
+    lib.mc_register_host.argtypes = [vp, i64]
+    lib.mc_unregister_host.argtypes = [vp]
     lib.mc_last_error.restype = C.c_char_p
     lib.mc_version.restype = C.c_char_p
     return lib
@@ -104,6 +107,29 @@ def _check(lib, rc: int) -> None:
 
 def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data
+
+
+_registered: dict = {}  # buffer address -> the array (kept alive while registered)
+
+
+def register_host(arr: np.ndarray) -> None:
+    """Page-lock a C-contiguous float64 array so batched lookups DMA straight from it
+    (mc_register_host); idempotent."""
+    if not arr.flags["C_CONTIGUOUS"]:
+        raise ValueError("register_host needs a C-contiguous array")
+    addr = arr.ctypes.data
+    if addr in _registered:
+        return
+    lib = load()
+    _check(lib, lib.mc_register_host(addr, arr.nbytes))
+    _registered[addr] = arr
+
+
+def unregister_host(arr: np.ndarray) -> None:
+    addr = arr.ctypes.data
+    if _registered.pop(addr, None) is not None:
+        lib = load()
+        _check(lib, lib.mc_unregister_host(addr))
 
 
 class DeviceRing:

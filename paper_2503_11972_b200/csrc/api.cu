@@ -347,6 +347,22 @@ GemvAppendArgs take_pending(mc_cache* h, const double* dev_rows) {
   return a;
 }
 
+// Host buffers the caller registered (mc_register_host): batches of queries that lie inside
+// one are copied to the device straight from it (DMA), without staging into the envelope.
+struct HostRange {
+  uintptr_t lo, hi;
+};
+std::mutex g_reg_mu;
+std::vector<HostRange> g_reg;
+
+bool host_registered(const void* p, size_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  for (const HostRange& r : g_reg)
+    if (a >= r.lo && a + bytes <= r.hi) return true;
+  return false;
+}
+
 // Upload the envelope prefix: pending rows, B queries (row-major, stride D),
 // then their int8 quantisation.  Returns device pointers to the queries and
 // to the quantisation block.
@@ -370,6 +386,23 @@ int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse,
   // host copy (the unquantised large-batch paths only; the int8 paths take B <= 4).
   constexpr size_t CHUNK_BYTES = 256 << 10;
   const int chunk = std::max<int>(1, (int)(CHUNK_BYTES / row));
+  if (!quantise && B > 2 * chunk && h->D == h->Dp && host_registered(queries, (size_t)B * row)) {
+    // registered caller memory: one DMA of the batch, no host staging copy
+    const double t1 = g_ht.on ? now_us() : 0.0;
+    const size_t head = (size_t)h->n_pending * row;
+    if (head) CU(cudaMemcpyAsync(h->d_env, h->h_env, head, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(h->d_env + (size_t)h->n_pending * h->Dp, queries, (size_t)B * row, cudaMemcpyHostToDevice,
+                       h->stream));
+    if (g_ht.on) g_ht.acc[1] += now_us() - t1;
+    if (async_reuse) {
+      CU(cudaEventRecord(h->env_ev, h->stream));
+      h->env_inflight = true;
+    }
+    *q_dev = h->d_env + (size_t)h->n_pending * h->Dp;
+    *prep_dev = nullptr;
+    *q8_dev = nullptr;
+    return MC_OK;
+  }
   if (!quantise && B > 2 * chunk) {
     const double t1 = g_ht.on ? now_us() : 0.0;
     const size_t head = (size_t)h->n_pending * row;
@@ -1584,6 +1617,31 @@ int mc_read_rows(mc_cache* h, int64_t first_live, int64_t n, double* out) {
                     cudaMemcpyDeviceToHost));
     done += run;
   }
+  return MC_OK;
+}
+
+int mc_register_host(void* ptr, int64_t bytes) {
+  if (!ptr || bytes <= 0) return fail(MC_ERR_ARG, "NULL or empty host buffer");
+  cudaError_t e = cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterPortable);
+  if (e != cudaSuccess) return fail(MC_ERR_CUDA, "cudaHostRegister(%lld bytes): %s", (long long)bytes,
+                                    cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  g_reg.push_back(HostRange{reinterpret_cast<uintptr_t>(ptr), reinterpret_cast<uintptr_t>(ptr) + (size_t)bytes});
+  return MC_OK;
+}
+
+int mc_unregister_host(void* ptr) {
+  if (!ptr) return fail(MC_ERR_ARG, "NULL host buffer");
+  {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    auto it = std::find_if(g_reg.begin(), g_reg.end(),
+                           [&](const HostRange& r) { return r.lo == reinterpret_cast<uintptr_t>(ptr); });
+    if (it == g_reg.end()) return fail(MC_ERR_ARG, "host buffer %p was not registered", ptr);
+    g_reg.erase(it);
+  }
+  // every handle's copies out of it are complete: the calls that use it are synchronous
+  cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) return fail(MC_ERR_CUDA, "cudaHostUnregister: %s", cudaGetErrorString(e));
   return MC_OK;
 }
 

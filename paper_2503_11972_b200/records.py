@@ -9,6 +9,7 @@ reference line each rule mirrors.
 """
 from __future__ import annotations
 
+from collections.abc import Sequence as _SequenceABC
 from dataclasses import dataclass
 from typing import Iterable, Sequence
 
@@ -98,6 +99,63 @@ def _result_factory(cls=None):
 
 
 make_result = _result_factory()
+
+
+class RetrievalBatch(_SequenceABC):
+    """The answers of one batched lookup (SemanticCache.retrieve_batch): a read-only sequence
+    of RetrievalResult, equal to the list B retrieve() calls return, whose objects are built on
+    first access (the hit entries are captured at lookup time, so later inserts and evictions
+    do not change them), plus the answers as arrays: ``similarity`` (float64, NaN on an empty
+    cache), ``k`` (int32, 0 = none) and ``hit`` (bool)."""
+
+    __slots__ = ("_ents", "similarity", "k", "flags", "_items", "_make", "_miss")
+
+    def __init__(self, ents, similarity, k, flags, make, miss):
+        self._ents = ents
+        self.similarity = similarity
+        self.k = k
+        self.flags = flags
+        self._items = None
+        self._make = make
+        self._miss = miss
+
+    @property
+    def hit(self):
+        return (self.flags & 1) != 0
+
+    def __len__(self) -> int:
+        return len(self._ents)
+
+    def _build(self):
+        make, miss = self._make, self._miss
+        out = []
+        for e, s, kk, f in zip(self._ents, self.similarity.tolist(), self.k.tolist(), self.flags.tolist()):
+            if e is not None:
+                out.append(make(e, s, kk or None))
+            elif f & 2:  # empty cache
+                out.append(miss)
+            else:
+                out.append(make(None, s, None))
+        self._items = out
+        return out
+
+    def __getitem__(self, i):
+        items = self._items if self._items is not None else self._build()
+        return items[i]
+
+    def __iter__(self):
+        items = self._items if self._items is not None else self._build()
+        return iter(items)
+
+    def __eq__(self, other):
+        if isinstance(other, RetrievalBatch):
+            other = list(other)
+        if not isinstance(other, (list, tuple)):
+            return NotImplemented
+        return list(self) == list(other)
+
+    def __repr__(self) -> str:
+        return f"RetrievalBatch({list(self)!r})"
 
 
 class ThresholdTable:

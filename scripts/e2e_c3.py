@@ -28,3 +28,14 @@ for i in range(iters):
     c.retrieve_batch(Q[i + 1], t)
 t1 = time.perf_counter()
 print(f"public retrieve_batch: {1e6 * (t1 - t0) / iters:.1f} us per batch")
+import os  # noqa: E402
+os.environ.setdefault("MC_HOST_TIMING", "1")
+import numpy as np  # noqa: E402
+lib = c.ring.lib
+# the pieces of one native batched call, from the library's host timers (printed at destroy)
+Qc = np.ascontiguousarray(Q[1])
+t0 = time.perf_counter()
+for i in range(iters):
+    np.copyto(Qc, Q[i + 1])
+t1 = time.perf_counter()
+print(f"host copy of a 2 MB float64 batch (numpy): {1e6 * (t1 - t0) / iters:.1f} us")
