@@ -414,30 +414,75 @@ class Dist:
         return float(t.item())
 
 
-def run_sharded(dist, dim, per_gpu, steps, warmup):
-    """C4-style: one cache of world x per_gpu entries sharded round-robin across the ranks; every
-    batch-1 lookup scans each shard (certified local scan) and all-gathers 32-byte records over NCCL,
-    then merges on the device.  Timed through the sharded public API (host in the loop), max over ranks."""
-    from paper_2503_11972_b200 import CacheEntry, ThresholdTable
-    from paper_2503_11972_b200.sharded import ShardedSemanticCache
+def run_sharded_c4(dist, n_total, B, steps, warmup, device=0):
+    """C4: ONE cache of `n_total` entries sharded over the job's GPUs, one shard per rank (entries
+    dealt round-robin by append position); at N = 1 the same code with one shard
+    and no collective.  A step = B lookups: every rank's certified local scan
+    (mc_retrieve_local_async) -> NCCL all-gather of the B x 32-byte records -> merge and decisions
+    on every rank (mc_merge_records, decisions read back to the host).  Strong scaling: the cache
+    and the batch stay fixed as N grows.  Timed by CUDA events on the step stream around the K
+    steps (the host's part of each step included), max over ranks.  Caches are generated on the
+    device (f4)."""
+    import torch
 
-    n = dist.world * per_gpu
-    rows, Q, _ = make_workload(dim, n, steps + warmup + 8)
-    sc = ShardedSemanticCache(capacity=n, dim=dim, device=dist.local)
-    sc.bulk_load([CacheEntry(f"e{i}", rows[i], "large", i, 0.0) for i in range(n)])
+    from paper_2503_11972_b200 import ThresholdTable, _native
+    from paper_2503_11972_b200.workload import GeneratedWorkload
+
+    G = dist.world if dist else 1
+    g = dist.rank if dist else 0
+    dim = 768
+    wl = GeneratedWorkload(dim, n_clusters=max(512, n_total // 200), seed=17)
+    n_local = (n_total - g + G - 1) // G  # positions p < n_total with p % G == g
+    ring = _native.DeviceRing(-(-n_total // G), dim, device)
+    ring.configure_shard(G, g)
+    wl.fill(ring, n_local, row0=g * n_local)
     table = ThresholdTable.default()
+    ring.set_table(table.pairs, table.total_steps)
+    Q = wl.queries((warmup + steps) * B).reshape(warmup + steps, B, dim)  # the same on every rank
+    if B > 4:  # batches DMA'd straight from the page-locked query array (no staging copy)
+        _native.register_host(Q)
+    nb = B * 32
+    dev = torch.device("cuda", device)
+    cs = torch.cuda.Stream(dev)
+    local = torch.empty(nb, dtype=torch.uint8, device=dev)
+    gathered = torch.empty(G * nb, dtype=torch.uint8, device=dev)
+    hits = 0
+
+    def step(i):
+        nonlocal hits
+        with torch.cuda.stream(cs):
+            if G > 1:
+                ring.retrieve_local_async(Q[i], local, cs.cuda_stream)
+                dist.td.all_gather_into_tensor(gathered, local)
+            else:
+                ring.retrieve_local_async(Q[i], gathered, cs.cuda_stream)
+        live, sim, k, flags = ring.merge_records(gathered, G, B, 0, cs.cuda_stream)
+        hits += int((flags & _native.MC_FLAG_HIT).astype(bool).sum())
+
     for i in range(warmup):
-        sc.retrieve(Q[i], table)
-    dist.barrier()
-    t0 = time.perf_counter()
+        step(i)
+    hits = 0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cs)
     for i in range(warmup, warmup + steps):
-        sc.retrieve(Q[i], table)
-    dt = dist.max_over_ranks(time.perf_counter() - t0)
-    sc.close()
-    return {"workload": f"C4: {n} entries ({per_gpu} per GPU) sharded round-robin over {dist.world} GPUs, "
-                        f"{dim}-dim, batch-1 lookups, NCCL all-gather of 32-byte records + device merge",
-            "value": steps / dt, "unit": "lookups/s", "ms_per_lookup": 1e3 * dt / steps, "scaling": "weak",
-            "timing": "public sharded API with the host in the loop (H2D, NCCL, merge, D2H), max over ranks"}
+        step(i)
+    e1.record(cs)
+    e1.synchronize()
+    dt = e0.elapsed_time(e1) * 1e-3
+    if dist:
+        dt = dist.max_over_ranks(dt)
+    if B > 4:
+        _native.unregister_host(Q)
+    ring.close()
+    return {"workload": f"C4: one {n_total:,}-entry cache x {dim} sharded over {G} GPU(s) (round-robin by append "
+                        f"position), batch {B}, local scan + NCCL all-gather of {B}x32-byte records + merge",
+            "value": B * steps / dt, "unit": "lookups/s", "ms_per_step": 1e3 * dt / steps, "batch": B,
+            "n_gpus": G, "rows_per_gpu": n_local, "scaling": "strong", "hit_fraction": hits / (B * steps),
+            "timing": "CUDA events on the step stream around the timed steps (host part of each step included), "
+                      "max over ranks"}
 
 
 def launch_share(kernel: str, group) -> float:
@@ -600,11 +645,13 @@ def main():
             except Exception as exc:  # reported, never fatal to the headline line
                 big[key] = {"workload": label, "error": f"{type(exc).__name__}: {exc}"}
         line["single_gpu_large"] = big
-    if dist:  # the path's real exchange step: an entry-sharded cache merged over NCCL
-        try:
-            line["c4"] = run_sharded(dist, 768, 100_000, min(2000, args.steps), args.warmup)
-        except Exception as exc:  # reported, never fatal to the headline line
-            line["c4"] = {"error": f"{type(exc).__name__}: {exc}"}
+    if not args.no_big:  # the path's exchange step: one 1M-entry cache sharded over the job's GPUs
+        line["c4_sharded"] = {}
+        for B, k in ((1, max(args.steps, 50)), (256, 20)):
+            try:
+                line["c4_sharded"][f"b{B}"] = run_sharded_c4(dist, 1_000_000, B, k, args.warmup, device=device)
+            except Exception as exc:  # reported, never fatal to the headline line
+                line["c4_sharded"][f"b{B}"] = {"error": f"{type(exc).__name__}: {exc}"}
     if rank == 0:
         line["cpu_baseline"] = cpu_baseline(c2["rows"], c2["Q"], c2["new_rows"], insert=True, seconds=args.cpu_seconds)
         print(json.dumps(line))
