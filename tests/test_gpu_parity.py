@@ -947,3 +947,24 @@ def test_pipelined_lookups_match_the_sequential_oracle(dim, cap, adds, dups):
     fallbacks = c.ring.stats()["fallbacks"]
     _record_parity(f"pipelined d{dim} cap{cap} adds{adds} dups{int(dups)}", {"queries": len(Q), "fallback": fallbacks})
     c.close()
+
+
+def test_registered_query_buffer_matches_staged_copy():
+    """Batched queries taken by DMA from a page-locked caller array (register_host_buffer) give
+    the same answers as the staged copy (B = 256, D = Dp = 1024: the direct path)."""
+    wl = ClusteredWorkload(1024, n_clusters=64, seed=77)
+    rows = wl.cache_rows(20_000)
+    c = SemanticCache(capacity=20_000, dim=1024)
+    c.bulk_load(CacheEntry(f"e{i}", rows[i], "large", i, 0.0) for i in range(len(rows)))
+    table = ThresholdTable.default()
+    Q = np.ascontiguousarray(wl.queries(3 * 256).reshape(3, 256, 1024))
+    staged = [c.retrieve_batch(Q[i], table) for i in range(3)]
+    c.register_host_buffer(Q)
+    try:
+        direct = [c.retrieve_batch(Q[i], table) for i in range(3)]
+    finally:
+        c.unregister_host_buffer(Q)
+    for a, b in zip(staged, direct):
+        assert a == b
+        assert np.array_equal(a.similarity, b.similarity) and np.array_equal(a.k, b.k)
+    c.close()

@@ -240,3 +240,56 @@ def test_threshold_table_nan_message_matches_the_reference():
         ThresholdTable([(5, float("nan")), (10, 0.3), (15, 0.4)])
     with pytest.raises(ValueError, match="strictly increasing"):
         ThresholdTable([(5, 0.3), (10, 0.3)])
+
+
+class TestPipelinedAndBatchResults:
+    def test_two_pending_lookups_answer_for_their_own_submit_state(self):
+        """Up to two retrieve_async lookups in flight: each answers for the cache as it was when
+        submitted; a third submit completes the oldest first."""
+        rng = np.random.default_rng(11)
+        c = SemanticCache(capacity=8, dim=8)
+        for i in range(8):
+            c.insert(entry(i, unit(rng, 8)))
+        table = ThresholdTable.default()
+        q0 = c.entries()[0].embedding  # e0: evicted by the next insert
+        f0 = c.retrieve_async(q0, table)
+        c.insert(entry(8, unit(rng, 8)))
+        q1 = c.entries()[0].embedding  # e1: evicted by the next insert
+        f1 = c.retrieve_async(q1, table)
+        assert len(c._pending) == 2
+        c.insert(entry(9, unit(rng, 8)))
+        f2 = c.retrieve_async(c.entries()[-1].embedding, table)  # completes f0 first
+        assert len(c._pending) == 2 and f0._cache is None
+        assert f1.result().entry.id == "e1" and f0.result().entry.id == "e0" and f2.result().entry.id == "e9"
+        assert not c._pending and c._store._pins == 0
+
+    def test_a_new_table_settles_pending_lookups(self):
+        rng = np.random.default_rng(12)
+        c = SemanticCache(capacity=8, dim=8)
+        for i in range(8):
+            c.insert(entry(i, unit(rng, 8)))
+        f = c.retrieve_async(c.entries()[3].embedding, ThresholdTable.default())
+        other = ThresholdTable([(5, 0.2), (10, 0.9)], 50)
+        r = c.retrieve(c.entries()[3].embedding, other)
+        assert not c._pending and f.result().k == 30 and r.k == 10
+
+    def test_retrieval_batch_is_the_list_of_answers(self):
+        from paper_2503_11972_b200 import RetrievalBatch
+
+        rng = np.random.default_rng(13)
+        c = SemanticCache(capacity=32, dim=8)
+        for i in range(32):
+            c.insert(entry(i, unit(rng, 8)))
+        table = ThresholdTable.default()
+        Q = np.stack([c.entries()[5].embedding] + [unit(rng, 8) for _ in range(6)])
+        got = c.retrieve_batch(Q, table)
+        want = [c.retrieve(q, table) for q in Q]
+        assert isinstance(got, RetrievalBatch) and len(got) == len(Q)
+        assert got == want and list(got) == want and got[0] == want[0] and got[-1] == want[-1]
+        assert got.hit.tolist() == [r.hit for r in want]
+        assert np.allclose(got.similarity, [r.similarity for r in want])
+        fresh = c.retrieve_batch(Q, table)  # no item built yet
+        for j in range(40):  # later inserts evict the hit entries: the batches keep their answers
+            c.insert(entry(100 + j, unit(rng, 8)))
+        assert fresh[0].entry.id == "e5" and fresh == want and got == want
+        assert SemanticCache(capacity=4, dim=8).retrieve_batch(Q[:2], table) == [RetrievalResult(None, None, None)] * 2
