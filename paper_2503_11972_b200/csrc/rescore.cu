@@ -33,7 +33,7 @@ cudaError_t launch_merge(const RingState* d_state, const double* ring64, int D, 
                          const Partials& part, const double* qscale, double eps_rel, double eps_a1, mc_record* rec,
                          ShardMap sm, const Thresholds* thr, OutRec* out, cudaStream_t s) {
   const size_t smem = (size_t)Dp * sizeof(double);
-  if (smem > 48 * 1024) {
+  if (smem > 32 * 1024) {  // dynamic + the kernel's static smem may pass the 48 KB default
     cudaError_t e = cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
@@ -161,7 +161,7 @@ cudaError_t launch_exact_rescan(const __half* ring16, const double* ring64, cons
                                 const double* q64, int B, mc_record* rec, mc_record* scratch, int grid,
                                 double eps_rel_gemv, double eps_a1, ShardMap sm, cudaStream_t s) {
   const size_t smem = (size_t)Dp * sizeof(double);
-  if (smem > 48 * 1024) {
+  if (smem > 32 * 1024) {  // dynamic + the kernel's static smem may pass the 48 KB default
     cudaError_t e = cudaFuncSetAttribute(k_exact_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }

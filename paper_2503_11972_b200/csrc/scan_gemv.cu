@@ -391,7 +391,7 @@ static cudaError_t launch_one(const __half* ring16, const RingState& st, int Dp,
   constexpr int R = rows_for(NJ, NB);
   auto kern = k_gemv_scan<NJ, NB, R>;
   const size_t smem = (size_t)NB * Dp * sizeof(double);
-  if (smem > 48 * 1024) {
+  if (smem > 32 * 1024) {  // dynamic + the kernel's static smem may pass the 48 KB default
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }

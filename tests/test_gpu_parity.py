@@ -968,3 +968,29 @@ def test_registered_query_buffer_matches_staged_copy():
         assert a == b
         assert np.array_equal(a.similarity, b.similarity) and np.array_equal(a.k, b.k)
     c.close()
+
+
+@pytest.mark.parametrize("dim", [1088, 1536])
+def test_dims_above_1024_take_the_fp16_scans(dim):
+    """D > 1024 (no int8 streamed scan): batch 1..4 on the fp16 GEMV scan, batch >= 5 on the
+    tensor-core scan, through ring wrap-around, against the float64 oracle."""
+    wl = ClusteredWorkload(dim, n_clusters=24, seed=dim)
+    cap = 3000
+    c = SemanticCache(capacity=cap, dim=dim)
+    o = OracleCache(cap, dim)
+    table, ot = ThresholdTable.default(), OracleTable()
+    rows = wl.cache_rows(cap + 700)
+    for i, v in enumerate(rows):
+        c.insert(CacheEntry(f"e{i}", v, "large", i, float(i)))
+        o.insert(OracleEntry(f"e{i}", v, "large", i, float(i)))
+        if i > 500 and i % 233 == 0:
+            for B in (1, 3, 8):
+                Q = wl.queries(B)
+                got = c.retrieve_batch(Q, table) if B > 1 else [c.retrieve(Q[0], table)]
+                for q, r in zip(Q, got):
+                    e, sim, k = o.retrieve_entry(q, ot)
+                    assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (dim, i, B)
+                    assert r.k == k and _close(r.similarity, sim), (dim, i, B, r, sim)
+    st = c.ring.stats()
+    assert st["gemv_launches"] > 0 and st["gemm_launches"] > 0
+    c.close()
