@@ -994,3 +994,28 @@ def test_dims_above_1024_take_the_fp16_scans(dim):
     st = c.ring.stats()
     assert st["gemv_launches"] > 0 and st["gemm_launches"] > 0
     c.close()
+
+
+@pytest.mark.parametrize("cap", [1, 2, 3])
+def test_tiny_capacities_every_path(cap):
+    """capacity >= 1 (cache.py:154-155): rings of 1-3 rows (plus the spare slots) through many
+    wrap-arounds, batch 1 (streamed int8 scan), 2 and 6 (tensor-core scan), against the oracle."""
+    rng = np.random.default_rng(cap)
+    dim = 96
+    c = SemanticCache(capacity=cap, dim=dim)
+    o = OracleCache(cap, dim)
+    table, ot = ThresholdTable.default(), OracleTable()
+    for i in range(40):
+        v = rng.standard_normal(dim)
+        v /= np.linalg.norm(v)
+        c.insert(CacheEntry(f"e{i}", v, "large", i, float(i)))
+        o.insert(OracleEntry(f"e{i}", v, "large", i, float(i)))
+        for B in (1, 2, 6):
+            Q = np.stack([v * 0.9 + 0.1 * rng.standard_normal(dim) for _ in range(B)])
+            Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+            got = c.retrieve_batch(Q, table) if B > 1 else [c.retrieve(Q[0], table)]
+            for q, r in zip(Q, got):
+                e, sim, k = o.retrieve_entry(q, ot)
+                assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (cap, i, B)
+                assert r.k == k and _close(r.similarity, sim), (cap, i, B, r, sim)
+    c.close()
