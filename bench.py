@@ -202,7 +202,9 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
 
     qd = Q[: total * B].reshape(total, B, dim)
     rd = new_rows[:total] if insert else None
-    _native.DeviceRing.profile_rotate(rings, qd[:warmup], None if rd is None else rd[:warmup], warmup)
+    n_wrep = max(1, -(-50 // warmup))  # at least 50 untimed warm-up steps (W of them per pass)
+    for _ in range(n_wrep):
+        _native.DeviceRing.profile_rotate(rings, qd[:warmup], None if rd is None else rd[:warmup], warmup)
     if dist:
         dist.barrier()  # every rank enters the timed region together
     with ClockSampler(device) as clk:
@@ -218,7 +220,7 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
     # keep host metadata in step with ring 0 (it received every n_rot-th insert of each rotation call,
     # then the cross-check's inserts)
     if insert:
-        idx = [i for i in range(warmup) if i % n_rot == 0] + [warmup + i for i in range(steps) if i % n_rot == 0]
+        idx = [i for i in range(warmup) if i % n_rot == 0] * n_wrep + [warmup + i for i in range(steps) if i % n_rot == 0]
         idx += [warmup + i for i in range(n_chk)]
         for i in idx:
             cache._store.append(CacheEntry(f"p{i}", new_rows[i], "large", cache._next_seq, 0.0))
@@ -299,7 +301,7 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
         "value": value, "ms_per_step": step_ms, "e2e": e2e, "roofline": roof, "clocks": clk.summary(),
         "gpu_launches": rot["launches_per_step"] * steps,
         "stats": st,
-        "profile": dict(prof, rotation={"caches": n_rot, **rot},
+        "profile": dict(prof, rotation={"caches": n_rot, **rot}, untimed_warmup_steps=n_wrep * warmup,
                         per_step_check="events around each step, 256 MiB L2 flush between steps (outside the events)"),
         "rows": rows, "Q": Q, "new_rows": new_rows,
     }
