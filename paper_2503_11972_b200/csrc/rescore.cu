@@ -20,6 +20,8 @@ __global__ void __launch_bounds__(MERGE_THREADS)
   // Programmatic dependent launch: the query and the ring state were written before the
   // scan's prep kernel started; the candidate lists are read only after the scan is done.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the next step's query prep may be placed now (it waits for this grid before writing)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const mc_record r = merge_one(st, ring64, D, Dp, sq, part_s + (size_t)b * n_chunks * KP,
                                 part_p + (size_t)b * n_chunks * KP, part_floor + (size_t)b * n_chunks, n_chunks,
                                 qscale ? qscale[b] : 1.0, eps_rel, eps_a1, sm, ms);

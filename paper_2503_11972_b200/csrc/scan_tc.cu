@@ -536,6 +536,9 @@ __global__ void __launch_bounds__(256) k_tc_prep(const double* __restrict__ q64,
   const double n = sqrt(a);
   const bool ok = b < B && n > 0.0 && isfinite(n);
   const double inv = ok ? 1.0 / n : 0.0;
+  // launched as a programmatic dependent of the previous step's merge, which still reads qscale:
+  // write only once that grid is done (the query reads above overlap its tail)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int i = 2 * lane; i < Dp; i += 64) {  // Dp is a multiple of 64
     const double x0 = ok && i < D ? src[i] * inv : 0.0;
     const double x1 = ok && i + 1 < D ? src[i + 1] * inv : 0.0;
@@ -646,9 +649,19 @@ cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const Rin
   const int groups = tc_chunks(p, B);
   if (groups < 1 || groups > part.n_chunks) return cudaErrorInvalidValue;
   const int rows = nm * 256;
-  k_tc_prep<<<(rows + 7) / 8, 256, 0, s>>>(q64, B, D, p->Dp, p->q16, p->qscale);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((rows + 7) / 8);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // griddepcontrol.wait in k_tc_prep
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_tc_prep, q64, B, D, p->Dp, p->q16, p->qscale);
+    if (e != cudaSuccess) return e;
+  }
   const float margin = tc_margin(p->Dp);
   {
     cudaLaunchConfig_t cfg = {};
