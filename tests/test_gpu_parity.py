@@ -1019,3 +1019,75 @@ def test_tiny_capacities_every_path(cap):
                 assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (cap, i, B)
                 assert r.k == k and _close(r.similarity, sim), (cap, i, B, r, sim)
     c.close()
+
+
+@pytest.mark.parametrize("seed", [7, 8, 9, 10])
+def test_random_operations_with_pending_lookups(seed):
+    """Randomised op logs with up to two retrieve_async lookups left pending across inserts (policy,
+    age and capacity churn), bulk loads, synchronous and batched lookups and path switches: every
+    pending lookup answers for the cache as it was at its submit, whenever it is read."""
+    rng = np.random.default_rng(2000 + seed)
+    dim = int(rng.choice([16, 96, 384, 768, 1000]))
+    cap = int(rng.integers(20, 1500))
+    age = float(rng.choice([0.0, 150.0]))
+    c = SemanticCache(capacity=cap, dim=dim, policy="all", max_age_s=age or None)
+    o = OracleCache(cap, dim, max_age_s=age or None)
+    table, ot = ThresholdTable.default(), OracleTable()
+    centers = rng.standard_normal((5, dim))
+    t, seq = 0.0, 0
+    pending = []  # (future, expected (entry, sim, k))
+
+    def fresh(n):
+        nonlocal t, seq
+        out = []
+        for _ in range(n):
+            if seq and rng.random() < 0.1:  # an exact duplicate of the previous row: ties, fallbacks
+                v = out[-1].embedding if out else c.entries()[-1].embedding if len(c) else rng.standard_normal(dim)
+            else:
+                v = centers[rng.integers(0, 5)] + 4.8 * rng.standard_normal(dim) / np.sqrt(dim)
+            t += float(rng.exponential(1.0))
+            out.append(CacheEntry(f"e{seq}", v / np.linalg.norm(v), "large" if rng.random() < 0.85 else "small",
+                                  seq, t))
+            seq += 1
+        return out
+
+    def query(n):
+        Q = centers[rng.integers(0, 5, n)] + 4.8 * rng.standard_normal((n, dim)) / np.sqrt(dim)
+        return Q / np.linalg.norm(Q, axis=1, keepdims=True)
+
+    def check(r, want, where, q):
+        e, sim, k = want[:3]
+        assert r.k == k and _close(r.similarity, sim), (seed, where, r, sim)
+        got_id, want_id = (r.entry.id if r.hit else None), (e.id if e is not None else None)
+        if got_id != want_id:  # only a near-duplicate row within numpy's own rounding may differ
+            assert r.hit and e is not None and abs(float(r.entry.embedding @ q) - sim) <= 1e-12, (seed, where, r, e)
+
+    for step in range(120):
+        op = rng.random()
+        if op < 0.3:
+            for e in fresh(int(rng.integers(1, 12))):
+                c.insert(e)
+                o.insert(OracleEntry(e.id, e.embedding, e.producer, e.seq, e.inserted_at))
+        elif op < 0.36:
+            batch = fresh(int(rng.integers(1, 300)))
+            c.bulk_load(batch)
+            for e in batch:
+                o.insert(OracleEntry(e.id, e.embedding, e.producer, e.seq, e.inserted_at))
+        elif op < 0.7:  # submit; keep at most two pending on our side too
+            q = query(1)[0]
+            pending.append((c.retrieve_async(q, table), o.retrieve_entry(q, ot) + (q,)))
+            if len(pending) > 2 or rng.random() < 0.3:
+                f, want = pending.pop(int(rng.integers(0, len(pending))))
+                check(f.result(), want, ("async", step), want[3])
+        elif op < 0.85:
+            q = query(1)[0]
+            check(c.retrieve(q, table), o.retrieve_entry(q, ot), ("sync", step), q)
+        else:
+            c.ring.set_path(int(rng.choice([_native.PATH_AUTO, _native.PATH_STREAM8, _native.PATH_GEMV])))
+            Q = query(int(rng.choice([2, 4, 7, 64])))
+            for q, r in zip(Q, c.retrieve_batch(Q, table)):
+                check(r, o.retrieve_entry(q, ot), ("batch", step), q)
+    for f, want in pending:
+        check(f.result(), want, "final", want[3])
+    assert len(c) == len(o.meta) == len(c.ring)
+    c.close()
