@@ -103,7 +103,7 @@ if launch_csv.exists():
     total = sum(sum(v) for v in per.values())
     with open(DST / f"{tag}_launches_bench.txt", "w") as fh:
         fh.write("ncu --metrics gpu__time_duration.sum --clock-control none over "
-                 "`python bench.py --steps 8 --warmup 3` (cold-cache, serialised: compare shares, not absolutes)\n"
+                 "`python bench.py --steps 8 --warmup 3 --no-big` (cold-cache, serialised: compare shares, not absolutes)\n"
                  "k_append = the bulk preload of the rotation caches (setup); k_l2_flush = the per-step cross-check's "
                  "L2 flush (outside its events); a C2 step launches only k_stream8_scan, a C3 step k_tc_prep + "
                  "k_tc_scan_pair + k_merge\n\n")
