@@ -449,11 +449,24 @@ def run_sharded_c4(dist, n_total, B, steps, warmup, device=0):
     local = torch.empty(nb, dtype=torch.uint8, device=dev)
     gathered = torch.empty(G * nb, dtype=torch.uint8, device=dev)
     hits = 0
+    # A batch enters the job once: each rank uploads its 1/G of the rows, and the ranks
+    # all-gather the batch over NVLink (instead of G host uploads of the whole batch).
+    split = dist is not None and B > 4 and B % G == 0 and (G > 1 or os.environ.get("MC_C4_SPLIT_UPLOAD"))
+    if split:
+        Qt = torch.from_numpy(Q)  # page-locked above: the slice copies are DMAs
+        part = B // G
+        local_q = torch.empty(part * dim, dtype=torch.float64, device=dev)
+        full_q = torch.empty(B * dim, dtype=torch.float64, device=dev)
 
     def step(i):
         nonlocal hits
         with torch.cuda.stream(cs):
-            if G > 1:
+            if split:
+                local_q.copy_(Qt[i, g * part:(g + 1) * part].reshape(-1), non_blocking=True)
+                dist.td.all_gather_into_tensor(full_q, local_q)
+                ring.retrieve_local_device(full_q, B, local, cs.cuda_stream)
+                dist.td.all_gather_into_tensor(gathered, local)
+            elif G > 1:
                 ring.retrieve_local_async(Q[i], local, cs.cuda_stream)
                 dist.td.all_gather_into_tensor(gathered, local)
             else:
@@ -483,6 +496,8 @@ def run_sharded_c4(dist, n_total, B, steps, warmup, device=0):
                         f"position), batch {B}, local scan + NCCL all-gather of {B}x32-byte records + merge",
             "value": B * steps / dt, "unit": "lookups/s", "ms_per_step": 1e3 * dt / steps, "batch": B,
             "n_gpus": G, "rows_per_gpu": n_local, "scaling": "strong", "hit_fraction": hits / (B * steps),
+            "query_upload": ("1/G of the batch per rank + NCCL all-gather of the queries" if split
+                             else "the whole batch from the host on every rank"),
             "timing": "CUDA events on the step stream around the timed steps (host part of each step included), "
                       "max over ranks"}
 

@@ -142,6 +142,11 @@ int mc_configure_shard(mc_cache* h, int32_t n_shards, int32_t shard_id);
  * NULL = the handle's stream); not synchronous. */
 int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream);
 
+/* mc_retrieve_local_async with the B query rows already in DEVICE memory (float64, row stride
+ * dim; dim a multiple of 64), written on `stream` — e.g. assembled by an all-gather of the
+ * ranks' slices of the batch, so each rank uploads only its share from the host. */
+int mc_retrieve_local_device(mc_cache* h, const double* d_queries, int32_t B, void* dev_records, void* stream);
+
 /* Merge G x B gathered records (device pointer, shard-major) on the device and
  * return final answers like mc_retrieve_batch.  p0 = global position of the
  * oldest live entry (live index = pos - p0).  Synchronous. */

@@ -36,7 +36,7 @@ EXPORTED = (
     "mc_merge_records", "mc_stats", "mc_last_error", "mc_version", "mc_profile_steps", "mc_profile_rotate",
     "mc_debug_gemv_timing", "mc_retrieve_submit", "mc_retrieve_wait", "mc_debug_read_row",
     "mc_retrieve_decisions", "mc_set_sigma_schedule", "mc_generate_rows", "mc_read_rows", "mc_register_host",
-    "mc_unregister_host",
+    "mc_unregister_host", "mc_retrieve_local_device",
 )
 
 
@@ -73,6 +73,7 @@ def _declare(lib):
     lib.mc_generate_rows.argtypes = [vp, i64, dp, i32, C.c_double, C.c_double, C.c_uint64, i64]
     lib.mc_read_rows.argtypes = [vp, i64, i64, dp]
     lib.mc_register_host.argtypes = [vp, i64]
+    lib.mc_retrieve_local_device.argtypes = [vp, vp, i32, vp, vp]
     lib.mc_unregister_host.argtypes = [vp]
     lib.mc_last_error.restype = C.c_char_p
     lib.mc_version.restype = C.c_char_p
@@ -292,6 +293,12 @@ class DeviceRing:
         Q = np.ascontiguousarray(Q, dtype=np.float64)
         _check(self.lib, self.lib.mc_retrieve_local_async(self._h, _ptr(Q), Q.shape[0], self._addr(dev_records),
                                                           stream_ptr or None))
+
+    def retrieve_local_device(self, dev_queries, B: int, dev_records, stream_ptr: int = 0) -> None:
+        """retrieve_local_async for B float64 query rows already on this ring's device (a torch
+        tensor or raw pointer, row stride dim), written on `stream` (mc_retrieve_local_device)."""
+        _check(self.lib, self.lib.mc_retrieve_local_device(self._h, self._addr(dev_queries), int(B),
+                                                           self._addr(dev_records), stream_ptr or None))
 
     def merge_records(self, dev_records, G: int, B: int, p0: int, stream_ptr: int = 0):
         """Merge G x B gathered records (shard-major) into decisions; p0 = oldest live global position."""

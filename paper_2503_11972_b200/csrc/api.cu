@@ -1256,6 +1256,41 @@ int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void*
   return MC_OK;
 }
 
+int mc_retrieve_local_device(mc_cache* h, const double* d_queries, int32_t B, void* dev_records, void* stream) {
+  if (!h || !dev_records || (!d_queries && B > 0)) return fail(MC_ERR_ARG, "NULL argument");
+  if (B <= 0) return fail(MC_ERR_ARG, "batch must be positive");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  if (h->D != h->Dp) return fail(MC_ERR_ARG, "device queries need dim %% 64 == 0 (dim %d)", h->D);
+  mc_record* rec = static_cast<mc_record*>(dev_records);
+  int rc = ensure_batch(h, B);
+  if (!rc) rc = flush(h);  // pending appends land first (k_append), as a host-fed lookup would fold them in
+  if (rc) return rc;
+  if (stream && stream != h->stream) {  // the queries were written on the caller's stream
+    CU(cudaEventRecord(h->rec_ev, (cudaStream_t)stream));
+    CU(cudaStreamWaitEvent(h->stream, h->rec_ev, 0));
+  }
+  if (h->count == 0) {
+    CU(cudaMemsetAsync(rec, 0xff, (size_t)B * sizeof(mc_record), h->stream));  // pos = -1 (NaN sims)
+  } else {
+    GemvAppendArgs none{};
+    none.rb = rbufs(h);
+    none.d_state = h->d_state;
+    // no host quantisation: batch >= 5 takes the tensor-core scan, smaller batches the fp16 GEMV scan
+    rc = scan_merge(h, d_queries, B, rec, nullptr, none, nullptr, nullptr);
+    if (rc) return rc;
+    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, d_queries, B, rec, h->d_scratch,
+                           exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
+    h->stats[7] += 2;
+  }
+  if (stream && stream != h->stream) {  // order the caller's stream (the exchange) after this shard's scan
+    CU(cudaEventRecord(h->rec_ev, h->stream));
+    CU(cudaStreamWaitEvent((cudaStream_t)stream, h->rec_ev, 0));
+  }
+  h->stats[0] += B;
+  return MC_OK;
+}
+
 int mc_merge_records(mc_cache* h, const void* dev_records, int32_t G, int32_t B, int64_t p0, void* stream,
                      int64_t* out_live, double* out_sim, int32_t* out_k, uint32_t* out_flags) {
   if (!h || !dev_records) return fail(MC_ERR_ARG, "NULL argument");

@@ -1091,3 +1091,33 @@ def test_random_operations_with_pending_lookups(seed):
         check(f.result(), want, "final", want[3])
     assert len(c) == len(o.meta) == len(c.ring)
     c.close()
+
+
+@pytest.mark.parametrize("B", [3, 64])
+def test_local_lookup_from_device_queries_matches_host_queries(B):
+    """mc_retrieve_local_device (queries already on the GPU, e.g. all-gathered from the ranks'
+    slices of a batch) gives the same shard records and merged decisions as the host-fed
+    mc_retrieve_local_async, on a shard ring with appends pending."""
+    import torch
+
+    wl = ClusteredWorkload(768, n_clusters=64, seed=B)
+    ring = _native.DeviceRing(6000, 768, 0)
+    ring.configure_shard(2, 1)
+    ring.append(wl.cache_rows(6500))
+    table = ThresholdTable.default()
+    ring.set_table(table.pairs, table.total_steps)
+    Q = np.ascontiguousarray(wl.queries(B))
+    dev = torch.device("cuda", 0)
+    rec_h = torch.empty(B * 32, dtype=torch.uint8, device=dev)
+    rec_d = torch.empty(B * 32, dtype=torch.uint8, device=dev)
+    qd = torch.from_numpy(Q).to(dev).reshape(-1)
+    torch.cuda.synchronize()
+    for rnd in range(3):
+        ring.append(wl.cache_rows(5 + rnd))  # pending rows: the device-query path lands them first
+        ring.retrieve_local_device(qd, B, rec_d)
+        ring.retrieve_local_async(Q, rec_h)
+        dev_ans = ring.merge_records(rec_d, 1, B, 0)
+        host_ans = ring.merge_records(rec_h, 1, B, 0)
+        for x, y in zip(dev_ans, host_ans):
+            assert np.array_equal(x, y), rnd
+    ring.close()
