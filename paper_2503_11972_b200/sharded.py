@@ -254,7 +254,17 @@ class ShardedSemanticCache:
             gathered = torch.empty(self.n_shards * nb, dtype=torch.uint8, device=dev)
             if self._dist is not None:  # one shard per rank: all-gather the B records (the only collective)
                 local = torch.empty(nb, dtype=torch.uint8, device=dev)
-                self.ring.retrieve_local_async(Q, local, sp)
+                G = self.n_shards
+                if dev.type == "cuda" and G > 1 and B > 4 and B % G == 0 and self.dim % 64 == 0:
+                    # the batch enters once: each rank uploads its 1/G of the rows and the ranks
+                    # all-gather the queries over NVLink (mc_retrieve_local_device)
+                    part = B // G
+                    mine = torch.from_numpy(Q[self.shard * part:(self.shard + 1) * part]).to(dev).reshape(-1)
+                    full = torch.empty(B * self.dim, dtype=torch.float64, device=dev)
+                    self._dist.all_gather_into_tensor(full, mine, group=self._group)
+                    self.ring.retrieve_local_device(full, B, local, sp)
+                else:
+                    self.ring.retrieve_local_async(Q, local, sp)
                 self._dist.all_gather_into_tensor(gathered, local, group=self._group)
                 return gathered, sp
             for g, ring in self._rings.items():  # every shard in this process: write the slices directly
