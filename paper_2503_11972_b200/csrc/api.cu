@@ -62,9 +62,6 @@ static int fail(int code, const char* fmt, ...) {
       return fail(MC_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
   } while (0)
 
-// Physical ring slots beyond the logical capacity (see mc_cache::Cp).
-constexpr long long PIPE_SLACK = 8;
-
 struct mc_cache {
   std::mutex mu;
   int dev = 0;
@@ -144,6 +141,7 @@ struct mc_cache {
   double* h_qkeep = nullptr;    // pinned, mapped [Dp]: the single-query launch's float64 query (read by the kernel)
   double* h_stage1[2] = {nullptr, nullptr};  // pinned, mapped [Dp] per result slot: its pending row
   double* d_gq64 = nullptr;     // [Dp] the kernel's L2 relay of the pending row
+  unsigned* d_sync = nullptr;   // [2] streamed-scan launch overlap: rows published / records read (epochs)
 
   TcPlan* tc = nullptr;           // fp16 tensor-core scan plan (MC_PATH_GEMM*), created on first use
   S8Plan* s8 = nullptr;           // TMA-streamed int8 scan plan (tensor maps of ring8 / ringq)
@@ -493,10 +491,14 @@ int ensure_tc(mc_cache* h, int B) {
 // t_mid (optional) is recorded between the scan and the standalone merge.
 // Epoch of the next streamed-scan launch (never 0: zeroed words belong to no launch).  On
 // wrap-around the bound words are cleared, so an old epoch can never outrank a new one.
+// Distance (uint4) between the two epoch-parity record buffers of the streamed scan in d_cta.
+unsigned s8_rec_par(const mc_cache* h) { return (unsigned)((size_t)h->Bcap * h->sm_count * 2); }
+
 unsigned s8_epoch(mc_cache* h) {
   if (++h->s8_epoch == 0) {
     cudaMemsetAsync(h->d_gmax8, 0, (size_t)h->Bcap * 128 * sizeof(unsigned long long), h->stream);
     cudaMemsetAsync(h->d_cta, 0, (size_t)h->Bcap * gemv_grid(h->sm_count) * sizeof(CtaRec), h->stream);
+    cudaMemsetAsync(h->d_sync, 0, 2 * sizeof(unsigned), h->stream);
     h->s8_epoch = 1;
   }
   return h->s8_epoch;
@@ -530,7 +532,7 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
     if (s8)
       CU(launch_stream8_scan(h->s8, rbufs(h), st, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0, h->sm_count, h->shard,
                              h->d_counter, h->d_gmax8, s8_epoch(h), h->thr, rec, out, a, prep + b0, q8 + (size_t)b0 * h->Dp,
-                             b0 + nb == B ? done_seq : nullptr, seq, outp, h->stream));
+                             b0 + nb == B ? done_seq : nullptr, seq, outp, h->d_sync, s8_rec_par(h), h->stream));
     else
       CU(launch_gemv_scan(h->ring16, st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
                           gemv_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax, h->ring64, h->thr, rec, out, a,
@@ -595,7 +597,8 @@ int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool
     *q = nullptr;
     CU(launch_stream8_direct(h->s8, rbufs(h), st, h->D, hq, stage_row, h->d_cta, h->sm_count, h->shard,
                              h->d_counter, h->d_gmax8, s8_epoch(h), h->thr, h->d_rec + slot, nullptr, h->d_state,
-                             nullptr, seq_tag(seq), h->d_outp + 2 * slot, quantize_query, h->d_gq64, h->stream));
+                             nullptr, seq_tag(seq), h->d_outp + 2 * slot, quantize_query, h->d_gq64, h->d_sync,
+                             s8_rec_par(h), h->stream));
     h->stats[5]++;
     h->stats[7]++;
     return MC_OK;
@@ -938,6 +941,12 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   if (const char* e = getenv("MC_PACKED_RESULT")) h->packed = atoi(e) != 0;
   // testing hook: start the streamed scan's bound epochs near the 32-bit wrap-around
   if (const char* e = getenv("MC_S8_EPOCH0")) h->s8_epoch = (unsigned)strtoul(e, nullptr, 0);
+  CUC(cudaMalloc(&h->d_sync, 2 * sizeof(unsigned)));
+  {  // both words start at the epoch before the first launch's
+    const unsigned z[2] = {h->s8_epoch, h->s8_epoch};
+    CUC(cudaMemcpyAsync(h->d_sync, z, sizeof z, cudaMemcpyHostToDevice, h->stream));
+    CUC(cudaStreamSynchronize(h->stream));
+  }
   if (const char* e = getenv("MC_PARAM_INPUT")) h->param_in = atoi(e) != 0;
   CUC(cudaHostAlloc(&h->h_qkeep, (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
   memset(h->h_qkeep, 0, (size_t)h->Dp * sizeof(double));
@@ -1005,6 +1014,7 @@ int mc_destroy(mc_cache* h) {
     cudaFree(h->d_qfb);
     cudaFree(h->d_state_fb);
     cudaFree(h->d_gq64);
+    cudaFree(h->d_sync);
     if (h->env_ev) cudaEventDestroy(h->env_ev);
     if (h->rec_ev) cudaEventDestroy(h->rec_ev);
     if (h->stream) cudaStreamDestroy(h->stream);

@@ -27,6 +27,10 @@ constexpr uint32_t FLAG_NEED_FALLBACK = 0x10000u;
 constexpr uint32_t FLAG_NEED_EXHAUSTIVE = 0x20000u;
 constexpr uint32_t FLAG_NEED_ANY = FLAG_NEED_FALLBACK | FLAG_NEED_EXHAUSTIVE;
 
+// Physical ring slots beyond the logical capacity: rows a launch is still scanning stay intact
+// while up to PIPE_SLACK rows are appended behind it (pipelined lookups, overlapping launches).
+constexpr long long PIPE_SLACK = 8;
+
 struct RingState {
   long long head;   // physical slot of the oldest live row
   long long count;  // live rows
@@ -132,7 +136,7 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
                                   OutRec* out,
                                   RingState* d_state, unsigned* done_seq, unsigned seq, uint4* outp,
                                   void (*quantise)(const double*, int, int, QPrep*, int8_t*), double* gq64,
-                                  cudaStream_t s);
+                                  unsigned* sync, unsigned rec_par, cudaStream_t s);
 S8Plan* s8_plan_create(int8_t* ring8, float2* ringq, long long C, int Dp, int P8, char* err, int errlen);
 void s8_plan_destroy(S8Plan* p);
 cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingState& st, const double* q64, int nb,
@@ -140,7 +144,7 @@ cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingS
                                 unsigned long long* gmax, unsigned epoch, const Thresholds& thr, mc_record* rec,
                                 OutRec* out, const GemvAppendArgs& app,
                                 const QPrep* prep, const int8_t* q8, unsigned* done_seq, unsigned seq,
-                                uint4* outp, cudaStream_t s);
+                                uint4* outp, unsigned* sync, unsigned rec_par, cudaStream_t s);
 
 int gemv_grid(int sm_count);
 cudaError_t launch_generate(long long n, long long first_slot, const RingState& ns, int D, int Dp, const RingBufs& rb,

@@ -126,7 +126,21 @@ struct S8Args {
   uint4* outp;                 // optional (host-mapped): packed decisions, one 16-byte store each (see below)
   unsigned epoch;              // this launch's tag on the gmax words (never 0)
   double* gq64;                // [Dp] L2 relay of the pending row (single-query launches, CTA 0)
+  // Overlap with the previous launch on this ring (the next lookup's scan starts while the
+  // previous grid's merge still runs; see the prologue): sync[0] = epoch whose pending rows
+  // are written and visible, sync[1] = epoch whose CTA records the merger has read.  Records
+  // alternate between two buffers by epoch parity, rec_par uint4 apart.  nullptr: no overlap.
+  unsigned* sync;
+  unsigned rec_par;
 };
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // The single-query launch's inputs (no host->device copy before the kernel):
 // the query and its int8 quantisation ride in the kernel parameter block
@@ -399,8 +413,12 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
   const int nb = x.nb;
   const unsigned tag = a.epoch;
   const long long pbase = global_pos(x.st, 0, x.sm);
+  if (a.sync) crec += (size_t)(tag & 1u) * a.rec_par;  // this epoch's record buffer
   if (lane == 0)
     while (ld_acq_cta(&S.pool_done) != S8_CW + 2) {  // the nine pool warps and the eager rescorer
+    }
+  if (lane == 0 && a.sync)  // the launch two back used this buffer: its merger must be done reading it
+    while ((int)(ld_acquire_gpu_u32(a.sync + 1) - (tag - 2u)) < 0) {
     }
   __syncwarp();
   for (int b = 0; b < nb; ++b) {
@@ -529,6 +547,7 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
     }
   }
   __syncwarp();
+  if (lane == 0 && a.sync) st_release_gpu_u32(a.sync + 1, tag);  // every record of this launch is read
   if (lane == 0) {
     if (a.done_seq) {  // zero-copy result: the decisions, then the sequence word, over the system fabric
       __threadfence_system();
@@ -610,9 +629,19 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
                                            : make_uint4(0u, 0u, 0u, 0u);
   }
   // Everything above reads only this launch's inputs (host-staged queries) and
-  // initialises shared memory; from here on the ring, the counters and the
-  // records the previous grid may still be writing are touched.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // initialises shared memory; from here on the ring is touched.
+  // With `sync`, this launch does not wait for the previous one on the ring to finish: it needs
+  // only the rows that launch appended (its CTA 0 publishes sync[0] once they are written).
+  // The previous launch's window survives the rows this one appends (<= PIPE_SLACK of them land
+  // in spare slots), the bound words are epoch-tagged and the records alternate by epoch parity
+  // (a record writer waits for sync[1]).  Otherwise: the full programmatic dependency.
+  if (a.sync && a.n_app <= PIPE_SLACK) {
+    if (threadIdx.x == 0)
+      while ((int)(ld_acquire_gpu_u32(a.sync) - (a.epoch - 1u)) < 0) {
+      }
+  } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0 && a.d_state) *a.d_state = st;
     if (timing) atomicMin(a.timing + 0, s8_timer());
@@ -632,7 +661,14 @@ __global__ void __launch_bounds__(S8_THREADS, 1)
     // hands over within one exact dot once the scan is over.
     // CTA 0's eager warp first writes and scores the rows appended since the last lookup: off the
     // rescorer, whose pool barrier (and CTA 0's record, which the merge waits for) it would delay
-    if (blockIdx.x == 0 && n_pend > 0) s8_pending(x, IN ? a.gq64 : stagep, a.n_app, n_pend, n_scan);
+    if (blockIdx.x == 0) {
+      if (n_pend > 0) s8_pending(x, IN ? a.gq64 : stagep, a.n_app, n_pend, n_scan);
+      __syncwarp();
+      if (lane == 0 && a.sync) {  // the rows appended before this launch are in the ring
+        __threadfence();
+        st_release_gpu_u32(a.sync, a.epoch);
+      }
+    }
     while (!*(volatile int*)&S.q_ready) {
     }
     while (*(volatile int*)&S.done != S8_CW) {
@@ -1002,7 +1038,7 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
                                   OutRec* out,
                                   RingState* d_state, unsigned* done_seq, unsigned seq, uint4* outp,
                                   void (*quantise)(const double*, int, int, QPrep*, int8_t*), double* gq64,
-                                  cudaStream_t s) {
+                                  unsigned* sync, unsigned rec_par, cudaStream_t s) {
   if (!p || p->Dp > 1024 || grid > 256) return cudaErrorInvalidValue;
   static thread_local S8In in;
   const int Dp = p->Dp;
@@ -1011,7 +1047,7 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
   quantise(in.q64, D, Dp, &in.prep, in.q8);
   in.hstage = stage_row;
   S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), nullptr, nullptr, nullptr, stage_row ? 1 : 0, d_state,
-           done_seq, seq, outp, epoch, gq64};
+           done_seq, seq, outp, epoch, gq64, sync, rec_par};
   switch (p->P8 / 128) {
     case 1: return s8_launch_in<1>(p, rb, st, cta, grid, sm, a, in, s);
     case 2: return s8_launch_in<2>(p, rb, st, cta, grid, sm, a, in, s);
@@ -1029,10 +1065,10 @@ cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingS
                                 CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter,
                                 unsigned long long* gmax, unsigned epoch, const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
                                 const QPrep* prep, const int8_t* q8, unsigned* done_seq, unsigned seq,
-                                uint4* outp, cudaStream_t s) {
+                                uint4* outp, unsigned* sync, unsigned rec_par, cudaStream_t s) {
   if (!p || nb < 1 || nb > 4 || grid > 256) return cudaErrorInvalidValue;  // grid <= 256: the merger's records
   S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), prep, q8, app.stage, app.n, app.d_state, done_seq, seq,
-           outp, epoch};
+           outp, epoch, nullptr, sync, rec_par};
   switch (p->P8 / 128) {
     case 1: return s8_launch<1>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
     case 2: return s8_launch<2>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);

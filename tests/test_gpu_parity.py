@@ -1121,3 +1121,37 @@ def test_local_lookup_from_device_queries_matches_host_queries(B):
         for x, y in zip(dev_ans, host_ans):
             assert np.array_equal(x, y), rnd
     ring.close()
+
+
+def test_overlapping_launches_c2_scale_request_stream():
+    """C2 shape (100k x 768) with one insert per request and two lookups in flight, so each
+    launch starts while the previous one still merges (its pending row published through the
+    ring's sync word, its records in the other parity buffer): 400 answers against the oracle
+    cache's sequential ones."""
+    wl = ClusteredWorkload(768, n_clusters=512, seed=23)
+    n = 100_000
+    rows = wl.cache_rows(n)
+    c = SemanticCache(capacity=n, dim=768)
+    c.bulk_load(CacheEntry(f"e{i}", rows[i], "large", i, 0.0) for i in range(n))
+    o = OracleCache(n, 768)
+    for i in range(n):
+        o.insert(OracleEntry(f"e{i}", rows[i], "large", i, 0.0))
+    table, ot = ThresholdTable.default(), OracleTable()
+    Q = wl.queries(400)
+    imgs = wl.images(Q)
+    prev = None
+    stats = {"queries": 0, "mismatch": 0}
+    for i, q in enumerate(Q):
+        want = o.retrieve_entry(q, ot)
+        p = c.retrieve_async(q, table)
+        c.add(f"n{i}", imgs[i], "large", 1.0 + i)
+        o.insert(OracleEntry(f"n{i}", imgs[i], "large", n + i, 1.0 + i))
+        if prev is not None:
+            r, (e, sim, k) = prev[0].result(), prev[1]
+            stats["queries"] += 1
+            assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (i, r, e)
+            assert r.k == k and _close(r.similarity, sim), (i, r, sim)
+        prev = (p, want)
+    prev[0].result()
+    _record_parity("overlapping launches C2 stream", stats)
+    c.close()
