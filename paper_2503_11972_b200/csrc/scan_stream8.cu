@@ -53,7 +53,14 @@
 
 namespace mc {
 
-constexpr int S8_CW = 8;                       // consumer warps (max)
+#ifndef S8_CONSUMERS
+#define S8_CONSUMERS 8
+#endif
+// Consumer warps (and stages in flight).  8: one CTA per SM.  4: a CTA of half the shared
+// memory and registers, so two co-reside and a launch's scan can start on an SM while the
+// previous launch's CTA there still rescores and merges.
+constexpr int S8_CW = S8_CONSUMERS;
+constexpr int S8_CTAS_PER_SM = S8_CONSUMERS <= 4 ? 2 : 1;
 constexpr int S8_THREADS = (S8_CW + 4) * 32;   // producer + consumers + rescorer + bound poller + eager rescorer
 constexpr int S8_EAGER = S8_CW + 1;            // S.best slot of the eager rescorer
 constexpr int S8_QCAP = 128;                   // candidate queue entries per consumer warp
@@ -559,7 +566,7 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
 }
 
 template <int KB, int NBQ, bool IN>
-__global__ void __launch_bounds__(S8_THREADS, 1)
+__global__ void __launch_bounds__(S8_THREADS, S8_CTAS_PER_SM)
     k_stream8_scan(RingBufs rb, const RingState st, const double* __restrict__ q64_dev, int nb,
                    CtaRec* __restrict__ cta, int b0, ShardMap sm, S8Args a, int nst, int Dp,
                    const __grid_constant__ std::conditional_t<IN, S8In, S8NoIn> in) {
