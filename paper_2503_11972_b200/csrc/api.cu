@@ -142,6 +142,7 @@ struct mc_cache {
   double* h_stage1[2] = {nullptr, nullptr};  // pinned, mapped [Dp] per result slot: its pending row
   double* d_gq64 = nullptr;     // [Dp] the kernel's L2 relay of the pending row
   unsigned* d_sync = nullptr;   // [2] streamed-scan launch overlap: rows published / records read (epochs)
+  bool tc_tail = false;         // the last kernel enqueued on the stream is the tensor path's merge (PDL-early)
 
   TcPlan* tc = nullptr;           // fp16 tensor-core scan plan (MC_PATH_GEMM*), created on first use
   S8Plan* s8 = nullptr;           // TMA-streamed int8 scan plan (tensor maps of ring8 / ringq)
@@ -494,6 +495,15 @@ int ensure_tc(mc_cache* h, int B) {
 // Distance (uint4) between the two epoch-parity record buffers of the streamed scan in d_cta.
 unsigned s8_rec_par(const mc_cache* h) { return (unsigned)((size_t)h->Bcap * h->sm_count * 2); }
 
+// A streamed-scan launch that failed took an epoch without publishing it: publish it from the
+// host so the next launch (which waits for the previous epoch's rows) does not wait forever.
+int s8_launch_failed(mc_cache* h, unsigned ep, cudaError_t e) {
+  const unsigned z[2] = {ep, ep};
+  cudaMemcpyAsync(h->d_sync, z, sizeof z, cudaMemcpyHostToDevice, h->stream);
+  cudaStreamSynchronize(h->stream);
+  return fail(MC_ERR_CUDA, "streamed scan launch: %s", cudaGetErrorString(e));
+}
+
 unsigned s8_epoch(mc_cache* h) {
   if (++h->s8_epoch == 0) {
     cudaMemsetAsync(h->d_gmax8, 0, (size_t)h->Bcap * 128 * sizeof(unsigned long long), h->stream);
@@ -519,6 +529,7 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
     if (t_mid) CU(cudaEventRecord(t_mid, h->stream));
     CU(launch_merge(h->d_state, h->ring64, h->D, h->Dp, q64, B, part, tc_qscale(h->tc), gemm_eps_rel(h->Dp),
                     eps_abs1(), rec, h->shard, &h->thr, out, h->stream));  // the decision is fused (G = 1)
+    h->tc_tail = true;  // k_merge lets its dependent start early: the next streamed scan must not overlap it
     h->stats[6]++;
     h->stats[7] += 3;
     return MC_OK;
@@ -529,11 +540,16 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
   const bool s8 = quant && h->s8;
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nb = std::min(4, B - b0);
-    if (s8)
-      CU(launch_stream8_scan(h->s8, rbufs(h), st, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0, h->sm_count, h->shard,
-                             h->d_counter, h->d_gmax8, s8_epoch(h), h->thr, rec, out, a, prep + b0, q8 + (size_t)b0 * h->Dp,
-                             b0 + nb == B ? done_seq : nullptr, seq, outp, h->d_sync, s8_rec_par(h), h->stream));
-    else
+    if (s8) {
+      const unsigned ep = s8_epoch(h);
+      const cudaError_t e = launch_stream8_scan(h->s8, rbufs(h), st, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
+                                                h->sm_count, h->shard, h->d_counter, h->d_gmax8, ep, h->thr, rec, out,
+                                                a, prep + b0, q8 + (size_t)b0 * h->Dp,
+                                                b0 + nb == B ? done_seq : nullptr, seq, outp, h->d_sync,
+                                                s8_rec_par(h), !h->tc_tail, h->stream);
+      if (e != cudaSuccess) return s8_launch_failed(h, ep, e);
+      h->tc_tail = false;
+    } else
       CU(launch_gemv_scan(h->ring16, st, h->D, h->Dp, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
                           gemv_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax, h->ring64, h->thr, rec, out, a,
                           h->stream));
@@ -595,10 +611,14 @@ int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool
     take_pending(h, nullptr);
     memset(h->h_outp + 2 * slot, 0, 2 * sizeof(uint4));
     *q = nullptr;
-    CU(launch_stream8_direct(h->s8, rbufs(h), st, h->D, hq, stage_row, h->d_cta, h->sm_count, h->shard,
-                             h->d_counter, h->d_gmax8, s8_epoch(h), h->thr, h->d_rec + slot, nullptr, h->d_state,
-                             nullptr, seq_tag(seq), h->d_outp + 2 * slot, quantize_query, h->d_gq64, h->d_sync,
-                             s8_rec_par(h), h->stream));
+    const unsigned ep = s8_epoch(h);
+    const cudaError_t e = launch_stream8_direct(h->s8, rbufs(h), st, h->D, hq, stage_row, h->d_cta, h->sm_count,
+                                                h->shard, h->d_counter, h->d_gmax8, ep, h->thr, h->d_rec + slot,
+                                                nullptr, h->d_state, nullptr, seq_tag(seq), h->d_outp + 2 * slot,
+                                                quantize_query, h->d_gq64, h->d_sync, s8_rec_par(h), !h->tc_tail,
+                                                h->stream);
+    if (e != cudaSuccess) return s8_launch_failed(h, ep, e);
+    h->tc_tail = false;
     h->stats[5]++;
     h->stats[7]++;
     return MC_OK;

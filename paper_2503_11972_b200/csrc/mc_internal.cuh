@@ -136,7 +136,7 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
                                   OutRec* out,
                                   RingState* d_state, unsigned* done_seq, unsigned seq, uint4* outp,
                                   void (*quantise)(const double*, int, int, QPrep*, int8_t*), double* gq64,
-                                  unsigned* sync, unsigned rec_par, cudaStream_t s);
+                                  unsigned* sync, unsigned rec_par, bool overlap, cudaStream_t s);
 S8Plan* s8_plan_create(int8_t* ring8, float2* ringq, long long C, int Dp, int P8, char* err, int errlen);
 void s8_plan_destroy(S8Plan* p);
 cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingState& st, const double* q64, int nb,
@@ -144,7 +144,7 @@ cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingS
                                 unsigned long long* gmax, unsigned epoch, const Thresholds& thr, mc_record* rec,
                                 OutRec* out, const GemvAppendArgs& app,
                                 const QPrep* prep, const int8_t* q8, unsigned* done_seq, unsigned seq,
-                                uint4* outp, unsigned* sync, unsigned rec_par, cudaStream_t s);
+                                uint4* outp, unsigned* sync, unsigned rec_par, bool overlap, cudaStream_t s);
 
 int gemv_grid(int sm_count);
 cudaError_t launch_generate(long long n, long long first_slot, const RingState& ns, int D, int Dp, const RingBufs& rb,

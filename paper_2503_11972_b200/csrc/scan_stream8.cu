@@ -139,6 +139,7 @@ struct S8Args {
   // alternate between two buffers by epoch parity, rec_par uint4 apart.  nullptr: no overlap.
   unsigned* sync;
   unsigned rec_par;
+  unsigned overlap;  // 0: the previous kernel on the stream may be another path's (wait for it in full)
 };
 __device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
   unsigned v;
@@ -642,7 +643,7 @@ __global__ void __launch_bounds__(S8_THREADS, S8_CTAS_PER_SM)
   // The previous launch's window survives the rows this one appends (<= PIPE_SLACK of them land
   // in spare slots), the bound words are epoch-tagged and the records alternate by epoch parity
   // (a record writer waits for sync[1]).  Otherwise: the full programmatic dependency.
-  if (a.sync && a.n_app <= PIPE_SLACK) {
+  if (a.sync && a.overlap && a.n_app <= PIPE_SLACK) {
     if (threadIdx.x == 0)
       while ((int)(ld_acquire_gpu_u32(a.sync) - (a.epoch - 1u)) < 0) {
       }
@@ -1045,7 +1046,7 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
                                   OutRec* out,
                                   RingState* d_state, unsigned* done_seq, unsigned seq, uint4* outp,
                                   void (*quantise)(const double*, int, int, QPrep*, int8_t*), double* gq64,
-                                  unsigned* sync, unsigned rec_par, cudaStream_t s) {
+                                  unsigned* sync, unsigned rec_par, bool overlap, cudaStream_t s) {
   if (!p || p->Dp > 1024 || grid > 256) return cudaErrorInvalidValue;
   static thread_local S8In in;
   const int Dp = p->Dp;
@@ -1054,7 +1055,7 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
   quantise(in.q64, D, Dp, &in.prep, in.q8);
   in.hstage = stage_row;
   S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), nullptr, nullptr, nullptr, stage_row ? 1 : 0, d_state,
-           done_seq, seq, outp, epoch, gq64, sync, rec_par};
+           done_seq, seq, outp, epoch, gq64, sync, rec_par, overlap ? 1u : 0u};
   switch (p->P8 / 128) {
     case 1: return s8_launch_in<1>(p, rb, st, cta, grid, sm, a, in, s);
     case 2: return s8_launch_in<2>(p, rb, st, cta, grid, sm, a, in, s);
@@ -1072,10 +1073,10 @@ cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingS
                                 CtaRec* cta, int b0, int grid, ShardMap sm, unsigned* counter,
                                 unsigned long long* gmax, unsigned epoch, const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
                                 const QPrep* prep, const int8_t* q8, unsigned* done_seq, unsigned seq,
-                                uint4* outp, unsigned* sync, unsigned rec_par, cudaStream_t s) {
+                                uint4* outp, unsigned* sync, unsigned rec_par, bool overlap, cudaStream_t s) {
   if (!p || nb < 1 || nb > 4 || grid > 256) return cudaErrorInvalidValue;  // grid <= 256: the merger's records
   S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), prep, q8, app.stage, app.n, app.d_state, done_seq, seq,
-           outp, epoch, nullptr, sync, rec_par};
+           outp, epoch, nullptr, sync, rec_par, overlap ? 1u : 0u};
   switch (p->P8 / 128) {
     case 1: return s8_launch<1>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
     case 2: return s8_launch<2>(p, rb, st, q64, nb, cta, b0, grid, sm, a, s);
