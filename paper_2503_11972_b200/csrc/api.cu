@@ -252,6 +252,13 @@ void quantize_query(const double* q, int D, int Dp, QPrep* p, int8_t* q8) {
   p->exotic = !(p->n1 <= 1e30) || !(p->n2 >= 1e-30);
 }
 
+// Per-CTA records: the GEMV scans' CtaRec per CTA, or the streamed scan's two 16-byte words per
+// CTA in two epoch-parity buffers; sized for the larger.
+size_t cta_bytes(const mc_cache* h, int cap) {
+  return std::max((size_t)gemv_grid(h->sm_count) * sizeof(CtaRec), (size_t)s8_grid(h->sm_count) * 2 * 2 * 16) *
+         (size_t)cap;
+}
+
 void free_batch(mc_cache* h) {
   cudaFree(h->d_part_s);
   cudaFree(h->d_part_p);
@@ -307,9 +314,9 @@ int ensure_batch(mc_cache* h, int B) {
   CU(cudaMalloc(&h->d_part_s, (size_t)cap * chunks * KP * sizeof(float)));
   CU(cudaMalloc(&h->d_part_p, (size_t)cap * chunks * KP * sizeof(long long)));
   CU(cudaMalloc(&h->d_part_floor, (size_t)cap * chunks * sizeof(float)));
-  CU(cudaMalloc(&h->d_cta, (size_t)cap * gemv_grid(h->sm_count) * sizeof(CtaRec)));
+  CU(cudaMalloc(&h->d_cta, cta_bytes(h, cap)));
   // the streamed scan's records are epoch-tagged: zero words belong to no launch
-  CU(cudaMemsetAsync(h->d_cta, 0, (size_t)cap * gemv_grid(h->sm_count) * sizeof(CtaRec), h->stream));
+  CU(cudaMemsetAsync(h->d_cta, 0, cta_bytes(h, cap), h->stream));
   // 256 words per query: the streamed scan keeps 8 replicas of its bound 128 B apart
   CU(cudaMalloc(&h->d_gmax, (size_t)cap * 256 * sizeof(unsigned)));
   CU(cudaMemsetAsync(h->d_gmax, 0, (size_t)cap * 256 * sizeof(unsigned), h->stream));
@@ -493,7 +500,7 @@ int ensure_tc(mc_cache* h, int B) {
 // Epoch of the next streamed-scan launch (never 0: zeroed words belong to no launch).  On
 // wrap-around the bound words are cleared, so an old epoch can never outrank a new one.
 // Distance (uint4) between the two epoch-parity record buffers of the streamed scan in d_cta.
-unsigned s8_rec_par(const mc_cache* h) { return (unsigned)((size_t)h->Bcap * h->sm_count * 2); }
+unsigned s8_rec_par(const mc_cache* h) { return (unsigned)((size_t)h->Bcap * s8_grid(h->sm_count) * 2); }
 
 // A streamed-scan launch that failed took an epoch without publishing it: publish it from the
 // host so the next launch (which waits for the previous epoch's rows) does not wait forever.
@@ -507,7 +514,7 @@ int s8_launch_failed(mc_cache* h, unsigned ep, cudaError_t e) {
 unsigned s8_epoch(mc_cache* h) {
   if (++h->s8_epoch == 0) {
     cudaMemsetAsync(h->d_gmax8, 0, (size_t)h->Bcap * 128 * sizeof(unsigned long long), h->stream);
-    cudaMemsetAsync(h->d_cta, 0, (size_t)h->Bcap * gemv_grid(h->sm_count) * sizeof(CtaRec), h->stream);
+    cudaMemsetAsync(h->d_cta, 0, cta_bytes(h, h->Bcap), h->stream);
     cudaMemsetAsync(h->d_sync, 0, 2 * sizeof(unsigned), h->stream);
     h->s8_epoch = 1;
   }
@@ -543,7 +550,8 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
     if (s8) {
       const unsigned ep = s8_epoch(h);
       const cudaError_t e = launch_stream8_scan(h->s8, rbufs(h), st, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
-                                                h->sm_count, h->shard, h->d_counter, h->d_gmax8, ep, h->thr, rec, out,
+                                                s8_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax8, ep, h->thr,
+                                                rec, out,
                                                 a, prep + b0, q8 + (size_t)b0 * h->Dp,
                                                 b0 + nb == B ? done_seq : nullptr, seq, outp, h->d_sync,
                                                 s8_rec_par(h), !h->tc_tail, h->stream);
@@ -612,7 +620,7 @@ int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool
     memset(h->h_outp + 2 * slot, 0, 2 * sizeof(uint4));
     *q = nullptr;
     const unsigned ep = s8_epoch(h);
-    const cudaError_t e = launch_stream8_direct(h->s8, rbufs(h), st, h->D, hq, stage_row, h->d_cta, h->sm_count,
+    const cudaError_t e = launch_stream8_direct(h->s8, rbufs(h), st, h->D, hq, stage_row, h->d_cta, s8_grid(h->sm_count),
                                                 h->shard, h->d_counter, h->d_gmax8, ep, h->thr, h->d_rec + slot,
                                                 nullptr, h->d_state, nullptr, seq_tag(seq), h->d_outp + 2 * slot,
                                                 quantize_query, h->d_gq64, h->d_sync, s8_rec_par(h), !h->tc_tail,

@@ -129,6 +129,7 @@ struct QPrep {
 // grid = one CTA per SM.  The plan holds the ring's tensor maps.
 struct S8Plan;
 bool stream8_supported(int Dp);
+int s8_grid(int sm_count);  // CTAs of one streamed-scan launch
 // One query (and <= 1 pending row, host pointers) carried in the kernel parameter block.
 cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const RingState& st, int D, const double* q64,
                                   const double* stage_row, CtaRec* cta, int grid, ShardMap sm, unsigned* counter,

@@ -54,13 +54,24 @@
 namespace mc {
 
 #ifndef S8_CONSUMERS
-#define S8_CONSUMERS 8
+#define S8_CONSUMERS 4
 #endif
-// Consumer warps (and stages in flight).  8: one CTA per SM.  4: a CTA of half the shared
-// memory and registers, so two co-reside and a launch's scan can start on an SM while the
-// previous launch's CTA there still rescores and merges.
+// Consumer warps (and stages in flight).  4 (default): a CTA of at most half the shared memory
+// and registers of an SM, so two co-reside and a launch's scan starts on an SM while the
+// previous launch's CTA there still rescores and merges (back-to-back C2 steps 16.2 -> 12.1 us,
+// profiles/r02_consumers_ab.txt).  8: one CTA per SM, no overlap between launches.
 constexpr int S8_CW = S8_CONSUMERS;
+#ifdef S8_CTAS
+constexpr int S8_CTAS_PER_SM = S8_CTAS;
+#else
 constexpr int S8_CTAS_PER_SM = S8_CONSUMERS <= 4 ? 2 : 1;
+#endif
+#ifndef S8_GRID_PER_SM
+#define S8_GRID_PER_SM 1
+#endif
+// CTAs per SM in one launch's grid (S8_GRID_PER_SM = 2 with 4 consumers: two half-size CTAs per
+// SM, so an SM frees half its room as soon as one of them retires).
+int s8_grid(int sm_count) { return S8_GRID_PER_SM * sm_count; }
 constexpr int S8_THREADS = (S8_CW + 4) * 32;   // producer + consumers + rescorer + bound poller + eager rescorer
 constexpr int S8_EAGER = S8_CW + 1;            // S.best slot of the eager rescorer
 constexpr int S8_QCAP = 128;                   // candidate queue entries per consumer warp
@@ -462,7 +473,7 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
   // (a second record at the best makes the runner-up equal to it, as in
   // Best2::merge).  Record similarities are finite here (exotic queries are
   // flagged for the exhaustive path).
-  constexpr int PER = 8;  // records per lane: grid <= 256 (the host clamps it)
+  constexpr int PER = 10;  // records per lane: grid <= 320 (the host clamps it)
   for (int b = 0; b < nb; ++b) {
     const int gb = b0 + b;
     const uint4* src = crec + (size_t)gb * gridDim.x * 2;
@@ -950,6 +961,12 @@ static cudaError_t s8_attr(S8Plan* p) {  // sizes the stages, raises the smem li
   cudaGetDevice(&dev);
   cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e != cudaSuccess) return e;
+  if (S8_CTAS_PER_SM > 1) {  // keep S8_CTAS_PER_SM CTAs co-resident (1 KB per CTA is reserved)
+    int per_sm = 0;
+    if ((e = cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev)) != cudaSuccess)
+      return e;
+    optin = std::min(optin, per_sm / S8_CTAS_PER_SM - 1024);
+  }
   cudaFuncAttributes fa1, fa4, fai;
   if ((e = cudaFuncGetAttributes(&fa1, k_stream8_scan<KB, 1, false>)) != cudaSuccess) return e;
   if ((e = cudaFuncGetAttributes(&fa4, k_stream8_scan<KB, 4, false>)) != cudaSuccess) return e;
@@ -1047,7 +1064,7 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
                                   RingState* d_state, unsigned* done_seq, unsigned seq, uint4* outp,
                                   void (*quantise)(const double*, int, int, QPrep*, int8_t*), double* gq64,
                                   unsigned* sync, unsigned rec_par, bool overlap, cudaStream_t s) {
-  if (!p || p->Dp > 1024 || grid > 256) return cudaErrorInvalidValue;
+  if (!p || p->Dp > 1024 || grid > 320) return cudaErrorInvalidValue;
   static thread_local S8In in;
   const int Dp = p->Dp;
   memcpy(in.q64, q64, (size_t)D * sizeof(double));
@@ -1074,7 +1091,7 @@ cudaError_t launch_stream8_scan(const S8Plan* p, const RingBufs& rb, const RingS
                                 unsigned long long* gmax, unsigned epoch, const Thresholds& thr, mc_record* rec, OutRec* out, const GemvAppendArgs& app,
                                 const QPrep* prep, const int8_t* q8, unsigned* done_seq, unsigned seq,
                                 uint4* outp, unsigned* sync, unsigned rec_par, bool overlap, cudaStream_t s) {
-  if (!p || nb < 1 || nb > 4 || grid > 256) return cudaErrorInvalidValue;  // grid <= 256: the merger's records
+  if (!p || nb < 1 || nb > 4 || grid > 320) return cudaErrorInvalidValue;  // grid <= 320: the merger's records
   S8Args a{counter, gmax, thr, rec, out, gemv_timing_buffer(), prep, q8, app.stage, app.n, app.d_state, done_seq, seq,
            outp, epoch, nullptr, sync, rec_par, overlap ? 1u : 0u};
   switch (p->P8 / 128) {
