@@ -377,6 +377,9 @@ def roofline(st, n_entries, dim, B, step_ms, rot, prof, n_rot, pk):
         roof = {"bound": "tensor", "achieved": flops / scan_s / 1e12, "peak": tc_burst, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["peak_source"] = f"{src} (MEASURED_PEAKS.json)" if src == "measured" else "fallback (B200_PROFILING.md)"
+    if roof["bound"] == "hbm":  # the measured peak is a read+write copy; a read-only scan can pass it
+        roof["frac_of_spec"] = roof["achieved"] / 7700.0
+        roof["spec_note"] = "7.7 TB/s: HGX B200 HBM3e nominal (B200_PROFILING.md)"
     roof["kernel"] = kname
     roof["algorithmic_bytes_per_launch"] = scan_bytes
     roof["bytes_definition"] = ("bytes the kernel must read: int8 ring rows + per-row (scale, L1) + queries"

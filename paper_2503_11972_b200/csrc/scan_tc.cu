@@ -245,8 +245,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
                    const __grid_constant__ CUtensorMap ring_map_q,
                    const RingState* __restrict__ d_state, int n_mp, int B, int n_kb, float* __restrict__ part_s,
                    long long* __restrict__ part_p, float* __restrict__ part_floor, int n_chunks, float margin,
-                   ShardMap sm, int dbg) {
+                   ShardMap sm, int dbg, unsigned long long* __restrict__ tim) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // tim (MC_GEMV_TIMING=1, measurement only): per-cluster cycle sums at tim[8 + 12 * cluster + i]:
+  // 0 MMA-issue loop, 1 MMA waits on full, 2 MMA waits on tempty, 3 units, 4 producer waits on
+  // empty, 5 epilogue waits on tfull, 6 epilogue busy, 7 prologue (to griddepcontrol.wait done),
+  // 8 MMA-issue loop in globaltimer ns
+  const long long t_k0 = clock64();
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + TQ_STAGES * TQ_SUB * TP_A_BYTES;
@@ -316,6 +321,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   // and the merge behind this kernel may be scheduled as CTAs retire (it waits for all of them)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  unsigned long long* tcl = tim ? tim + 8 + 12 * (size_t)cid : nullptr;
+  if (tcl && rank == 0 && threadIdx.x == 0) atomicAdd(tcl + 7, (unsigned long long)(clock64() - t_k0));
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -324,13 +331,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
     const uint32_t leader_full0 = mapa_shared(smem_u32(&full[0]), 0);
     int stage = 0;
     uint32_t phase = 0;
+    long long tw_empty = 0;
     for (int u = 0; u < n_units; ++u) {
       int t, hsel;
       unit(u, t, hsel);
       const int bbytes = hsel < 0 ? TP_B_BYTES : TP_B_BYTES / 2;
       for (int kg = 0; kg < n_kg; ++kg) {
         const int ns = min(TQ_SUB, n_kb - kg * TQ_SUB);
+        const long long w0 = tcl ? clock64() : 0;
         mbar_wait2(&empty[stage], phase ^ 1, dbg & 16);
+        if (tcl) tw_empty += clock64() - w0;
         if (lane == 0) {
           if (rank == 0)
             mbar_expect_tx(&full[stage], (dbg & 1) ? 0 : 2 * ns * (TP_A_BYTES + bbytes));
@@ -355,9 +365,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
         }
       }
     }
+    if (tcl && rank == 0 && lane == 0) atomicAdd(tcl + 4, (unsigned long long)tw_empty);
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader only)
     if (rank == 0) {
+      const long long tm0 = clock64();
+      unsigned long long g0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+      long long tw_full = 0, tw_tempty = 0;
       constexpr uint32_t idesc_full = umma_idesc_f16(256, TC_BN);
       constexpr uint32_t idesc_half = umma_idesc_f16(256, TC_BN / 2);
       int stage = 0;
@@ -368,12 +383,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
         const uint32_t idesc = hsel < 0 ? idesc_full : idesc_half;
         const int acc = u & 1;
         const uint32_t acc_phase = (u >> 1) & 1;
+        long long w0 = tcl ? clock64() : 0;
         mbar_wait2(&tempty[acc], acc_phase ^ 1, dbg & 16);
+        if (tcl) tw_tempty += clock64() - w0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * TC_BN);
         for (int kg = 0; kg < n_kg; ++kg) {
           const int ns = min(TQ_SUB, n_kb - kg * TQ_SUB);
+          w0 = tcl ? clock64() : 0;
           mbar_wait2(&full[stage], phase, dbg & 16);
+          if (tcl) tw_full += clock64() - w0;
           tc_fence_after();
           if (lane == 0) {
             for (int sb = 0; sb < ns; ++sb) {
@@ -402,6 +421,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
         if (lane == 0) umma_commit_pair(&tfull[acc]);
         __syncwarp();
       }
+      if (tcl && lane == 0) {
+        atomicAdd(tcl + 0, (unsigned long long)(clock64() - tm0));
+        atomicAdd(tcl + 1, (unsigned long long)tw_full);
+        atomicAdd(tcl + 2, (unsigned long long)tw_tempty);
+        atomicAdd(tcl + 3, (unsigned long long)n_units);
+        unsigned long long g1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+        atomicAdd(tcl + 8, g1 - g0);  // ns of the MMA-issue loop (clock = tcl[0] / tcl[8])
+      }
     }
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
@@ -413,6 +441,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
     const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
     TopK top;
     top.init();
+    long long tw_tfull = 0;
+    const long long te0 = clock64();
     for (int u = 0; u < n_units; ++u) {
       const int acc = u & 1;
       const uint32_t acc_phase = (u >> 1) & 1;
@@ -421,7 +451,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
       const int width = hsel < 0 ? TC_BN : TC_BN / 2;  // accumulator columns of this unit
       const int nch = width / 64;                        // 32-column chunks per epilogue warp
       const long long slot0 = (long long)t * TC_BN + (hsel < 0 ? 0 : hsel * 128);
+      const long long w0 = tcl ? clock64() : 0;
       mbar_wait(&tfull[acc], acc_phase);
+      if (tcl) tw_tfull += clock64() - w0;
       tc_fence_after();
       long long l0 = slot0 - st.head;
       if (l0 < 0) l0 += st.cap;
@@ -462,6 +494,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(leader_tempty0 + acc * 8);
+    }
+    if (tcl && rank == 0 && warp == 2 && lane == 0) {
+      atomicAdd(tcl + 5, (unsigned long long)tw_tfull);
+      atomicAdd(tcl + 6, (unsigned long long)(clock64() - te0 - tw_tfull));
     }
     // column half 1 hands its list to half 0 of the same query row
     float* xs = reinterpret_cast<float*>(bars + 32);  // [KP][128] scores (past the 256-byte barrier block)
@@ -676,7 +712,7 @@ cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const Rin
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k_tc_scan_pair, p->q_map, p->ring_map_half, p->ring_map_q, d_state, nm, B,
                               p->Dp / TC_BK,
-                              part.s, part.p, part.floor_, groups, margin, sm, p->dbg);
+                              part.s, part.p, part.floor_, groups, margin, sm, p->dbg, gemv_timing_buffer());
   }
   return cudaGetLastError();
 }

@@ -17,7 +17,7 @@ those modules too with ``modules=``.
 from __future__ import annotations
 
 from .cache import SemanticCache
-from .records import _result_factory
+from .records import _entry_factory, _result_factory
 
 
 def dropin_class(cache_module, base=SemanticCache):
@@ -27,6 +27,7 @@ def dropin_class(cache_module, base=SemanticCache):
         "__module__": base.__module__,
         "__doc__": base.__doc__,
         "_Entry": cache_module.CacheEntry,
+        "_new_entry": staticmethod(_entry_factory(cache_module.CacheEntry)),
         "_EmbeddingError": cache_module.EmbeddingError,
         "_make": staticmethod(_result_factory(rr)),
         "_MISS": rr(None, None, None),

@@ -101,6 +101,29 @@ def _result_factory(cls=None):
 make_result = _result_factory()
 
 
+def _entry_factory(cls=None):
+    """A constructor for CacheEntry (or the host application's frozen dataclass with the same
+    five fields) that fills the instance dict directly instead of five object.__setattr__
+    calls; add() mints one entry per request.  The objects are ordinary `cls` instances."""
+    new = object.__new__
+    cls = CacheEntry if cls is None else cls
+
+    def make(id, embedding, producer, seq, inserted_at):
+        e = new(cls)
+        d = e.__dict__
+        d["id"] = id
+        d["embedding"] = embedding
+        d["producer"] = producer
+        d["seq"] = seq
+        d["inserted_at"] = inserted_at
+        return e
+
+    return make
+
+
+make_entry = _entry_factory()
+
+
 class RetrievalBatch(_SequenceABC):
     """The answers of one batched lookup (SemanticCache.retrieve_batch): a read-only sequence
     of RetrievalResult, equal to the list B retrieve() calls return, whose objects are built on

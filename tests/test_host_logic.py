@@ -293,3 +293,43 @@ class TestPipelinedAndBatchResults:
             c.insert(entry(100 + j, unit(rng, 8)))
         assert fresh[0].entry.id == "e5" and fresh == want and got == want
         assert SemanticCache(capacity=4, dim=8).retrieve_batch(Q[:2], table) == [RetrievalResult(None, None, None)] * 2
+
+
+def test_add_mints_ordinary_entries_for_every_policy():
+    """add() builds entries without the dataclass __init__ (records._entry_factory): they must be
+    ordinary instances (equality, hash, repr, frozen), for ours and a drop-in's entry class; the
+    inlined admits() must agree with admits() for every policy and producer."""
+    import dataclasses
+    import types
+
+    from paper_2503_11972_b200 import dropin
+
+    rng = np.random.default_rng(3)
+    e = unit(rng, 8)
+    c = SemanticCache(capacity=4, dim=8)
+    c.add("a", e, "large", 1.5)
+    got = c.entries()[0]
+    want = CacheEntry("a", e, "large", 0, 1.5)
+    assert type(got) is CacheEntry and got == want and repr(got) == repr(want)
+    with pytest.raises(dataclasses.FrozenInstanceError):
+        got.seq = 3
+
+    @dataclasses.dataclass(frozen=True)
+    class OtherEntry:
+        id: str
+        embedding: np.ndarray
+        producer: str
+        seq: int
+        inserted_at: float
+
+    mod = types.SimpleNamespace(CacheEntry=OtherEntry, EmbeddingError=EmbeddingError,
+                                RetrievalResult=RetrievalResult)
+    d = dropin.dropin_class(mod)(capacity=4, dim=8)
+    d.add("b", e, "small", 2.0)
+    assert d.entries()[0] == OtherEntry("b", e, "small", 0, 2.0)
+
+    for policy in ("all", "large", "disabled"):
+        for producer in ("large", "small"):
+            c = SemanticCache(capacity=4, dim=8, policy=policy)
+            c.add("x", e, producer, 0.0)
+            assert len(c) == int(c.admits(producer)), (policy, producer)
