@@ -296,7 +296,7 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
                              "latency_us": 1e6 * seq_s / e2e_steps,
                              "mode": "one request at a time: retrieve_async, add, .result()"}
     st = cache.ring.stats()
-    roof = roofline(st, n_entries, dim, B, step_ms, rot, prof, n_rot, pk)
+    roof = roofline(st, n_entries, dim, B, step_ms, rot, prof, n_rot, pk, cfg=name)
     out = {
         "value": value, "ms_per_step": step_ms, "e2e": e2e, "roofline": roof, "clocks": clk.summary(),
         "gpu_launches": rot["launches_per_step"] * steps,
@@ -338,7 +338,7 @@ def run_generated(label, workload, dim, n_entries, B, steps, warmup, flush_bytes
             "data": f"device-generated clustered unit rows (f4, {max(512, n_entries // 200)} clusters), host queries"}
 
 
-def roofline(st, n_entries, dim, B, step_ms, rot, prof, n_rot, pk):
+def roofline(st, n_entries, dim, B, step_ms, rot, prof, n_rot, pk, cfg=None):
     """The dominant kernel's roofline entry (bench contract ④), from the library's launch counters."""
     dp = (dim + 63) // 64 * 64
     p8 = (dp + 127) // 128 * 128
@@ -389,8 +389,15 @@ def roofline(st, n_entries, dim, B, step_ms, rot, prof, n_rot, pk):
     roof["flops_per_launch"] = flops
     roof["max_of_floors_frac"] = max(t_hbm, t_tc) / scan_s
     roof["step_roofline_frac"] = max(t_hbm, t_tc) / (step_ms * 1e-3)
-    roof["traffic"] = traffic_from_profiles(kname)
-    roof["traffic_source"] = "dram__bytes_read.sum + dram__bytes_write.sum per launch, profiles/ncu_summary.json"
+    # ncu --set full captures exist for the C2 streamed scan and the C3 pair kernel only: their DRAM
+    # bytes describe those shapes, so other sizes report no traffic rather than a borrowed figure
+    captured = {"k_stream8_scan": "c2", "k_tc_scan_pair": "c3"}.get(kname)
+    if cfg is not None and cfg == captured:
+        roof["traffic"] = traffic_from_profiles(kname)
+        roof["traffic_source"] = "dram__bytes_read.sum + dram__bytes_write.sum per launch, profiles/ncu_summary.json"
+    else:
+        roof["traffic"] = None
+        roof["traffic_source"] = f"no ncu --set full capture at this shape (captures: {kname} at {captured or 'none'})"
     roof["timing"] = timing
     return roof
 
@@ -423,11 +430,14 @@ def run_sharded_c4(dist, n_total, B, steps, warmup, device=0):
     """C4: ONE cache of `n_total` entries sharded over the job's GPUs, one shard per rank (entries
     dealt round-robin by append position); at N = 1 the same code with one shard
     and no collective.  A step = B lookups: every rank's certified local scan
-    (mc_retrieve_local_async) -> NCCL all-gather of the B x 32-byte records -> merge and decisions
-    on every rank (mc_merge_records, decisions read back to the host).  Strong scaling: the cache
-    and the batch stay fixed as N grows.  Timed by CUDA events on the step stream around the K
-    steps (the host's part of each step included), max over ranks.  Caches are generated on the
-    device (f4)."""
+    (mc_retrieve_local_submit: no exhaustive-rescan launches behind it) -> NCCL all-gather of the
+    B x 32-byte records -> merge and decisions on every rank (mc_merge_records_submit, decisions
+    written to mapped host memory), read by mc_merge_records_wait one step later: two lookups in
+    flight.  A merged MC_FLAG_NEED_RESCAN (a failed certificate on some shard) runs the second
+    round (mc_rescan_local, all-gather, merge) on every rank.  Strong scaling: the cache and the
+    batch stay fixed as N grows.  Timed by CUDA events on the step stream around the K steps
+    (the host's enqueue and read-back of every step inside), max over ranks.  Caches are
+    generated on the device (f4)."""
     import torch
 
     from paper_2503_11972_b200 import ThresholdTable, _native
@@ -449,44 +459,72 @@ def run_sharded_c4(dist, n_total, B, steps, warmup, device=0):
     nb = B * 32
     dev = torch.device("cuda", device)
     cs = torch.cuda.Stream(dev)
-    local = torch.empty(nb, dtype=torch.uint8, device=dev)
-    gathered = torch.empty(G * nb, dtype=torch.uint8, device=dev)
-    hits = 0
+    NS = _native.DeviceRing.MERGE_SLOTS  # lookups in flight: step i+1 is enqueued before step i is read
+    local = [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(NS)]
+    gathered = [torch.empty(G * nb, dtype=torch.uint8, device=dev) for _ in range(NS)]
+    hits = rescans = 0
     # A batch enters the job once: each rank uploads its 1/G of the rows, and the ranks
     # all-gather the batch over NVLink (instead of G host uploads of the whole batch).
     split = dist is not None and B > 4 and B % G == 0 and (G > 1 or os.environ.get("MC_C4_SPLIT_UPLOAD"))
     if split:
         Qt = torch.from_numpy(Q)  # page-locked above: the slice copies are DMAs
         part = B // G
-        local_q = torch.empty(part * dim, dtype=torch.float64, device=dev)
-        full_q = torch.empty(B * dim, dtype=torch.float64, device=dev)
+        local_q = [torch.empty(part * dim, dtype=torch.float64, device=dev) for _ in range(NS)]
+        full_q = [torch.empty(B * dim, dtype=torch.float64, device=dev) for _ in range(NS)]
 
-    def step(i):
-        nonlocal hits
+    csp = cs.cuda_stream
+    gptr = [t.data_ptr() for t in gathered]  # raw pointers: no per-step tensor attribute lookups
+
+    def submit(i):
+        j = i % NS
+        if G == 1 and not split:  # no collective: the ring's own calls order themselves after csp
+            ring.retrieve_local_submit(Q[i], gptr[j], csp)
+            ring.merge_submit(gptr[j], G, B, 0, csp, j)
+            return
         with torch.cuda.stream(cs):
             if split:
-                local_q.copy_(Qt[i, g * part:(g + 1) * part].reshape(-1), non_blocking=True)
-                dist.td.all_gather_into_tensor(full_q, local_q)
-                ring.retrieve_local_device(full_q, B, local, cs.cuda_stream)
-                dist.td.all_gather_into_tensor(gathered, local)
-            elif G > 1:
-                ring.retrieve_local_async(Q[i], local, cs.cuda_stream)
-                dist.td.all_gather_into_tensor(gathered, local)
+                local_q[j].copy_(Qt[i, g * part:(g + 1) * part].reshape(-1), non_blocking=True)
+                dist.td.all_gather_into_tensor(full_q[j], local_q[j])
+                ring.retrieve_local_device(full_q[j], B, local[j], cs.cuda_stream)
+                dist.td.all_gather_into_tensor(gathered[j], local[j])
+            elif G > 1:  # the scan without the exhaustive rescan behind it (second round on demand)
+                ring.retrieve_local_submit(Q[i], local[j], cs.cuda_stream)
+                dist.td.all_gather_into_tensor(gathered[j], local[j])
             else:
-                ring.retrieve_local_async(Q[i], gathered, cs.cuda_stream)
-        live, sim, k, flags = ring.merge_records(gathered, G, B, 0, cs.cuda_stream)
+                ring.retrieve_local_submit(Q[i], gathered[j], cs.cuda_stream)
+        ring.merge_submit(gathered[j], G, B, 0, cs.cuda_stream, j)
+
+    def collect(i):
+        nonlocal hits, rescans
+        j = i % NS
+        live, sim, k, flags = ring.merge_wait(j)
+        if not split and (flags & _native.MC_FLAG_NEED_RESCAN).any():  # same decision on every rank
+            rescans += 1
+            with torch.cuda.stream(cs):
+                own = local[j] if G > 1 else gathered[j]
+                ring.rescan_local(Q[i], own, cs.cuda_stream)
+                if G > 1:
+                    dist.td.all_gather_into_tensor(gathered[j], local[j])
+            ring.merge_submit(gathered[j], G, B, 0, cs.cuda_stream, j)
+            live, sim, k, flags = ring.merge_wait(j)
         hits += int((flags & _native.MC_FLAG_HIT).astype(bool).sum())
 
-    for i in range(warmup):
-        step(i)
-    hits = 0
+    def run(first, last):  # NS - 1 lookups stay in flight while the host prepares the next
+        for i in range(first, last):
+            submit(i)
+            if i - first >= NS - 1:
+                collect(i - NS + 1)
+        for i in range(max(first, last - NS + 1), last):
+            collect(i)
+
+    run(0, warmup)
+    hits = rescans = 0
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(cs)
-    for i in range(warmup, warmup + steps):
-        step(i)
+    run(warmup, warmup + steps)
     e1.record(cs)
     e1.synchronize()
     dt = e0.elapsed_time(e1) * 1e-3
@@ -501,7 +539,10 @@ def run_sharded_c4(dist, n_total, B, steps, warmup, device=0):
             "n_gpus": G, "rows_per_gpu": n_local, "scaling": "strong", "hit_fraction": hits / (B * steps),
             "query_upload": ("1/G of the batch per rank + NCCL all-gather of the queries" if split
                              else "the whole batch from the host on every rank"),
-            "timing": "CUDA events on the step stream around the timed steps (host part of each step included), "
+            "second_rounds": rescans,
+            "pipelining": f"{NS} lookups in flight (step i+1 enqueued before step i's decisions are read)",
+            "timing": "CUDA events on the step stream around the timed steps (the host's enqueue and read-back "
+                      "of every step inside; the last step's decisions read before the end event is waited on), "
                       "max over ranks"}
 
 

@@ -39,6 +39,8 @@ extern "C" {
 #define MC_FLAG_NEAR_TAU 0x10u  /* best within 1e-12 of some tau_k (ulp-ambiguous) */
 #define MC_FLAG_FALLBACK 0x20u  /* top-K' certificate failed; exhaustive exact rescan answered */
 #define MC_FLAG_NONFINITE 0x40u /* query had NaN/Inf; answered by exhaustive float64 scan */
+#define MC_FLAG_NEED_RESCAN 0x80u /* merge of mc_retrieve_local_submit records: some shard's certificate
+                                     failed; run mc_rescan_local on every shard, gather, merge again */
 
 /* Scan-path selection for mc_set_path (default MC_PATH_AUTO: B <= 4 -> the
  * TMA-streamed int8 scan when Dp <= 1024 (Dp = D rounded up to 64), else the
@@ -142,6 +144,14 @@ int mc_configure_shard(mc_cache* h, int32_t n_shards, int32_t shard_id);
  * NULL = the handle's stream); not synchronous. */
 int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream);
 
+/* mc_retrieve_local_async without the exhaustive rescan behind the scan (two launches fewer per
+ * lookup): a record whose top-K' certificate failed keeps a rescan request, which the merge
+ * reports as MC_FLAG_NEED_RESCAN.  Every shard then runs mc_rescan_local on the same queries and
+ * its own records (in place), the records are gathered again and merged again.  The rescan
+ * must run before a later lookup or flush applies appends / evictions on the handle. */
+int mc_retrieve_local_submit(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream);
+int mc_rescan_local(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream);
+
 /* mc_retrieve_local_async with the B query rows already in DEVICE memory (float64, row stride
  * dim; dim a multiple of 64), written on `stream` — e.g. assembled by an all-gather of the
  * ranks' slices of the batch, so each rank uploads only its share from the host. */
@@ -153,6 +163,19 @@ int mc_retrieve_local_device(mc_cache* h, const double* d_queries, int32_t B, vo
 int mc_merge_records(mc_cache* h, const void* dev_records, int32_t G, int32_t B, int64_t p0,
                      void* stream, int64_t* out_live, double* out_sim, int32_t* out_k,
                      uint32_t* out_flags);
+
+/* Pipelined form of mc_merge_records (replaces the same reference call, cache.py:244-260, for a
+ * caller that keeps several sharded lookups in flight).  _submit enqueues the merge of G x B
+ * records on `stream` and returns at once; the decisions land in result slot `slot`
+ * (0 <= slot < MC_MERGE_SLOTS), which must be free.  _wait blocks until that merge is done,
+ * writes the answers like mc_retrieve_batch and frees the slot.  The record buffer must stay
+ * untouched until the merge completes (stream order on `stream` guarantees it for later work
+ * enqueued there). */
+#define MC_MERGE_SLOTS 2
+int mc_merge_records_submit(mc_cache* h, const void* dev_records, int32_t G, int32_t B, int64_t p0,
+                            void* stream, int32_t slot);
+int mc_merge_records_wait(mc_cache* h, int32_t slot, int64_t* out_live, double* out_sim,
+                          int32_t* out_k, uint32_t* out_flags);
 
 /* Measurement hook (bench.py): runs `iters` hot-path steps with all inputs
  * already resident in HBM and times them with CUDA events on the handle's

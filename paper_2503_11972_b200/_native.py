@@ -22,6 +22,7 @@ MC_FLAG_NEAR_TIE = 0x08
 MC_FLAG_NEAR_TAU = 0x10
 MC_FLAG_FALLBACK = 0x20
 MC_FLAG_NONFINITE = 0x40
+MC_FLAG_NEED_RESCAN = 0x80  # merge of mc_retrieve_local_submit records: run rescan_local, gather, merge again
 
 PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_STREAM8 = 0, 1, 2, 6
 
@@ -36,7 +37,8 @@ EXPORTED = (
     "mc_merge_records", "mc_stats", "mc_last_error", "mc_version", "mc_profile_steps", "mc_profile_rotate",
     "mc_debug_gemv_timing", "mc_retrieve_submit", "mc_retrieve_wait", "mc_debug_read_row",
     "mc_retrieve_decisions", "mc_set_sigma_schedule", "mc_generate_rows", "mc_read_rows", "mc_register_host",
-    "mc_unregister_host", "mc_retrieve_local_device",
+    "mc_unregister_host", "mc_retrieve_local_device", "mc_merge_records_submit", "mc_merge_records_wait",
+    "mc_retrieve_local_submit", "mc_rescan_local",
 )
 
 
@@ -75,6 +77,10 @@ def _declare(lib):
     lib.mc_register_host.argtypes = [vp, i64]
     lib.mc_retrieve_local_device.argtypes = [vp, vp, i32, vp, vp]
     lib.mc_unregister_host.argtypes = [vp]
+    lib.mc_merge_records_submit.argtypes = [vp, vp, i32, i32, i64, vp, i32]
+    lib.mc_merge_records_wait.argtypes = [vp, i32, dp, dp, dp, dp]
+    lib.mc_retrieve_local_submit.argtypes = [vp, dp, i32, vp, vp]
+    lib.mc_rescan_local.argtypes = [vp, dp, i32, vp, vp]
     lib.mc_last_error.restype = C.c_char_p
     lib.mc_version.restype = C.c_char_p
     return lib
@@ -161,6 +167,7 @@ class DeviceRing:
         # call -> copy-out, so concurrent readers ("many readers or one writer", cache.py:144)
         # never see each other's queries or answers.
         self._lock = threading.Lock()
+        self._merge_B = {}  # merge slot -> batch of the merge submitted into it
 
     # -- lifecycle -----------------------------------------------------------
     def close(self) -> None:
@@ -294,6 +301,19 @@ class DeviceRing:
         _check(self.lib, self.lib.mc_retrieve_local_async(self._h, _ptr(Q), Q.shape[0], self._addr(dev_records),
                                                           stream_ptr or None))
 
+    def retrieve_local_submit(self, Q: np.ndarray, dev_records, stream_ptr: int = 0) -> None:
+        """retrieve_local_async without the exhaustive rescan behind the scan: records whose
+        certificate failed surface as MC_FLAG_NEED_RESCAN in the merge (mc_retrieve_local_submit)."""
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        _check(self.lib, self.lib.mc_retrieve_local_submit(self._h, _ptr(Q), Q.shape[0], self._addr(dev_records),
+                                                           stream_ptr or None))
+
+    def rescan_local(self, Q: np.ndarray, dev_records, stream_ptr: int = 0) -> None:
+        """Exhaustive float64 rescan of the records that ask for it, in place (mc_rescan_local)."""
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        _check(self.lib, self.lib.mc_rescan_local(self._h, _ptr(Q), Q.shape[0], self._addr(dev_records),
+                                                  stream_ptr or None))
+
     def retrieve_local_device(self, dev_queries, B: int, dev_records, stream_ptr: int = 0) -> None:
         """retrieve_local_async for B float64 query rows already on this ring's device (a torch
         tensor or raw pointer, row stride dim), written on `stream` (mc_retrieve_local_device)."""
@@ -307,6 +327,27 @@ class DeviceRing:
             _check(self.lib, self.lib.mc_merge_records(
                 self._h, self._addr(dev_records), int(G), int(B), int(p0), stream_ptr or None, *self._out_ptrs))
             return self._live[:B].copy(), self._sim[:B].copy(), self._k[:B].copy(), self._flags[:B].copy()
+
+    MERGE_SLOTS = 2  # MC_MERGE_SLOTS
+
+    def merge_submit(self, dev_records, G: int, B: int, p0: int, stream_ptr: int, slot: int) -> None:
+        """Enqueue the merge of G x B records on `stream` into result slot `slot` and return at once
+        (mc_merge_records_submit); merge_wait(slot) collects it."""
+        _check(self.lib, self.lib.mc_merge_records_submit(self._h, self._addr(dev_records), int(G), int(B), int(p0),
+                                                          stream_ptr or None, int(slot)))
+        self._merge_B[slot] = int(B)
+
+    def merge_wait(self, slot: int):
+        """(live, sim, k, flags) arrays of the merge submitted into `slot` (mc_merge_records_wait)."""
+        B = self._merge_B.get(slot, 0)
+        live = np.empty(B, dtype=np.int64)
+        sim = np.empty(B, dtype=np.float64)
+        k = np.empty(B, dtype=np.int32)
+        flags = np.empty(B, dtype=np.uint32)
+        _check(self.lib, self.lib.mc_merge_records_wait(self._h, int(slot), _ptr(live), _ptr(sim), _ptr(k),
+                                                        _ptr(flags)))
+        self._merge_B[slot] = 0
+        return live, sim, k, flags
 
     def profile_steps(self, Q: np.ndarray, rows: np.ndarray | None, iters: int, flush_bytes: int):
         """Device-timed steps (see mc_profile_steps). Q: [iters, B, dim]; rows: [iters, dim] or None."""

@@ -143,6 +143,17 @@ struct mc_cache {
   double* d_gq64 = nullptr;     // [Dp] the kernel's L2 relay of the pending row
   unsigned* d_sync = nullptr;   // [2] streamed-scan launch overlap: rows published / records read (epochs)
   bool tc_tail = false;         // the last kernel enqueued on the stream is the tensor path's merge (PDL-early)
+  bool s8_isolated = false;     // the streamed scan being enqueued cannot overlap a neighbour (local lookups)
+  long long s8_wide_rows = 1LL << 17;  // isolated launches over windows this large take the wide grid
+                                       // (MC_S8_WIDE_ROWS)
+
+  // pipelined shard merges (mc_merge_records_submit / _wait): per slot, k_finalize writes the
+  // decisions straight into a mapped host block and an event marks them complete
+  OutRec* h_merge[MC_MERGE_SLOTS] = {};
+  OutRec* d_merge[MC_MERGE_SLOTS] = {};
+  cudaEvent_t merge_ev[MC_MERGE_SLOTS] = {};
+  int merge_B[MC_MERGE_SLOTS] = {};  // batch of the merge in the slot, 0 = none
+  int merge_cap = 0;
 
   TcPlan* tc = nullptr;           // fp16 tensor-core scan plan (MC_PATH_GEMM*), created on first use
   S8Plan* s8 = nullptr;           // TMA-streamed int8 scan plan (tensor maps of ring8 / ringq)
@@ -252,10 +263,19 @@ void quantize_query(const double* q, int D, int Dp, QPrep* p, int8_t* q8) {
   p->exotic = !(p->n1 <= 1e30) || !(p->n2 >= 1e-30);
 }
 
+int s8_grid_max(const mc_cache* h) { return std::max(s8_grid(h->sm_count), s8_grid_wide(h->sm_count)); }
+
+// Grid of a streamed-scan launch: the overlap-friendly grid, or every co-resident CTA slot for an
+// isolated lookup (h->s8_isolated) over a window of at least s8_wide_rows rows.
+int s8_launch_grid(const mc_cache* h) {
+  if (h->s8_isolated && h->count >= h->s8_wide_rows) return std::min(320, s8_grid_wide(h->sm_count));
+  return s8_grid(h->sm_count);
+}
+
 // Per-CTA records: the GEMV scans' CtaRec per CTA, or the streamed scan's two 16-byte words per
 // CTA in two epoch-parity buffers; sized for the larger.
 size_t cta_bytes(const mc_cache* h, int cap) {
-  return std::max((size_t)gemv_grid(h->sm_count) * sizeof(CtaRec), (size_t)s8_grid(h->sm_count) * 2 * 2 * 16) *
+  return std::max((size_t)gemv_grid(h->sm_count) * sizeof(CtaRec), (size_t)s8_grid_max(h) * 2 * 2 * 16) *
          (size_t)cap;
 }
 
@@ -500,7 +520,7 @@ int ensure_tc(mc_cache* h, int B) {
 // Epoch of the next streamed-scan launch (never 0: zeroed words belong to no launch).  On
 // wrap-around the bound words are cleared, so an old epoch can never outrank a new one.
 // Distance (uint4) between the two epoch-parity record buffers of the streamed scan in d_cta.
-unsigned s8_rec_par(const mc_cache* h) { return (unsigned)((size_t)h->Bcap * s8_grid(h->sm_count) * 2); }
+unsigned s8_rec_par(const mc_cache* h) { return (unsigned)((size_t)h->Bcap * s8_grid_max(h) * 2); }
 
 // A streamed-scan launch that failed took an epoch without publishing it: publish it from the
 // host so the next launch (which waits for the previous epoch's rows) does not wait forever.
@@ -550,7 +570,7 @@ int scan_merge(mc_cache* h, const double* q64, int B, mc_record* rec, OutRec* ou
     if (s8) {
       const unsigned ep = s8_epoch(h);
       const cudaError_t e = launch_stream8_scan(h->s8, rbufs(h), st, q64 + (size_t)b0 * h->Dp, nb, h->d_cta, b0,
-                                                s8_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax8, ep, h->thr,
+                                                s8_launch_grid(h), h->shard, h->d_counter, h->d_gmax8, ep, h->thr,
                                                 rec, out,
                                                 a, prep + b0, q8 + (size_t)b0 * h->Dp,
                                                 b0 + nb == B ? done_seq : nullptr, seq, outp, h->d_sync,
@@ -976,6 +996,7 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
     CUC(cudaStreamSynchronize(h->stream));
   }
   if (const char* e = getenv("MC_PARAM_INPUT")) h->param_in = atoi(e) != 0;
+  if (const char* e = getenv("MC_S8_WIDE_ROWS")) h->s8_wide_rows = atoll(e);
   CUC(cudaHostAlloc(&h->h_qkeep, (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
   memset(h->h_qkeep, 0, (size_t)h->Dp * sizeof(double));
   for (int k = 0; k < 2; ++k) {  // mapped: the parameter-block launches read the query from here
@@ -1043,6 +1064,10 @@ int mc_destroy(mc_cache* h) {
     cudaFree(h->d_state_fb);
     cudaFree(h->d_gq64);
     cudaFree(h->d_sync);
+    for (int i = 0; i < MC_MERGE_SLOTS; ++i) {
+      cudaFreeHost(h->h_merge[i]);
+      if (h->merge_ev[i]) cudaEventDestroy(h->merge_ev[i]);
+    }
     if (h->env_ev) cudaEventDestroy(h->env_ev);
     if (h->rec_ev) cudaEventDestroy(h->rec_ev);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -1266,7 +1291,16 @@ int mc_retrieve_wait(mc_cache* h, uint32_t ticket, int64_t* out_live, double* ou
   return copy_out(h, B, out_live, out_sim, out_k, out_flags);
 }
 
-int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream) {
+namespace {
+// Merged flags as the C ABI reports them: MC_FLAG_* plus MC_FLAG_NEED_RESCAN for a record that
+// still asks for the exhaustive rescan (mc_retrieve_local_submit records).
+uint32_t public_flags(unsigned f) { return (f & 0xffffu) | ((f & FLAG_NEED_ANY) ? MC_FLAG_NEED_RESCAN : 0u); }
+
+// A shard's certified local records for B host queries.  exact: the exhaustive rescan of
+// records whose certificate failed follows on the stream (always launched; it skips unflagged
+// queries).  Otherwise such records keep their FLAG_NEED_* bits, the merge reports
+// MC_FLAG_NEED_RESCAN and the caller runs mc_rescan_local before the window changes.
+int local_lookup(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream, bool exact) {
   if (!h || !dev_records || (!queries && B > 0)) return fail(MC_ERR_ARG, "NULL argument");
   if (B <= 0) return fail(MC_ERR_ARG, "batch must be positive");
   std::lock_guard<std::mutex> lk(h->mu);
@@ -1280,17 +1314,62 @@ int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void*
     CU(cudaMemsetAsync(rec, 0xff, (size_t)B * sizeof(mc_record), h->stream));  // pos = -1 (NaN sims)
   } else {
     const double* q = nullptr;
+    // with the exact rescan behind it on the stream, the scan cannot overlap a neighbour
+    h->s8_isolated = true;  // local lookups are stream-ordered behind the previous one's exchange
     int rc = lookup_enqueue(h, queries, B, rec, nullptr, true, &q);
+    h->s8_isolated = false;
     if (rc) return rc;
-    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, q, B, rec, h->d_scratch,
-                           exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
-    h->stats[7] += 2;
+    if (exact) {
+      CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, q, B, rec, h->d_scratch,
+                             exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
+      h->stats[7] += 2;
+    }
   }
   if (stream && stream != h->stream) {  // order the caller's stream (the exchange) after this shard's scan
     CU(cudaEventRecord(h->rec_ev, h->stream));
     CU(cudaStreamWaitEvent((cudaStream_t)stream, h->rec_ev, 0));
   }
   h->stats[0] += B;
+  return MC_OK;
+}
+}  // namespace
+
+int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream) {
+  return local_lookup(h, queries, B, dev_records, stream, true);
+}
+
+int mc_retrieve_local_submit(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream) {
+  return local_lookup(h, queries, B, dev_records, stream, false);
+}
+
+int mc_rescan_local(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream) {
+  if (!h || !dev_records || (!queries && B > 0)) return fail(MC_ERR_ARG, "NULL argument");
+  if (B <= 0) return fail(MC_ERR_ARG, "batch must be positive");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  int rc = ensure_batch(h, B);
+  if (rc) return rc;
+  if (stream && stream != h->stream) {  // the records were last written on the caller's stream
+    CU(cudaEventRecord(h->rec_ev, (cudaStream_t)stream));
+    CU(cudaStreamWaitEvent(h->stream, h->rec_ev, 0));
+  }
+  if (h->count > 0) {
+    const double* q = nullptr;
+    const QPrep* prep = nullptr;
+    const int8_t* q8 = nullptr;
+    // queries only: pending appends / evictions are not applied (the rescan must see the
+    // window the scan saw; the device ring state changes only when a lookup or flush applies them)
+    rc = upload_envelope(h, queries, B, true, false, &q, &prep, &q8);
+    if (rc) return rc;
+    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, q, B,
+                           static_cast<mc_record*>(dev_records), h->d_scratch, exact_grid(h->sm_count),
+                           gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
+    h->stats[7] += 2;
+  }
+  if (stream && stream != h->stream) {
+    CU(cudaEventRecord(h->rec_ev, h->stream));
+    CU(cudaStreamWaitEvent((cudaStream_t)stream, h->rec_ev, 0));
+  }
   return MC_OK;
 }
 
@@ -1347,8 +1426,64 @@ int mc_merge_records(mc_cache* h, const void* dev_records, int32_t G, int32_t B,
     if (out_live) out_live[b] = o.live;
     if (out_sim) out_sim[b] = o.sim;
     if (out_k) out_k[b] = o.k;
-    if (out_flags) out_flags[b] = o.flags & 0xffffu;
+    if (out_flags) out_flags[b] = public_flags(o.flags);
   }
+  return MC_OK;
+}
+
+int mc_merge_records_submit(mc_cache* h, const void* dev_records, int32_t G, int32_t B, int64_t p0, void* stream,
+                            int32_t slot) {
+  if (!h || !dev_records) return fail(MC_ERR_ARG, "NULL argument");
+  if (G < 1 || B <= 0 || p0 < 0) return fail(MC_ERR_ARG, "bad merge shape G=%d B=%d p0=%lld", G, B, (long long)p0);
+  if (slot < 0 || slot >= MC_MERGE_SLOTS) return fail(MC_ERR_ARG, "merge slot %d outside [0, %d)", slot, MC_MERGE_SLOTS);
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard guard(h->dev);
+  if (h->merge_B[slot]) return fail(MC_ERR_STATE, "merge slot %d still holds an unread result", slot);
+  if (B > h->merge_cap) {  // grow every slot (none holds a result that is still in flight)
+    for (int i = 0; i < MC_MERGE_SLOTS; ++i)
+      if (h->merge_B[i]) CU(cudaEventSynchronize(h->merge_ev[i]));
+    int cap = 4;
+    while (cap < B) cap <<= 1;
+    for (int i = 0; i < MC_MERGE_SLOTS; ++i) {
+      cudaFreeHost(h->h_merge[i]);
+      h->h_merge[i] = nullptr;
+      CU(cudaHostAlloc(&h->h_merge[i], (size_t)cap * sizeof(OutRec), cudaHostAllocMapped));
+      CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_merge[i]), h->h_merge[i], 0));
+      if (!h->merge_ev[i]) CU(cudaEventCreateWithFlags(&h->merge_ev[i], cudaEventDisableTiming));
+    }
+    h->merge_cap = cap;
+  }
+  cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+  // decisions go straight to the mapped host block (kernel completion publishes them)
+  CU(launch_finalize(static_cast<const mc_record*>(dev_records), G, B, p0, h->d_state, h->thr, h->d_merge[slot], s));
+  CU(cudaEventRecord(h->merge_ev[slot], s));
+  h->merge_B[slot] = B;
+  h->stats[7]++;
+  return MC_OK;
+}
+
+int mc_merge_records_wait(mc_cache* h, int32_t slot, int64_t* out_live, double* out_sim, int32_t* out_k,
+                          uint32_t* out_flags) {
+  if (!h) return fail(MC_ERR_ARG, "NULL argument");
+  if (slot < 0 || slot >= MC_MERGE_SLOTS) return fail(MC_ERR_ARG, "merge slot %d outside [0, %d)", slot, MC_MERGE_SLOTS);
+  cudaEvent_t ev;
+  int B;
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    B = h->merge_B[slot];
+    if (!B) return fail(MC_ERR_STATE, "merge slot %d holds no submitted merge", slot);
+    ev = h->merge_ev[slot];
+  }
+  CU(cudaEventSynchronize(ev));  // outside the lock: other lookups may be enqueued meanwhile
+  std::lock_guard<std::mutex> lk(h->mu);
+  const OutRec* o = h->h_merge[slot];
+  for (int b = 0; b < B; ++b) {
+    if (out_live) out_live[b] = o[b].live;
+    if (out_sim) out_sim[b] = o[b].sim;
+    if (out_k) out_k[b] = o[b].k;
+    if (out_flags) out_flags[b] = public_flags(o[b].flags);
+  }
+  h->merge_B[slot] = 0;
   return MC_OK;
 }
 

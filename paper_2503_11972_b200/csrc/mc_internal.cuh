@@ -130,6 +130,7 @@ struct QPrep {
 struct S8Plan;
 bool stream8_supported(int Dp);
 int s8_grid(int sm_count);  // CTAs of one streamed-scan launch
+int s8_grid_wide(int sm_count);  // CTAs of an isolated streamed-scan launch (every co-resident slot)
 // One query (and <= 1 pending row, host pointers) carried in the kernel parameter block.
 cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const RingState& st, int D, const double* q64,
                                   const double* stage_row, CtaRec* cta, int grid, ShardMap sm, unsigned* counter,

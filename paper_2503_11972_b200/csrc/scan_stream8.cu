@@ -72,6 +72,11 @@ constexpr int S8_CTAS_PER_SM = S8_CONSUMERS <= 4 ? 2 : 1;
 // CTAs per SM in one launch's grid (S8_GRID_PER_SM = 2 with 4 consumers: two half-size CTAs per
 // SM, so an SM frees half its room as soon as one of them retires).
 int s8_grid(int sm_count) { return S8_GRID_PER_SM * sm_count; }
+// A launch that cannot overlap a neighbouring lookup (a shard's local lookup: the exact-rescan
+// and merge kernels sit between consecutive scans) fills every co-resident CTA slot instead:
+// one 148-CTA launch alone streams a 1M-row window at ~5.2 TB/s, two CTAs per SM keep more
+// bytes in flight.  The record buffers are sized for this grid.
+int s8_grid_wide(int sm_count) { return S8_CTAS_PER_SM * sm_count; }
 constexpr int S8_THREADS = (S8_CW + 4) * 32;   // producer + consumers + rescorer + bound poller + eager rescorer
 constexpr int S8_EAGER = S8_CW + 1;            // S.best slot of the eager rescorer
 constexpr int S8_QCAP = 128;                   // candidate queue entries per consumer warp

@@ -60,6 +60,7 @@ from .records import (
 )
 
 RECORD_BYTES = 32  # sizeof(mc_record)
+_NEED_RESCAN = 0x80  # MC_FLAG_NEED_RESCAN
 
 
 def _count_owned(p_lo: int, n: int, g: int, G: int) -> int:
@@ -239,7 +240,12 @@ class ShardedSemanticCache:
         return st[dev]
 
     def _records(self, Q: np.ndarray):
-        """Every shard's local records -> one [G, B] record buffer on the merging device."""
+        """Every shard's local records -> one [G, B] record buffer on the merging device.
+
+        Host-fed lookups take the scan without the exhaustive rescan behind it
+        (mc_retrieve_local_submit); a record whose certificate failed comes back from the merge
+        as MC_FLAG_NEED_RESCAN and ``_rescan`` runs the second round.  Returns the gathered
+        buffer, the exchange stream and the per-shard record buffers (for that round)."""
         import contextlib
 
         import torch
@@ -250,6 +256,7 @@ class ShardedSemanticCache:
         cs = self._comm_stream(dev)
         ctx = torch.cuda.stream(cs) if cs is not None else contextlib.nullcontext()
         sp = cs.cuda_stream if cs is not None else 0
+        locals_ = []
         with ctx:
             gathered = torch.empty(self.n_shards * nb, dtype=torch.uint8, device=dev)
             if self._dist is not None:  # one shard per rank: all-gather the B records (the only collective)
@@ -257,28 +264,59 @@ class ShardedSemanticCache:
                 G = self.n_shards
                 if dev.type == "cuda" and G > 1 and B > 4 and B % G == 0 and self.dim % 64 == 0:
                     # the batch enters once: each rank uploads its 1/G of the rows and the ranks
-                    # all-gather the queries over NVLink (mc_retrieve_local_device)
+                    # all-gather the queries over NVLink (mc_retrieve_local_device, rescan included)
                     part = B // G
                     mine = torch.from_numpy(Q[self.shard * part:(self.shard + 1) * part]).to(dev).reshape(-1)
                     full = torch.empty(B * self.dim, dtype=torch.float64, device=dev)
                     self._dist.all_gather_into_tensor(full, mine, group=self._group)
                     self.ring.retrieve_local_device(full, B, local, sp)
                 else:
-                    self.ring.retrieve_local_async(Q, local, sp)
+                    self.ring.retrieve_local_submit(Q, local, sp)
+                    locals_.append((self.ring, local))
                 self._dist.all_gather_into_tensor(gathered, local, group=self._group)
-                return gathered, sp
+                return gathered, sp, locals_
             for g, ring in self._rings.items():  # every shard in this process: write the slices directly
                 rdev = ring.records_device()
                 if rdev == dev:
-                    ring.retrieve_local_async(Q, gathered[g * nb:(g + 1) * nb], sp)
+                    part = gathered[g * nb:(g + 1) * nb]
+                    ring.retrieve_local_submit(Q, part, sp)
+                    locals_.append((ring, part))
                 else:  # shard on a peer GPU: its records cross NVLink as one peer copy
                     rs = self._comm_stream(rdev)
                     local = torch.empty(nb, dtype=torch.uint8, device=rdev)
-                    ring.retrieve_local_async(Q, local, rs.cuda_stream)
+                    ring.retrieve_local_submit(Q, local, rs.cuda_stream)
                     cs.wait_stream(rs)
                     gathered[g * nb:(g + 1) * nb].copy_(local, non_blocking=True)
                     local.record_stream(cs)
-        return gathered, sp
+                    locals_.append((ring, local))
+        return gathered, sp, locals_
+
+    def _rescan(self, Q: np.ndarray, gathered, sp, locals_) -> None:
+        """Second round after a merge reported MC_FLAG_NEED_RESCAN (the same on every rank: all
+        ranks merged the same gathered records): each shard rescans the flagged queries
+        exhaustively in float64, in place, and the records are gathered again."""
+        import torch
+
+        nb = Q.shape[0] * RECORD_BYTES
+        dev = self.ring.records_device()
+        cs = self._comm_stream(dev)
+        with torch.cuda.stream(cs):
+            if self._dist is not None:
+                ring, local = locals_[0]
+                ring.rescan_local(Q, local, sp)
+                self._dist.all_gather_into_tensor(gathered, local, group=self._group)
+                return
+            for g, (ring, buf) in zip(sorted(self._rings), locals_):
+                rdev = ring.records_device()
+                if rdev == dev:
+                    ring.rescan_local(Q, buf, sp)
+                else:
+                    rs = self._comm_stream(rdev)
+                    rs.wait_stream(cs)
+                    ring.rescan_local(Q, buf, rs.cuda_stream)
+                    cs.wait_stream(rs)
+                    gathered[g * nb:(g + 1) * nb].copy_(buf, non_blocking=True)
+                    buf.record_stream(cs)
 
     def retrieve_batch(self, Q: np.ndarray, table: ThresholdTable) -> list[RetrievalResult]:
         Q = np.ascontiguousarray(Q, dtype=np.float64)
@@ -293,9 +331,13 @@ class ShardedSemanticCache:
             for ring in self._rings.values():
                 ring.set_table(table.pairs, table.total_steps)
             self._table_key = key
-        gathered, stream = self._records(Q)
+        gathered, stream, locals_ = self._records(Q)
         live, sim, k, flags = self.ring.merge_records(gathered, self.n_shards, Q.shape[0], self.oldest_position,
                                                       stream)
+        if locals_ and (flags & _NEED_RESCAN).any():
+            self._rescan(Q, gathered, stream, locals_)
+            live, sim, k, flags = self.ring.merge_records(gathered, self.n_shards, Q.shape[0], self.oldest_position,
+                                                          stream)
         at = self._store.live
         out = []
         for i, f in enumerate(np.asarray(flags).tolist()):

@@ -68,6 +68,30 @@ class FakeShardRing:
                           _native.MC_FLAG_TIE if idx.size > 1 else 0, 0)
         out.copy_(torch.from_numpy(rec.view(np.uint8).copy()))
 
+    NEED = 0x10000  # FLAG_NEED_FALLBACK (mc_internal.cuh): the record asks for the exhaustive rescan
+
+    def retrieve_local_submit(self, Q, out, stream=0):
+        """Like the native submit: no rescan behind the scan.  Every third query's record (by a
+        per-ring counter) comes back degraded and flagged, as a failed certificate would."""
+        self.retrieve_local_async(Q, out, stream)
+        rec = out.numpy().view(REC)
+        self._submits = getattr(self, "_submits", 0) + 1
+        for b in range(Q.shape[0]):
+            if rec[b]["pos"] >= 0 and (b + self._submits) % 3 == 0:
+                rec[b]["sim"] -= 0.5
+                rec[b]["flags"] |= self.NEED
+
+    def rescan_local(self, Q, out, stream=0):
+        rec = out.numpy().view(REC)
+        need = [b for b in range(Q.shape[0]) if rec[b]["pos"] >= 0 and rec[b]["flags"] & self.NEED]
+        exact = torch.empty_like(out)
+        self.retrieve_local_async(Q, exact, stream)
+        ex = exact.numpy().view(REC)
+        for b in need:
+            rec[b] = ex[b]
+            rec[b]["flags"] |= _native.MC_FLAG_FALLBACK
+        self.rescans = getattr(self, "rescans", 0) + len(need)
+
     def merge_records(self, gathered, G, B, p0, stream=0):
         recs = gathered.numpy().view(REC).reshape(G, B)
         t = OracleTable(self.pairs, self.total_steps)
@@ -84,6 +108,8 @@ class FakeShardRing:
             live[b], sim[b] = p - p0, s
             k[b] = t.select_k(s) or 0
             flags[b] = 0 if s < t.tau else _native.MC_FLAG_HIT
+            if any(r["flags"] & self.NEED for r in recs[:, b] if r["pos"] >= 0):
+                flags[b] |= _native.MC_FLAG_NEED_RESCAN
         return live, sim, k, flags
 
     def close(self):

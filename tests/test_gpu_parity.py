@@ -1155,3 +1155,112 @@ def test_overlapping_launches_c2_scale_request_stream():
     prev[0].result()
     _record_parity("overlapping launches C2 stream", stats)
     c.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B", [1, 40])
+def test_pipelined_shard_merges_match_blocking_merges(B):
+    """mc_merge_records_submit / _wait with both result slots in flight (the C4 bench loop: the
+    next lookup is enqueued before the previous decisions are read) give the answers of the
+    blocking mc_merge_records on the same gathered records; slot misuse fails loudly."""
+    import torch
+
+    G = 2
+    wl = ClusteredWorkload(768, n_clusters=64, seed=77 + B)
+    rows = wl.cache_rows(9000)
+    rings = []
+    for g in range(G):
+        r = _native.DeviceRing(4500, 768, 0)
+        r.configure_shard(G, g)
+        r.append(rows[g::G])
+        rings.append(r)
+    table = ThresholdTable.default()
+    for r in rings:
+        r.set_table(table.pairs, table.total_steps)
+    dev = torch.device("cuda", 0)
+    cs = torch.cuda.Stream(dev)
+    nb = B * 32
+    gathered = [torch.empty(G * nb, dtype=torch.uint8, device=dev) for _ in range(2)]
+    Qs = [np.ascontiguousarray(wl.queries(B)) for _ in range(8)]
+    got, want = [], []
+    for i, Q in enumerate(Qs):
+        j = i % 2
+        for g, r in enumerate(rings):
+            r.retrieve_local_async(Q, gathered[j][g * nb:(g + 1) * nb], cs.cuda_stream)
+        rings[0].merge_submit(gathered[j], G, B, 0, cs.cuda_stream, j)
+        if i >= 1:
+            got.append(rings[0].merge_wait((i - 1) % 2))
+            cs.synchronize()
+            want.append(rings[0].merge_records(gathered[(i - 1) % 2], G, B, 0, cs.cuda_stream))
+    got.append(rings[0].merge_wait((len(Qs) - 1) % 2))
+    want.append(rings[0].merge_records(gathered[(len(Qs) - 1) % 2], G, B, 0, cs.cuda_stream))
+    for i, (a, b) in enumerate(zip(got, want)):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y), i
+    # exact answers against a float64 scan of the whole (unsharded) cache
+    S = rows @ Qs[-1].T
+    live, sim, k, flags = got[-1]
+    for b in range(B):
+        best = S[:, b].max()
+        assert abs(sim[b] - best) <= 1e-12
+        assert live[b] == np.flatnonzero(S[:, b] == best).max()
+    with pytest.raises(_native.NativeError):
+        rings[0].merge_wait(0)  # nothing submitted into the slot
+    rings[0].merge_submit(gathered[0], G, B, 0, cs.cuda_stream, 0)
+    with pytest.raises(_native.NativeError):
+        rings[0].merge_submit(gathered[0], G, B, 0, cs.cuda_stream, 0)  # slot still holds a result
+    with pytest.raises(_native.NativeError):
+        rings[0].merge_submit(gathered[0], G, B, 0, cs.cuda_stream, 2)  # no such slot
+    rings[0].merge_wait(0)
+    for r in rings:
+        r.close()
+
+
+def test_deferred_shard_rescan_second_round():
+    """mc_retrieve_local_submit leaves a failed certificate to the caller: every row an exact
+    duplicate overflows the streamed scan's candidate queues on both shards, the merge reports
+    MC_FLAG_NEED_RESCAN, mc_rescan_local answers exhaustively in place and the second merge
+    returns the newest duplicate flagged as a tie and a fallback — the answer the rescan-included
+    mc_retrieve_local_async gives in one round."""
+    import torch
+
+    rng = np.random.default_rng(32)
+    d, n, G = 1024, 240_000, 2
+    v = rng.standard_normal(d)
+    v /= np.linalg.norm(v)
+    Q = np.stack([v] + [wl_noise(v[None, :], rng)[0] for _ in range(2)])
+    B = Q.shape[0]
+    rings = []
+    for g in range(G):
+        r = _native.DeviceRing(n // G, d, 0)
+        r.configure_shard(G, g)
+        block = np.repeat(v[None, :], 10_000, axis=0)
+        for _ in range(n // G // 10_000):
+            r.append(block)
+        r.set_table(*(lambda t: (t.pairs, t.total_steps))(ThresholdTable.default()))
+        rings.append(r)
+    nb = B * 32
+    dev = torch.device("cuda", 0)
+    gat = torch.empty(G * nb, dtype=torch.uint8, device=dev)
+    one = torch.empty(G * nb, dtype=torch.uint8, device=dev)
+    for g, r in enumerate(rings):
+        r.retrieve_local_submit(Q, gat[g * nb:(g + 1) * nb])
+        r.retrieve_local_async(Q, one[g * nb:(g + 1) * nb])
+    torch.cuda.synchronize()
+    live, sim, k, flags = rings[0].merge_records(gat, G, B, 0)
+    assert all(f & _native.MC_FLAG_NEED_RESCAN for f in flags), flags
+    for g, r in enumerate(rings):
+        r.rescan_local(Q, gat[g * nb:(g + 1) * nb])
+    torch.cuda.synchronize()
+    second = rings[0].merge_records(gat, G, B, 0)
+    first = rings[0].merge_records(one, G, B, 0)
+    for x, y in zip(second, first):
+        assert np.array_equal(x, y)
+    live, sim, k, flags = second
+    for b in range(B):
+        assert int(live[b]) == n - 1, (b, live[b])
+        assert abs(sim[b] - float(v @ Q[b])) <= 1e-12
+        assert flags[b] & _native.MC_FLAG_TIE and flags[b] & _native.MC_FLAG_FALLBACK, flags[b]
+        assert not flags[b] & _native.MC_FLAG_NEED_RESCAN
+    for r in rings:
+        r.close()

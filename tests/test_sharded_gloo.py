@@ -77,6 +77,11 @@ def _worker(rank, world, port, errq):
         sizes = [None] * world
         dist.all_gather_object(sizes, len(sc.ring))
         assert sum(sizes) == len(sc), (sizes, len(sc))
+        # degraded records (a failed certificate on some shard) went through the second round:
+        # every rank rescanned and re-gathered together, and the answers above stayed exact
+        rescans = [None] * world
+        dist.all_gather_object(rescans, getattr(sc.ring, "rescans", 0))
+        assert sum(rescans) > 0, rescans
         dist.destroy_process_group()
     except BaseException as exc:  # pragma: no cover - reported to the parent
         import traceback
