@@ -143,6 +143,7 @@ struct mc_cache {
   double* d_gq64 = nullptr;     // [Dp] the kernel's L2 relay of the pending row
   unsigned* d_sync = nullptr;   // [2] streamed-scan launch overlap: rows published / records read (epochs)
   bool tc_tail = false;         // the last kernel enqueued on the stream is the tensor path's merge (PDL-early)
+  bool local_param = true;      // local lookups of one query carry it in the launch (MC_LOCAL_PARAM=0: envelope)
   bool s8_isolated = false;     // the streamed scan being enqueued cannot overlap a neighbour (local lookups)
   long long s8_wide_rows = 1LL << 17;  // isolated launches over windows this large take the wide grid
                                        // (MC_S8_WIDE_ROWS)
@@ -997,6 +998,7 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   }
   if (const char* e = getenv("MC_PARAM_INPUT")) h->param_in = atoi(e) != 0;
   if (const char* e = getenv("MC_S8_WIDE_ROWS")) h->s8_wide_rows = atoll(e);
+  if (const char* e = getenv("MC_LOCAL_PARAM")) h->local_param = atoi(e) != 0;
   CUC(cudaHostAlloc(&h->h_qkeep, (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
   memset(h->h_qkeep, 0, (size_t)h->Dp * sizeof(double));
   for (int k = 0; k < 2; ++k) {  // mapped: the parameter-block launches read the query from here
@@ -1312,10 +1314,26 @@ int local_lookup(mc_cache* h, const double* queries, int32_t B, void* dev_record
     int rc = flush(h);
     if (rc) return rc;
     CU(cudaMemsetAsync(rec, 0xff, (size_t)B * sizeof(mc_record), h->stream));  // pos = -1 (NaN sims)
+  } else if (!exact && h->local_param && B == 1 && h->n_pending == 0 && h->s8 && h->Dp <= 1024 &&
+             h->path != MC_PATH_GEMV && !use_gemm(h, 1)) {
+    // One query, no rows to append: the query and its quantisation ride in the launch's parameter
+    // block (no host->device copy between consecutive local scans), and the scan may start while
+    // the previous local scan on this ring still merges (the streamed scan's launch overlap).
+    take_pending(h, nullptr);  // evictions only: the kernel publishes the window to d_state
+    const unsigned ep = s8_epoch(h);
+    const cudaError_t e = launch_stream8_direct(h->s8, rbufs(h), mirror(h), h->D, queries, nullptr, h->d_cta,
+                                                s8_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax8, ep, h->thr,
+                                                rec, nullptr, h->d_state, nullptr, 0, nullptr, quantize_query,
+                                                h->d_gq64, h->d_sync, s8_rec_par(h), !h->tc_tail, h->stream);
+    if (e != cudaSuccess) return s8_launch_failed(h, ep, e);
+    h->tc_tail = false;
+    h->stats[5]++;
+    h->stats[7]++;
   } else {
     const double* q = nullptr;
-    // with the exact rescan behind it on the stream, the scan cannot overlap a neighbour
-    h->s8_isolated = true;  // local lookups are stream-ordered behind the previous one's exchange
+    // an envelope copy (and, with `exact`, the rescan) sits between consecutive local scans:
+    // no launch overlap, so a large window takes the wide grid
+    h->s8_isolated = true;
     int rc = lookup_enqueue(h, queries, B, rec, nullptr, true, &q);
     h->s8_isolated = false;
     if (rc) return rc;

@@ -1264,3 +1264,51 @@ def test_deferred_shard_rescan_second_round():
         assert not flags[b] & _native.MC_FLAG_NEED_RESCAN
     for r in rings:
         r.close()
+
+
+def test_single_query_local_submit_matches_local_async():
+    """mc_retrieve_local_submit of one query with no pending rows carries it in the launch's
+    parameter block (consecutive scans may overlap): the same records as the envelope-fed,
+    rescan-included mc_retrieve_local_async, through evict-only window changes and a pending
+    append (which takes the envelope path), over 40 lookups in flight two at a time."""
+    import torch
+
+    G = 2
+    wl = ClusteredWorkload(768, n_clusters=48, seed=404)
+    rows = wl.cache_rows(20_000)
+    rings = []
+    for g in range(G):
+        r = _native.DeviceRing(10_000, 768, 0)
+        r.configure_shard(G, g)
+        r.append(rows[g::G])
+        t = ThresholdTable.default()
+        r.set_table(t.pairs, t.total_steps)
+        rings.append(r)
+    dev = torch.device("cuda", 0)
+    cs = torch.cuda.Stream(dev)
+    nb = 32
+    bufs = [torch.empty(G * nb, dtype=torch.uint8, device=dev) for _ in range(2)]
+    ref = torch.empty(G * nb, dtype=torch.uint8, device=dev)
+    p0 = 0
+    Q = wl.queries(40)
+    for i, q in enumerate(Q):
+        if i % 10 == 5:  # evict-only change: 10 oldest global positions (5 per shard)
+            for r in rings:
+                r.evict_front(5)
+            p0 += 10
+        if i == 33:  # one pending row on shard 0 (the envelope path folds it in)
+            extra = wl.cache_rows(1)
+            rings[0].append(extra)
+        j = i % 2
+        for g, r in enumerate(rings):
+            r.retrieve_local_submit(q[None, :], bufs[j][g * nb:(g + 1) * nb], cs.cuda_stream)
+        cs.synchronize()
+        for g, r in enumerate(rings):
+            r.retrieve_local_async(q[None, :], ref[g * nb:(g + 1) * nb], cs.cuda_stream)
+        got = rings[0].merge_records(bufs[j], G, 1, p0, cs.cuda_stream)
+        want = rings[0].merge_records(ref, G, 1, p0, cs.cuda_stream)
+        assert not got[3][0] & _native.MC_FLAG_NEED_RESCAN, i
+        for x, y in zip(got, want):
+            assert np.array_equal(x, y), (i, got, want)
+    for r in rings:
+        r.close()
