@@ -144,6 +144,9 @@ struct mc_cache {
   unsigned* d_sync = nullptr;   // [2] streamed-scan launch overlap: rows published / records read (epochs)
   bool tc_tail = false;         // the last kernel enqueued on the stream is the tensor path's merge (PDL-early)
   bool local_param = true;      // local lookups of one query carry it in the launch (MC_LOCAL_PARAM=0: envelope)
+  long long s8_rows_per_cta = 128;  // streamed-scan grid = ceil(rows / this), at most the full grid: windows
+                                    // under 19k rows merge fewer CTA records (C1 back-to-back 10.5 -> 8.7 us,
+                                    // profiles/r02_s8_rows_ab.txt); MC_S8_ROWS_PER_CTA, 0 = always the full grid
   bool s8_isolated = false;     // the streamed scan being enqueued cannot overlap a neighbour (local lookups)
   long long s8_wide_rows = 1LL << 17;  // isolated launches over windows this large take the wide grid
                                        // (MC_S8_WIDE_ROWS)
@@ -270,7 +273,10 @@ int s8_grid_max(const mc_cache* h) { return std::max(s8_grid(h->sm_count), s8_gr
 // isolated lookup (h->s8_isolated) over a window of at least s8_wide_rows rows.
 int s8_launch_grid(const mc_cache* h) {
   if (h->s8_isolated && h->count >= h->s8_wide_rows) return std::min(320, s8_grid_wide(h->sm_count));
-  return s8_grid(h->sm_count);
+  const int g = s8_grid(h->sm_count);
+  if (h->s8_rows_per_cta > 0)  // small windows: fewer CTAs, so fewer records to merge
+    return (int)std::max(1LL, std::min((long long)g, (h->count + h->s8_rows_per_cta - 1) / h->s8_rows_per_cta));
+  return g;
 }
 
 // Per-CTA records: the GEMV scans' CtaRec per CTA, or the streamed scan's two 16-byte words per
@@ -641,7 +647,7 @@ int enqueue_direct(mc_cache* h, const double* queries, int B, unsigned seq, bool
     memset(h->h_outp + 2 * slot, 0, 2 * sizeof(uint4));
     *q = nullptr;
     const unsigned ep = s8_epoch(h);
-    const cudaError_t e = launch_stream8_direct(h->s8, rbufs(h), st, h->D, hq, stage_row, h->d_cta, s8_grid(h->sm_count),
+    const cudaError_t e = launch_stream8_direct(h->s8, rbufs(h), st, h->D, hq, stage_row, h->d_cta, s8_launch_grid(h),
                                                 h->shard, h->d_counter, h->d_gmax8, ep, h->thr, h->d_rec + slot,
                                                 nullptr, h->d_state, nullptr, seq_tag(seq), h->d_outp + 2 * slot,
                                                 quantize_query, h->d_gq64, h->d_sync, s8_rec_par(h), !h->tc_tail,
@@ -999,6 +1005,7 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   if (const char* e = getenv("MC_PARAM_INPUT")) h->param_in = atoi(e) != 0;
   if (const char* e = getenv("MC_S8_WIDE_ROWS")) h->s8_wide_rows = atoll(e);
   if (const char* e = getenv("MC_LOCAL_PARAM")) h->local_param = atoi(e) != 0;
+  if (const char* e = getenv("MC_S8_ROWS_PER_CTA")) h->s8_rows_per_cta = atoll(e);
   CUC(cudaHostAlloc(&h->h_qkeep, (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
   memset(h->h_qkeep, 0, (size_t)h->Dp * sizeof(double));
   for (int k = 0; k < 2; ++k) {  // mapped: the parameter-block launches read the query from here
@@ -1322,7 +1329,7 @@ int local_lookup(mc_cache* h, const double* queries, int32_t B, void* dev_record
     take_pending(h, nullptr);  // evictions only: the kernel publishes the window to d_state
     const unsigned ep = s8_epoch(h);
     const cudaError_t e = launch_stream8_direct(h->s8, rbufs(h), mirror(h), h->D, queries, nullptr, h->d_cta,
-                                                s8_grid(h->sm_count), h->shard, h->d_counter, h->d_gmax8, ep, h->thr,
+                                                s8_launch_grid(h), h->shard, h->d_counter, h->d_gmax8, ep, h->thr,
                                                 rec, nullptr, h->d_state, nullptr, 0, nullptr, quantize_query,
                                                 h->d_gq64, h->d_sync, s8_rec_par(h), !h->tc_tail, h->stream);
     if (e != cudaSuccess) return s8_launch_failed(h, ep, e);
