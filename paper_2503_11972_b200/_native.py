@@ -276,6 +276,24 @@ class DeviceRing:
                 _check(self.lib, rc)
             return int(self._ticket[0])
 
+    def submit(self, Q: np.ndarray) -> int:
+        """Enqueue a batch of lookups (mc_retrieve_submit) and return its ticket at once; a
+        registered query array must stay untouched until wait()."""
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        with self._lock:
+            _check(self.lib, self._submit(self._hv, _ptr(Q), Q.shape[0], self._ticket_ptr))
+            return int(self._ticket[0])
+
+    def wait(self, ticket: int, B: int):
+        """(live, sim, k, flags) arrays of the submitted batch (mc_retrieve_wait)."""
+        live = np.empty(B, dtype=np.int64)
+        sim = np.empty(B, dtype=np.float64)
+        k = np.empty(B, dtype=np.int32)
+        flags = np.empty(B, dtype=np.uint32)
+        with self._lock:
+            _check(self.lib, self._wait(self._hv, ticket, _ptr(live), _ptr(sim), _ptr(k), _ptr(flags)))
+        return live, sim, k, flags
+
     def wait1(self, ticket: int):
         """The submitted lookup's (live, sim, k, flags) as Python scalars (mc_retrieve_wait)."""
         with self._lock:

@@ -121,6 +121,22 @@ struct mc_cache {
   const double* inflight_q = nullptr;
   bool inflight_ready = false;  // completed (and any fallback applied) while staging appends
   bool inflight_direct = false; // its result comes back zero-copy
+  bool inflight_async = false;  // a batch whose decisions come back by an async D2H copy (batch_ev)
+  cudaEvent_t batch_ev = nullptr;
+  // A submitted batch answered when the next lookup was submitted (its decisions kept here until
+  // its mc_retrieve_wait): batches pipeline one deep, the next one's upload and scan overlap the
+  // caller's work on this one's answers.
+  std::vector<OutRec> old_batch;
+  // Query prefetch for pipelined batches: a batch submitted while the previous one runs has its
+  // queries DMA'd from the caller's registered array into a query slot on a copy stream first,
+  // so the copy overlaps the previous batch's scan.
+  cudaStream_t cstream = nullptr;
+  double* d_qslot[2] = {nullptr, nullptr};
+  cudaEvent_t q_ev[2] = {nullptr, nullptr};
+  int qslot_cap = 0;        // rows per query slot
+  int qslot_next = 0;       // slot the next prefetch fills
+  const double* pf_src = nullptr;  // caller rows the prefetched slot holds (nullptr: none)
+  int pf_B = 0, pf_slot = 0;
   int inflight_slot = 0;        // its result slot: h_outp + 2 slot, d_rec + slot (single-query lookups)
   RingState inflight_st{};      // the window it scans
   // Pipelined single-query lookups: a second mc_retrieve_submit while one is in flight moves
@@ -419,6 +435,21 @@ int upload_envelope(mc_cache* h, const double* queries, int B, bool async_reuse,
   // host copy (the unquantised large-batch paths only; the int8 paths take B <= 4).
   constexpr size_t CHUNK_BYTES = 256 << 10;
   const int chunk = std::max<int>(1, (int)(CHUNK_BYTES / row));
+  const bool prefetched = !quantise && h->pf_src == queries && h->pf_B == B;
+  h->pf_src = nullptr;  // a prefetch serves only the upload right after it
+  if (prefetched) {  // the batch was DMA'd into a query slot on the copy stream
+    const size_t head = (size_t)h->n_pending * row;
+    if (head) CU(cudaMemcpyAsync(h->d_env, h->h_env, head, cudaMemcpyHostToDevice, h->stream));
+    if (async_reuse && head) {
+      CU(cudaEventRecord(h->env_ev, h->stream));
+      h->env_inflight = true;
+    }
+    CU(cudaStreamWaitEvent(h->stream, h->q_ev[h->pf_slot], 0));
+    *q_dev = h->d_qslot[h->pf_slot];
+    *prep_dev = nullptr;
+    *q8_dev = nullptr;
+    return MC_OK;
+  }
   if (!quantise && B > 2 * chunk && h->D == h->Dp && host_registered(queries, (size_t)B * row)) {
     // registered caller memory: one DMA of the batch, no host staging copy
     const double t1 = g_ht.on ? now_us() : 0.0;
@@ -718,7 +749,14 @@ int finish_inflight(mc_cache* h) {
   if (rc0) return rc0;
   if (!h->inflight_seq || h->inflight_ready) return MC_OK;
   const int B = h->inflight_B;
-  int rc = h->inflight_direct ? wait_direct(h, h->inflight_seq, B, h->inflight_slot) : wait_seq(h, h->inflight_seq);
+  int rc = MC_OK;
+  if (h->inflight_direct)
+    rc = wait_direct(h, h->inflight_seq, B, h->inflight_slot);
+  else if (h->inflight_async) {
+    CU(cudaEventSynchronize(h->batch_ev));
+    h->inflight_async = false;
+  } else
+    rc = wait_seq(h, h->inflight_seq);
   if (rc) return rc;
   bool need = false;
   for (int b = 0; b < B; ++b) need |= (h->h_out[b].flags & FLAG_NEED_ANY) != 0;
@@ -972,6 +1010,7 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   CUC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   CUC(cudaEventCreateWithFlags(&h->env_ev, cudaEventDisableTiming));
   CUC(cudaEventCreateWithFlags(&h->rec_ev, cudaEventDisableTiming));
+  CUC(cudaEventCreateWithFlags(&h->batch_ev, cudaEventDisableTiming));
   const size_t n16 = (size_t)h->Cp * h->Dp * sizeof(__half);
   const size_t n64 = (size_t)h->Cp * h->Dp * sizeof(double);
   const size_t n8 = (size_t)h->Cp * h->P8;
@@ -1079,6 +1118,12 @@ int mc_destroy(mc_cache* h) {
     }
     if (h->env_ev) cudaEventDestroy(h->env_ev);
     if (h->rec_ev) cudaEventDestroy(h->rec_ev);
+    if (h->batch_ev) cudaEventDestroy(h->batch_ev);
+    for (int i = 0; i < 2; ++i) {
+      cudaFree(h->d_qslot[i]);
+      if (h->q_ev[i]) cudaEventDestroy(h->q_ev[i]);
+    }
+    if (h->cstream) cudaStreamDestroy(h->cstream);
     if (h->stream) cudaStreamDestroy(h->stream);
   }
   delete h;
@@ -1204,6 +1249,40 @@ int mc_set_sigma_schedule(mc_cache* h, const double* schedule, int32_t n) {
   return MC_OK;
 }
 
+// Start the DMA of a batch's queries (registered caller memory, tensor-core path) into a query
+// slot on the copy stream, before the previous batch is waited for.  The slot alternates: the
+// other one may still be read by the batch in flight; this one was last read by a batch that has
+// completed (batches pipeline one deep).
+int prefetch_queries(mc_cache* h, const double* queries, int B) {
+  h->pf_src = nullptr;
+  const size_t row = (size_t)h->Dp * sizeof(double);
+  if (h->D != h->Dp || !use_gemm(h, B) || !host_registered(queries, (size_t)B * row)) return MC_OK;
+  if (!h->cstream) {
+    CU(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) CU(cudaEventCreateWithFlags(&h->q_ev[i], cudaEventDisableTiming));
+  }
+  if (B > h->qslot_cap) {
+    CU(cudaStreamSynchronize(h->stream));
+    CU(cudaStreamSynchronize(h->cstream));
+    int cap = 64;
+    while (cap < B) cap <<= 1;
+    for (int i = 0; i < 2; ++i) {
+      cudaFree(h->d_qslot[i]);
+      h->d_qslot[i] = nullptr;
+      CU(cudaMalloc(&h->d_qslot[i], (size_t)cap * row));
+    }
+    h->qslot_cap = cap;
+  }
+  const int s = h->qslot_next;
+  h->qslot_next ^= 1;
+  CU(cudaMemcpyAsync(h->d_qslot[s], queries, (size_t)B * row, cudaMemcpyHostToDevice, h->cstream));
+  CU(cudaEventRecord(h->q_ev[s], h->cstream));
+  h->pf_src = queries;
+  h->pf_B = B;
+  h->pf_slot = s;
+  return MC_OK;
+}
+
 int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* out_ticket) {
   if (!h || !out_ticket || (!queries && B > 0)) return fail(MC_ERR_ARG, "NULL argument");
   if (B < 1) return fail(MC_ERR_ARG, "batch must be positive");
@@ -1213,6 +1292,20 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
   // is still in flight (its answer is collected later by its own mc_retrieve_wait).
   const bool pipe = B == 1 && h->count > 0 && h->packed && direct_result(h, 1) && h->n_pending <= PIPE_SLACK;
   if (h->inflight_seq && h->old_seq) return fail(MC_ERR_STATE, "two lookups are in flight: mc_retrieve_wait first");
+  if (h->inflight_seq && h->inflight_B != 1) {  // a batch: answer it now, keep it for its wait
+    if (B > 1 && h->count > 0) {  // this batch's queries start moving while that one still scans
+      int rc = prefetch_queries(h, queries, B);
+      if (rc) return rc;
+    }
+    int rc = finish_inflight(h);
+    if (rc) return rc;
+    h->old_batch.assign(h->h_out, h->h_out + h->inflight_B);
+    h->old_slot = 1;  // a single-query lookup submitted next takes slot 0
+    h->old_seq = h->inflight_seq;
+    h->old_ready = true;
+    h->inflight_seq = 0;
+    h->inflight_ready = false;
+  }
   if (h->inflight_seq) {
     if (h->inflight_B != 1) return fail(MC_ERR_STATE, "an asynchronous lookup is already in flight");
     if (!pipe || !h->inflight_direct) {  // cannot run beside it: answer it now (kept for its wait)
@@ -1240,7 +1333,8 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
   const unsigned seq = ++h->seq;
   h->inflight_B = B;
   h->inflight_q = nullptr;
-  h->inflight_slot = h->old_seq ? 1 - h->old_slot : 0;
+  // a batch (B > 1) runs only beside an older lookup that is already answered: slot 0 is free
+  h->inflight_slot = h->old_seq && B == 1 ? 1 - h->old_slot : 0;
   h->inflight_st = mirror(h);
   if (h->count == 0) {  // cache.py:252-253: answered now
     for (int b = 0; b < B; ++b) h->h_out[b] = empty_out(h);
@@ -1256,6 +1350,18 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
     h->inflight_q = q;
     h->inflight_ready = false;
     h->inflight_direct = true;
+  } else if (B > 1) {  // batches: the decisions come back by an async copy; mc_retrieve_wait (or the
+                      // next submit) waits for it.  The caller's query array must stay untouched until
+                      // then when it is a registered buffer (the batch is DMA'd straight from it).
+    const double* q = nullptr;
+    rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_out, true, &q);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaEventRecord(h->batch_ev, h->stream));
+    h->inflight_q = q;
+    h->inflight_ready = false;
+    h->inflight_direct = false;
+    h->inflight_async = true;
   } else {  // paths without a zero-copy result complete synchronously
     const double* q = nullptr;
     rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_out, false, &q);
@@ -1279,6 +1385,26 @@ int mc_retrieve_wait(mc_cache* h, uint32_t ticket, int64_t* out_live, double* ou
   if (!h) return fail(MC_ERR_ARG, "NULL handle");
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard guard(h->dev);
+  if (ticket && ticket == h->old_seq && !h->old_batch.empty()) {  // a batch answered at the next submit
+    const OutRec* src = h->old_batch.data();
+    const int B = (int)h->old_batch.size();
+    for (int b = 0; b < B; ++b) {
+      const OutRec& o = src[b];
+      if (out_live) out_live[b] = o.live;
+      if (out_sim) out_sim[b] = o.sim;
+      if (out_k) out_k[b] = o.k;
+      const unsigned f = o.flags & 0xffffu;
+      if (out_flags) out_flags[b] = f;
+      if (f & MC_FLAG_FALLBACK) h->stats[1]++;
+      if (f & MC_FLAG_NONFINITE) h->stats[2]++;
+      if (f & MC_FLAG_TIE) h->stats[3]++;
+    }
+    h->stats[0] += B;
+    h->old_batch.clear();
+    h->old_seq = 0;
+    h->old_ready = false;
+    return MC_OK;
+  }
   if (ticket && ticket == h->old_seq) {
     int rc = finish_old(h);
     if (rc) return rc;

@@ -174,3 +174,38 @@ def test_fast_result_objects_equal_dataclass_ones():
         assert (a.entry, a.similarity, a.k) == (b.entry, b.similarity, b.k)
         with pytest.raises(dataclasses.FrozenInstanceError):
             a.k = 1
+
+
+def test_async_batches_resolve_against_their_submit_state():
+    """retrieve_batch_async pipelined one deep (batch i+1 submitted before batch i is read), with
+    inserts and capacity evictions between: every RetrievalBatch equals retrieve_batch() at its
+    submit time, entries by identity; a dropped future is completed by the next lookup."""
+    from paper_2503_11972_b200 import ThresholdTable
+
+    rng = np.random.default_rng(29)
+    d, cap = 8, 40
+    a, b = SemanticCache(cap, d), SemanticCache(cap, d)
+    table = ThresholdTable.default()
+    ents = _entries(rng, 400, d)
+    for e in ents[:cap]:
+        a.insert(e)
+        b.insert(e)
+    prev = None
+    for i, e in enumerate(ents[cap:]):
+        Q = np.stack([normalize(ents[cap + i - j].embedding + 0.3 * rng.standard_normal(d)) for j in (1, 5, 9)])
+        want = a.retrieve_batch(Q, table)
+        a.insert(e)
+        pend = b.retrieve_batch_async(Q, table)
+        b.insert(e)
+        if prev is not None:
+            got, exp = prev[0].result(), prev[1]
+            assert list(got) == list(exp), i
+            assert all(x.entry is y.entry for x, y in zip(got, exp))
+            assert np.array_equal(got.similarity, exp.similarity) and np.array_equal(got.k, exp.k)
+        prev = (pend, want)
+        if i % 50 == 49:  # dropped future: the next lookup completes it
+            b.retrieve_batch_async(Q, table)
+            want2 = a.retrieve_batch(Q, table)
+            assert list(b.retrieve_batch(Q, table)) == list(want2)
+            prev = None
+    assert _state(a) == _state(b)

@@ -1312,3 +1312,50 @@ def test_single_query_local_submit_matches_local_async():
             assert np.array_equal(x, y), (i, got, want)
     for r in rings:
         r.close()
+
+
+@pytest.mark.parametrize("registered", [False, True])
+def test_pipelined_batches_match_the_oracle(registered):
+    """retrieve_batch_async one deep on the tensor-core path (batch i+1 uploaded and scanned
+    while the host reads batch i), with an insert and capacity evictions between batches and
+    exact duplicates (ties, exhaustive fallbacks answered when the next batch is submitted):
+    every answer equals the float64 oracle cache's at submit time."""
+    rng = np.random.default_rng(808)
+    wl = ClusteredWorkload(1024, n_clusters=64, seed=808)
+    cap, B = 6000, 64
+    rows = wl.cache_rows(cap)
+    rows[100:140] = rows[99]  # 41 exact duplicates
+    c = SemanticCache(capacity=cap, dim=1024)
+    o = OracleCache(cap, 1024)
+    for i, r in enumerate(rows):
+        c.insert(CacheEntry(f"e{i}", r, "large", i, float(i)))
+        o.insert(OracleEntry(f"e{i}", r, "large", i, float(i)))
+    table, ot = ThresholdTable.default(), OracleTable()
+    n_b = 24
+    Qall = np.ascontiguousarray(wl.queries(n_b * B).reshape(n_b, B, 1024))
+    Qall[:, 0] = rows[99]  # every batch asks for the duplicated row
+    if registered:
+        c.register_host_buffer(Qall)
+    new = wl.cache_rows(n_b)
+    prev = None
+    checked = 0
+    for i in range(n_b):
+        want = [o.retrieve_entry(q, ot) for q in Qall[i]]
+        pend = c.retrieve_batch_async(Qall[i], table)
+        c.insert(CacheEntry(f"n{i}", new[i], "large", cap + i, float(cap + i)))
+        o.insert(OracleEntry(f"n{i}", new[i], "large", cap + i, float(cap + i)))
+        if prev is not None:
+            got, exp = prev[0].result(), prev[1]
+            for r, (e, sim, k) in zip(got, exp):
+                assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), i
+                assert r.k == k and _close(r.similarity, sim), (i, r, sim)
+                checked += 1
+            assert got[0].entry.id == "e139"  # the newest duplicate
+        prev = (pend, want)
+    got = prev[0].result()
+    for r, (e, sim, k) in zip(got, prev[1]):
+        assert (r.entry.id if r.hit else None) == (e.id if e is not None else None)
+    if registered:
+        c.unregister_host_buffer(Qall)
+    assert checked == (n_b - 1) * B
+    c.close()
