@@ -463,7 +463,13 @@ def run_sharded_c4(dist, n_total, B, steps, warmup, device=0):
     wl.fill(ring, n_local, row0=g * n_local)
     table = ThresholdTable.default()
     ring.set_table(table.pairs, table.total_steps)
-    Q = wl.queries((warmup + steps) * B).reshape(warmup + steps, B, dim)  # the same on every rank
+    # the same trace on every rank: temporal locality (a drifting window of active clusters)
+    Q = np.ascontiguousarray(wl.trace_queries((warmup + steps) * B).reshape(warmup + steps, B, dim))
+    # batch 1: every request also stores its generated image (FIFO insert, evicting the oldest
+    # entry of the full cache); global position n_total + i lands on shard (n_total + i) % G only
+    inserts = B == 1
+    new_rows = wl.images(Q[:, 0]) if inserts else None
+    n_ins = 0  # inserts so far = the oldest live global position (the cache is full)
     if B > 4:  # batches DMA'd straight from the page-locked query array (no staging copy)
         _native.register_host(Q)
     nb = B * 32
@@ -485,12 +491,23 @@ def run_sharded_c4(dist, n_total, B, steps, warmup, device=0):
     csp = cs.cuda_stream
     gptr = [t.data_ptr() for t in gathered]  # raw pointers: no per-step tensor attribute lookups
 
+    p0s = [0] * NS  # oldest live global position at each in-flight lookup's submit
+
     def submit(i):
+        nonlocal n_ins
         j = i % NS
+        p0 = p0s[j] = n_ins
         if G == 1 and not split:  # no collective: the ring's own calls order themselves after csp
             ring.retrieve_local_submit(Q[i], gptr[j], csp)
-            ring.merge_submit(gptr[j], G, B, 0, csp, j)
-            return
+            ring.merge_submit(gptr[j], G, B, p0, csp, j)
+        else:
+            submit_collective(i, j, p0)
+        if inserts:  # this request's image, appended after its lookup was enqueued
+            if (n_total + n_ins) % G == g:
+                ring.append1(new_rows[i])
+            n_ins += 1
+
+    def submit_collective(i, j, p0):
         with torch.cuda.stream(cs):
             if split:
                 local_q[j].copy_(Qt[i, g * part:(g + 1) * part].reshape(-1), non_blocking=True)
@@ -502,7 +519,7 @@ def run_sharded_c4(dist, n_total, B, steps, warmup, device=0):
                 dist.td.all_gather_into_tensor(gathered[j], local[j])
             else:
                 ring.retrieve_local_submit(Q[i], gathered[j], cs.cuda_stream)
-        ring.merge_submit(gathered[j], G, B, 0, cs.cuda_stream, j)
+        ring.merge_submit(gathered[j], G, B, p0, cs.cuda_stream, j)
 
     def collect(i):
         nonlocal hits, rescans
@@ -515,7 +532,7 @@ def run_sharded_c4(dist, n_total, B, steps, warmup, device=0):
                 ring.rescan_local(Q[i], own, cs.cuda_stream)
                 if G > 1:
                     dist.td.all_gather_into_tensor(gathered[j], local[j])
-            ring.merge_submit(gathered[j], G, B, 0, cs.cuda_stream, j)
+            ring.merge_submit(gathered[j], G, B, p0s[j], cs.cuda_stream, j)
             live, sim, k, flags = ring.merge_wait(j)
         hits += int((flags & _native.MC_FLAG_HIT).astype(bool).sum())
 
@@ -550,6 +567,10 @@ def run_sharded_c4(dist, n_total, B, steps, warmup, device=0):
             "query_upload": ("1/G of the batch per rank + NCCL all-gather of the queries" if split
                              else "the whole batch from the host on every rank"),
             "second_rounds": rescans,
+            "trace": ("temporal locality: each request's cluster drawn from a window of 64 active clusters that "
+                      "advances one cluster every 256 requests (workload.py:93-121's lifetimes, vectorised)"
+                      + ("; every request also inserts its generated image (FIFO, evicting the oldest of the full "
+                         "cache) on the owning shard" if inserts else "")),
             "pipelining": f"{NS} lookups in flight (step i+1 enqueued before step i's decisions are read)",
             "timing": "CUDA events on the step stream around the timed steps (the host's enqueue and read-back "
                       "of every step inside; the last step's decisions read before the end event is waited on), "

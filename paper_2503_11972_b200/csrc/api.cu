@@ -159,6 +159,15 @@ struct mc_cache {
   double* d_gq64 = nullptr;     // [Dp] the kernel's L2 relay of the pending row
   unsigned* d_sync = nullptr;   // [2] streamed-scan launch overlap: rows published / records read (epochs)
   bool tc_tail = false;         // the last kernel enqueued on the stream is the tensor path's merge (PDL-early)
+  // The windows the last local lookups scanned, by record buffer: mc_rescan_local runs against the
+  // window its records came from, while at most PIPE_SLACK rows have been appended since (the
+  // spare physical slots keep those rows intact), whatever later lookups applied meanwhile.
+  struct LocalWin {
+    const void* rec = nullptr;
+    RingState st{};
+    long long appended = 0;
+  } local_win[4];
+  int local_win_next = 0;
   bool local_param = true;      // local lookups of one query carry it in the launch (MC_LOCAL_PARAM=0: envelope)
   long long s8_rows_per_cta = 128;  // streamed-scan grid = ceil(rows / this), at most the full grid: windows
                                     // under 19k rows merge fewer CTA records (C1 back-to-back 10.5 -> 8.7 us,
@@ -1431,6 +1440,14 @@ namespace {
 // still asks for the exhaustive rescan (mc_retrieve_local_submit records).
 uint32_t public_flags(unsigned f) { return (f & 0xffffu) | ((f & FLAG_NEED_ANY) ? MC_FLAG_NEED_RESCAN : 0u); }
 
+void remember_window(mc_cache* h, const void* rec) {
+  mc_cache::LocalWin& w = h->local_win[h->local_win_next];
+  h->local_win_next = (h->local_win_next + 1) % 4;
+  w.rec = rec;
+  w.st = mirror(h);  // pending rows were folded into this lookup: the window it scanned
+  w.appended = h->appended;
+}
+
 // A shard's certified local records for B host queries.  exact: the exhaustive rescan of
 // records whose certificate failed follows on the stream (always launched; it skips unflagged
 // queries).  Otherwise such records keep their FLAG_NEED_* bits, the merge reports
@@ -1462,6 +1479,7 @@ int local_lookup(mc_cache* h, const double* queries, int32_t B, void* dev_record
     h->tc_tail = false;
     h->stats[5]++;
     h->stats[7]++;
+    remember_window(h, dev_records);
   } else {
     const double* q = nullptr;
     // an envelope copy (and, with `exact`, the rescan) sits between consecutive local scans:
@@ -1470,6 +1488,7 @@ int local_lookup(mc_cache* h, const double* queries, int32_t B, void* dev_record
     int rc = lookup_enqueue(h, queries, B, rec, nullptr, true, &q);
     h->s8_isolated = false;
     if (rc) return rc;
+    remember_window(h, dev_records);
     if (exact) {
       CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, q, B, rec, h->d_scratch,
                              exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
@@ -1504,15 +1523,25 @@ int mc_rescan_local(mc_cache* h, const double* queries, int32_t B, void* dev_rec
     CU(cudaEventRecord(h->rec_ev, (cudaStream_t)stream));
     CU(cudaStreamWaitEvent(h->stream, h->rec_ev, 0));
   }
-  if (h->count > 0) {
+  const mc_cache::LocalWin* win = nullptr;
+  for (int i = 1; i <= 4 && !win; ++i) {  // the most recent lookup into these records
+    const mc_cache::LocalWin& w = h->local_win[(h->local_win_next - i + 4) % 4];
+    if (w.rec == dev_records) win = &w;
+  }
+  if (!win) return fail(MC_ERR_STATE, "no recent local lookup wrote these records");
+  if (h->appended - win->appended > PIPE_SLACK)
+    return fail(MC_ERR_STATE, "%lld rows were appended since the lookup (at most %lld keep its window intact)",
+                h->appended - win->appended, PIPE_SLACK);
+  if (win->st.count > 0) {
     const double* q = nullptr;
     const QPrep* prep = nullptr;
     const int8_t* q8 = nullptr;
-    // queries only: pending appends / evictions are not applied (the rescan must see the
-    // window the scan saw; the device ring state changes only when a lookup or flush applies them)
+    // queries only; pending appends / evictions are not applied here
     rc = upload_envelope(h, queries, B, true, false, &q, &prep, &q8);
     if (rc) return rc;
-    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state, h->D, h->Dp, q, B,
+    const RingState st = win->st;  // the window the lookup scanned (later lookups may have moved d_state)
+    CU(cudaMemcpyAsync(h->d_state_fb, &st, sizeof st, cudaMemcpyHostToDevice, h->stream));
+    CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state_fb, h->D, h->Dp, q, B,
                            static_cast<mc_record*>(dev_records), h->d_scratch, exact_grid(h->sm_count),
                            gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
     h->stats[7] += 2;

@@ -94,3 +94,15 @@ class GeneratedWorkload:
     def queries(self, n: int) -> np.ndarray:
         idx = self.rng.integers(0, len(self.centers), n)
         return _unit_rows(self.centers[idx] + self.spread * self.rng.standard_normal((n, self.dim)))
+
+    def trace_queries(self, n: int, active: int = 64, turnover: int = 256) -> np.ndarray:
+        """Queries with temporal locality, the reference's cluster lifetimes vectorised
+        (workload.py:93-121): request i draws its cluster from a window of `active` clusters that
+        advances by one cluster every `turnover` requests, so popular prompts recur for a while
+        and then fade."""
+        idx = (np.arange(n) // turnover + self.rng.integers(0, active, n)) % len(self.centers)
+        return _unit_rows(self.centers[idx] + self.spread * self.rng.standard_normal((n, self.dim)))
+
+    def images(self, q: np.ndarray) -> np.ndarray:
+        """Generated-image embeddings for queries q (workload.py:141-154's model)."""
+        return _unit_rows(self.beta * q + (1.0 - self.beta) * self.rng.standard_normal(q.shape))

@@ -1249,6 +1249,12 @@ def test_deferred_shard_rescan_second_round():
     torch.cuda.synchronize()
     live, sim, k, flags = rings[0].merge_records(gat, G, B, 0)
     assert all(f & _native.MC_FLAG_NEED_RESCAN for f in flags), flags
+    # later lookups apply new rows (fewer than PIPE_SLACK per shard): the rescan still answers on
+    # the window the first lookup scanned, kept intact by the ring's spare slots
+    later = torch.empty(G * nb, dtype=torch.uint8, device=dev)
+    for g, r in enumerate(rings):
+        r.append(np.repeat(v[None, :], 3, axis=0))
+        r.retrieve_local_submit(Q, later[g * nb:(g + 1) * nb])
     for g, r in enumerate(rings):
         r.rescan_local(Q, gat[g * nb:(g + 1) * nb])
     torch.cuda.synchronize()
@@ -1262,6 +1268,11 @@ def test_deferred_shard_rescan_second_round():
         assert abs(sim[b] - float(v @ Q[b])) <= 1e-12
         assert flags[b] & _native.MC_FLAG_TIE and flags[b] & _native.MC_FLAG_FALLBACK, flags[b]
         assert not flags[b] & _native.MC_FLAG_NEED_RESCAN
+    # past PIPE_SLACK appended rows the scanned window may be overwritten: refused
+    for r in rings:
+        r.append(np.repeat(v[None, :], 9, axis=0))
+    with pytest.raises(_native.NativeError):
+        rings[0].rescan_local(Q, gat[:nb])
     for r in rings:
         r.close()
 
