@@ -148,7 +148,9 @@ int mc_retrieve_local_async(mc_cache* h, const double* queries, int32_t B, void*
  * lookup): a record whose top-K' certificate failed keeps a rescan request, which the merge
  * reports as MC_FLAG_NEED_RESCAN.  Every shard then runs mc_rescan_local on the same queries and
  * its own records (in place), the records are gathered again and merged again.  The rescan
- * must run before a later lookup or flush applies appends / evictions on the handle. */
+ * runs against the window the lookup that wrote `dev_records` scanned (the handle remembers its
+ * last four local lookups), even if later lookups applied appends meanwhile, as long as at most
+ * PIPE_SLACK (8) rows were appended since; otherwise it fails with MC_ERR_STATE. */
 int mc_retrieve_local_submit(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream);
 int mc_rescan_local(mc_cache* h, const double* queries, int32_t B, void* dev_records, void* stream);
 
