@@ -1619,15 +1619,18 @@ int mc_merge_records_submit(mc_cache* h, const void* dev_records, int32_t G, int
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard guard(h->dev);
   if (h->merge_B[slot]) return fail(MC_ERR_STATE, "merge slot %d still holds an unread result", slot);
-  if (B > h->merge_cap) {  // grow every slot (none holds a result that is still in flight)
-    for (int i = 0; i < MC_MERGE_SLOTS; ++i)
-      if (h->merge_B[i]) CU(cudaEventSynchronize(h->merge_ev[i]));
+  if (B > h->merge_cap) {  // grow every slot; an unread result in another slot moves along
     int cap = 4;
     while (cap < B) cap <<= 1;
     for (int i = 0; i < MC_MERGE_SLOTS; ++i) {
+      OutRec* nh = nullptr;
+      CU(cudaHostAlloc(&nh, (size_t)cap * sizeof(OutRec), cudaHostAllocMapped));
+      if (h->merge_B[i]) {  // its merge must land before the copy
+        CU(cudaEventSynchronize(h->merge_ev[i]));
+        memcpy(nh, h->h_merge[i], (size_t)h->merge_B[i] * sizeof(OutRec));
+      }
       cudaFreeHost(h->h_merge[i]);
-      h->h_merge[i] = nullptr;
-      CU(cudaHostAlloc(&h->h_merge[i], (size_t)cap * sizeof(OutRec), cudaHostAllocMapped));
+      h->h_merge[i] = nh;
       CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_merge[i]), h->h_merge[i], 0));
       if (!h->merge_ev[i]) CU(cudaEventCreateWithFlags(&h->merge_ev[i], cudaEventDisableTiming));
     }

@@ -1204,6 +1204,20 @@ def test_pipelined_shard_merges_match_blocking_merges(B):
         best = S[:, b].max()
         assert abs(sim[b] - best) <= 1e-12
         assert live[b] == np.flatnonzero(S[:, b] == best).max()
+    # a larger batch grows the result slots while the other slot holds an unread result
+    big = torch.empty(G * 32 * 64, dtype=torch.uint8, device=dev)
+    Qb = np.ascontiguousarray(wl.queries(64))
+    for g, r in enumerate(rings):
+        r.retrieve_local_async(Qs[0], gathered[0][g * nb:(g + 1) * nb], cs.cuda_stream)
+        r.retrieve_local_async(Qb, big[g * 32 * 64:(g + 1) * 32 * 64], cs.cuda_stream)
+    rings[0].merge_submit(gathered[0], G, B, 0, cs.cuda_stream, 0)
+    rings[0].merge_submit(big, G, 64, 0, cs.cuda_stream, 1)
+    small_ans, big_ans = rings[0].merge_wait(0), rings[0].merge_wait(1)
+    cs.synchronize()
+    for x, y in zip(small_ans, rings[0].merge_records(gathered[0], G, B, 0, cs.cuda_stream)):
+        assert np.array_equal(x, y)
+    for x, y in zip(big_ans, rings[0].merge_records(big, G, 64, 0, cs.cuda_stream)):
+        assert np.array_equal(x, y)
     with pytest.raises(_native.NativeError):
         rings[0].merge_wait(0)  # nothing submitted into the slot
     rings[0].merge_submit(gathered[0], G, B, 0, cs.cuda_stream, 0)
@@ -1370,3 +1384,38 @@ def test_pipelined_batches_match_the_oracle(registered):
         c.unregister_host_buffer(Qall)
     assert checked == (n_b - 1) * B
     c.close()
+
+
+def test_wide_grid_local_lookups_match_the_scan():
+    """Local lookups over >= 128k rows that cannot overlap a neighbour (a pending row sends them
+    through the envelope copy) take the streamed scan's wide grid (two CTAs per SM): records and
+    merged decisions equal the reference scan formula (test_acceptance.py:429-436) on the rows."""
+    import torch
+
+    d, n = 256, 150_000
+    wl = ClusteredWorkload(d, n_clusters=256, seed=150)
+    rows = wl.cache_rows(n + 4)
+    ring = _native.DeviceRing(n, d, 0)
+    ring.append(rows[:n])
+    t = ThresholdTable.default()
+    ring.set_table(t.pairs, t.total_steps)
+    ot = OracleTable()
+    rec = torch.empty(32, dtype=torch.uint8, device="cuda")
+    for i in range(4):
+        ring.append(rows[n + i][None, :])  # pending row -> envelope path; FIFO evicts the oldest
+        window = rows[i + 1:n + i + 1]
+        q = wl.queries(1)
+        ring.retrieve_local_submit(q, rec)
+        torch.cuda.synchronize()
+        live, sim, k, flags = ring.merge_records(rec, 1, 1, i + 1)
+        if flags[0] & _native.MC_FLAG_NEED_RESCAN:
+            ring.rescan_local(q, rec)
+            torch.cuda.synchronize()
+            live, sim, k, flags = ring.merge_records(rec, 1, 1, i + 1)
+        s = window @ q[0]
+        best = s.max()
+        assert live[0] == np.flatnonzero(s == best)[-1], i
+        assert abs(sim[0] - best) <= 1e-12
+        assert k[0] == (ot.select_k(best) or 0)
+    assert ring.stats()["kernel_launches"] > 0
+    ring.close()
