@@ -1021,7 +1021,7 @@ def test_tiny_capacities_every_path(cap):
     c.close()
 
 
-@pytest.mark.parametrize("seed", [7, 8, 9, 10])
+@pytest.mark.parametrize("seed", [7, 8, 9, 10, 11, 12, 13, 14])
 def test_random_operations_with_pending_lookups(seed):
     """Randomised op logs with up to two retrieve_async lookups left pending across inserts (policy,
     age and capacity churn), bulk loads, synchronous and batched lookups and path switches: every
@@ -1062,6 +1062,16 @@ def test_random_operations_with_pending_lookups(seed):
         if got_id != want_id:  # only a near-duplicate row within numpy's own rounding may differ
             assert r.hit and e is not None and abs(float(r.entry.embedding @ q) - sim) <= 1e-12, (seed, where, r, e)
 
+    def check_any(res, want, where):
+        if isinstance(want, list):  # a batch: every answer at its submit state
+            assert len(res) == len(want)
+            for r, w in zip(res, want):
+                check(r, w, where, w[3])
+        else:
+            check(res, want, where, want[3])
+
+    qpool = np.ascontiguousarray(query(3000))
+    c.register_host_buffer(qpool)
     for step in range(120):
         op = rng.random()
         if op < 0.3:
@@ -1074,11 +1084,20 @@ def test_random_operations_with_pending_lookups(seed):
             for e in batch:
                 o.insert(OracleEntry(e.id, e.embedding, e.producer, e.seq, e.inserted_at))
         elif op < 0.7:  # submit; keep at most two pending on our side too
-            q = query(1)[0]
-            pending.append((c.retrieve_async(q, table), o.retrieve_entry(q, ot) + (q,)))
+            if rng.random() < 0.35:  # a batch: from the registered pool (copy-stream prefetch) or not
+                nb = int(rng.choice([2, 3, 7, 40]))
+                if rng.random() < 0.6:
+                    at = int(rng.integers(0, len(qpool) - nb))
+                    Q = qpool[at:at + nb]
+                else:
+                    Q = query(nb)
+                pending.append((c.retrieve_batch_async(Q, table), [o.retrieve_entry(q, ot) + (q,) for q in Q]))
+            else:
+                q = query(1)[0]
+                pending.append((c.retrieve_async(q, table), o.retrieve_entry(q, ot) + (q,)))
             if len(pending) > 2 or rng.random() < 0.3:
                 f, want = pending.pop(int(rng.integers(0, len(pending))))
-                check(f.result(), want, ("async", step), want[3])
+                check_any(f.result(), want, ("async", step))
         elif op < 0.85:
             q = query(1)[0]
             check(c.retrieve(q, table), o.retrieve_entry(q, ot), ("sync", step), q)
@@ -1088,7 +1107,8 @@ def test_random_operations_with_pending_lookups(seed):
             for q, r in zip(Q, c.retrieve_batch(Q, table)):
                 check(r, o.retrieve_entry(q, ot), ("batch", step), q)
     for f, want in pending:
-        check(f.result(), want, "final", want[3])
+        check_any(f.result(), want, "final")
+    c.unregister_host_buffer(qpool)
     assert len(c) == len(o.meta) == len(c.ring)
     c.close()
 
