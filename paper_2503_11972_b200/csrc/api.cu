@@ -122,7 +122,18 @@ struct mc_cache {
   bool inflight_ready = false;  // completed (and any fallback applied) while staging appends
   bool inflight_direct = false; // its result comes back zero-copy
   bool inflight_async = false;  // a batch whose decisions come back by an async D2H copy (batch_ev)
-  cudaEvent_t batch_ev = nullptr;
+  // Batches pipeline two deep: the in-flight batch uses batch slot `batch_slot` (0: d_rec / d_out /
+  // h_out, 1: the *2 buffers); an older batch still unanswered (old_async) uses the other one.
+  cudaEvent_t batch_ev[2] = {nullptr, nullptr};
+  int batch_slot = 0;
+  long long inflight_appended = 0;  // h->appended when the in-flight batch was enqueued
+  mc_record* d_rec2 = nullptr;
+  OutRec* d_out2 = nullptr;
+  OutRec* h_out2 = nullptr;
+  bool old_async = false;       // the older lookup is a batch still in flight (answered by finish_old)
+  int old_B = 0, old_bslot = 0;
+  const double* old_q = nullptr;
+  long long old_appended = 0;
   // A submitted batch answered when the next lookup was submitted (its decisions kept here until
   // its mc_retrieve_wait): batches pipeline one deep, the next one's upload and scan overlap the
   // caller's work on this one's answers.
@@ -323,6 +334,12 @@ void free_batch(mc_cache* h) {
   cudaFree(h->d_out);
   cudaFreeHost(h->h_out);
   cudaFreeHost(h->h_outp);
+  cudaFree(h->d_rec2);
+  cudaFree(h->d_out2);
+  cudaFreeHost(h->h_out2);
+  h->d_rec2 = nullptr;
+  h->d_out2 = nullptr;
+  h->h_out2 = nullptr;
   h->d_part_s = nullptr;
   h->d_part_p = nullptr;
   h->d_part_floor = nullptr;
@@ -377,6 +394,9 @@ int ensure_batch(mc_cache* h, int B) {
   CU(cudaMalloc(&h->d_rec, (size_t)cap * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_scratch, (size_t)cap * exact_grid(h->sm_count) * sizeof(mc_record)));
   CU(cudaMalloc(&h->d_out, (size_t)cap * sizeof(OutRec)));
+  CU(cudaMalloc(&h->d_rec2, (size_t)cap * sizeof(mc_record)));
+  CU(cudaMalloc(&h->d_out2, (size_t)cap * sizeof(OutRec)));
+  CU(cudaMallocHost(&h->h_out2, (size_t)cap * sizeof(OutRec)));
   CU(cudaHostAlloc(&h->h_out, (size_t)cap * sizeof(OutRec), cudaHostAllocMapped));
   CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_outm), h->h_out, 0));
   CU(cudaHostAlloc(&h->h_outp, (size_t)cap * 2 * sizeof(uint4), cudaHostAllocMapped));
@@ -737,9 +757,41 @@ int fallback_single(mc_cache* h, int slot, const RingState& st, OutRec* dst) {
   return MC_OK;
 }
 
+// A batch slot's records, device decisions and host decisions.
+mc_record* brec(const mc_cache* h, int s) { return s ? h->d_rec2 : h->d_rec; }
+OutRec* bdout(const mc_cache* h, int s) { return s ? h->d_out2 : h->d_out; }
+OutRec* bhout(const mc_cache* h, int s) { return s ? h->h_out2 : h->h_out; }
+
+// Wait for an asynchronous batch in slot s and apply the exhaustive fallback to the queries that
+// need it, on window st (the one the batch scanned; later batches may have applied up to
+// PIPE_SLACK rows since, which land in spare slots) with device queries q.
+int finish_batch(mc_cache* h, int s, int B, const RingState& st, const double* q) {
+  CU(cudaEventSynchronize(h->batch_ev[s]));
+  OutRec* ho = bhout(h, s);
+  bool need = false;
+  for (int b = 0; b < B; ++b) need |= (ho[b].flags & FLAG_NEED_ANY) != 0;
+  if (!need) return MC_OK;
+  CU(cudaMemcpyAsync(h->d_state_fb, &st, sizeof st, cudaMemcpyHostToDevice, h->stream));
+  CU(launch_exact_rescan(h->ring16, h->ring64, h->d_state_fb, h->D, h->Dp, q, B, brec(h, s), h->d_scratch,
+                         exact_grid(h->sm_count), gemv_eps_rel(h->Dp), eps_abs1(), h->shard, h->stream));
+  CU(launch_finalize(brec(h, s), 1, B, -1, h->d_state_fb, h->thr, bdout(h, s), h->stream));
+  h->stats[7] += 3;
+  CU(cudaMemcpyAsync(ho, bdout(h, s), (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return MC_OK;
+}
+
 // Complete the older pipelined lookup, if any (its answer stays in old_out for mc_retrieve_wait).
 int finish_old(mc_cache* h) {
   if (!h->old_seq || h->old_ready) return MC_OK;
+  if (h->old_async) {  // a batch: answered into old_batch
+    int rc = finish_batch(h, h->old_bslot, h->old_B, h->old_st, h->old_q);
+    if (rc) return rc;
+    h->old_batch.assign(bhout(h, h->old_bslot), bhout(h, h->old_bslot) + h->old_B);
+    h->old_async = false;
+    h->old_ready = true;
+    return MC_OK;
+  }
   int rc = wait_packed(h, h->old_seq, 1, h->old_slot, &h->old_out);
   if (rc) return rc;
   if (h->old_out.flags & FLAG_NEED_ANY) {
@@ -762,8 +814,11 @@ int finish_inflight(mc_cache* h) {
   if (h->inflight_direct)
     rc = wait_direct(h, h->inflight_seq, B, h->inflight_slot);
   else if (h->inflight_async) {
-    CU(cudaEventSynchronize(h->batch_ev));
+    rc = finish_batch(h, h->batch_slot, B, h->inflight_st, h->inflight_q);
+    if (rc) return rc;
     h->inflight_async = false;
+    h->inflight_ready = true;
+    return MC_OK;
   } else
     rc = wait_seq(h, h->inflight_seq);
   if (rc) return rc;
@@ -1019,7 +1074,8 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   CUC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   CUC(cudaEventCreateWithFlags(&h->env_ev, cudaEventDisableTiming));
   CUC(cudaEventCreateWithFlags(&h->rec_ev, cudaEventDisableTiming));
-  CUC(cudaEventCreateWithFlags(&h->batch_ev, cudaEventDisableTiming));
+  CUC(cudaEventCreateWithFlags(&h->batch_ev[0], cudaEventDisableTiming));
+  CUC(cudaEventCreateWithFlags(&h->batch_ev[1], cudaEventDisableTiming));
   const size_t n16 = (size_t)h->Cp * h->Dp * sizeof(__half);
   const size_t n64 = (size_t)h->Cp * h->Dp * sizeof(double);
   const size_t n8 = (size_t)h->Cp * h->P8;
@@ -1127,7 +1183,8 @@ int mc_destroy(mc_cache* h) {
     }
     if (h->env_ev) cudaEventDestroy(h->env_ev);
     if (h->rec_ev) cudaEventDestroy(h->rec_ev);
-    if (h->batch_ev) cudaEventDestroy(h->batch_ev);
+    for (cudaEvent_t e : h->batch_ev)
+      if (e) cudaEventDestroy(e);
     for (int i = 0; i < 2; ++i) {
       cudaFree(h->d_qslot[i]);
       if (h->q_ev[i]) cudaEventDestroy(h->q_ev[i]);
@@ -1301,19 +1358,40 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
   // is still in flight (its answer is collected later by its own mc_retrieve_wait).
   const bool pipe = B == 1 && h->count > 0 && h->packed && direct_result(h, 1) && h->n_pending <= PIPE_SLACK;
   if (h->inflight_seq && h->old_seq) return fail(MC_ERR_STATE, "two lookups are in flight: mc_retrieve_wait first");
-  if (h->inflight_seq && h->inflight_B != 1) {  // a batch: answer it now, keep it for its wait
+  if (h->inflight_seq && h->inflight_B != 1) {  // a batch in flight
     if (B > 1 && h->count > 0) {  // this batch's queries start moving while that one still scans
       int rc = prefetch_queries(h, queries, B);
       if (rc) return rc;
     }
-    int rc = finish_inflight(h);
-    if (rc) return rc;
-    h->old_batch.assign(h->h_out, h->h_out + h->inflight_B);
-    h->old_slot = 1;  // a single-query lookup submitted next takes slot 0
-    h->old_seq = h->inflight_seq;
-    h->old_ready = true;
-    h->inflight_seq = 0;
-    h->inflight_ready = false;
+    // Two deep: a prefetched batch queues behind the one in flight (the other batch slot), as
+    // long as the rows applied since that one's scan stay within the ring's spare slots.
+    // Its queries must sit in a query slot: the envelope may be rewritten by this submit, and a
+    // late exhaustive fallback of that batch re-reads them.
+    const bool in_slot = h->inflight_q && (h->inflight_q == h->d_qslot[0] || h->inflight_q == h->d_qslot[1]);
+    const bool deep = h->inflight_async && !h->inflight_ready && in_slot && B > 1 && h->pf_src == queries &&
+                      h->appended - h->inflight_appended <= PIPE_SLACK;
+    if (deep) {
+      h->old_seq = h->inflight_seq;
+      h->old_ready = false;
+      h->old_async = true;
+      h->old_B = h->inflight_B;
+      h->old_bslot = h->batch_slot;
+      h->old_st = h->inflight_st;
+      h->old_q = h->inflight_q;
+      h->old_appended = h->inflight_appended;
+      h->old_slot = 1;
+      h->inflight_seq = 0;
+      h->inflight_async = false;
+    } else {  // answer it now, keep it for its wait
+      int rc = finish_inflight(h);
+      if (rc) return rc;
+      h->old_batch.assign(bhout(h, h->batch_slot), bhout(h, h->batch_slot) + h->inflight_B);
+      h->old_slot = 1;  // a single-query lookup submitted next takes slot 0
+      h->old_seq = h->inflight_seq;
+      h->old_ready = true;
+      h->inflight_seq = 0;
+      h->inflight_ready = false;
+    }
   }
   if (h->inflight_seq) {
     if (h->inflight_B != 1) return fail(MC_ERR_STATE, "an asynchronous lookup is already in flight");
@@ -1329,17 +1407,22 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
     h->old_written = 0;
     h->inflight_seq = 0;
   }
-  if (h->old_seq && !pipe) {  // the new lookup cannot run beside it: answer the older one first
+  if (h->old_seq && !pipe && !h->old_async) {  // the new lookup cannot run beside it: answer the older one first
     int rc = finish_old(h);
     if (rc) return rc;
   }
-  if (h->old_seq && !h->old_ready && h->old_written + h->n_pending > PIPE_SLACK) {
+  if (h->old_seq && !h->old_ready && !h->old_async && h->old_written + h->n_pending > PIPE_SLACK) {
     int rc = finish_old(h);  // the rows this launch writes would reach the older lookup's window
+    if (rc) return rc;
+  }
+  if (B > h->Bcap && h->old_async) {  // growing the batch buffers: the older batch's answers move first
+    int rc = finish_old(h);
     if (rc) return rc;
   }
   int rc = ensure_batch(h, B);
   if (rc) return rc;
   const unsigned seq = ++h->seq;
+  h->batch_slot = 0;
   h->inflight_B = B;
   h->inflight_q = nullptr;
   // a batch (B > 1) runs only beside an older lookup that is already answered: slot 0 is free
@@ -1363,10 +1446,13 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
                       // next submit) waits for it.  The caller's query array must stay untouched until
                       // then when it is a registered buffer (the batch is DMA'd straight from it).
     const double* q = nullptr;
-    rc = lookup_enqueue(h, queries, B, h->d_rec, h->d_out, true, &q);
+    const int bs = h->old_async ? 1 - h->old_bslot : 0;
+    h->batch_slot = bs;
+    rc = lookup_enqueue(h, queries, B, brec(h, bs), bdout(h, bs), true, &q);
     if (rc) return rc;
-    CU(cudaMemcpyAsync(h->h_out, h->d_out, (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
-    CU(cudaEventRecord(h->batch_ev, h->stream));
+    CU(cudaMemcpyAsync(bhout(h, bs), bdout(h, bs), (size_t)B * sizeof(OutRec), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaEventRecord(h->batch_ev[bs], h->stream));
+    h->inflight_appended = h->appended;
     h->inflight_q = q;
     h->inflight_ready = false;
     h->inflight_direct = false;
@@ -1394,7 +1480,9 @@ int mc_retrieve_wait(mc_cache* h, uint32_t ticket, int64_t* out_live, double* ou
   if (!h) return fail(MC_ERR_ARG, "NULL handle");
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard guard(h->dev);
-  if (ticket && ticket == h->old_seq && !h->old_batch.empty()) {  // a batch answered at the next submit
+  if (ticket && ticket == h->old_seq && (h->old_async || !h->old_batch.empty())) {  // an older batch
+    int rc = finish_old(h);
+    if (rc) return rc;
     const OutRec* src = h->old_batch.data();
     const int B = (int)h->old_batch.size();
     for (int b = 0; b < B; ++b) {
@@ -1432,6 +1520,13 @@ int mc_retrieve_wait(mc_cache* h, uint32_t ticket, int64_t* out_live, double* ou
   const int B = h->inflight_B;
   h->inflight_seq = 0;
   h->inflight_ready = false;
+  if (h->batch_slot != 0) {  // an asynchronous batch answered in the second slot
+    OutRec* keep = h->h_out;
+    h->h_out = bhout(h, h->batch_slot);
+    rc = copy_out(h, B, out_live, out_sim, out_k, out_flags);
+    h->h_out = keep;
+    return rc;
+  }
   return copy_out(h, B, out_live, out_sim, out_k, out_flags);
 }
 
