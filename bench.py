@@ -386,6 +386,9 @@ def roofline(st, n_entries, dim, B, step_ms, rot, prof, n_rot, pk, cfg=None):
     else:
         roof = {"bound": "tensor", "achieved": flops / scan_s / 1e12, "peak": tc_burst, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    if roof["bound"] == "tensor":  # the back-to-back (power-limited) cuBLAS figure, beside the burst one
+        roof["frac_of_sustained"] = roof["achieved"] / tc_sust
+        roof["sustained_peak"] = tc_sust
     roof["peak_source"] = f"{src} (MEASURED_PEAKS.json)" if src == "measured" else "fallback (B200_PROFILING.md)"
     if roof["bound"] == "hbm":  # the measured peak is a read+write copy; a read-only scan can pass it
         roof["frac_of_spec"] = roof["achieved"] / 7700.0
