@@ -439,7 +439,7 @@ __device__ __forceinline__ void s8_finish(const S8Ctx x, const S8Args& a, const 
   const long long pbase = global_pos(x.st, 0, x.sm);
   if (a.sync) crec += (size_t)(tag & 1u) * a.rec_par;  // this epoch's record buffer
   if (lane == 0)
-    while (ld_acq_cta(&S.pool_done) != S8_CW + 2) {  // the nine pool warps and the eager rescorer
+    while (ld_acq_cta(&S.pool_done) != S8_CW + 2) {  // the pool warps (consumers + rescorer) and the eager rescorer
     }
   if (lane == 0 && a.sync)  // the launch two back used this buffer: its merger must be done reading it
     while ((int)(ld_acquire_gpu_u32(a.sync + 1) - (tag - 2u)) < 0) {
