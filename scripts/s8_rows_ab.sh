@@ -5,7 +5,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 for rep in 1 2; do
-for rpc in 0 128 256 512; do
+for rpc in ${RPCS:-0 128 256 512}; do
 MC_S8_ROWS_PER_CTA=$rpc python - <<'PY'
 import os, bench
 pk = bench.peaks()
