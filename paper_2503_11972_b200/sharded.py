@@ -61,6 +61,60 @@ from .records import (
 
 RECORD_BYTES = 32  # sizeof(mc_record)
 _NEED_RESCAN = 0x80  # MC_FLAG_NEED_RESCAN
+_MERGE_SLOTS = 2  # MC_MERGE_SLOTS
+_SLACK = 8  # PIPE_SLACK: rows a shard may append while a submitted lookup can still need its rescan
+
+
+class _ShardedPending:
+    """A submitted sharded lookup (ShardedSemanticCache.retrieve_async / retrieve_batch_async).
+    Its records are gathered and its merge is enqueued at submit; ``result()`` reads the
+    decisions (running the rescan round first if a shard's certificate failed) and returns what
+    retrieve() / retrieve_batch() would have returned at submit time.  A later lookup, a bulk
+    load or enough inserts complete it first, so a dropped future never wedges the cache."""
+
+    __slots__ = ("_c", "_Q", "_slot", "_p0", "_rec", "_single", "_appended", "_done", "_error")
+
+    def __init__(self, cache, Q, slot, p0, rec, single):
+        self._c, self._Q, self._slot, self._p0, self._rec, self._single = cache, Q, slot, p0, rec, single
+        self._appended = cache._appended
+        self._done = self._error = None
+
+    def _complete(self) -> None:
+        c = self._c
+        if c is None:
+            return
+        self._c = None
+        try:
+            c._pending.remove(self)
+        except ValueError:
+            pass
+        try:
+            gathered, stream, locals_ = self._rec
+            live, sim, k, flags = c.ring.merge_wait(self._slot)
+            if locals_ and (flags & _NEED_RESCAN).any():  # the same on every rank (SPMD)
+                c._rescan(self._Q, gathered, stream, locals_)
+                live, sim, k, flags = c.ring.merge_records(gathered, c.n_shards, self._Q.shape[0], self._p0, stream)
+            at = c._store.at_position
+            out = []
+            for i, f in enumerate(np.asarray(flags).tolist()):
+                if f & _HIT:
+                    out.append(make_result(at(self._p0 + int(live[i])), float(sim[i]), int(k[i]) or None))
+                elif f & _EMPTY:
+                    out.append(_MISS_EMPTY)
+                else:
+                    out.append(make_result(None, float(sim[i]), None))
+            self._done = out[0] if self._single else out
+        except BaseException as exc:  # kept: result() re-raises it
+            self._error = exc
+        finally:
+            c._store.unpin()
+
+    def result(self):
+        if self._c is not None:
+            self._complete()
+        if self._error is not None:
+            raise self._error
+        return self._done
 
 
 def _count_owned(p_lo: int, n: int, g: int, G: int) -> int:
@@ -123,6 +177,7 @@ class ShardedSemanticCache:
             self._rings[g] = ring
         self.ring = self._rings[min(self._rings)]  # the merging shard's ring
         self._table_key = None
+        self._pending: list[_ShardedPending] = []  # submitted lookups, oldest first (at most two)
 
     # -- bookkeeping -------------------------------------------------------------
     def __len__(self) -> int:
@@ -172,6 +227,8 @@ class ShardedSemanticCache:
         store = self._store
         if store and entry.seq <= store[-1].seq:
             raise ValueError(f"seq must increase: got {entry.seq} after {store[-1].seq}")
+        if self._pending and self._appended - self._pending[0]._appended >= _SLACK:
+            self._settle()  # a rescan of theirs must still find the window they scanned
         evicted: list[CacheEntry] = []
         if self.max_age_s is not None:
             horizon = entry.inserted_at - self.max_age_s
@@ -202,6 +259,7 @@ class ShardedSemanticCache:
         from .cache import _validated_prefix
 
         entries = list(entries)
+        self._settle()
         batch, bad = _validated_prefix(self, entries)
         if self.max_age_s is not None or len(batch) > self.capacity:  # the per-entry path decides evictions
             out: list[CacheEntry] = []
@@ -324,6 +382,7 @@ class ShardedSemanticCache:
             raise EmbeddingError(f"query batch has shape {Q.shape}, cache dim is {self.dim}")
         if Q.shape[0] == 0:
             return []
+        self._settle()
         if not self._store:
             return [_MISS_EMPTY] * Q.shape[0]
         key = (table.pairs, table.total_steps)
@@ -354,10 +413,58 @@ class ShardedSemanticCache:
             raise EmbeddingError(f"query has shape {q.shape}, cache dim is {self.dim}")
         return self.retrieve_batch(q[None, :], table)[0]
 
+    # -- pipelined lookups ----------------------------------------------------------
+    def _settle(self) -> None:
+        """Complete the submitted lookups (their answers stay in their futures)."""
+        while self._pending:
+            self._pending[0]._complete()
+
+    def _submit(self, Q: np.ndarray, table: ThresholdTable, single: bool):
+        from .cache import _Ready
+
+        if not self._store:
+            return _Ready(_MISS_EMPTY if single else [_MISS_EMPTY] * Q.shape[0])
+        key = (table.pairs, table.total_steps)
+        if key != self._table_key:
+            self._settle()  # a rescan round merges with the table of its submit
+            for ring in self._rings.values():
+                ring.set_table(table.pairs, table.total_steps)
+            self._table_key = key
+        if len(self._pending) >= _MERGE_SLOTS:
+            self._pending[0]._complete()
+        slot = min({0, 1} - {p._slot for p in self._pending})
+        rec = self._records(Q)
+        p0 = self.oldest_position
+        self.ring.merge_submit(rec[0], self.n_shards, Q.shape[0], p0, rec[1], slot)
+        self._store.pin()
+        fut = _ShardedPending(self, Q, slot, p0, rec, single)
+        self._pending.append(fut)
+        return fut
+
+    def retrieve_async(self, q: np.ndarray, table: ThresholdTable):
+        """retrieve() split in two (SemanticCache.retrieve_async): the lookup is enqueued against
+        the current cache and ``.result()`` returns what retrieve() would have returned then.
+        Inserts may go on meanwhile; two lookups may be pending."""
+        if q.shape != (self.dim,):
+            raise EmbeddingError(f"query has shape {q.shape}, cache dim is {self.dim}")
+        return self._submit(np.ascontiguousarray(q[None, :], dtype=np.float64), table, True)
+
+    def retrieve_batch_async(self, Q: np.ndarray, table: ThresholdTable):
+        """retrieve_batch() split in two, like retrieve_async."""
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        if Q.ndim != 2 or Q.shape[1] != self.dim:
+            raise EmbeddingError(f"query batch has shape {Q.shape}, cache dim is {self.dim}")
+        if Q.shape[0] == 0:
+            from .cache import _Ready
+
+            return _Ready([])
+        return self._submit(Q, table, False)
+
     def shard_sizes(self) -> list[int]:
         """Live rows per shard held by this process (shard id order)."""
         return [len(self._rings[g]) for g in sorted(self._rings)]
 
     def close(self) -> None:
+        self._settle()
         for ring in self._rings.values():
             ring.close()

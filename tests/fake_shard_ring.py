@@ -75,6 +75,8 @@ class FakeShardRing:
         per-ring counter) comes back degraded and flagged, as a failed certificate would."""
         self.retrieve_local_async(Q, out, stream)
         rec = out.numpy().view(REC)
+        # like the native ring: the window this lookup scanned, for a later rescan of its records
+        self.__dict__.setdefault("_windows", {})[out.data_ptr()] = (list(self.rows), list(self.pos))
         self._submits = getattr(self, "_submits", 0) + 1
         for b in range(Q.shape[0]):
             if rec[b]["pos"] >= 0 and (b + self._submits) % 3 == 0:
@@ -85,7 +87,12 @@ class FakeShardRing:
         rec = out.numpy().view(REC)
         need = [b for b in range(Q.shape[0]) if rec[b]["pos"] >= 0 and rec[b]["flags"] & self.NEED]
         exact = torch.empty_like(out)
-        self.retrieve_local_async(Q, exact, stream)
+        rows, pos = self.rows, self.pos
+        self.rows, self.pos = (list(x) for x in self._windows[out.data_ptr()])  # the scanned window
+        try:
+            self.retrieve_local_async(Q, exact, stream)
+        finally:
+            self.rows, self.pos = rows, pos
         ex = exact.numpy().view(REC)
         for b in need:
             rec[b] = ex[b]
@@ -111,6 +118,14 @@ class FakeShardRing:
             if any(r["flags"] & self.NEED for r in recs[:, b] if r["pos"] >= 0):
                 flags[b] |= _native.MC_FLAG_NEED_RESCAN
         return live, sim, k, flags
+
+    def merge_submit(self, gathered, G, B, p0, stream, slot):
+        slots = self.__dict__.setdefault("_slots", {})
+        assert slot not in slots, "merge slot still holds an unread result"
+        slots[slot] = self.merge_records(gathered, G, B, p0, stream)
+
+    def merge_wait(self, slot):
+        return self._slots.pop(slot)
 
     def close(self):
         pass

@@ -1439,3 +1439,19 @@ def test_wide_grid_local_lookups_match_the_scan():
         assert k[0] == (ot.select_k(best) or 0)
     assert ring.stats()["kernel_launches"] > 0
     ring.close()
+
+
+@pytest.mark.parametrize("G", [1, 3])
+def test_native_sharded_pipelined_lookups(G):
+    """ShardedSemanticCache.retrieve_async / retrieve_batch_async on native shard rings (one
+    device): merges enqueued at submit into the two result slots, read a request later, through
+    insert, capacity and age churn, against the oracle cache at submit time."""
+    from paper_2503_11972_b200.sharded import ShardedSemanticCache
+    from tests.test_sharded_gloo import _pipelined_against_oracle
+
+    sc = ShardedSemanticCache(37, 24, max_age_s=60.0, local_shards=G)
+    assert _pipelined_against_oracle(sc, 24, 37) > 300
+    sc.close()
+    sc = ShardedSemanticCache(900, 768, max_age_s=60.0, local_shards=G)
+    assert _pipelined_against_oracle(sc, 768, 900, steps=200, seed=5) > 200
+    sc.close()

@@ -82,6 +82,12 @@ def _worker(rank, world, port, errq):
         rescans = [None] * world
         dist.all_gather_object(rescans, getattr(sc.ring, "rescans", 0))
         assert sum(rescans) > 0, rescans
+        # pipelined lookups over the process group: futures complete in the same order on every
+        # rank, so the rescan round's all-gather stays SPMD
+        sp = ShardedSemanticCache(cap, d, max_age_s=60.0, ring_factory=FakeShardRing)
+        from tests.test_sharded_gloo import _pipelined_against_oracle
+
+        assert _pipelined_against_oracle(sp, d, cap, steps=150) > 150
         dist.destroy_process_group()
     except BaseException as exc:  # pragma: no cover - reported to the parent
         import traceback
@@ -165,3 +171,56 @@ def test_local_shards_match_oracle_on_cpu(G):
     n = _churn_against_oracle(lambda cap, d, pol, age: ShardedSemanticCache(
         cap, d, policy=pol, max_age_s=age, ring_factory=FakeShardRing, local_shards=G))
     assert n > 100
+
+
+def _pipelined_against_oracle(sc, d, cap, steps=300, seed=321):
+    """retrieve_async / retrieve_batch_async submitted before the request's insert and read one
+    request later (two pending), through capacity and age churn: every answer is the oracle's at
+    its submit state, entries by id."""
+    from oracle.retrieval import OracleCache, OracleEntry, OracleTable
+    from paper_2503_11972_b200 import CacheEntry, ThresholdTable
+
+    rng = np.random.default_rng(seed)
+    table, ot = ThresholdTable.default(), OracleTable()
+    centers = rng.standard_normal((5, d))
+    oc = OracleCache(cap, d, max_age_s=60.0)
+    t, prev, n_checked = 0.0, None, 0
+
+    def check(res, want):
+        nonlocal n_checked
+        res = [res] if not isinstance(res, list) else res
+        for r, (e, sim, k) in zip(res, want):
+            assert (r.entry.id if r.hit else None) == (e.id if e is not None else None)
+            assert r.k == k and (r.similarity is None) == (sim is None)
+            if sim is not None:
+                assert abs(r.similarity - sim) < 1e-12
+            n_checked += 1
+
+    for i in range(steps):
+        t += float(rng.exponential(1.0)) + (80.0 if i in (120, 240) else 0.0)
+        B = 1 if i % 3 else 3
+        Q = centers[rng.integers(0, 5, B)] + 0.7 * rng.standard_normal((B, d))
+        Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+        want = [oc.retrieve_entry(q, ot) for q in Q]
+        fut = sc.retrieve_async(Q[0], table) if B == 1 else sc.retrieve_batch_async(Q, table)
+        v = centers[i % 5] + 0.7 * rng.standard_normal(d)
+        v /= np.linalg.norm(v)
+        sc.insert(CacheEntry(f"e{i}", v, "large", i, t))
+        oc.insert(OracleEntry(f"e{i}", v, "large", i, t))
+        if prev is not None:
+            check(prev[0].result(), prev[1])
+        prev = (fut, want)
+    check(prev[0].result(), prev[1])
+    return n_checked
+
+
+@pytest.mark.parametrize("G", [1, 3])
+def test_local_shards_pipelined_lookups_on_cpu(G):
+    """ShardedSemanticCache.retrieve_async / retrieve_batch_async over FakeShardRing (degraded
+    records every third query: the rescan round runs at result time)."""
+    from paper_2503_11972_b200.sharded import ShardedSemanticCache
+    from tests.fake_shard_ring import FakeShardRing
+
+    sc = ShardedSemanticCache(37, 24, max_age_s=60.0, ring_factory=FakeShardRing, local_shards=G)
+    assert _pipelined_against_oracle(sc, 24, 37) > 300
+    assert sum(getattr(r, "rescans", 0) for r in sc._rings.values()) > 0
