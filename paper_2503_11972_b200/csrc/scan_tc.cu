@@ -553,19 +553,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TP_THREADS, 1)
 
 // q16[b] = fp16(q[b] / ||q[b]||), zero rows for b >= B and zero padding columns;
 // qscale[b] = ||q[b]|| turns a scan score back into query units.
-__global__ void __launch_bounds__(256) k_tc_prep(const double* __restrict__ q64, int B, int D, int Dp,
-                                                  __half* __restrict__ q16, double* __restrict__ qscale) {
+__global__ void __launch_bounds__(64) k_tc_prep(const double* __restrict__ q64, int B, int D, int Dp,
+                                                 __half* __restrict__ q16, double* __restrict__ qscale) {
   // the pair scan (launched as a programmatic dependent) may start its prologue now
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  // one warp per query row: all of the row's loads in flight at once, a warp reduction
+  // one warp per query row, two rows per CTA (B / 2 CTAs spread the 2 MB of C3 queries over
+  // the SMs); 16-byte loads, all of a row's loads in flight at once, a warp reduction
   const int lane = threadIdx.x & 31;
-  const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const double* src = q64 + (size_t)b * Dp;
+  const int b = blockIdx.x * 2 + (threadIdx.x >> 5);
+  const double2* src = reinterpret_cast<const double2*>(q64 + (size_t)b * Dp);  // Dp: a multiple of 64
+  const int n2 = Dp >> 1;
   double a = 0.0;
   if (b < B)
-    for (int i = lane; i < D; i += 32) {
-      const double x = src[i];
-      a = fma(x, x, a);
+    for (int i = lane; i < n2; i += 32) {
+      const double2 v = src[i];
+      const double x0 = 2 * i < D ? v.x : 0.0, x1 = 2 * i + 1 < D ? v.y : 0.0;
+      a = fma(x0, x0, a);
+      a = fma(x1, x1, a);
     }
 #pragma unroll
   for (int off = 16; off; off >>= 1) a += __shfl_xor_sync(FULL, a, off);
@@ -575,10 +579,11 @@ __global__ void __launch_bounds__(256) k_tc_prep(const double* __restrict__ q64,
   // launched as a programmatic dependent of the previous step's merge, which still reads qscale:
   // write only once that grid is done (the query reads above overlap its tail)
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  for (int i = 2 * lane; i < Dp; i += 64) {  // Dp is a multiple of 64
-    const double x0 = ok && i < D ? src[i] * inv : 0.0;
-    const double x1 = ok && i + 1 < D ? src[i + 1] * inv : 0.0;
-    *reinterpret_cast<__half2*>(q16 + (size_t)b * Dp + i) = __halves2half2(__double2half(x0), __double2half(x1));
+  for (int i = lane; i < n2; i += 32) {
+    double2 v = make_double2(0.0, 0.0);
+    if (ok) v = src[i];
+    const double x0 = 2 * i < D ? v.x * inv : 0.0, x1 = 2 * i + 1 < D ? v.y * inv : 0.0;
+    reinterpret_cast<__half2*>(q16 + (size_t)b * Dp)[i] = __halves2half2(__double2half(x0), __double2half(x1));
   }
   if (lane == 0 && b < B) qscale[b] = ok ? n : 0.0;
 }
@@ -687,8 +692,8 @@ cudaError_t launch_tc_scan(TcPlan* p, const double* q64, int B, int D, const Rin
   const int rows = nm * 256;
   {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((rows + 7) / 8);
-    cfg.blockDim = dim3(256);
+    cfg.gridDim = dim3((rows + 1) / 2);
+    cfg.blockDim = dim3(64);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // griddepcontrol.wait in k_tc_prep
