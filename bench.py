@@ -18,6 +18,7 @@ e2e    = the same steps through the public API (SemanticCache.retrieve + add)
 from __future__ import annotations
 
 import argparse
+import collections
 import json
 import os
 import subprocess
@@ -241,18 +242,19 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
         """`count` requests through the public API.  B = 1: each request is its lookup and its FIFO
         insert, the insert staged while the scan runs (retrieve_async: the lookup sees the cache
         as retrieve() would; the insert only affects later lookups).  Pipelined: request i+1 is
-        submitted before request i's answer is read (two lookups in flight, the API's limit), so
+        submitted before request i's answer is read (up to three lookups in flight, the API's limit), so
         the host's work overlaps the device's; the answers are those of the sequential loop."""
         prev = None
+        ahead = collections.deque()  # batch 1, pipelined: up to three lookups in flight
         for i in range(first, first + count):
             if B == 1:
                 pend = cache.retrieve_async(Qe[i][0], table)
                 if insert:
                     cache.add(f"{tag}{i}", re[i], "large", t_base + i)
                 if pipelined:
-                    if prev is not None:
-                        prev.result()
-                    prev = pend
+                    ahead.append(pend)
+                    if len(ahead) == 3:
+                        ahead.popleft().result()
                 else:
                     pend.result()
             elif pipelined:  # batch i+1 uploaded and scanned while the host reads batch i's answers
@@ -267,6 +269,8 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
                 int(res.hit.sum())  # the answers read back as arrays (result objects build on access)
                 if insert:
                     cache.add(f"{tag}{i}", re[i], "large", t_base + i)
+        while ahead:
+            ahead.popleft().result()
         if prev is not None:
             r = prev.result()
             if B > 1:
@@ -294,7 +298,8 @@ def run_config(name, dim, n_entries, B, steps, warmup, insert, flush_bytes, pk, 
         "h2d_bytes_per_step": B * dim * 8 + (dim * 8 if insert else 0),
         "d2h_bytes_per_step": B * 24,
         "kernel_launches_per_step": e2e_launches,
-        "mode": ("pipelined: retrieve_async of request i+1 before .result() of request i (two lookups in flight)"
+        "mode": ("pipelined: retrieve_async of requests i+1 and i+2 before .result() of request i (three lookups "
+                 "in flight)"
                  if B == 1 else "pipelined: retrieve_batch_async of batch i+1 before .result() of batch i"),
     }
     if B > 4:

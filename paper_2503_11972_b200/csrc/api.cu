@@ -160,13 +160,22 @@ struct mc_cache {
   RingState old_st{};
   OutRec old_out{};
   long long old_written = 0;    // rows launches after it have written into the ring
-  double* h_qslot[2] = {nullptr, nullptr};  // pinned [Dp]: the single-query lookups' queries (fallback uploads)
+  // A third single-query lookup in flight: the oldest of the three (older than `old`), in result
+  // slot old2_slot.  Same contract as `old`: its window survives the <= PIPE_SLACK rows later
+  // launches write, its answer is kept for its own mc_retrieve_wait.
+  unsigned old2_seq = 0;
+  bool old2_ready = false;
+  int old2_slot = 0;
+  RingState old2_st{};
+  OutRec old2_out{};
+  long long old2_written = 0;
+  double* h_qslot[3] = {nullptr, nullptr, nullptr};  // pinned [Dp]: the single-query lookups' queries (fallback uploads)
   double* d_qfb = nullptr;      // [Dp] fallback query
   RingState* d_state_fb = nullptr;  // the fallback's window
   bool param_in = false;        // MC_PARAM_INPUT=1: single-query lookups carry their inputs in the launch
                                 // parameters (measured equal to the pinned-envelope copy on B200)
   double* h_qkeep = nullptr;    // pinned, mapped [Dp]: the single-query launch's float64 query (read by the kernel)
-  double* h_stage1[2] = {nullptr, nullptr};  // pinned, mapped [Dp] per result slot: its pending row
+  double* h_stage1[3] = {nullptr, nullptr, nullptr};  // pinned, mapped [Dp] per result slot: its pending row
   double* d_gq64 = nullptr;     // [Dp] the kernel's L2 relay of the pending row
   unsigned* d_sync = nullptr;   // [2] streamed-scan launch overlap: rows published / records read (epochs)
   bool tc_tail = false;         // the last kernel enqueued on the stream is the tensor path's merge (PDL-early)
@@ -781,8 +790,23 @@ int finish_batch(mc_cache* h, int s, int B, const RingState& st, const double* q
   return MC_OK;
 }
 
+// Complete the oldest of three pipelined single-query lookups, if any (answer kept in old2_out).
+int finish_old2(mc_cache* h) {
+  if (!h->old2_seq || h->old2_ready) return MC_OK;
+  int rc = wait_packed(h, h->old2_seq, 1, h->old2_slot, &h->old2_out);
+  if (rc) return rc;
+  if (h->old2_out.flags & FLAG_NEED_ANY) {
+    rc = fallback_single(h, h->old2_slot, h->old2_st, &h->old2_out);
+    if (rc) return rc;
+  }
+  h->old2_ready = true;
+  return MC_OK;
+}
+
 // Complete the older pipelined lookup, if any (its answer stays in old_out for mc_retrieve_wait).
 int finish_old(mc_cache* h) {
+  int rc2 = finish_old2(h);  // the oldest first
+  if (rc2) return rc2;
   if (!h->old_seq || h->old_ready) return MC_OK;
   if (h->old_async) {  // a batch: answered into old_batch
     int rc = finish_batch(h, h->old_bslot, h->old_B, h->old_st, h->old_q);
@@ -959,7 +983,7 @@ void apply_sigma(mc_cache* h) {
 // The lookup of mc_retrieve_batch / mc_retrieve_decisions: B answers into h->h_out
 // (the caller holds the mutex and the device guard).
 int retrieve_into_hout(mc_cache* h, const double* queries, int32_t B) {
-  if (h->inflight_seq || h->old_seq)
+  if (h->inflight_seq || h->old_seq || h->old2_seq)
     return fail(MC_ERR_STATE, "an asynchronous lookup is in flight: mc_retrieve_wait first");
   int rc = ensure_batch(h, B);  // may reallocate d_rec / d_out / h_out: evaluate them after
   if (rc) return rc;
@@ -1112,13 +1136,13 @@ int mc_create(mc_cache** out, int64_t capacity, int32_t dim, int32_t device) {
   if (const char* e = getenv("MC_S8_ROWS_PER_CTA")) h->s8_rows_per_cta = atoll(e);
   CUC(cudaHostAlloc(&h->h_qkeep, (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
   memset(h->h_qkeep, 0, (size_t)h->Dp * sizeof(double));
-  for (int k = 0; k < 2; ++k) {  // mapped: the parameter-block launches read the query from here
+  for (int k = 0; k < 3; ++k) {  // mapped: the parameter-block launches read the query from here
     CUC(cudaHostAlloc(&h->h_qslot[k], (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
     memset(h->h_qslot[k], 0, (size_t)h->Dp * sizeof(double));
   }
   CUC(cudaMalloc(&h->d_qfb, (size_t)h->Dp * sizeof(double)));
   CUC(cudaMalloc(&h->d_state_fb, sizeof(RingState)));
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 3; ++k) {
     CUC(cudaHostAlloc(&h->h_stage1[k], (size_t)h->Dp * sizeof(double), cudaHostAllocMapped));
     memset(h->h_stage1[k], 0, (size_t)h->Dp * sizeof(double));
   }
@@ -1169,10 +1193,10 @@ int mc_destroy(mc_cache* h) {
     cudaFree(h->d_counter);
     cudaFreeHost(h->h_seq);
     cudaFreeHost(h->h_qkeep);
-    cudaFreeHost(h->h_stage1[0]);
-    cudaFreeHost(h->h_stage1[1]);
-    cudaFreeHost(h->h_qslot[0]);
-    cudaFreeHost(h->h_qslot[1]);
+    for (int k = 0; k < 3; ++k) {
+      cudaFreeHost(h->h_stage1[k]);
+      cudaFreeHost(h->h_qslot[k]);
+    }
     cudaFree(h->d_qfb);
     cudaFree(h->d_state_fb);
     cudaFree(h->d_gq64);
@@ -1357,7 +1381,25 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
   // Pipelining: a single-query lookup may be submitted while one other single-query lookup
   // is still in flight (its answer is collected later by its own mc_retrieve_wait).
   const bool pipe = B == 1 && h->count > 0 && h->packed && direct_result(h, 1) && h->n_pending <= PIPE_SLACK;
-  if (h->inflight_seq && h->old_seq) return fail(MC_ERR_STATE, "two lookups are in flight: mc_retrieve_wait first");
+  if (h->inflight_seq && h->old_seq) {
+    // Three deep: a single-query lookup beside two single-query lookups in flight; the older
+    // of those moves one level down (old -> old2).
+    if (h->old2_seq || B != 1 || h->inflight_B != 1 || h->old_async || !h->old_batch.empty())
+      return fail(MC_ERR_STATE, "lookups in flight: mc_retrieve_wait first (three single queries, or two with a batch)");
+    const bool deeper = pipe && h->inflight_direct;
+    if (!deeper) {  // it cannot run three deep: answer the oldest now (kept for its wait)
+      int rc = finish_old(h);
+      if (rc) return rc;
+    }
+    h->old2_seq = h->old_seq;
+    h->old2_ready = h->old_ready;
+    h->old2_slot = h->old_slot;
+    h->old2_st = h->old_st;
+    h->old2_out = h->old_out;
+    h->old2_written = h->old_written;
+    h->old_seq = 0;
+    h->old_ready = false;
+  }
   if (h->inflight_seq && h->inflight_B != 1) {  // a batch in flight
     if (B > 1 && h->count > 0) {  // this batch's queries start moving while that one still scans
       int rc = prefetch_queries(h, queries, B);
@@ -1411,6 +1453,10 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
     int rc = finish_old(h);
     if (rc) return rc;
   }
+  if (h->old2_seq && !h->old2_ready && h->old2_written + h->n_pending > PIPE_SLACK) {
+    int rc = finish_old2(h);  // the rows this launch writes would reach the oldest lookup's window
+    if (rc) return rc;
+  }
   if (h->old_seq && !h->old_ready && !h->old_async && h->old_written + h->n_pending > PIPE_SLACK) {
     int rc = finish_old(h);  // the rows this launch writes would reach the older lookup's window
     if (rc) return rc;
@@ -1426,7 +1472,13 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
   h->inflight_B = B;
   h->inflight_q = nullptr;
   // a batch (B > 1) runs only beside an older lookup that is already answered: slot 0 is free
-  h->inflight_slot = h->old_seq && B == 1 ? 1 - h->old_slot : 0;
+  if (B == 1 && h->old_seq) {  // a result slot no older lookup holds
+    int s = 0;
+    while (s == h->old_slot || (h->old2_seq && s == h->old2_slot)) ++s;
+    h->inflight_slot = s;
+  } else {
+    h->inflight_slot = 0;
+  }
   h->inflight_st = mirror(h);
   if (h->count == 0) {  // cache.py:252-253: answered now
     for (int b = 0; b < B; ++b) h->h_out[b] = empty_out(h);
@@ -1435,6 +1487,7 @@ int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* 
   } else if (direct_result(h, B)) {  // the kernel publishes into mapped memory; the caller returns now
     const double* q = nullptr;
     if (h->old_seq) h->old_written += std::min(h->n_pending, h->C);
+    if (h->old2_seq) h->old2_written += std::min(h->n_pending, h->C);
     // beside an older lookup: inputs in the launch (no envelope copy in the stream, which would
     // serialise behind the older kernel and hold back the host's next append)
     rc = enqueue_direct(h, queries, B, seq, /*async_reuse=*/true, &q, h->inflight_slot, h->old_seq != 0);
@@ -1501,6 +1554,18 @@ int mc_retrieve_wait(mc_cache* h, uint32_t ticket, int64_t* out_live, double* ou
     h->old_seq = 0;
     h->old_ready = false;
     return MC_OK;
+  }
+  if (ticket && ticket == h->old2_seq) {  // the oldest of three
+    int rc = finish_old2(h);
+    if (rc) return rc;
+    h->old2_seq = 0;
+    h->old2_ready = false;
+    OutRec* keep = h->h_out;
+    const OutRec saved = keep[0];
+    keep[0] = h->old2_out;
+    rc = copy_out(h, 1, out_live, out_sim, out_k, out_flags);
+    keep[0] = saved;
+    return rc;
   }
   if (ticket && ticket == h->old_seq) {
     int rc = finish_old(h);

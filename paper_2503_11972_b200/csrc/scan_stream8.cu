@@ -171,10 +171,13 @@ __device__ __forceinline__ void st_release_gpu_u32(unsigned* p, unsigned v) {
 // (~9 KB; every CTA needs them); the pending row stays in mapped host memory
 // and only CTA 0, which writes it into the ring, reads it (over PCIe, once,
 // with every load in flight) into an L2 relay buffer.
+#ifndef S8IN_DMAX
+#define S8IN_DMAX 1024  // measurement knob: a smaller parameter block (valid only for Dp <= S8IN_DMAX)
+#endif
 struct S8In {
   QPrep prep;
-  alignas(16) int8_t q8[1024];
-  alignas(16) double q64[1024];  // the float64 query, zero-padded to Dp
+  alignas(16) int8_t q8[S8IN_DMAX];
+  alignas(16) double q64[S8IN_DMAX];  // the float64 query, zero-padded to Dp
   const double* hstage;          // host-mapped pending row (zero-padded to Dp), or nullptr
 };
 struct S8NoIn {
@@ -1069,7 +1072,7 @@ cudaError_t launch_stream8_direct(const S8Plan* p, const RingBufs& rb, const Rin
                                   RingState* d_state, unsigned* done_seq, unsigned seq, uint4* outp,
                                   void (*quantise)(const double*, int, int, QPrep*, int8_t*), double* gq64,
                                   unsigned* sync, unsigned rec_par, bool overlap, cudaStream_t s) {
-  if (!p || p->Dp > 1024 || grid > 320) return cudaErrorInvalidValue;
+  if (!p || p->Dp > S8IN_DMAX || grid > 320) return cudaErrorInvalidValue;
   static thread_local S8In in;
   const int Dp = p->Dp;
   memcpy(in.q64, q64, (size_t)D * sizeof(double));

@@ -61,9 +61,11 @@ class FakeRing:
         return int(live[0]), float(sim[0]), int(k[0]), int(flags[0])
 
     def submit1(self, q):
-        # answered against the rows as they are now; like the native ring, at most two in flight
+        # answered against the rows as they are now; like the native ring, at most three single
+        # queries in flight (two beside a batch)
         pend = self.__dict__.setdefault("_inflight", {})
-        assert len(pend) < 2, "a third lookup submitted while two are in flight"
+        batches = self.__dict__.setdefault("_batch_tickets", set())
+        assert len(pend) < 3 and not (len(pend) >= 2 and batches & set(pend)), "too many lookups in flight"
         self._ticket = getattr(self, "_ticket", 6) + 1
         pend[self._ticket] = self.retrieve1(q)
         return self._ticket
@@ -76,6 +78,7 @@ class FakeRing:
         assert len(pend) < 2, "a third lookup submitted while two are in flight"
         self._ticket = getattr(self, "_ticket", 6) + 1
         pend[self._ticket] = self.retrieve(Q)
+        self.__dict__.setdefault("_batch_tickets", set()).add(self._ticket)
         return self._ticket
 
     def wait(self, ticket, B):

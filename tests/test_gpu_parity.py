@@ -902,11 +902,12 @@ def test_generated_million_entry_caches_match_the_oracle(n, nq):
     ring.close()
 
 
+@pytest.mark.parametrize("depth", [2, 3])
 @pytest.mark.parametrize("dim,cap,adds,dups", [(768, 3000, 1, False), (64, 50, 3, False), (64, 40, 1, True),
-                                                (32, 64, 9, True)])
-def test_pipelined_lookups_match_the_sequential_oracle(dim, cap, adds, dups):
-    """Two retrieve_async lookups in flight (request i submitted before request i-1's answer is
-    read), `adds` inserts between them, through FIFO wrap-around: every answer equals the oracle
+                                                (32, 64, 9, True), (1536, 200, 1, True)])
+def test_pipelined_lookups_match_the_sequential_oracle(dim, cap, adds, dups, depth):
+    """Two or three retrieve_async lookups in flight (request i submitted before request
+    i-depth+1's answer is read), `adds` inserts between them, through FIFO wrap-around: every answer equals the oracle
     cache's answer for the state at submit time.  `dups` inserts exact duplicates so certificates
     fail and the older lookup's exhaustive fallback runs after the newer launch (on the window it
     scanned: the spare physical slots keep it intact; 9 inserts exceed them and force the older
@@ -927,9 +928,14 @@ def test_pipelined_lookups_match_the_sequential_oracle(dim, cap, adds, dups):
     for v in rows[:cap]:
         add(v)
     Q = wl.queries(300)
-    prev = None
+    ahead = []  # (future, expected), up to depth - 1 unread while the next one is submitted
     nxt = cap
-    fallbacks = 0
+
+    def check(fut, want, i):
+        r, (e, sim, k) = fut.result(), want
+        assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (i, r, e)
+        assert r.k == k and _close(r.similarity, sim), (i, r, sim)
+
     for i, q in enumerate(Q):
         want = o.retrieve_entry(q, ot)
         p = c.retrieve_async(q, table)
@@ -937,15 +943,14 @@ def test_pipelined_lookups_match_the_sequential_oracle(dim, cap, adds, dups):
             v = rows[nxt % len(rows)] if not (dups and i % 3 == 0) else rows[(nxt - 1) % len(rows)]
             add(v)
             nxt += 1
-        if prev is not None:
-            r, (e, sim, k) = prev[0].result(), prev[1]
-            assert (r.entry.id if r.hit else None) == (e.id if e is not None else None), (i, r, e)
-            assert r.k == k and _close(r.similarity, sim), (i, r, sim)
-        prev = (p, want)
-    r, (e, sim, k) = prev[0].result(), prev[1]
-    assert (r.entry.id if r.hit else None) == (e.id if e is not None else None)
+        ahead.append((p, want))
+        if len(ahead) == depth:
+            check(*ahead.pop(0), i)
+    for f, w in ahead:
+        check(f, w, "final")
     fallbacks = c.ring.stats()["fallbacks"]
-    _record_parity(f"pipelined d{dim} cap{cap} adds{adds} dups{int(dups)}", {"queries": len(Q), "fallback": fallbacks})
+    _record_parity(f"pipelined depth{depth} d{dim} cap{cap} adds{adds} dups{int(dups)}",
+                   {"queries": len(Q), "fallback": fallbacks})
     c.close()
 
 

@@ -243,9 +243,9 @@ def test_threshold_table_nan_message_matches_the_reference():
 
 
 class TestPipelinedAndBatchResults:
-    def test_two_pending_lookups_answer_for_their_own_submit_state(self):
-        """Up to two retrieve_async lookups in flight: each answers for the cache as it was when
-        submitted; a third submit completes the oldest first."""
+    def test_pending_lookups_answer_for_their_own_submit_state(self):
+        """Up to three retrieve_async lookups in flight: each answers for the cache as it was when
+        submitted; a fourth submit completes the oldest first."""
         rng = np.random.default_rng(11)
         c = SemanticCache(capacity=8, dim=8)
         for i in range(8):
@@ -258,10 +258,22 @@ class TestPipelinedAndBatchResults:
         f1 = c.retrieve_async(q1, table)
         assert len(c._pending) == 2
         c.insert(entry(9, unit(rng, 8)))
-        f2 = c.retrieve_async(c.entries()[-1].embedding, table)  # completes f0 first
-        assert len(c._pending) == 2 and f0._cache is None
-        assert f1.result().entry.id == "e1" and f0.result().entry.id == "e0" and f2.result().entry.id == "e9"
+        q2 = c.entries()[0].embedding  # e2: evicted by the next insert
+        f2 = c.retrieve_async(q2, table)
+        assert len(c._pending) == 3 and f0._cache is not None
+        c.insert(entry(10, unit(rng, 8)))
+        f3 = c.retrieve_async(c.entries()[-1].embedding, table)  # completes f0 first
+        assert len(c._pending) == 3 and f0._cache is None
+        assert f1.result().entry.id == "e1" and f0.result().entry.id == "e0" and f2.result().entry.id == "e2"
+        assert f3.result().entry.id == "e10"
         assert not c._pending and c._store._pins == 0
+        # beside a batch, two: a single submit with a batch pending completes down to one
+        fb = c.retrieve_batch_async(np.stack([c.entries()[1].embedding, c.entries()[2].embedding]), table)
+        fs = c.retrieve_async(c.entries()[3].embedding, table)
+        fs2 = c.retrieve_async(c.entries()[4].embedding, table)  # completes the batch first
+        assert fb._cache is None and len(c._pending) == 2
+        assert [r.entry.id for r in fb.result()] == ["e4", "e5"] and fs.result().entry.id == "e6"
+        assert fs2.result().entry.id == "e7"
 
     def test_a_new_table_settles_pending_lookups(self):
         rng = np.random.default_rng(12)
