@@ -124,9 +124,14 @@ int mc_set_sigma_schedule(mc_cache* h, const double* schedule, int32_t n);
 /* Asynchronous form of mc_retrieve_batch (the serving loop's overlap of host
  * work with the scan): submit enqueues the lookup against the current cache
  * state and returns a ticket; wait returns its answers exactly as
- * mc_retrieve_batch would have.  One lookup may be in flight per handle.
- * mc_append / mc_evict_front between submit and wait only change what LATER
- * lookups see (a forced device flush first completes the lookup in flight). */
+ * mc_retrieve_batch would have.  Up to three single-query lookups may be in
+ * flight per handle (each newer launch queues behind the older kernels), or
+ * two when one is a batch (B > 1; a batch from registered memory has its
+ * queries DMA'd on a copy stream while the older batch scans); each ticket is
+ * collected by its own wait, in any order, and a further submit fails with
+ * MC_ERR_STATE.  mc_append / mc_evict_front between submit and wait only change
+ * what LATER lookups see (a forced device flush first completes the lookups in
+ * flight). */
 int mc_retrieve_submit(mc_cache* h, const double* queries, int32_t B, uint32_t* out_ticket);
 int mc_retrieve_wait(mc_cache* h, uint32_t ticket, int64_t* out_live, double* out_sim, int32_t* out_k,
                      uint32_t* out_flags);

@@ -444,7 +444,7 @@ class ShardedSemanticCache:
     def retrieve_async(self, q: np.ndarray, table: ThresholdTable):
         """retrieve() split in two (SemanticCache.retrieve_async): the lookup is enqueued against
         the current cache and ``.result()`` returns what retrieve() would have returned then.
-        Inserts may go on meanwhile; two lookups may be pending."""
+        Inserts may go on meanwhile; two lookups may be pending (the merge's two result slots)."""
         if q.shape != (self.dim,):
             raise EmbeddingError(f"query has shape {q.shape}, cache dim is {self.dim}")
         return self._submit(np.ascontiguousarray(q[None, :], dtype=np.float64), table, True)

@@ -1149,7 +1149,7 @@ def test_local_lookup_from_device_queries_matches_host_queries(B):
 
 
 def test_overlapping_launches_c2_scale_request_stream():
-    """C2 shape (100k x 768) with one insert per request and two lookups in flight, so each
+    """C2 shape (100k x 768) with one insert per request and lookups in flight, so each
     launch starts while the previous one still merges (its pending row published through the
     ring's sync word, its records in the other parity buffer): 400 answers against the oracle
     cache's sequential ones."""
