@@ -1460,3 +1460,26 @@ def test_native_sharded_pipelined_lookups(G):
     sc = ShardedSemanticCache(900, 768, max_age_s=60.0, local_shards=G)
     assert _pipelined_against_oracle(sc, 768, 900, steps=200, seed=5) > 200
     sc.close()
+
+
+def test_three_lookups_in_flight_at_the_c_abi():
+    """mc_retrieve_submit: three single-query lookups in flight, collected out of order, each equal
+    to the synchronous answer for its submit state; a fourth submit fails loudly; a batch beside two
+    single queries fails too (the Python layer completes older lookups first)."""
+    wl = ClusteredWorkload(768, n_clusters=32, seed=333)
+    ring = _native.DeviceRing(20_000, 768, 0)
+    ring.append(wl.cache_rows(20_000))
+    t = ThresholdTable.default()
+    ring.set_table(t.pairs, t.total_steps)
+    Q = wl.queries(4)
+    want = [ring.retrieve1(q) for q in Q[:3]]
+    tk = [ring.submit1(q) for q in Q[:3]]
+    with pytest.raises(_native.NativeError):
+        ring.submit1(Q[3])
+    for i in (1, 2, 0):  # out of order
+        assert ring.wait1(tk[i]) == want[i], i
+    tk = [ring.submit1(q) for q in Q[:2]]
+    with pytest.raises(_native.NativeError):
+        ring.submit(np.ascontiguousarray(wl.queries(8)))
+    assert [ring.wait1(x) for x in tk] == want[:2]
+    ring.close()
