@@ -40,6 +40,7 @@ to displace anything on its own.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -320,7 +321,8 @@ class ShardedSemanticCache:
             if self._dist is not None:  # one shard per rank: all-gather the B records (the only collective)
                 local = torch.empty(nb, dtype=torch.uint8, device=dev)
                 G = self.n_shards
-                if dev.type == "cuda" and G > 1 and B > 4 and B % G == 0 and self.dim % 64 == 0:
+                split = G > 1 or os.environ.get("MC_SHARD_SPLIT_UPLOAD") == "1"  # (1: test the path at G = 1)
+                if dev.type == "cuda" and split and B > 4 and B % G == 0 and self.dim % 64 == 0:
                     # the batch enters once: each rank uploads its 1/G of the rows and the ranks
                     # all-gather the queries over NVLink (mc_retrieve_local_device, rescan included)
                     part = B // G

@@ -1483,3 +1483,44 @@ def test_three_lookups_in_flight_at_the_c_abi():
         ring.submit(np.ascontiguousarray(wl.queries(8)))
     assert [ring.wait1(x) for x in tk] == want[:2]
     ring.close()
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_sharded_group_mode_over_nccl_world_one(split, monkeypatch):
+    """ShardedSemanticCache in group mode (one shard per rank) on a real NCCL process group of one
+    rank: the record all-gather, and with split = 1 the batch upload split over the ranks plus the
+    query all-gather (mc_retrieve_local_device), against the oracle cache through churn; sync and
+    pipelined lookups."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_11972_b200.sharded import ShardedSemanticCache
+    from tests.test_sharded_gloo import _pipelined_against_oracle
+
+    monkeypatch.setenv("MC_SHARD_SPLIT_UPLOAD", split)
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    monkeypatch.setenv("MASTER_ADDR", "127.0.0.1")
+    monkeypatch.setenv("MASTER_PORT", str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        sc = ShardedSemanticCache(900, 768, max_age_s=60.0, device=0)
+        assert _pipelined_against_oracle(sc, 768, 900, steps=120, seed=9) > 120
+        rng = np.random.default_rng(4)
+        table, ot = ThresholdTable.default(), OracleTable()
+        o = OracleCache(900, 768)
+        for e in sc.entries():
+            o.insert(OracleEntry(e.id, e.embedding, e.producer, e.seq, e.inserted_at))
+        Q = rng.standard_normal((16, 768))
+        Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+        Q[:8] = np.stack([sc.entries()[i].embedding for i in range(8)])  # exact hits
+        for q, r in zip(Q, sc.retrieve_batch(Q, table)):
+            e, sim, k = o.retrieve_entry(q, ot)
+            assert (r.entry.id if r.hit else None) == (e.id if e is not None else None)
+            assert r.k == k and _close(r.similarity, sim)
+        sc.close()
+    finally:
+        dist.destroy_process_group()
